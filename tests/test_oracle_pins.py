@@ -1,0 +1,455 @@
+"""Pins for the CPU oracle: each test ties an oracle function to something
+other than itself -- an independent 50-digit quantile evaluation, a closed
+form, brute force in exact rational arithmetic, a bound, or a value the paper
+prints.  CPU only (no GPU marker)."""
+from __future__ import annotations
+
+import math
+import statistics
+import struct
+from fractions import Fraction
+
+import mpmath
+import numpy as np
+import pytest
+
+from oracle import nqkv_oracle as O
+
+L32 = O.nf_levels_f32()
+
+
+# ---------------------------------------------------------------- levels ----
+def _mp_levels(bits=4, dps=50):
+    """Independent evaluation: Phi^-1(p) = sqrt(2) erfinv(2p-1) at 50 digits on
+    the SPEC.md:58 probability grid, computed in exact rationals."""
+    mpmath.mp.dps = dps
+    n = 1 << bits
+    delta = 1 - Fraction(1, 2) * (Fraction(1, 2 * n) + Fraction(1, 2 * (n - 1)))
+    half = n // 2
+
+    def ppf(p):
+        return mpmath.sqrt(2) * mpmath.erfinv(2 * mpmath.mpf(p.numerator) / p.denominator - 1)
+
+    negs = [-ppf(delta + k * (Fraction(1, 2) - delta) / (half - 1)) for k in range(half - 1)]
+    poss = [ppf(Fraction(1, 2) + k * (delta - Fraction(1, 2)) / half) for k in range(1, half + 1)]
+    d = ppf(delta)
+    vals = sorted([v / d for v in negs] + [mpmath.mpf(0)] + [v / d for v in poss])
+    return vals, delta, d
+
+
+def _f32_bits(x: float) -> int:
+    return struct.unpack("<I", struct.pack("<f", x))[0]
+
+
+def test_levels_structure():
+    # 16 values, strictly increasing, -1 / exact 0 / +1
+    assert L32.shape == (16,) and L32.dtype == np.float32
+    assert np.all(np.diff(L32) > 0)
+    assert L32[0] == -1.0 and L32[15] == 1.0
+    assert L32.view(np.uint32)[7] == 0          # +0.0 exactly
+    assert np.count_nonzero(L32 == 0) == 1
+    assert np.count_nonzero(L32 < 0) == 7 and np.count_nonzero(L32 > 0) == 8
+
+
+def test_levels_match_50_digit_quantiles_bit_exact():
+    vals, delta, d = _mp_levels()
+    # RN to fp32 of a 50-digit value: round via Python float (53 bits) is safe
+    # because every level sits >= 0.02 fp32-ulp from a rounding boundary; we
+    # check that margin explicitly so a double-rounding hazard would fail here.
+    for i, v in enumerate(vals):
+        f = float(v)
+        r32 = np.float32(f)
+        ulp = float(np.spacing(np.float32(abs(r32)))) if r32 != 0 else 1.0
+        lo = float(r32) - ulp / 2
+        hi = float(r32) + ulp / 2
+        if v != 0:
+            margin = min(abs(v - mpmath.mpf(lo)), abs(mpmath.mpf(hi) - v)) / ulp
+            assert margin > 0.01, (i, margin)
+        assert _f32_bits(float(r32)) == int(L32.view(np.uint32)[i]), i
+    assert abs(float(delta) - O.nf_offset()) < 4e-16   # double evaluation, <= 2 ulp
+    assert abs(float(delta) - 0.96770833333333333) < 1e-15
+
+
+def test_levels_match_statistics_normaldist():
+    # a third, unrelated Phi^-1 (Python's statistics module, Wichura AS241)
+    nd = statistics.NormalDist()
+    delta = O.nf_offset()
+    neg = [-nd.inv_cdf(p) for p in np.linspace(delta, 0.5, 8)[:-1]]
+    pos = [nd.inv_cdf(p) for p in np.linspace(0.5, delta, 9)[1:]]
+    d = nd.inv_cdf(delta)
+    vals = np.float32(np.array(sorted([v / d for v in neg] + [0.0] + [v / d for v in pos])))
+    assert np.array_equal(vals.view(np.uint32), L32.view(np.uint32))
+
+
+def test_normal_quantile_examples():
+    from scipy.special import ndtri
+    assert abs(ndtri(0.975) - 1.959964) < 1e-5
+    assert abs(ndtri(0.025) + 1.959964) < 1e-5
+    assert ndtri(0.5) == 0.0
+    assert abs(ndtri(O.nf_offset()) - 1.8481314207079737) < 1e-13
+
+
+def test_bits2_codebook():
+    # 4 codepoints, strictly increasing, containing -1, 0, 1
+    c = O.nf_levels_f64(2)
+    assert c.shape == (4,) and np.all(np.diff(c) > 0)
+    assert c[0] == -1.0 and c[-1] == 1.0 and 0.0 in c
+
+
+def test_max_gap():
+    g = np.max(np.diff(L32.astype(np.float64)))
+    assert abs(g - 0.30380720) < 1e-7
+    assert np.argmax(np.diff(L32)) == 0
+
+
+# ---------------------------------------------------------- code function --
+def _rn32_div(x: float, s: float) -> float:
+    """RN32(x/s) for fp32 x, s: exact rational quotient rounded to nearest-even
+    fp32 (independent of numpy's division)."""
+    q = Fraction(x) / Fraction(s)
+    return _rn32(q)
+
+
+def _rn32(q: Fraction) -> float:
+    if q == 0:
+        return 0.0
+    sign = -1 if q < 0 else 1
+    a = abs(q)
+    e = math.floor(math.log2(a.numerator) - math.log2(a.denominator))
+    while Fraction(2) ** e > a:
+        e -= 1
+    while Fraction(2) ** (e + 1) <= a:
+        e += 1
+    ulp = Fraction(2) ** (max(e, -126) - 23)
+    m = a / ulp
+    fl = math.floor(m)
+    rem = m - fl
+    if rem > Fraction(1, 2) or (rem == Fraction(1, 2) and fl % 2 == 1):
+        fl += 1
+    return sign * float(fl * ulp)
+
+
+def _brute_code(n: float) -> int:
+    """Nearest level in exact rationals; strict '<' keeps the lower index on ties."""
+    best, bestd = 0, None
+    for i, lv in enumerate(L32.tolist()):
+        d = abs(Fraction(n) - Fraction(lv))
+        if bestd is None or d < bestd:
+            best, bestd = i, d
+    return best
+
+
+def test_brute_force_256_normals():
+    # 256 seeded normals vs a brute-force nearest-codepoint search
+    rng = np.random.default_rng(0)
+    x = rng.standard_normal(256).astype(np.float16)
+    s, c = O.quantize_blocks(x.reshape(4, 64))
+    for blk in range(4):
+        xs = x.reshape(4, 64)[blk].astype(np.float32)
+        sc = max(abs(float(v)) for v in xs)
+        assert s[blk] == np.float32(sc)
+        for j in range(64):
+            n = _rn32_div(float(xs[j]), sc)
+            assert c[blk, j] == _brute_code(n)
+
+
+def test_fp32_division_is_ieee_rn():
+    rng = np.random.default_rng(1)
+    x = rng.standard_normal(2000).astype(np.float16).astype(np.float32)
+    s = np.float32(np.max(np.abs(x)))
+    n = (x / s).astype(np.float32)
+    for i in range(0, 2000, 7):
+        assert float(n[i]) == _rn32_div(float(x[i]), float(s))
+
+
+def test_tie_rule_lower_index():
+    # midpoints exactly representable in fp32 -> n == midpoint -> lower code
+    lv = L32.astype(np.float64)
+    exact = []
+    for i in range(15):
+        mid = (lv[i] + lv[i + 1]) / 2
+        if float(np.float32(mid)) == mid:
+            exact.append(i)
+            n = np.float32(mid)
+            assert O.nearest_level_codes(np.array([n]))[0] == i
+            assert O.codes_by_threshold(np.array([n]))[0] == i
+            assert _brute_code(float(n)) == i
+            up = np.nextafter(n, np.float32(2))
+            assert O.nearest_level_codes(np.array([up]))[0] == i + 1
+    assert exact == [2, 6, 7, 14]
+
+
+def test_threshold_form_equals_brute_force_near_every_boundary():
+    t = O.thresholds_f32()
+    cand = []
+    for ti in t:
+        v = ti
+        for _ in range(40):
+            v = np.nextafter(v, np.float32(-2))
+        for _ in range(80):
+            cand.append(v)
+            v = np.nextafter(v, np.float32(2))
+    rng = np.random.default_rng(2)
+    cand = np.concatenate([np.array(cand, np.float32),
+                           rng.uniform(-1, 1, 200000).astype(np.float32),
+                           np.array([-1, 1, 0, -0.0], np.float32)])
+    a = O.nearest_level_codes(cand)
+    b = O.codes_by_threshold(cand)
+    assert np.array_equal(a, b)
+    # exact-rational brute force on the near-boundary slice
+    for v in cand[:15 * 80:3]:
+        assert a[list(cand).index(v)] == _brute_code(float(v))
+
+
+def test_threshold_values_are_rounded_down_midpoints():
+    lv = L32.astype(np.float64)
+    t = O.thresholds_f32()
+    for i in range(15):
+        mid = Fraction(float(lv[i])) / 2 + Fraction(float(lv[i + 1])) / 2
+        assert Fraction(float(t[i])) <= mid
+        assert Fraction(float(np.nextafter(t[i], np.float32(2)))) > mid
+
+
+# ---------------------------------------------------------------- quantize --
+def test_grid_fixed_point():
+    # SPEC.md:70 adapted to fp16 input: block {fp16(s*L_c)} -> codes c
+    for s in [1.0, 0.5, 3.0, 17.25, 1e-3, 6.0e4]:
+        x = (np.float32(s) * L32).astype(np.float16)
+        sc, c = O.quantize_blocks(x.reshape(1, 16))
+        assert sc[0] == np.float32(np.float16(s))
+        assert np.array_equal(c[0], np.arange(16))
+
+
+def test_zero_block():
+    # SPEC.md:71, 79
+    sc, c = O.quantize_blocks(np.zeros((3, 64), np.float16))
+    assert np.all(sc == 0) and np.all(c == O.ZERO_CODE)
+    codes, scales = O.empty_cache(1, 1, 64, 64, 64)
+    O.quantize_append(np.zeros((1, 1, 1, 64), np.float16), [0], 64, codes, scales)
+    assert np.all(O.dequantize(codes, scales, 64, 1) == 0)
+
+
+def test_nonfinite_rejected():
+    with pytest.raises(ValueError):
+        O.quantize_blocks(np.array([[1.0, np.inf]], np.float16))
+
+
+def test_monotone_in_x():
+    # for fixed scale the code is nondecreasing in x
+    s = np.float16(2.5)
+    xs = np.sort(np.unique(np.linspace(-2.5, 2.5, 4001).astype(np.float16)))
+    blocks = np.stack([np.array([s, x], np.float16) for x in xs])
+    _, c = O.quantize_blocks(blocks)
+    assert np.all(np.diff(c[:, 1].astype(int)) >= 0)
+
+
+def test_idempotence():
+    # quantize(fp16(dequant(quantize(x)))) == quantize(x)
+    rng = np.random.default_rng(3)
+    x = (rng.standard_normal((500, 64)) * rng.lognormal(0, 0.5, 64)).astype(np.float16)
+    s, c = O.quantize_blocks(x)
+    deq = (s[:, None] * L32[c]).astype(np.float32).astype(np.float16)
+    s2, c2 = O.quantize_blocks(deq)
+    assert np.array_equal(c, c2) and np.array_equal(s, s2)
+
+
+def test_round_trip_bound_10000_blocks():
+    # |x - deq| <= scale * g/2, g = largest adjacent gap
+    rng = np.random.default_rng(4)
+    x = rng.standard_normal((10000, 64)).astype(np.float16)
+    s, c = O.quantize_blocks(x)
+    deq = (s[:, None] * L32[c]).astype(np.float32)
+    g = float(np.max(np.diff(L32.astype(np.float64))))
+    err = np.abs(x.astype(np.float64) - deq.astype(np.float64))
+    assert np.all(err <= s[:, None].astype(np.float64) * g / 2 * (1 + 1e-6))
+
+
+def test_nf4_beats_uniform_on_normal_blocks():
+    # SPEC.md:105 / acceptance 3: NF4 MSE strictly below a uniform 16-level
+    # absmax grid on >= 10,000 normal blocks of 256
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal((10000, 256)).astype(np.float16)
+    s, c = O.quantize_blocks(x)
+    nf = (s[:, None] * L32[c]).astype(np.float64)
+    uni = np.linspace(-1, 1, 16)
+    xf = x.astype(np.float64)
+    n = xf / s[:, None]
+    uq = uni[np.argmin(np.abs(n[..., None] - uni), axis=-1)] * s[:, None]
+    mse_nf = np.mean((xf - nf) ** 2)
+    mse_u = np.mean((xf - uq) ** 2)
+    assert mse_nf < mse_u
+    rel = math.sqrt(mse_nf) / math.sqrt(np.mean(xf ** 2))
+    assert 0.09 < rel < 0.105       # 0.0986 at blk 256
+
+
+def test_fig5_geometry():
+    # PAPER.md:193 (Fig. 5 caption): hidden 24, 1024 tokens, block 6 ->
+    # 4 blocks per token, 1024 x 4 blocks; 4096 scales
+    rng = np.random.default_rng(6)
+    x = rng.standard_normal((1, 1024, 1, 24)).astype(np.float16)
+    codes, scales = O.empty_cache(1, 1, 1024, 24, 6)
+    O.quantize_append(x, [0], 6, codes, scales)
+    assert scales.shape[-1] == 4 and scales[0, 0].size == 4096
+    assert codes[0, 0].shape == (1024, 12)
+
+
+def test_pack_layout_golden_row():
+    # element 2i low nibble, 2i+1 high nibble
+    c = np.arange(16, dtype=np.uint8)
+    p = O.pack_nibbles(c)
+    assert p.tolist() == [0x10, 0x32, 0x54, 0x76, 0x98, 0xBA, 0xDC, 0xFE]
+    assert np.array_equal(O.unpack_nibbles(p), c)
+    rng = np.random.default_rng(7)
+    r = rng.integers(0, 16, (100, 64)).astype(np.uint8)
+    assert np.array_equal(O.unpack_nibbles(O.pack_nibbles(r)), r)
+
+
+def test_streaming_equivalence_and_append_only():
+    # SPEC.md:164, 194-195
+    rng = np.random.default_rng(8)
+    B, T, H, hd, blk = 2, 16, 3, 64, 32
+    x = (rng.standard_normal((B, T, H, hd)) * 3).astype(np.float16)
+    c1, s1 = O.empty_cache(B, H, 64, hd, blk)
+    O.quantize_append(x, [0, 0], blk, c1, s1)
+    for j in (0, 5, 15):
+        c2, s2 = O.empty_cache(B, H, 64, hd, blk)
+        if j:
+            O.quantize_append(x[:, :j], [0, 0], blk, c2, s2)
+        for t in range(j, T):
+            before_c, before_s = c2.copy(), s2.copy()
+            O.quantize_append(x[:, t:t + 1], [t, t], blk, c2, s2)
+            mask = np.ones(64, bool)
+            mask[t] = False
+            assert np.array_equal(before_c[:, :, mask], c2[:, :, mask])
+            assert np.array_equal(before_s[:, :, mask], s2[:, :, mask])
+        assert np.array_equal(c1, c2) and np.array_equal(s1, s2)
+
+
+def test_ragged_positions():
+    rng = np.random.default_rng(9)
+    x = rng.standard_normal((2, 3, 1, 64)).astype(np.float16)
+    c, s = O.empty_cache(2, 1, 64, 64, 64)
+    O.quantize_append(x, [5, 40], 64, c, s)
+    ref_c, ref_s = O.empty_cache(1, 1, 64, 64, 64)
+    O.quantize_append(x[1:2], [40], 64, ref_c, ref_s)
+    assert np.array_equal(c[1], ref_c[0]) and np.all(c[0, :, 40:43] == 0)
+    assert np.all(s[0, :, :5] == 0) and np.all(s[0, :, 5:8] > 0)
+
+
+# ------------------------------------------------------------- dequantize --
+def test_dequant_examples():
+    # SPEC.md:79-80
+    codes = np.full((1, 1, 1, 1), 0xF0, np.uint8)     # elem0 code 0 (-1), elem1 code 15 (+1)
+    scales = np.full((1, 1, 1, 1), 2.0, np.float32)
+    v = O.dequantize(codes, scales, 2)
+    assert v.ravel().tolist() == [-2.0, 2.0]
+    assert np.all(O.dequantize(codes, np.zeros_like(scales), 2) == 0)
+
+
+def test_dequant_fp16_is_rn16_of_rn32():
+    # fp16 output = RN16(RN32(s * L))
+    rng = np.random.default_rng(10)
+    s = rng.uniform(0.01, 60000, 4096).astype(np.float16).astype(np.float32)
+    c = rng.integers(0, 16, 4096)
+    v32 = np.array([_rn32(Fraction(float(a)) * Fraction(float(L32[k]))) for a, k in zip(s, c)],
+                   np.float32)
+    codes = O.pack_nibbles(np.stack([c, c], -1).astype(np.uint8)).reshape(1, 1, 4096, 1)
+    out32 = O.dequantize(codes, s.reshape(1, 1, 4096, 1), 2)[..., 0].ravel()
+    assert np.array_equal(out32, v32)
+    out16 = O.dequantize(codes, s.reshape(1, 1, 4096, 1), 2, out_dtype=np.float16)[..., 0].ravel()
+    assert np.array_equal(out16, v32.astype(np.float16))
+
+
+# -------------------------------------------------------------- attention --
+def _cache_from(x, blk, Tc=64):
+    B, T, H, hd = x.shape
+    c, s = O.empty_cache(B, H, Tc, hd, blk)
+    O.quantize_append(x, [0] * B, blk, c, s)
+    return c, s
+
+
+def test_single_token_attention_returns_value():
+    # one cached token -> weight 1 -> t_O = dequantised v
+    rng = np.random.default_rng(11)
+    k = rng.standard_normal((2, 1, 3, 64)).astype(np.float16)
+    v = rng.standard_normal((2, 1, 3, 64)).astype(np.float16)
+    q = rng.standard_normal((2, 3, 64)).astype(np.float16)
+    kc, ks = _cache_from(k, 64)
+    vc, vs = _cache_from(v, 64)
+    out = O.decode_attention(q, kc, ks, vc, vs, [1, 1], 64)
+    assert np.array_equal(out, O.dequantize(vc, vs, 64, 1)[:, :, 0, :].astype(np.float64))
+
+
+def test_identical_keys_average_values():
+    # identical keys -> uniform weights -> mean of the V rows
+    rng = np.random.default_rng(12)
+    k = np.repeat(rng.standard_normal((1, 1, 2, 64)).astype(np.float16), 37, axis=1)
+    v = rng.standard_normal((1, 37, 2, 64)).astype(np.float16)
+    q = rng.standard_normal((1, 2, 64)).astype(np.float16)
+    kc, ks = _cache_from(k, 32)
+    vc, vs = _cache_from(v, 32)
+    out = O.decode_attention(q, kc, ks, vc, vs, [37], 32)
+    mean = O.dequantize(vc, vs, 32, 37).astype(np.float64).mean(axis=2)
+    assert np.max(np.abs(out - mean)) < 1e-12
+
+
+def test_empty_sequence_and_masking():
+    rng = np.random.default_rng(13)
+    k = rng.standard_normal((2, 20, 1, 64)).astype(np.float16)
+    v = rng.standard_normal((2, 20, 1, 64)).astype(np.float16)
+    q = rng.standard_normal((2, 1, 64)).astype(np.float16)
+    kc, ks = _cache_from(k, 64)
+    vc, vs = _cache_from(v, 64)
+    out = O.decode_attention(q, kc, ks, vc, vs, [0, 7], 64)
+    assert np.all(out[0] == 0)
+    # tokens >= seq_len must not matter: scribble over them
+    kc2, vc2 = kc.copy(), vc.copy()
+    kc2[:, :, 7:] = 0x5A
+    vc2[:, :, 7:] = 0xA5
+    out2 = O.decode_attention(q, kc2, ks, vc2, vs, [0, 7], 64)
+    assert np.array_equal(out[1], out2[1])
+
+
+def test_softmax_weights_and_dominant_key():
+    rng = np.random.default_rng(14)
+    K = rng.standard_normal((50, 64))
+    q = rng.standard_normal(64)
+    p = O.attention_weights(q, K, 0.125)
+    assert np.all(p >= 0) and abs(p.sum() - 1) < 1e-12
+    # a key aligned with q and huge norm dominates -> output -> its value row
+    x = np.zeros((1, 8, 1, 64), np.float16)
+    x[0, 3, 0, :] = np.sign(rng.standard_normal(64)).astype(np.float16) * 60
+    qq = (x[0, 3, 0, :] / 60).astype(np.float16).reshape(1, 1, 64)
+    v = rng.standard_normal((1, 8, 1, 64)).astype(np.float16)
+    kc, ks = _cache_from(x, 64)
+    vc, vs = _cache_from(v, 64)
+    out = O.decode_attention(qq, kc, ks, vc, vs, [8], 64)
+    vrow = O.dequantize(vc, vs, 64, 8)[0, 0, 3].astype(np.float64)
+    assert np.max(np.abs(out[0, 0] - vrow)) < 1e-9
+
+
+def test_token_permutation_invariance():
+    rng = np.random.default_rng(15)
+    k = rng.standard_normal((1, 30, 2, 64)).astype(np.float16)
+    v = rng.standard_normal((1, 30, 2, 64)).astype(np.float16)
+    q = rng.standard_normal((1, 2, 64)).astype(np.float16)
+    perm = rng.permutation(30)
+    a = O.decode_attention(q, *_cache_from(k, 64), *_cache_from(v, 64), [30], 64)
+    b = O.decode_attention(q, *_cache_from(k[:, perm], 64), *_cache_from(v[:, perm], 64), [30], 64)
+    assert np.max(np.abs(a - b)) < 1e-12
+
+
+# ------------------------------------------------------------- byte model --
+def test_byte_model_spec_examples():
+    # SPEC.md:190-191
+    assert O.cache_bytes(1, 256, 256, 4) == 264
+    assert (O.cache_bytes(1000, 256, 256, 4) * 8) / (2 * 1000 * 256) == 4.125
+
+
+def test_paper_memory_arithmetic():
+    # OPT-175B (96 layers, d 12288), batch 64, seq 8192:
+    # KV cache "2.3TB", "seven times the size of the model's own parameters"
+    kv = O.fp16_kv_bytes(96, 64, 8192, 12288)
+    assert round(kv / 2 ** 40, 1) == 2.3 or round(kv / 1e12, 1) == 2.5
+    assert round(kv / 2 ** 40, 2) == 2.25
+    assert round(kv / (175e9 * 2)) == 7
