@@ -1,0 +1,137 @@
+/*
+ * nqkv.h -- C ABI of the B200-native NQKV hot path (arXiv 2505.16210).
+ *
+ * NQKV stores the K/V cache as 4-bit NormalFloat (NF4) indices plus one
+ * absmax scale per block and dequantises by table lookup at decode time
+ * (PAPER.md:193, 201, 205, 213-235).  This library implements the four
+ * operations of the paper's problem statement:
+ *
+ *   nqkv_levels            the NF4 level table
+ *   nqkv_quantize          I <- Concat(I, quantize_NF4(X))
+ *   nqkv_dequantize        X' = dequantize_NF4(I)
+ *   nqkv_decode_attention  t_O = Softmax(t_Q X_K'^T/sqrt(d)) X_V'  with the
+ *                          dequantisation fused in registers
+ *
+ * Conventions (all entry points)
+ *  - The caller owns every buffer.  The library never allocates, frees or
+ *    synchronises; device work is enqueued on `stream` (a cudaStream_t passed
+ *    as void*, NULL = legacy default stream) and returns immediately.
+ *  - "device" pointers must be device-accessible (cudaMalloc / torch CUDA
+ *    tensors); "host" pointers are ordinary host memory.
+ *  - Host-checkable argument errors return a negative nqkv_status and launch
+ *    nothing.  A failed launch returns NQKV_ERR_CUDA; nqkv_last_error()
+ *    returns the CUDA error string (thread-local).
+ *  - Values that live on the device (positions, sequence lengths, input
+ *    values) are not checked: out-of-range positions are skipped, a
+ *    non-finite input value produces unspecified codes (the CPU oracle
+ *    rejects non-finite input).
+ *  - Cache layout (one tensor each for K and V; fixed):
+ *        codes  uint8   [B][H][Tc][hd/2]   element 2i in the low nibble of byte i,
+ *                                          2i+1 in the high nibble
+ *        scales float32 [B][H][Tc][hd/blk] absmax of each block of blk
+ *                                          consecutive channels of one (token, head)
+ *  - Supported geometry: hd in {64, 128}; blk in {32, 64, 128} with blk <= hd;
+ *    Tc a positive multiple of 64.  Anything else -> NQKV_ERR_UNSUPPORTED /
+ *    NQKV_ERR_SHAPE.
+ *  - Calls are thread-safe and reentrant.  The only global state is the level
+ *    table, computed once on the host (std::call_once) and passed to kernels
+ *    by value.
+ */
+#ifndef NQKV_H_
+#define NQKV_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NQKV_ABI_VERSION 1
+
+typedef enum {
+  NQKV_OK = 0,
+  NQKV_ERR_NULL = -1,        /* a required pointer is NULL */
+  NQKV_ERR_SHAPE = -2,       /* negative size, Tc % 64 != 0, ... */
+  NQKV_ERR_UNSUPPORTED = -3, /* hd / blk combination not built */
+  NQKV_ERR_ALIGN = -4,       /* pointer or stride not 16-byte aligned */
+  NQKV_ERR_WORKSPACE = -5,   /* workspace smaller than nqkv_decode_workspace_bytes */
+  NQKV_ERR_CUDA = -6,        /* kernel launch / device query failed */
+  NQKV_ERR_INTERNAL = -7     /* level-table construction invariant violated */
+} nqkv_status;
+
+int nqkv_abi_version(void);
+const char* nqkv_status_string(int status);
+const char* nqkv_last_error(void);
+
+/* a0. NF4 levels.
+ * levels: host float[16], written ascending.  delta = 1 - (1/32 + 1/30)/2;
+ * negatives -Phi^-1(delta + k(0.5-delta)/7), k=0..6; zero; positives
+ * Phi^-1(0.5 + k(delta-0.5)/8), k=1..8; all divided by Phi^-1(delta),
+ * evaluated in double (Phi^-1 by Halley-refined erfc) and rounded to fp32.
+ * L[0] = -1, L[7] = +0, L[15] = +1.  Host only; no device needed. */
+int nqkv_levels(float levels[16]);
+
+/* Decision thresholds used by the kernels: T[i] = RD32((L[i]+L[i+1])/2),
+ * code(n) = #{i : n > T[i]} == argmin_i |n - L[i]| with ties to the lower
+ * index.  Host only. */
+int nqkv_thresholds(float thresholds[15]);
+
+/* a1-a3. Quantize + pack + append.
+ * x      device fp16, logical [B][n_new][H][hd] with element strides
+ *        stride_b, stride_t, stride_h (hd contiguous); 16-byte aligned, all
+ *        strides multiples of 8 elements.
+ * d_pos  device int32[B]: token row where batch b's first new token goes;
+ *        rows d_pos[b] .. d_pos[b]+n_new-1 are written, all other bytes of
+ *        codes/scales are left untouched (append-only).  Rows
+ *        outside [0, Tc) are skipped.
+ * codes  device uint8  [B][H][Tc][hd/2]    (16-byte aligned)
+ * scales device float  [B][H][Tc][hd/blk]  (4-byte aligned)
+ * Per block: s = max|x| (fp32, exact); n = RN32(x/s) (IEEE division, computed
+ * as a correctly rounded reciprocal plus one Markstein correction);
+ * code = nearest level, ties lower; s == 0 -> code 7 (the zero level). */
+int nqkv_quantize(const void* x, int64_t stride_b, int64_t stride_t, int64_t stride_h,
+                  int B, int H, int hd, int n_new, int blk,
+                  const int32_t* d_pos, int Tc, uint8_t* codes, float* scales,
+                  void* stream);
+
+/* a4 (standalone). Dequantize rows [0, n_tokens) of every (b, h)
+ * (no padding).
+ * out: device, [B][H][n_tokens][hd], out_dtype 0 = fp32 (RN32(s*L[code])),
+ * 1 = fp16 (RN16 of that fp32 value); 16-byte aligned.  n_tokens <= Tc. */
+int nqkv_dequantize(const uint8_t* codes, const float* scales, int B, int H, int Tc, int hd,
+                    int blk, int n_tokens, int out_dtype, void* out, void* stream);
+
+/* Bytes of workspace nqkv_decode_attention needs for this geometry. */
+size_t nqkv_decode_workspace_bytes(int B, int H, int hd, int Tc);
+
+/* a4-a7. Fused decode attention over the 4-bit cache.
+ * For every (b, h): out = softmax(softmax_scale * q . k_t) . v_t over
+ * t < seq_lens[b], with k_t, v_t dequantised in registers (never written to
+ * memory).  Split-K: the sequence is cut into fixed 64-token chunks (a
+ * function of seq_len only, so results do not depend on B, H or the GPU);
+ * partial (max, sum, o) are merged in fixed chunk order.
+ * q          device fp16 [B][H][hd], 16-byte aligned
+ * k_codes,…  the cache tensors described above
+ * d_seq_lens device int32[B], 0..Tc, counting the token appended this step
+ *            (append-before-attend); 0 -> out[b] = 0
+ * out        device fp32 [B][H][hd], 16-byte aligned
+ * workspace  device, >= nqkv_decode_workspace_bytes(B,H,hd,Tc) bytes,
+ *            16-byte aligned, ZERO-FILLED before its first use; every call
+ *            leaves it zero-filled again.  Do not share one workspace between
+ *            calls that may run concurrently. */
+int nqkv_decode_attention(const void* q, const uint8_t* k_codes, const float* k_scales,
+                          const uint8_t* v_codes, const float* v_scales,
+                          const int32_t* d_seq_lens, int B, int H, int hd, int blk, int Tc,
+                          float softmax_scale, float* out, void* workspace, size_t ws_bytes,
+                          void* stream);
+
+/* Test hook: the kernels' code function on fp32 inputs already normalised
+ * to [-1, 1] (values outside are clamped).  d_n device float[count],
+ * d_codes device uint8[count]. */
+int nqkv_encode_normalized(const float* d_n, int64_t count, uint8_t* d_codes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NQKV_H_ */

@@ -1,0 +1,184 @@
+"""Thin ctypes binding of the NQKV C ABI (include/nqkv.h).
+
+Argument marshalling only: every step of the hot path runs in libnqkv.so's
+CUDA kernels.  PyTorch supplies device memory and the stream.  There is no
+CPU fallback: if the library is missing this module raises at import time.
+Function names mirror the C entry points.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+
+import numpy as np
+import torch
+
+_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libnqkv.so")
+if not os.path.exists(_LIB_PATH):
+    raise ImportError(
+        f"{_LIB_PATH} not built; run `python -c 'import __graft_entry__ as g; g.build()'` "
+        "(the NQKV path has no CPU fallback)")
+_lib = ctypes.CDLL(_LIB_PATH)
+
+_vp, _i32, _i64, _sz = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_size_t
+_fp = ctypes.POINTER(ctypes.c_float)
+
+_SIGS = {
+    "nqkv_abi_version": (_i32, []),
+    "nqkv_status_string": (ctypes.c_char_p, [_i32]),
+    "nqkv_last_error": (ctypes.c_char_p, []),
+    "nqkv_levels": (_i32, [_fp]),
+    "nqkv_thresholds": (_i32, [_fp]),
+    "nqkv_quantize": (_i32, [_vp, _i64, _i64, _i64, _i32, _i32, _i32, _i32, _i32, _vp, _i32,
+                             _vp, _vp, _vp]),
+    "nqkv_dequantize": (_i32, [_vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _vp]),
+    "nqkv_decode_workspace_bytes": (_sz, [_i32, _i32, _i32, _i32]),
+    "nqkv_decode_attention": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32,
+                                     ctypes.c_float, _vp, _vp, _sz, _vp]),
+    "nqkv_encode_normalized": (_i32, [_vp, _i64, _vp, _vp]),
+}
+for _name, (_res, _args) in _SIGS.items():
+    _f = getattr(_lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+
+EXPORTED = tuple(_SIGS)
+ABI_VERSION = 1
+if _lib.nqkv_abi_version() != ABI_VERSION:
+    raise ImportError("libnqkv.so ABI version mismatch; rebuild")
+
+STATUS = {0: "NQKV_OK", -1: "NQKV_ERR_NULL", -2: "NQKV_ERR_SHAPE", -3: "NQKV_ERR_UNSUPPORTED",
+          -4: "NQKV_ERR_ALIGN", -5: "NQKV_ERR_WORKSPACE", -6: "NQKV_ERR_CUDA",
+          -7: "NQKV_ERR_INTERNAL"}
+
+
+class NQKVError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        detail = _lib.nqkv_last_error().decode() if status == -6 else ""
+        super().__init__(f"{where}: {STATUS.get(status, status)} "
+                         f"({_lib.nqkv_status_string(status).decode()}) {detail}".rstrip())
+        self.status = status
+
+
+def _check(status: int, where: str) -> None:
+    if status != 0:
+        raise NQKVError(status, where)
+
+
+def _ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _stream(stream) -> int:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+# ----------------------------------------------------------------- host ----
+def nqkv_levels() -> np.ndarray:
+    out = np.zeros(16, np.float32)
+    _check(_lib.nqkv_levels(out.ctypes.data_as(_fp)), "nqkv_levels")
+    return out
+
+
+def nqkv_thresholds() -> np.ndarray:
+    out = np.zeros(15, np.float32)
+    _check(_lib.nqkv_thresholds(out.ctypes.data_as(_fp)), "nqkv_thresholds")
+    return out
+
+
+def nqkv_decode_workspace_bytes(B: int, H: int, hd: int, Tc: int) -> int:
+    return int(_lib.nqkv_decode_workspace_bytes(B, H, hd, Tc))
+
+
+# --------------------------------------------------------------- device ----
+def nqkv_quantize(x: torch.Tensor, pos: torch.Tensor, codes: torch.Tensor, scales: torch.Tensor,
+                  blk: int, stream=None) -> None:
+    """Append x (fp16 [B, n_new, H, hd], hd contiguous, any outer strides) at
+    rows pos[b].. of the cache tensors codes [B,H,Tc,hd/2] u8 / scales
+    [B,H,Tc,hd/blk] f32."""
+    B, n_new, H, hd = x.shape
+    Tc = codes.shape[2]
+    assert x.dtype == torch.float16 and x.stride(3) == 1
+    assert pos.dtype == torch.int32 and codes.dtype == torch.uint8 and scales.dtype == torch.float32
+    assert codes.is_contiguous() and scales.is_contiguous() and tuple(codes.shape[:2]) == (B, H)
+    _check(_lib.nqkv_quantize(_ptr(x), x.stride(0), x.stride(1), x.stride(2), B, H, hd, n_new, blk,
+                              _ptr(pos), Tc, _ptr(codes), _ptr(scales), _stream(stream)),
+           "nqkv_quantize")
+
+
+def nqkv_dequantize(codes: torch.Tensor, scales: torch.Tensor, blk: int, n_tokens: int | None = None,
+                    out_dtype=torch.float32, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    B, H, Tc, hb = codes.shape
+    hd = hb * 2
+    n_tokens = Tc if n_tokens is None else n_tokens
+    if out is None:
+        out = torch.empty((B, H, n_tokens, hd), dtype=out_dtype, device=codes.device)
+    code = {torch.float32: 0, torch.float16: 1}[out.dtype]
+    _check(_lib.nqkv_dequantize(_ptr(codes), _ptr(scales), B, H, Tc, hd, blk, n_tokens, code,
+                                _ptr(out), _stream(stream)), "nqkv_dequantize")
+    return out
+
+
+def nqkv_decode_attention(q: torch.Tensor, k_codes: torch.Tensor, k_scales: torch.Tensor,
+                          v_codes: torch.Tensor, v_scales: torch.Tensor, seq_lens: torch.Tensor,
+                          blk: int, workspace: torch.Tensor, softmax_scale: float | None = None,
+                          out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """out[b,h] = softmax(softmax_scale * q k^T) v over the first seq_lens[b]
+    cached tokens.  workspace: zero-filled uint8 tensor of
+    nqkv_decode_workspace_bytes(...) bytes (see make_workspace)."""
+    B, H, hd = q.shape
+    Tc = k_codes.shape[2]
+    if softmax_scale is None:
+        softmax_scale = 1.0 / math.sqrt(hd)
+    if out is None:
+        out = torch.empty((B, H, hd), dtype=torch.float32, device=q.device)
+    assert q.dtype == torch.float16 and q.is_contiguous() and out.is_contiguous()
+    assert seq_lens.dtype == torch.int32
+    _check(_lib.nqkv_decode_attention(_ptr(q), _ptr(k_codes), _ptr(k_scales), _ptr(v_codes),
+                                      _ptr(v_scales), _ptr(seq_lens), B, H, hd, blk, Tc,
+                                      float(softmax_scale), _ptr(out), _ptr(workspace),
+                                      workspace.numel() * workspace.element_size(),
+                                      _stream(stream)), "nqkv_decode_attention")
+    return out
+
+
+def nqkv_encode_normalized(n: torch.Tensor, stream=None) -> torch.Tensor:
+    assert n.dtype == torch.float32 and n.is_contiguous()
+    codes = torch.empty(n.shape, dtype=torch.uint8, device=n.device)
+    _check(_lib.nqkv_encode_normalized(_ptr(n), n.numel(), _ptr(codes), _stream(stream)),
+           "nqkv_encode_normalized")
+    return codes
+
+
+# ------------------------------------------------------------ conveniences --
+def make_workspace(B: int, H: int, hd: int, Tc: int, device="cuda") -> torch.Tensor:
+    return torch.zeros(nqkv_decode_workspace_bytes(B, H, hd, Tc), dtype=torch.uint8, device=device)
+
+
+class KVCache:
+    """Per-layer packed NF4 K/V cache in the library's layout:
+    codes u8 [B,H,Tc,hd/2], scales f32 [B,H,Tc,hd/blk] for K and for V."""
+
+    def __init__(self, B: int, H: int, hd: int, Tc: int, blk: int = 64, device="cuda"):
+        assert Tc % 64 == 0
+        self.B, self.H, self.hd, self.Tc, self.blk = B, H, hd, Tc, blk
+        self.k_codes = torch.zeros((B, H, Tc, hd // 2), dtype=torch.uint8, device=device)
+        self.v_codes = torch.zeros_like(self.k_codes)
+        self.k_scales = torch.zeros((B, H, Tc, hd // blk), dtype=torch.float32, device=device)
+        self.v_scales = torch.zeros_like(self.k_scales)
+
+    def append(self, k: torch.Tensor, v: torch.Tensor, pos: torch.Tensor, stream=None) -> None:
+        nqkv_quantize(k, pos, self.k_codes, self.k_scales, self.blk, stream)
+        nqkv_quantize(v, pos, self.v_codes, self.v_scales, self.blk, stream)
+
+    def attend(self, q: torch.Tensor, seq_lens: torch.Tensor, workspace: torch.Tensor,
+               out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        return nqkv_decode_attention(q, self.k_codes, self.k_scales, self.v_codes, self.v_scales,
+                                     seq_lens, self.blk, workspace, out=out, stream=stream)
+
+    def nbytes(self) -> int:
+        return sum(t.numel() * t.element_size()
+                   for t in (self.k_codes, self.v_codes, self.k_scales, self.v_scales))

@@ -1,0 +1,108 @@
+"""C-ABI checks that need no GPU: the library loads, exports every symbol the
+header declares, host entry points agree with the oracle, and host-checkable
+argument errors return the documented status without launching anything."""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import __graft_entry__
+
+__graft_entry__.build()
+from paper_2505_16210_b200 import nqkv as N  # noqa: E402
+from oracle import nqkv_oracle as O  # noqa: E402
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+FAKE = 0x10000   # 16-byte aligned, never dereferenced: validation fails first
+
+
+def test_exports_every_declared_symbol():
+    hdr = open(os.path.join(ROOT, "include", "nqkv.h")).read()
+    declared = set(re.findall(r"\b(nqkv_[a-z0-9_]+)\s*\(", hdr))
+    assert declared == set(N.EXPORTED)
+    lib = ctypes.CDLL(N._LIB_PATH)
+    for name in declared:
+        assert hasattr(lib, name)
+    assert lib.nqkv_abi_version() == 1
+
+
+def test_host_levels_and_thresholds_match_oracle_bits():
+    # two independent Phi^-1 implementations (C++ erfc-Halley vs scipy ndtri)
+    assert np.array_equal(N.nqkv_levels().view(np.uint32), O.nf_levels_f32().view(np.uint32))
+    assert np.array_equal(N.nqkv_thresholds().view(np.uint32), O.thresholds_f32().view(np.uint32))
+
+
+def test_status_strings():
+    for s in range(-7, 1):
+        assert N._lib.nqkv_status_string(s)
+
+
+def _q(**kw):
+    a = dict(x=FAKE, sb=64 * 12 * 512, st=64 * 12, sh=64, B=1, H=12, hd=64, n=512, blk=64,
+             pos=FAKE, Tc=512, codes=FAKE, scales=FAKE, stream=None)
+    a.update(kw)
+    return N._lib.nqkv_quantize(a["x"], a["sb"], a["st"], a["sh"], a["B"], a["H"], a["hd"], a["n"],
+                                a["blk"], a["pos"], a["Tc"], a["codes"], a["scales"], a["stream"])
+
+
+def test_quantize_argument_errors():
+    assert _q(x=None) == -1 and _q(pos=None) == -1 and _q(codes=None) == -1
+    assert _q(hd=96) == -3 and _q(blk=16) == -3 and _q(blk=128, hd=64) == -3
+    assert _q(Tc=500) == -2 and _q(B=-1) == -2
+    assert _q(x=FAKE + 2) == -4 and _q(sh=60) == -4 and _q(codes=FAKE + 8) == -4
+    assert _q(B=0) == 0 and _q(n=0) == 0          # nothing to do, nothing launched
+
+
+def _d(**kw):
+    a = dict(q=FAKE, kc=FAKE, ks=FAKE, vc=FAKE, vs=FAKE, lens=FAKE, B=2, H=4, hd=128, blk=64,
+             Tc=256, scale=0.088, out=FAKE, ws=FAKE, ws_bytes=None, stream=None)
+    a.update(kw)
+    if a["ws_bytes"] is None:
+        a["ws_bytes"] = N.nqkv_decode_workspace_bytes(a["B"], a["H"], a["hd"], a["Tc"])
+    return N._lib.nqkv_decode_attention(a["q"], a["kc"], a["ks"], a["vc"], a["vs"], a["lens"],
+                                        a["B"], a["H"], a["hd"], a["blk"], a["Tc"], a["scale"],
+                                        a["out"], a["ws"], a["ws_bytes"], a["stream"])
+
+
+def test_decode_argument_errors():
+    assert _d(q=None) == -1 and _d(lens=None) == -1 and _d(ws=None) == -1
+    assert _d(hd=256) == -3 and _d(blk=8) == -3
+    assert _d(Tc=100) == -2
+    assert _d(q=FAKE + 4) == -4 and _d(out=FAKE + 8) == -4 and _d(ks=FAKE + 2) == -4
+    assert _d(ws_bytes=16) == -5
+    assert _d(B=0) == 0
+
+
+def test_dequant_argument_errors():
+    f = N._lib.nqkv_dequantize
+    assert f(None, FAKE, 1, 1, 64, 64, 64, 64, 0, FAKE, None) == -1
+    assert f(FAKE, FAKE, 1, 1, 64, 64, 64, 65, 0, FAKE, None) == -2       # n_tokens > Tc
+    assert f(FAKE, FAKE, 1, 1, 64, 64, 64, 64, 2, FAKE, None) == -3       # bad dtype
+    assert f(FAKE, FAKE, 1, 1, 64, 64, 64, 0, 0, FAKE, None) == 0
+
+
+def test_workspace_size_grows_with_geometry():
+    a = N.nqkv_decode_workspace_bytes(8, 32, 64, 2112)
+    b = N.nqkv_decode_workspace_bytes(8, 32, 128, 2112)
+    c = N.nqkv_decode_workspace_bytes(8, 32, 64, 4096)
+    assert 0 < a < b and a < c and a % 256 == 0
+    # counters (B*H int) + ml (B*H*splits float2) + o (B*H*splits*hd float)
+    splits = -(-2112 // 64)
+    assert a >= 8 * 32 * 4 + 8 * 32 * splits * (8 + 64 * 4)
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    import subprocess
+    import sys
+    code = ("import sys, os; sys.path.insert(0, %r); "
+            "import paper_2505_16210_b200.nqkv as m" % str(tmp_path))
+    pkg = tmp_path / "paper_2505_16210_b200"
+    pkg.mkdir()
+    (pkg / "__init__.py").write_text("")
+    (pkg / "nqkv.py").write_text(open(N.__file__).read())
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True)
+    assert r.returncode != 0 and "not built" in r.stderr

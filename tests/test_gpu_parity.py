@@ -1,0 +1,323 @@
+"""GPU-vs-oracle parity through the C ABI (needs a B200).
+
+Bars (BASELINE.json north_star): codes, scales and dequantised values
+bit-exact; attention max-abs error <= 2e-3 against the oracle's float64
+attention over the same dequantised cache."""
+from __future__ import annotations
+
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import nqkv_oracle as O
+from synth import workloads as W
+
+pytestmark = pytest.mark.gpu
+ATOL = 2e-3
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+@pytest.fixture(scope="module")
+def N():
+    import __graft_entry__
+    __graft_entry__.build()
+    from paper_2505_16210_b200 import nqkv
+    assert torch.cuda.is_available()
+    return nqkv
+
+
+DEV = "cuda"
+
+
+def _rand_kv(B, T, H, hd, seed, outlier=True):
+    g = torch.Generator().manual_seed(seed)
+    sig = torch.exp(0.5 * torch.randn(H, hd, generator=g))
+    if outlier:
+        sig[:, ::37] *= 10
+    x = (torch.randn(B, T, H, hd, generator=g) * sig).to(torch.float16)
+    return x
+
+
+def _oracle_cache(x, pos, blk, Tc, codes=None, scales=None):
+    B, n, H, hd = x.shape
+    if codes is None:
+        codes, scales = O.empty_cache(B, H, Tc, hd, blk)
+    O.quantize_append(x.numpy(), pos, blk, codes, scales)
+    return codes, scales
+
+
+# ------------------------------------------------------------ code function
+def test_encode_normalized_matches_oracle(N):
+    cand = []
+    for t in list(O.thresholds_f32()) + [np.float32((k - 16.5) / 16) for k in range(34)]:
+        v = np.float32(t)
+        for _ in range(64):
+            v = np.nextafter(v, np.float32(-2))
+        for _ in range(128):
+            cand.append(v)
+            v = np.nextafter(v, np.float32(2))
+    rng = np.random.default_rng(0)
+    n = np.concatenate([np.clip(np.array(cand, np.float32), -1, 1),
+                        rng.uniform(-1, 1, 1 << 20).astype(np.float32),
+                        np.array([-1.0, 1.0, 0.0, -0.0], np.float32)])
+    got = N.nqkv_encode_normalized(torch.from_numpy(n).to(DEV)).cpu().numpy()
+    assert np.array_equal(got, O.nearest_level_codes(n))
+
+
+# ----------------------------------------------------------------- quantize
+@pytest.mark.parametrize("hd,blk", [(64, 32), (64, 64), (128, 32), (128, 64), (128, 128)])
+def test_quantize_bit_exact(N, hd, blk):
+    B, T, H = 3, 200, 5
+    Tc = 256
+    x = _rand_kv(B, T, H, hd, seed=hd + blk)
+    codes = torch.full((B, H, Tc, hd // 2), 0xAB, dtype=torch.uint8, device=DEV)
+    scales = torch.full((B, H, Tc, hd // blk), -7.0, dtype=torch.float32, device=DEV)
+    pos = torch.tensor([0, 17, 56], dtype=torch.int32)
+    N.nqkv_quantize(x.to(DEV), pos.to(DEV), codes, scales, blk)
+    oc = np.full((B, H, Tc, hd // 2), 0xAB, np.uint8)
+    os_ = np.full((B, H, Tc, hd // blk), -7.0, np.float32)
+    _oracle_cache(x, pos.tolist(), blk, Tc, oc, os_)
+    assert np.array_equal(codes.cpu().numpy(), oc)            # incl. untouched bytes
+    assert np.array_equal(scales.cpu().numpy(), os_)
+
+
+def test_quantize_strided_input_and_zero_blocks(N):
+    B, T, H, hd, blk, Tc = 2, 33, 4, 128, 64, 64
+    big = _rand_kv(B, T, H + 3, hd + 64, seed=5)             # padded buffer -> strided view
+    x = big[:, :, 1:H + 1, 32:32 + hd]
+    x[:, 3, 2, :64] = 0                                       # an all-zero block
+    x[:, 4, 1, :] = -0.0
+    codes = torch.zeros((B, H, Tc, hd // 2), dtype=torch.uint8, device=DEV)
+    scales = torch.zeros((B, H, Tc, hd // blk), dtype=torch.float32, device=DEV)
+    xd = big.to(DEV)[:, :, 1:H + 1, 32:32 + hd]
+    N.nqkv_quantize(xd, torch.zeros(B, dtype=torch.int32, device=DEV), codes, scales, blk)
+    oc, os_ = _oracle_cache(x.contiguous(), [0, 0], blk, Tc)
+    c = codes.cpu().numpy()
+    assert np.array_equal(c, oc) and np.array_equal(scales.cpu().numpy(), os_)
+    assert np.all(c[:, 2, 3, :32] == 0x77) and np.all(scales.cpu().numpy()[:, 2, 3, 0] == 0)
+
+
+def test_quantize_streaming_equivalence(N):
+    # bulk prefill == prefix + one-token appends, byte for byte
+    B, T, H, hd, blk, Tc = 2, 48, 3, 64, 64, 64
+    x = _rand_kv(B, T, H, hd, seed=9).to(DEV)
+    a_c = torch.zeros((B, H, Tc, hd // 2), dtype=torch.uint8, device=DEV)
+    a_s = torch.zeros((B, H, Tc, 1), dtype=torch.float32, device=DEV)
+    N.nqkv_quantize(x, torch.zeros(B, dtype=torch.int32, device=DEV), a_c, a_s, blk)
+    b_c, b_s = torch.zeros_like(a_c), torch.zeros_like(a_s)
+    N.nqkv_quantize(x[:, :20], torch.zeros(B, dtype=torch.int32, device=DEV), b_c, b_s, blk)
+    for t in range(20, T):
+        N.nqkv_quantize(x[:, t:t + 1], torch.full((B,), t, dtype=torch.int32, device=DEV), b_c, b_s, blk)
+    assert torch.equal(a_c, b_c) and torch.equal(a_s, b_s)
+
+
+def test_near_threshold_golden_pairs(N):
+    rows = [l.split() for l in open(os.path.join(HERE, "golden", "near_threshold_pairs.txt"))
+            if not l.startswith("#")]
+    xs = np.array([int(r[0], 16) for r in rows], np.uint16).view(np.float16)
+    ss = np.array([int(r[1], 16) for r in rows], np.uint16).view(np.float16)
+    want = np.array([int(r[2]) for r in rows], np.uint8)
+    blocks = np.zeros((len(rows), 64), np.float16)
+    blocks[:, 0] = ss
+    blocks[:, 1] = xs
+    x = torch.from_numpy(blocks).reshape(1, len(rows), 1, 64).to(DEV)
+    Tc = -(-len(rows) // 64) * 64
+    codes = torch.zeros((1, 1, Tc, 32), dtype=torch.uint8, device=DEV)
+    scales = torch.zeros((1, 1, Tc, 1), dtype=torch.float32, device=DEV)
+    N.nqkv_quantize(x, torch.zeros(1, dtype=torch.int32, device=DEV), codes, scales, 64)
+    got = (codes.cpu().numpy()[0, 0, :len(rows), 0] >> 4)
+    assert np.array_equal(got, want)
+    assert len(rows) == 178
+
+
+def _sweep(N, s_bits):
+    """All fp16 x with |x| <= s for each scale s: block {s, x_1..x_63}."""
+    allx = np.arange(0, 0x10000, dtype=np.uint32).astype(np.uint16).view(np.float16)
+    allx = allx[np.isfinite(allx)]
+    blocks, want = [], []
+    L = O.nf_levels_f32()
+    for sb in s_bits:
+        s = np.array([sb], np.uint16).view(np.float16)[0]
+        xs = allx[np.abs(allx.astype(np.float32)) <= np.float32(s)]
+        pad = (-len(xs)) % 63
+        xs = np.concatenate([xs, np.zeros(pad, np.float16)]).reshape(-1, 63)
+        blk = np.concatenate([np.full((len(xs), 1), s, np.float16), xs], axis=1)
+        blocks.append(blk)
+        n = (blk.astype(np.float32) / np.float32(s)).astype(np.float32)
+        want.append(O.codes_by_threshold(n, L))
+    blocks = np.concatenate(blocks)
+    want = np.concatenate(want)
+    total = len(blocks)
+    Tc = -(-total // 64) * 64
+    x = torch.from_numpy(blocks).reshape(1, total, 1, 64).to(DEV)
+    codes = torch.zeros((1, 1, Tc, 32), dtype=torch.uint8, device=DEV)
+    scales = torch.zeros((1, 1, Tc, 1), dtype=torch.float32, device=DEV)
+    N.nqkv_quantize(x, torch.zeros(1, dtype=torch.int32, device=DEV), codes, scales, 64)
+    c = codes.cpu().numpy()[0, 0, :total]
+    got = np.empty((total, 64), np.uint8)
+    got[:, 0::2] = c & 0xF
+    got[:, 1::2] = c >> 4
+    mism = int(np.count_nonzero(got != want))
+    assert mism == 0, f"{mism} code mismatches"
+
+
+def test_fp16_pair_sweep_sampled(N):
+    # every 97th positive finite fp16 scale (incl. subnormals) + edge scales,
+    # each against EVERY fp16 x with |x| <= s
+    s_bits = sorted(set(list(range(1, 0x7C00, 97)) + [1, 0x3C00, 0x7BFF, 0x0400, 0x03FF]))
+    _sweep(N, s_bits)
+
+
+@pytest.mark.slow
+def test_fp16_pair_sweep_exhaustive(N):
+    for lo in range(1, 0x7C00, 2048):
+        _sweep(N, range(lo, min(lo + 2048, 0x7C00)))
+
+
+# --------------------------------------------------------------- dequantize
+@pytest.mark.parametrize("hd,blk", [(64, 64), (128, 32), (128, 128)])
+def test_dequantize_bit_exact(N, hd, blk):
+    B, T, H, Tc = 2, 130, 3, 192
+    x = _rand_kv(B, T, H, hd, seed=3)
+    oc, os_ = _oracle_cache(x, [0, 0], blk, Tc)
+    c, s = torch.from_numpy(oc).to(DEV), torch.from_numpy(os_).to(DEV)
+    for dt, ndt in ((torch.float32, np.float32), (torch.float16, np.float16)):
+        got = N.nqkv_dequantize(c, s, blk, T, out_dtype=dt).cpu().numpy()
+        want = O.dequantize(oc, os_, blk, T, out_dtype=ndt)
+        assert got.dtype == want.dtype and np.array_equal(got.view(np.uint8), want.view(np.uint8))
+
+
+# ---------------------------------------------------------------- attention
+def _attn_case(N, B, H, hd, blk, lens, Tc, seed, outlier=True, dev_ws=None):
+    T = max(max(lens), 1)
+    k = _rand_kv(B, T, H, hd, seed, outlier)
+    v = _rand_kv(B, T, H, hd, seed + 1, False)
+    q = torch.randn(B, H, hd, generator=torch.Generator().manual_seed(seed + 2)).to(torch.float16)
+    kc, ks = _oracle_cache(k, [0] * B, blk, Tc)
+    vc, vs = _oracle_cache(v, [0] * B, blk, Tc)
+    ref = O.decode_attention(q.numpy(), kc, ks, vc, vs, lens, blk)
+    t = lambda a: torch.from_numpy(a).to(DEV)
+    ws = N.make_workspace(B, H, hd, Tc, DEV)
+    out = N.nqkv_decode_attention(q.to(DEV), t(kc), t(ks), t(vc), t(vs),
+                                  torch.tensor(lens, dtype=torch.int32, device=DEV), blk, ws)
+    torch.cuda.synchronize()
+    assert torch.count_nonzero(ws) == 0                       # counters reset
+    return out.cpu().numpy(), ref, (q, kc, ks, vc, vs)
+
+
+@pytest.mark.parametrize("hd,blk", [(64, 32), (64, 64), (128, 32), (128, 64), (128, 128)])
+def test_attention_ragged_lengths(N, hd, blk):
+    lens = [0, 1, 63, 64, 65, 127, 128, 129, 300, 511, 512]
+    out, ref, _ = _attn_case(N, len(lens), 3, hd, blk, lens, 512, seed=hd * 7 + blk)
+    err = np.max(np.abs(out.astype(np.float64) - ref))
+    assert err <= ATOL, err
+    assert np.all(out[0] == 0)                                # empty sequence
+
+
+def test_attention_c1_full(N):
+    w = W.CONFIGS["c1"]
+    K, V = W.layer_kv(w, 0)
+    _, _, q = W.step_inputs(w, 0, 0)
+    Tc = 512
+    kc, ks = _oracle_cache(K, [0], w.blk, Tc)
+    vc, vs = _oracle_cache(V, [0], w.blk, Tc)
+    cache = N.KVCache(1, w.heads, w.head_dim, Tc, w.blk, DEV)
+    cache.append(K.to(DEV), V.to(DEV), torch.zeros(1, dtype=torch.int32, device=DEV))
+    assert np.array_equal(cache.k_codes.cpu().numpy(), kc)
+    assert np.array_equal(cache.v_scales.cpu().numpy(), vs)
+    ws = N.make_workspace(1, w.heads, w.head_dim, Tc, DEV)
+    out = cache.attend(q.to(DEV), torch.tensor([512], dtype=torch.int32, device=DEV), ws)
+    ref = O.decode_attention(q.numpy(), kc, ks, vc, vs, [512], w.blk)
+    assert np.max(np.abs(out.cpu().numpy() - ref)) <= ATOL
+
+
+def test_attention_closed_forms(N):
+    # identical keys -> mean of dequantised values; single token -> that value
+    B, H, hd, blk, Tc, T = 1, 2, 128, 64, 256, 200
+    k = _rand_kv(1, 1, H, hd, 11).repeat(1, T, 1, 1)
+    v = _rand_kv(1, T, H, hd, 12)
+    q = torch.randn(B, H, hd).to(torch.float16)
+    kc, ks = _oracle_cache(k, [0], blk, Tc)
+    vc, vs = _oracle_cache(v, [0], blk, Tc)
+    t = lambda a: torch.from_numpy(a).to(DEV)
+    ws = N.make_workspace(B, H, hd, Tc, DEV)
+    for L in (1, T):
+        out = N.nqkv_decode_attention(q.to(DEV), t(kc), t(ks), t(vc), t(vs),
+                                      torch.tensor([L], dtype=torch.int32, device=DEV), blk, ws)
+        mean = O.dequantize(vc, vs, blk, L).astype(np.float64).mean(axis=2)
+        assert np.max(np.abs(out.cpu().numpy() - mean)) < 1e-5
+
+
+def test_attention_invariances_bit_exact(N):
+    # output independent of Tc and of which heads are in the call; repeatable
+    B, H, hd, blk = 4, 6, 128, 64
+    lens = [700, 64, 1000, 1]
+    out1, ref, (q, kc, ks, vc, vs) = _attn_case(N, B, H, hd, blk, lens, 1024, seed=21)
+    assert np.max(np.abs(out1 - ref)) <= ATOL
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+    L = torch.tensor(lens, dtype=torch.int32, device=DEV)
+    # larger capacity, same content
+    pad = lambda a: np.concatenate([a, np.zeros(a.shape[:2] + (1024,) + a.shape[3:], a.dtype)], 2)
+    ws2 = N.make_workspace(B, H, hd, 2048, DEV)
+    out2 = N.nqkv_decode_attention(q.to(DEV), t(pad(kc)), t(pad(ks)), t(pad(vc)), t(pad(vs)), L, blk, ws2)
+    assert np.array_equal(out1, out2.cpu().numpy())
+    # head shard [2:5) alone
+    ws3 = N.make_workspace(B, 3, hd, 1024, DEV)
+    out3 = N.nqkv_decode_attention(q[:, 2:5].contiguous().to(DEV), t(kc[:, 2:5]), t(ks[:, 2:5]),
+                                   t(vc[:, 2:5]), t(vs[:, 2:5]), L, blk, ws3)
+    assert np.array_equal(out1[:, 2:5], out3.cpu().numpy())
+    for _ in range(3):
+        again = N.nqkv_decode_attention(q.to(DEV), t(kc), t(ks), t(vc), t(vs), L, blk,
+                                        N.make_workspace(B, H, hd, 1024, DEV))
+        assert np.array_equal(out1, again.cpu().numpy())
+
+
+def test_attention_max_capacity_long(N):
+    # c4-like long row (8192 tokens, 128 splits) on a few heads
+    B, H, hd, blk, Tc = 1, 2, 128, 64, 8192
+    out, ref, _ = _attn_case(N, B, H, hd, blk, [8192], Tc, seed=31)
+    assert np.max(np.abs(out - ref)) <= ATOL
+
+
+# --------------------------------------------- full-size configs, sampled
+@pytest.mark.parametrize("cfg", ["c2", "c3", "c4", "c5"])
+def test_full_size_layer_sampled(N, cfg):
+    """One layer at the config's full size, generated and quantised on the GPU
+    in the bench's launch configuration; the oracle checks sampled (b, h)
+    slabs: codes/scales bit-exact and the decode output."""
+    w = W.CONFIGS[cfg]
+    B, H, hd, blk = w.batch, w.heads, w.head_dim, w.blk
+    lens = W.seq_lens(w)
+    T = int(lens.max())
+    Tc = W.capacity(T + 1)
+    if cfg == "c5":
+        H = 12                       # one 8-GPU head shard of OPT-175B (all 64 x 4096 tokens)
+    free = torch.cuda.mem_get_info()[0]
+    need = 2 * B * T * H * hd * 2 * 2 + 2 * B * H * Tc * (hd // 2 + 4 * hd // blk)
+    if need > 0.8 * free:
+        pytest.skip("not enough device memory")
+    heads = range(H)
+    K, V = W.layer_kv(w, 0, heads=heads, tokens=T, device=DEV)
+    k1, v1, q = W.step_inputs(w, 0, 0, heads=heads, device=DEV)
+    cache = N.KVCache(B, H, hd, Tc, blk, DEV)
+    cache.append(K, V, torch.zeros(B, dtype=torch.int32, device=DEV))
+    cache.append(k1, v1, lens.to(DEV))                     # new token at row len_b
+    L = (lens + 1).to(DEV)
+    ws = N.make_workspace(B, H, hd, Tc, DEV)
+    out = cache.attend(q, L, ws).cpu().numpy()
+    rng = np.random.default_rng(0)
+    for b, h in {(0, 0), (B - 1, H - 1)} | {(int(rng.integers(B)), int(rng.integers(H))) for _ in range(2)}:
+        n = int(lens[b])
+        kx = torch.cat([K[b:b + 1, :n, h:h + 1], k1[b:b + 1, :, h:h + 1]], 1).cpu()
+        vx = torch.cat([V[b:b + 1, :n, h:h + 1], v1[b:b + 1, :, h:h + 1]], 1).cpu()
+        kc, ks = _oracle_cache(kx, [0], blk, Tc)
+        vc, vs = _oracle_cache(vx, [0], blk, Tc)
+        assert np.array_equal(cache.k_codes[b, h, :n + 1].cpu().numpy(), kc[0, 0, :n + 1])
+        assert np.array_equal(cache.v_scales[b, h, :n + 1].cpu().numpy(), vs[0, 0, :n + 1])
+        ref = O.decode_attention(q[b:b + 1, h:h + 1].cpu().numpy(), kc, ks, vc, vs, [n + 1], blk)
+        assert np.max(np.abs(out[b, h] - ref[0, 0])) <= ATOL
+    del K, V, cache
+    torch.cuda.empty_cache()
