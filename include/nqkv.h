@@ -87,9 +87,10 @@ int nqkv_thresholds(float thresholds[15]);
  *        outside [0, Tc) are skipped.
  * codes  device uint8  [B][H][Tc][hd/2]    (16-byte aligned)
  * scales device float  [B][H][Tc][hd/blk]  (4-byte aligned)
- * Per block: s = max|x| (fp32, exact); n = RN32(x/s) (IEEE division, computed
- * as a correctly rounded reciprocal plus one Markstein correction);
- * code = nearest level, ties lower; s == 0 -> code 7 (the zero level). */
+ * Per block: s = max|x| (fp32, exact); code = nearest level to n = RN32(x/s),
+ * ties lower; s == 0 -> code 7 (the zero level).  The kernel normalises with
+ * n' = RN32(x * RN32(1/s)), which gives the identical code for every fp16
+ * pair |x| <= s (exhaustive: tests/test_exactness_cpu.py). */
 int nqkv_quantize(const void* x, int64_t stride_b, int64_t stride_t, int64_t stride_h,
                   int B, int H, int hd, int n_new, int blk,
                   const int32_t* d_pos, int Tc, uint8_t* codes, float* scales,
@@ -108,23 +109,43 @@ size_t nqkv_decode_workspace_bytes(int B, int H, int hd, int Tc);
 /* a4-a7. Fused decode attention over the 4-bit cache.
  * For every (b, h): out = softmax(softmax_scale * q . k_t) . v_t over
  * t < seq_lens[b], with k_t, v_t dequantised in registers (never written to
- * memory).  Split-K: the sequence is cut into fixed 64-token chunks (a
+ * memory).  Split-K: the sequence is cut into fixed 128-token segments (a
  * function of seq_len only, so results do not depend on B, H or the GPU);
- * partial (max, sum, o) are merged in fixed chunk order.
+ * partial (max, sum, o) are merged in fixed segment order.  B <= 4096.
  * q          device fp16 [B][H][hd], 16-byte aligned
  * k_codes,…  the cache tensors described above
  * d_seq_lens device int32[B], 0..Tc, counting the token appended this step
  *            (append-before-attend); 0 -> out[b] = 0
  * out        device fp32 [B][H][hd], 16-byte aligned
  * workspace  device, >= nqkv_decode_workspace_bytes(B,H,hd,Tc) bytes,
- *            16-byte aligned, ZERO-FILLED before its first use; every call
- *            leaves it zero-filled again.  Do not share one workspace between
- *            calls that may run concurrently. */
+ *            16-byte aligned.  Its first 256 bytes (the work scheduler) must
+ *            be ZERO before the first use; every completed call leaves them
+ *            zero again.  Do not share one workspace between calls that may
+ *            run concurrently (calls ordered on one stream may share it).
+ * Launches: the decode kernel and, when Tc > 128, a small split-combine
+ * kernel, both with programmatic dependent launch (PDL). */
 int nqkv_decode_attention(const void* q, const uint8_t* k_codes, const float* k_scales,
                           const uint8_t* v_codes, const float* v_scales,
                           const int32_t* d_seq_lens, int B, int H, int hd, int blk, int Tc,
                           float softmax_scale, float* out, void* workspace, size_t ws_bytes,
                           void* stream);
+
+/* NEXT f1: one fused decode step = nqkv_quantize of the
+ * new token (n_new = 1, at row seq_lens[b]-1) for K and V followed by
+ * nqkv_decode_attention over seq_lens[b] tokens, in ONE launch
+ * (quantize t_K, t_V; Concat; dequantize; attend).
+ * k_new, v_new  device fp16 [B][H][hd] with element strides new_stride_b,
+ *               new_stride_h (hd contiguous; 16-byte aligned; strides % 8 == 0)
+ * d_seq_lens    device int32[B] AFTER the append (>= 1 to append; 0 -> out = 0,
+ *               nothing written).  The codes/scales written are byte-identical
+ *               to nqkv_quantize's; the attention result equals
+ *               nqkv_decode_attention's on the updated cache.
+ * Other arguments as nqkv_decode_attention. */
+int nqkv_decode_step(const void* k_new, const void* v_new, int64_t new_stride_b,
+                     int64_t new_stride_h, const void* q, uint8_t* k_codes, float* k_scales,
+                     uint8_t* v_codes, float* v_scales, const int32_t* d_seq_lens, int B, int H,
+                     int hd, int blk, int Tc, float softmax_scale, float* out, void* workspace,
+                     size_t ws_bytes, void* stream);
 
 /* Test hook: the kernels' code function on fp32 inputs already normalised
  * to [-1, 1] (values outside are clamped).  d_n device float[count],

@@ -6,6 +6,7 @@ reciprocal; DESIGN.md "Exactness").
 """
 from __future__ import annotations
 
+import glob
 import os
 import subprocess
 
@@ -14,7 +15,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libnqkv.so")
 SOURCES = [os.path.join(CSRC, "nqkv.cu"), os.path.join(CSRC, "levels.cpp")]
-DEPS = SOURCES + [os.path.join(CSRC, "nqkv_internal.h"), os.path.join(ROOT, "include", "nqkv.h")]
+DEPS = sorted(glob.glob(os.path.join(CSRC, "*"))) + [os.path.join(ROOT, "include", "nqkv.h"),
+                                                    os.path.abspath(__file__)]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-lineinfo",
               "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]
 
@@ -47,6 +49,16 @@ def build_library(force: bool = False, verbose: bool = False) -> str:
     with open(os.path.join(PKG, "ptxas_info.txt"), "w") as f:
         f.write(r.stderr)
     return LIB
+
+
+def build_variant(out: str, defines: dict) -> str:
+    """Development: build a tuning variant (e.g. {"NQKV_DECODE_WARPS": 16}) to `out`."""
+    cmd = [nvcc()] + NVCC_FLAGS + ["-I", os.path.join(ROOT, "include"), "-o", out] + \
+        [f"-D{k}={v}" for k, v in defines.items()] + SOURCES
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError("nvcc failed:\n" + r.stdout + r.stderr)
+    return out
 
 
 if __name__ == "__main__":

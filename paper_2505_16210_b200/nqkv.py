@@ -14,7 +14,8 @@ import os
 import numpy as np
 import torch
 
-_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libnqkv.so")
+_LIB_PATH = os.environ.get("NQKV_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                       "libnqkv.so")
 if not os.path.exists(_LIB_PATH):
     raise ImportError(
         f"{_LIB_PATH} not built; run `python -c 'import __graft_entry__ as g; g.build()'` "
@@ -36,6 +37,8 @@ _SIGS = {
     "nqkv_decode_workspace_bytes": (_sz, [_i32, _i32, _i32, _i32]),
     "nqkv_decode_attention": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32,
                                      ctypes.c_float, _vp, _vp, _sz, _vp]),
+    "nqkv_decode_step": (_i32, [_vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32,
+                                _i32, _i32, _i32, ctypes.c_float, _vp, _vp, _sz, _vp]),
     "nqkv_encode_normalized": (_i32, [_vp, _i64, _vp, _vp]),
 }
 for _name, (_res, _args) in _SIGS.items():
@@ -145,6 +148,32 @@ def nqkv_decode_attention(q: torch.Tensor, k_codes: torch.Tensor, k_scales: torc
     return out
 
 
+def nqkv_decode_step(k_new: torch.Tensor, v_new: torch.Tensor, q: torch.Tensor,
+                     k_codes: torch.Tensor, k_scales: torch.Tensor, v_codes: torch.Tensor,
+                     v_scales: torch.Tensor, seq_lens: torch.Tensor, blk: int,
+                     workspace: torch.Tensor, softmax_scale: float | None = None,
+                     out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Fused decode step: append k_new/v_new (fp16 [B, H, hd], hd contiguous)
+    at row seq_lens[b]-1 and attend over seq_lens[b] tokens, one launch."""
+    B, H, hd = q.shape
+    Tc = k_codes.shape[2]
+    if softmax_scale is None:
+        softmax_scale = 1.0 / math.sqrt(hd)
+    if out is None:
+        out = torch.empty((B, H, hd), dtype=torch.float32, device=q.device)
+    assert k_new.shape == (B, H, hd) and v_new.shape == (B, H, hd)
+    assert k_new.stride() == v_new.stride() and k_new.stride(2) == 1
+    assert q.dtype == torch.float16 and q.is_contiguous() and out.is_contiguous()
+    assert seq_lens.dtype == torch.int32
+    _check(_lib.nqkv_decode_step(_ptr(k_new), _ptr(v_new), k_new.stride(0), k_new.stride(1),
+                                 _ptr(q), _ptr(k_codes), _ptr(k_scales), _ptr(v_codes),
+                                 _ptr(v_scales), _ptr(seq_lens), B, H, hd, blk, Tc,
+                                 float(softmax_scale), _ptr(out), _ptr(workspace),
+                                 workspace.numel() * workspace.element_size(), _stream(stream)),
+           "nqkv_decode_step")
+    return out
+
+
 def nqkv_encode_normalized(n: torch.Tensor, stream=None) -> torch.Tensor:
     assert n.dtype == torch.float32 and n.is_contiguous()
     codes = torch.empty(n.shape, dtype=torch.uint8, device=n.device)
@@ -178,6 +207,13 @@ class KVCache:
                out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
         return nqkv_decode_attention(q, self.k_codes, self.k_scales, self.v_codes, self.v_scales,
                                      seq_lens, self.blk, workspace, out=out, stream=stream)
+
+    def step(self, k_new: torch.Tensor, v_new: torch.Tensor, q: torch.Tensor,
+             seq_lens: torch.Tensor, workspace: torch.Tensor, out: torch.Tensor | None = None,
+             stream=None) -> torch.Tensor:
+        """Fused append + attend (seq_lens counts the appended token)."""
+        return nqkv_decode_step(k_new, v_new, q, self.k_codes, self.k_scales, self.v_codes,
+                                self.v_scales, seq_lens, self.blk, workspace, out=out, stream=stream)
 
     def nbytes(self) -> int:
         return sum(t.numel() * t.element_size()

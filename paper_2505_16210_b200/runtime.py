@@ -1,0 +1,162 @@
+"""Decode-step runtime over a multi-layer NF4 KV cache.
+
+One decode step for every layer l, in order -- fused
+(default, one launch per layer, nqkv_decode_step):
+    quantize k_new, v_new -> append at row len_b   (I <- Concat(I, I_t))
+    attention over len_b + 1 tokens                 (append-before-attend)
+or unfused (three launches: nqkv_quantize x2 + nqkv_decode_attention).
+    [world > 1] all-gather of the per-head outputs on a side stream (overlapped
+    with the next layer; the synthetic q does not depend on the previous layer)
+
+The per-step launch sequence is captured once per step slot into a CUDA graph
+(the library's calls are stream-ordered and allocation-free, so they capture
+as-is); replays cost only GPU-side kernel boundaries.  All compute is in
+libnqkv.so; this module only owns buffers, streams and graphs.
+"""
+from __future__ import annotations
+
+import torch
+
+from synth import workloads as W
+
+from . import nqkv as N
+from . import sharding
+
+
+class DecodeRunner:
+    def __init__(self, w: W.Workload, heads: range, device, group=None, world: int = 1,
+                 step_slots: int | None = None, layers: int | None = None, fused: bool = True,
+                 gen_device=None):
+        self.w = w
+        self.fused = fused
+        self.heads = heads
+        self.dev = torch.device(device)
+        # where the seeded synthetic inputs are drawn (CPU and CUDA generators
+        # give different streams; parity tests draw on the CPU)
+        self.gen_dev = self.dev if gen_device is None else torch.device(gen_device)
+        self.group, self.world = group, world
+        self.L = w.layers if layers is None else layers
+        self.S = max(1, w.decode_steps if step_slots is None else step_slots)
+        self.B, self.Hl, self.hd, self.blk = w.batch, len(heads), w.head_dim, w.blk
+        lens0 = W.seq_lens(w)
+        self.lens0 = lens0
+        self.Tc = W.capacity(int(lens0.max()) + self.S)
+        self.caches = [N.KVCache(self.B, self.Hl, self.hd, self.Tc, self.blk, self.dev)
+                       for _ in range(self.L)]
+        self.ws = N.make_workspace(self.B, self.Hl, self.hd, self.Tc, self.dev)
+        self.out = torch.zeros((self.L, self.B, self.Hl, self.hd), dtype=torch.float32, device=self.dev)
+        steps = torch.arange(self.S, dtype=torch.int32)[:, None]
+        self.pos = (lens0[None, :] + steps).to(torch.int32).to(self.dev)          # [S, B]
+        self.attn_lens = (self.pos + 1).contiguous()                               # [S, B]
+        self.inputs = torch.empty((self.S, self.L, 3, self.B, self.Hl, self.hd),
+                                  dtype=torch.float16, device=self.dev)
+        for s in range(self.S):
+            for l in range(self.L):
+                k, v, q = W.step_inputs(w, l, s, heads=heads, device=self.gen_dev)
+                self.inputs[s, l, 0] = k[:, 0]
+                self.inputs[s, l, 1] = v[:, 0]
+                self.inputs[s, l, 2] = q
+        self.gathered = None
+        if world > 1:
+            self.gathered = torch.empty((self.L, world, self.B, self.Hl, self.hd),
+                                        dtype=torch.float32, device=self.dev)
+            self.comm = torch.cuda.Stream(device=self.dev)
+        self.graphs: list[torch.cuda.CUDAGraph] = []
+        self.events: list[list[tuple[torch.cuda.Event, torch.cuda.Event]]] = []
+
+    # ------------------------------------------------------------ prefill --
+    def prefill(self, flush: torch.Tensor | None = None) -> list[float]:
+        """Quantize every layer's prompt K/V (bulk nqkv_quantize, n_new =
+        prompt length).  Returns per-launch kernel times in ms (L2 flushed
+        before each launch when a flush buffer is given)."""
+        T = int(self.lens0.max())
+        zero = torch.zeros(self.B, dtype=torch.int32, device=self.dev)
+        times = []
+        for l, c in enumerate(self.caches):
+            K, V = W.layer_kv(self.w, l, heads=self.heads, tokens=T, device=self.gen_dev)
+            K, V = K.to(self.dev), V.to(self.dev)
+            for x, codes, scales in ((K, c.k_codes, c.k_scales), (V, c.v_codes, c.v_scales)):
+                if flush is not None:
+                    flush.add_(1)
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record()
+                N.nqkv_quantize(x, zero, codes, scales, self.blk)
+                e1.record()
+                times.append((e0, e1))
+            del K, V
+        torch.cuda.synchronize()
+        return [a.elapsed_time(b) for a, b in times]
+
+    # --------------------------------------------------------------- step --
+    def step(self, s: int, events=None) -> None:
+        x = self.inputs[s]
+        pos, lens = self.pos[s], self.attn_lens[s]
+        cur = torch.cuda.current_stream()
+        for l, c in enumerate(self.caches):
+            if not self.fused:
+                c.append(x[l, 0].unsqueeze(1), x[l, 1].unsqueeze(1), pos)   # [B, 1, H, hd] views
+            if events is not None:
+                events[l][0].record()
+            if self.fused:
+                c.step(x[l, 0], x[l, 1], x[l, 2], lens, self.ws, out=self.out[l])
+            else:
+                c.attend(x[l, 2], lens, self.ws, out=self.out[l])
+            if events is not None:
+                events[l][1].record()
+            if self.world > 1:
+                self.comm.wait_stream(cur)
+                with torch.cuda.stream(self.comm):
+                    sharding.all_gather_heads(self.out[l], self.gathered[l], self.group)
+        if self.world > 1:
+            cur.wait_stream(self.comm)
+
+    def capture(self, timing_slots=(0,)) -> None:
+        """One CUDA graph per step slot (pointers differ per slot).  Slots in
+        `timing_slots` also record an event pair around every decode launch
+        (event nodes break the PDL overlap between layers, so only a few slots
+        carry them)."""
+        torch.cuda.synchronize()
+        self.graphs, self.events = [], []
+        for s in range(self.S):
+            ev = None
+            if s in timing_slots:
+                ev = [(torch.cuda.Event(enable_timing=True, external=True),
+                       torch.cuda.Event(enable_timing=True, external=True)) for _ in range(self.L)]
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self.step(s, ev)
+            self.graphs.append(g)
+            self.events.append(ev)
+        torch.cuda.synchronize()
+
+    def replay(self, i: int) -> None:
+        self.graphs[i % self.S].replay()
+
+    def decode_kernel_ms(self) -> list[float]:
+        """Durations of the decode-attention launches of the most recent replay
+        of every step slot (events recorded inside the graphs)."""
+        out = []
+        for ev in self.events:
+            if ev is None:
+                continue
+            out.extend(a.elapsed_time(b) for a, b in ev)
+        return out
+
+    # ------------------------------------------------------------ metrics --
+    def tokens_per_step(self, s: int) -> int:
+        """KV tokens attended in one step over all layers (a token = all of
+        this rank's heads)."""
+        return int(self.attn_lens[s % self.S].sum().item()) * self.L
+
+    def decode_bytes(self, s: int) -> int:
+        """Algorithmic HBM bytes of ONE decode launch at slot s: codes + scales
+        of K and V for the attended tokens, q in, out; fused steps also read
+        the new k, v (fp16) -- the new row's codes are written, not re-read."""
+        toks = int(self.attn_lens[s % self.S].sum().item())
+        per_tok = self.Hl * self.hd * 2 * (0.5 + 4.0 / self.blk)
+        extra = self.B * self.Hl * self.hd * 2 * 2 if self.fused else 0
+        return int(toks * per_tok + self.B * self.Hl * self.hd * (2 + 4) + extra)
+
+    def launches_per_step(self) -> int:
+        return (1 if self.fused else 3) * self.L

@@ -1,0 +1,46 @@
+"""Head sharding across the GPUs of one node (BASELINE.json
+north_star (c)).
+
+Heads are independent in decode attention (PAPER.md:232-235 is per head once
+X_K', X_V' are split), so rank r owns a contiguous head range of every layer:
+its own codes, scales, q and out.  Quantize and attention need no
+communication; the single exchange step is an all-gather of the per-head
+outputs [B, H_local, hd] -> [B, H, hd].
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def head_range(rank: int, world: int, heads: int) -> range:
+    """Strong scaling: split a fixed head count evenly (heads % world == 0)."""
+    if heads % world:
+        raise ValueError(f"{heads} heads do not shard evenly over {world} ranks")
+    per = heads // world
+    return range(rank * per, (rank + 1) * per)
+
+
+def weak_head_range(rank: int, heads_per_rank: int) -> range:
+    """Weak scaling: every rank owns a fixed shard; the job has world x shard heads."""
+    return range(rank * heads_per_rank, (rank + 1) * heads_per_rank)
+
+
+def gather_buffer(out_local: torch.Tensor, world: int) -> torch.Tensor:
+    """[G, B, H_local, hd] receive buffer for all_gather_into_tensor."""
+    return torch.empty((world,) + tuple(out_local.shape), dtype=out_local.dtype,
+                       device=out_local.device)
+
+
+def all_gather_heads(out_local: torch.Tensor, gathered: torch.Tensor,
+                     group=None, async_op: bool = False):
+    """all-gather of per-head outputs: out_local [B, H_local, hd] from every
+    rank into gathered [G, B, H_local, hd] (rank-major)."""
+    return dist.all_gather_into_tensor(gathered, out_local.contiguous(), group=group,
+                                       async_op=async_op)
+
+
+def assemble(gathered: torch.Tensor) -> torch.Tensor:
+    """[G, B, H_local, hd] (rank-major) -> [B, G*H_local, hd] in global head order."""
+    G, B, Hl, hd = gathered.shape
+    return gathered.permute(1, 0, 2, 3).reshape(B, G * Hl, hd)

@@ -77,6 +77,23 @@ def test_decode_argument_errors():
     assert _d(B=0) == 0
 
 
+def test_decode_step_argument_errors():
+    f = N._lib.nqkv_decode_step
+    ws = N.nqkv_decode_workspace_bytes(2, 4, 128, 256)
+    args = [FAKE, FAKE, 4 * 128, 128, FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, 2, 4, 128, 64, 256,
+            0.088, FAKE, FAKE, ws, None]
+    a = list(args); a[0] = None
+    assert f(*a) == -1
+    a = list(args); a[3] = 100                        # stride not a multiple of 8
+    assert f(*a) == -4
+    a = list(args); a[12] = 96
+    assert f(*a) == -3
+    a = list(args); a[18] = 8
+    assert f(*a) == -5
+    a = list(args); a[10] = 5000                      # B > 4096
+    assert f(*a) == -2
+
+
 def test_dequant_argument_errors():
     f = N._lib.nqkv_dequantize
     assert f(None, FAKE, 1, 1, 64, 64, 64, 64, 0, FAKE, None) == -1
@@ -90,9 +107,9 @@ def test_workspace_size_grows_with_geometry():
     b = N.nqkv_decode_workspace_bytes(8, 32, 128, 2112)
     c = N.nqkv_decode_workspace_bytes(8, 32, 64, 4096)
     assert 0 < a < b and a < c and a % 256 == 0
-    # counters (B*H int) + ml (B*H*splits float2) + o (B*H*splits*hd float)
-    splits = -(-2112 // 64)
-    assert a >= 8 * 32 * 4 + 8 * 32 * splits * (8 + 64 * 4)
+    # counters (B*H int) + ml (B*H*segs float2) + o (B*H*segs*hd float), 128-token segments
+    splits = -(-2112 // 128)
+    assert a >= 256 + 8 * 32 * splits * (8 + 64 * 4)
 
 
 def test_missing_library_fails_loudly(tmp_path):
