@@ -58,7 +58,7 @@ class DecodeRunner:
                 self.inputs[s, l, 2] = q
         self.gathered = None
         if world > 1:
-            self.gathered = torch.empty((self.L, world, self.B, self.Hl, self.hd),
+            self.gathered = torch.empty((self.L, world * self.B, self.Hl, self.hd),
                                         dtype=torch.float32, device=self.dev)
             self.comm = torch.cuda.Stream(device=self.dev)
         self.graphs: list[torch.cuda.CUDAGraph] = []

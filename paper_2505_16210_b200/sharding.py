@@ -27,20 +27,23 @@ def weak_head_range(rank: int, heads_per_rank: int) -> range:
 
 
 def gather_buffer(out_local: torch.Tensor, world: int) -> torch.Tensor:
-    """[G, B, H_local, hd] receive buffer for all_gather_into_tensor."""
-    return torch.empty((world,) + tuple(out_local.shape), dtype=out_local.dtype,
+    """Receive buffer for all_gather_into_tensor: the rank-major concatenation
+    [G*B, H_local, hd] (the layout both NCCL and gloo accept)."""
+    B = out_local.shape[0]
+    return torch.empty((world * B,) + tuple(out_local.shape[1:]), dtype=out_local.dtype,
                        device=out_local.device)
 
 
 def all_gather_heads(out_local: torch.Tensor, gathered: torch.Tensor,
                      group=None, async_op: bool = False):
     """all-gather of per-head outputs: out_local [B, H_local, hd] from every
-    rank into gathered [G, B, H_local, hd] (rank-major)."""
+    rank into gathered [G*B, H_local, hd] (rank-major)."""
     return dist.all_gather_into_tensor(gathered, out_local.contiguous(), group=group,
                                        async_op=async_op)
 
 
-def assemble(gathered: torch.Tensor) -> torch.Tensor:
-    """[G, B, H_local, hd] (rank-major) -> [B, G*H_local, hd] in global head order."""
-    G, B, Hl, hd = gathered.shape
-    return gathered.permute(1, 0, 2, 3).reshape(B, G * Hl, hd)
+def assemble(gathered: torch.Tensor, world: int) -> torch.Tensor:
+    """[G*B, H_local, hd] (rank-major) -> [B, G*H_local, hd] in global head order."""
+    GB, Hl, hd = gathered.shape
+    B = GB // world
+    return gathered.view(world, B, Hl, hd).permute(1, 0, 2, 3).reshape(B, world * Hl, hd)
