@@ -100,6 +100,19 @@ __device__ __forceinline__ uint32_t nf4_code(float n, uint32_t tab_base) {
   return __float_as_uint(e.y) + (n > e.x ? 1u : 0u);
 }
 
+// Same code function with the table base pre-folded: tabc = tab_base - 0x5A000000,
+// so the entry address is ONE integer multiply-add of the fma result's bits;
+// the comparison is a set.gt mask subtracted from lo (no predicate/select).
+__device__ __forceinline__ uint32_t nf4_code_c(float n, uint32_t tabc) {
+  const float y = __fmaf_rn(n, 16.0f, 12582928.0f);
+  uint32_t addr;
+  asm("mad.lo.u32 %0, %1, 8, %2;" : "=r"(addr) : "r"(__float_as_uint(y)), "r"(tabc));
+  const float2 e = unpack2(lds64(addr));
+  uint32_t gt;
+  asm("set.gt.u32.f32 %0, %1, %2;" : "=r"(gt) : "f"(n), "f"(e.x));
+  return __float_as_uint(e.y) - gt;       // gt = 0xFFFFFFFF (true) or 0
+}
+
 // Normalisation n' = RN32(x * RN32(1/s)).  For every fp16 pair with |x| <= s
 // this yields the same code as n = RN32(x / s) (exhaustive proof:
 // tests/test_exactness_cpu.py; GPU sweep: tests/test_gpu_parity.py).
@@ -117,6 +130,21 @@ __device__ __forceinline__ uint32_t encode8(const uint4 raw, float r, uint32_t t
     word |= nf4_code(__fmul_rn(xf.y, r), tab) << (8 * k + 4);
   }
   return word;
+}
+// encode8 with the pre-folded table constant (see nf4_code_c); nibble pairs are
+// combined with one multiply-add each.
+__device__ __forceinline__ uint32_t encode8c(const uint4 raw, float r, uint32_t tabc) {
+  __half2 hv[4];
+  memcpy(hv, &raw, 16);
+  uint32_t b[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float2 xf = __half22float2(hv[k]);
+    const uint32_t lo = nf4_code_c(__fmul_rn(xf.x, r), tabc);
+    const uint32_t hi = nf4_code_c(__fmul_rn(xf.y, r), tabc);
+    b[k] = hi * 16u + lo;
+  }
+  return __byte_perm(__byte_perm(b[0], b[1], 0x0040), __byte_perm(b[2], b[3], 0x0040), 0x5410);
 }
 __device__ __forceinline__ float absmax8(const uint4 raw) {
   __half2 hv[4];

@@ -17,6 +17,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <utility>
@@ -123,9 +124,9 @@ int launch_decode(const DecodeParams& p, cudaStream_t st) {
     CombineParams c;
     c.seq_lens = p.seq_lens; c.ws_o = p.ws_o; c.ws_ml = p.ws_ml; c.out = p.out;
     c.B = p.B; c.H = p.H; c.Tc = p.Tc; c.max_segs = p.max_segs;
-    const long long warps = static_cast<long long>(p.B) * p.H;
-    e = launch_pdl(combine_kernel<HD>, dim3(static_cast<unsigned>((warps + 7) / 8)), dim3(256), 0,
-                   st, c);
+    const long long threads = static_cast<long long>(p.B) * p.H * HD;
+    e = launch_pdl(combine_kernel<HD>, dim3(static_cast<unsigned>((threads + 255) / 256)), dim3(256),
+                   0, st, c);
     if (e != cudaSuccess) return cuda_fail(e);
   }
   return NQKV_OK;
@@ -157,7 +158,7 @@ int decode_common(const void* q, const uint8_t* k_codes, const float* k_scales,
   if (int s = check_geometry(hd, blk)) return s;
   if (B < 0 || H < 0 || Tc <= 0 || Tc % 64 || B > kMaxBatch) return NQKV_ERR_SHAPE;
   if (!aligned16(q) || !aligned16(k_codes) || !aligned16(v_codes) || !aligned16(out) ||
-      (reinterpret_cast<uintptr_t>(k_scales) & 3u) || (reinterpret_cast<uintptr_t>(v_scales) & 3u))
+      !aligned16(k_scales) || !aligned16(v_scales))   // TMA bulk copies need 16-byte alignment
     return NQKV_ERR_ALIGN;
   if (k_new && (!aligned16(k_new) || !aligned16(v_new) || (new_sb % 8) || (new_sh % 8)))
     return NQKV_ERR_ALIGN;
@@ -175,7 +176,6 @@ int decode_common(const void* q, const uint8_t* k_codes, const float* k_scales,
   p.v_new = static_cast<const __half*>(v_new);
   p.new_sb = new_sb; p.new_sh = new_sh;
   unsigned char* ws = static_cast<unsigned char*>(workspace);
-  p.sched = reinterpret_cast<int*>(ws + w.sched);
   p.ws_ml = reinterpret_cast<float2*>(ws + w.ml);
   p.ws_o = reinterpret_cast<float*>(ws + w.o);
   p.max_segs = (Tc + kSeg - 1) / kSeg;
@@ -184,6 +184,10 @@ int decode_common(const void* q, const uint8_t* k_codes, const float* k_scales,
   p.scale_log2 = softmax_scale * 1.4426950408889634f;
   p.lv = make_levels();
   p.tab = make_bucket_tab();
+  p.trace = nullptr;
+#ifdef NQKV_TRACE
+  if (const char* t = std::getenv("NQKV_TRACE_PTR")) p.trace = reinterpret_cast<unsigned long long*>(std::strtoull(t, nullptr, 0));
+#endif
   return hd == 64 ? launch_decode<64>(p, st) : launch_decode<128>(p, st);
 }
 
@@ -236,22 +240,18 @@ int nqkv_quantize(const void* x, int64_t stride_b, int64_t stride_t, int64_t str
       (stride_b % 8) || (stride_t % 8) || (stride_h % 8))
     return NQKV_ERR_ALIGN;
   if (tables_status() != 0) return NQKV_ERR_INTERNAL;
-  const long long rows = static_cast<long long>(B) * n_new * H;
-  if (rows == 0) return NQKV_OK;
+  const long long rows = static_cast<long long>(B) * n_new;   // token rows (b, t)
+  if (rows == 0 || H == 0) return NQKV_OK;
   if (rows >= (1ll << 31)) return NQKV_ERR_SHAPE;
   QuantParams p;
   p.x = static_cast<const __half*>(x);
   p.sb = stride_b; p.st = stride_t; p.sh = stride_h;
   p.pos = d_pos; p.codes = codes; p.scales = scales;
-  p.rows = static_cast<uint32_t>(rows);
-  p.divH = make_fastdiv(static_cast<uint32_t>(H));
-  p.divN = make_fastdiv(static_cast<uint32_t>(n_new));
-  p.H = H; p.n_new = n_new; p.Tc = Tc;
+  p.B = B; p.n_new = n_new; p.H = H; p.Tc = Tc;
   p.blk_shift = blk_shift_of(blk);
   p.tab = make_bucket_tab();
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const long long threads_needed = rows * (hd / 8);
-  const dim3 grid(static_cast<unsigned>(grid_for(threads_needed, 256, 8)));
+  const dim3 grid(static_cast<unsigned>(grid_for(rows * 32, 256, 8)));
   cudaError_t e;
   if (hd == 64) {
     e = blk == 32 ? launch_pdl(quantize_kernel<64, 4>, grid, dim3(256), 0, st, p)

@@ -12,48 +12,67 @@ struct QuantParams {
   const int32_t* pos;
   uint8_t* codes;
   float* scales;
-  uint32_t rows;                 // B * n_new * H
-  FastDiv divH, divN;
-  int H, n_new, Tc, blk_shift;
+  int B, n_new, H, Tc, blk_shift;
   BucketTab tab;
 };
 
-// One thread = one 8-element chunk (16 B of fp16); blk/8 consecutive lanes
-// form a block and reduce the absmax with xor-shuffles.  A warp covers
-// 32/(HD/8) consecutive (b, t, h) rows per iteration.
+// Quantize one 16-byte chunk (8 fp16 values) against the block absmax shared
+// by the GS lanes of its block; returns the 8 packed nibbles.
+template <int GS>
+__device__ __forceinline__ uint32_t quantize_chunk(const uint4 raw, uint32_t tabc, float& s) {
+  s = absmax8(raw);
+#pragma unroll
+  for (int o = 1; o < GS; o <<= 1) s = fmaxf(s, __shfl_xor_sync(0xffffffffu, s, o));
+  return encode8c(raw, block_rcp(s), tabc);
+}
+
+// A warp owns one token row (b, t) at a time: the row's (b, t) decode, the
+// append position and base pointers are computed once per row; the lanes then
+// sweep the row's H * hd/8 chunks, two per lane per step (both loads issued
+// before either is used).  blk/8 consecutive lanes form a block and reduce its
+// absmax with xor-shuffles (a 32-chunk step always holds whole heads).
 template <int HD, int GS>   // GS = lanes per block = blk / 8
 __global__ void __launch_bounds__(256) quantize_kernel(const QuantParams p) {
-  constexpr int CPR = HD / 8, RPW = 32 / CPR;
+  constexpr int CPR = HD / 8;                  // chunks per (token, head)
+  constexpr int LOG_CPR = CPR == 8 ? 3 : 4;
   __shared__ float2 s_tab[kNumBuckets];
   for (int i = threadIdx.x; i < kNumBuckets; i += blockDim.x) s_tab[i] = p.tab.e[i];
   pdl_trigger();
   __syncthreads();
   pdl_wait();
-  const uint32_t tab = static_cast<uint32_t>(__cvta_generic_to_shared(s_tab));
+  const uint32_t tabc = static_cast<uint32_t>(__cvta_generic_to_shared(s_tab)) - 0x5A000000u;
   const int lane = threadIdx.x & 31;
-  const int cr = lane % CPR;
-  const uint32_t gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t nwarp = (gridDim.x * blockDim.x) >> 5;
-  for (uint32_t r0 = gwarp * RPW; r0 < p.rows; r0 += nwarp * RPW) {
-    const uint32_t r = r0 + lane / CPR;
-    const bool valid = r < p.rows;
-    const uint32_t rr = valid ? r : 0;
-    const uint32_t bt = fdiv(rr, p.divH);
-    const int h = static_cast<int>(rr - bt * p.H);
-    const uint32_t b = fdiv(bt, p.divN);
-    const int t = static_cast<int>(bt - b * p.n_new);
-    uint4 raw = make_uint4(0, 0, 0, 0);
-    if (valid) raw = ldg_stream_128(p.x + b * p.sb + t * p.st + h * p.sh + cr * 8);
-    float s = absmax8(raw);
-#pragma unroll
-    for (int o = 1; o < GS; o <<= 1) s = fmaxf(s, __shfl_xor_sync(0xffffffffu, s, o));
-    const uint32_t word = encode8(raw, block_rcp(s), tab);
-    if (valid) {
-      const int row = p.pos[b] + t;
-      if (row >= 0 && row < p.Tc) {
-        const long long rowid = (static_cast<long long>(b) * p.H + h) * p.Tc + row;
-        reinterpret_cast<uint32_t*>(p.codes + rowid * (HD / 2))[cr] = word;
-        if ((cr & (GS - 1)) == 0) p.scales[rowid * (HD >> p.blk_shift) + cr / GS] = s;
+  const int gw = static_cast<int>((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int nw = static_cast<int>((gridDim.x * blockDim.x) >> 5);
+  const int rows = p.B * p.n_new;
+  const int chunks = p.H * CPR;
+  const int nblk = HD >> p.blk_shift;
+  for (int row = gw; row < rows; row += nw) {
+    const int b = row / p.n_new, t = row - b * p.n_new;
+    const int pos = __ldg(p.pos + b) + t;
+    const bool in_range = pos >= 0 && pos < p.Tc;
+    const __half* xrow = p.x + b * p.sb + t * p.st;
+    const long long orow = static_cast<long long>(b) * p.H * p.Tc + pos;   // + h*Tc
+    for (int c0 = 0; c0 < chunks; c0 += 64) {
+      const int ca = c0 + lane, cb = c0 + 32 + lane;
+      const bool va = ca < chunks, vb = cb < chunks;
+      uint4 ra = make_uint4(0, 0, 0, 0), rb = ra;
+      if (va) ra = ldg_stream_128(xrow + (ca >> LOG_CPR) * p.sh + (ca & (CPR - 1)) * 8);
+      if (vb) rb = ldg_stream_128(xrow + (cb >> LOG_CPR) * p.sh + (cb & (CPR - 1)) * 8);
+      float sa, sb;
+      const uint32_t wa = quantize_chunk<GS>(ra, tabc, sa);
+      if (c0 + 32 < chunks) {                // warp-uniform
+        const uint32_t wb = quantize_chunk<GS>(rb, tabc, sb);
+        if (vb && in_range) {
+          const long long r = orow + static_cast<long long>(cb >> LOG_CPR) * p.Tc;
+          reinterpret_cast<uint32_t*>(p.codes + r * (HD / 2))[cb & (CPR - 1)] = wb;
+          if ((cb & (GS - 1)) == 0) p.scales[r * nblk + ((cb & (CPR - 1)) / GS)] = sb;
+        }
+      }
+      if (va && in_range) {
+        const long long r = orow + static_cast<long long>(ca >> LOG_CPR) * p.Tc;
+        reinterpret_cast<uint32_t*>(p.codes + r * (HD / 2))[ca & (CPR - 1)] = wa;
+        if ((ca & (GS - 1)) == 0) p.scales[r * nblk + ((ca & (CPR - 1)) / GS)] = sa;
       }
     }
   }
