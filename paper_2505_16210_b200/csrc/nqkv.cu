@@ -253,13 +253,14 @@ int nqkv_quantize(const void* x, int64_t stride_b, int64_t stride_t, int64_t str
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const dim3 grid(static_cast<unsigned>(grid_for(rows * 32, 256, 8)));
   cudaError_t e;
+  const size_t sm = kQuantSmem;
   if (hd == 64) {
-    e = blk == 32 ? launch_pdl(quantize_kernel<64, 4>, grid, dim3(256), 0, st, p)
-                  : launch_pdl(quantize_kernel<64, 8>, grid, dim3(256), 0, st, p);
+    e = blk == 32 ? launch_pdl(quantize_kernel<64, 2>, grid, dim3(256), sm, st, p)
+                  : launch_pdl(quantize_kernel<64, 4>, grid, dim3(256), sm, st, p);
   } else {
-    e = blk == 32   ? launch_pdl(quantize_kernel<128, 4>, grid, dim3(256), 0, st, p)
-        : blk == 64 ? launch_pdl(quantize_kernel<128, 8>, grid, dim3(256), 0, st, p)
-                    : launch_pdl(quantize_kernel<128, 16>, grid, dim3(256), 0, st, p);
+    e = blk == 32   ? launch_pdl(quantize_kernel<128, 2>, grid, dim3(256), sm, st, p)
+        : blk == 64 ? launch_pdl(quantize_kernel<128, 4>, grid, dim3(256), sm, st, p)
+                    : launch_pdl(quantize_kernel<128, 8>, grid, dim3(256), sm, st, p);
   }
   return e == cudaSuccess ? NQKV_OK : cuda_fail(e);
 }

@@ -16,36 +16,70 @@ struct QuantParams {
   BucketTab tab;
 };
 
-// Quantize one 16-byte chunk (8 fp16 values) against the block absmax shared
-// by the GS lanes of its block; returns the 8 packed nibbles.
-template <int GS>
-__device__ __forceinline__ uint32_t quantize_chunk(const uint4 raw, uint32_t tabc, float& s) {
-  s = absmax8(raw);
+// Bucket table replicated per lane: entry e for lane l at shared address
+// 0x400 + e*256 + l*8 (conflict-free lookups).  The dynamic shared window of
+// this kernel starts at 0x400 (1 KB driver reserve, no static smem -- checked on
+// device), so idx = RN(16 n + 16) taken from the low byte of the fma result
+// with +4 folded into the magic constant gives the full address with ONE PRMT:
+// byte 0 = lane*8, byte 1 = idx + 4, bytes 2-3 = 0.
+constexpr int kRepEntryBytes = 256;
+constexpr size_t kQuantSmem = static_cast<size_t>(kNumBuckets) * kRepEntryBytes;
+
+__device__ __forceinline__ uint32_t nf4_code_rep(float n, uint32_t lane8) {
+  const float y = __fmaf_rn(n, 16.0f, 12582932.0f);             // 1.5*2^23 + 16 + 4
+  const float2 e = unpack2(lds64(__byte_perm(__float_as_uint(y), lane8, 0x5504)));
+  // lo + (n > thr): the sign bit of thr - n (thr = +inf -> never; equal -> +0)
+  return __float_as_uint(e.y) + (__float_as_uint(__fsub_rn(e.x, n)) >> 31);
+}
+
+__device__ __forceinline__ uint32_t encode8_rep(const uint4 raw, float r, uint32_t lane8) {
+  __half2 hv[4];
+  memcpy(hv, &raw, 16);
+  uint32_t b[4];
 #pragma unroll
-  for (int o = 1; o < GS; o <<= 1) s = fmaxf(s, __shfl_xor_sync(0xffffffffu, s, o));
-  return encode8c(raw, block_rcp(s), tabc);
+  for (int k = 0; k < 4; ++k) {
+    const float2 xf = __half22float2(hv[k]);
+    const uint32_t lo = nf4_code_rep(__fmul_rn(xf.x, r), lane8);
+    const uint32_t hi = nf4_code_rep(__fmul_rn(xf.y, r), lane8);
+    b[k] = hi * 16u + lo;
+  }
+  return __byte_perm(__byte_perm(b[0], b[1], 0x0040), __byte_perm(b[2], b[3], 0x0040), 0x5410);
+}
+
+constexpr int kQPairs = 2;   // 32-byte pair-chunks per lane per step (all loads issued first)
+
+__device__ __forceinline__ float absmax16(const uint4 a, const uint4 b) {
+  __half2 ha[4], hb[4];
+  memcpy(ha, &a, 16);
+  memcpy(hb, &b, 16);
+  const __half2 m = __hmax2(__hmax2(__hmax2(__habs2(ha[0]), __habs2(ha[1])), __hmax2(__habs2(ha[2]), __habs2(ha[3]))),
+                            __hmax2(__hmax2(__habs2(hb[0]), __habs2(hb[1])), __hmax2(__habs2(hb[2]), __habs2(hb[3]))));
+  return fmaxf(__low2float(m), __high2float(m));
 }
 
 // A warp owns one token row (b, t) at a time: the row's (b, t) decode, the
-// append position and base pointers are computed once per row; the lanes then
-// sweep the row's H * hd/8 chunks, two per lane per step (both loads issued
-// before either is used).  blk/8 consecutive lanes form a block and reduce its
-// absmax with xor-shuffles (a 32-chunk step always holds whole heads).
-template <int HD, int GS>   // GS = lanes per block = blk / 8
+// append position and base pointers are computed once per row; each lane then
+// quantizes 16 consecutive elements (two 16-byte chunks of one block) at a
+// time, kQPairs such pairs per step with every load issued before any use.
+// blk/16 consecutive lanes form a block and reduce its absmax with
+// xor-shuffles (a 32-lane step always holds whole heads).
+template <int HD, int GS>   // GS = lanes per block = blk / 16
 __global__ void __launch_bounds__(256) quantize_kernel(const QuantParams p) {
-  constexpr int CPR = HD / 8;                  // chunks per (token, head)
-  constexpr int LOG_CPR = CPR == 8 ? 3 : 4;
-  __shared__ float2 s_tab[kNumBuckets];
-  for (int i = threadIdx.x; i < kNumBuckets; i += blockDim.x) s_tab[i] = p.tab.e[i];
+  constexpr int PPR = HD / 16;                 // pairs per (token, head)
+  constexpr int LOG_PPR = PPR == 4 ? 2 : 3;
+  extern __shared__ __align__(16) unsigned char qsmem[];
+  for (int i = threadIdx.x; i < kNumBuckets * 32; i += blockDim.x)
+    reinterpret_cast<float2*>(qsmem)[i] = p.tab.e[i >> 5];
+  if (static_cast<uint32_t>(__cvta_generic_to_shared(qsmem)) != 0x400u) __trap();
   pdl_trigger();
   __syncthreads();
   pdl_wait();
-  const uint32_t tabc = static_cast<uint32_t>(__cvta_generic_to_shared(s_tab)) - 0x5A000000u;
   const int lane = threadIdx.x & 31;
+  const uint32_t lane8 = lane * 8u;
   const int gw = static_cast<int>((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int nw = static_cast<int>((gridDim.x * blockDim.x) >> 5);
   const int rows = p.B * p.n_new;
-  const int chunks = p.H * CPR;
+  const int pairs = p.H * PPR;
   const int nblk = HD >> p.blk_shift;
   for (int row = gw; row < rows; row += nw) {
     const int b = row / p.n_new, t = row - b * p.n_new;
@@ -53,26 +87,33 @@ __global__ void __launch_bounds__(256) quantize_kernel(const QuantParams p) {
     const bool in_range = pos >= 0 && pos < p.Tc;
     const __half* xrow = p.x + b * p.sb + t * p.st;
     const long long orow = static_cast<long long>(b) * p.H * p.Tc + pos;   // + h*Tc
-    for (int c0 = 0; c0 < chunks; c0 += 64) {
-      const int ca = c0 + lane, cb = c0 + 32 + lane;
-      const bool va = ca < chunks, vb = cb < chunks;
-      uint4 ra = make_uint4(0, 0, 0, 0), rb = ra;
-      if (va) ra = ldg_stream_128(xrow + (ca >> LOG_CPR) * p.sh + (ca & (CPR - 1)) * 8);
-      if (vb) rb = ldg_stream_128(xrow + (cb >> LOG_CPR) * p.sh + (cb & (CPR - 1)) * 8);
-      float sa, sb;
-      const uint32_t wa = quantize_chunk<GS>(ra, tabc, sa);
-      if (c0 + 32 < chunks) {                // warp-uniform
-        const uint32_t wb = quantize_chunk<GS>(rb, tabc, sb);
-        if (vb && in_range) {
-          const long long r = orow + static_cast<long long>(cb >> LOG_CPR) * p.Tc;
-          reinterpret_cast<uint32_t*>(p.codes + r * (HD / 2))[cb & (CPR - 1)] = wb;
-          if ((cb & (GS - 1)) == 0) p.scales[r * nblk + ((cb & (CPR - 1)) / GS)] = sb;
+    for (int c0 = 0; c0 < pairs; c0 += 32 * kQPairs) {
+      uint4 ra[kQPairs], rb[kQPairs];
+#pragma unroll
+      for (int u = 0; u < kQPairs; ++u) {
+        const int c = c0 + u * 32 + lane;
+        ra[u] = rb[u] = make_uint4(0, 0, 0, 0);
+        if (c < pairs) {
+          const __half* src = xrow + (c >> LOG_PPR) * p.sh + (c & (PPR - 1)) * 16;
+          ra[u] = ldg_stream_128(src);
+          rb[u] = ldg_stream_128(src + 8);
         }
       }
-      if (va && in_range) {
-        const long long r = orow + static_cast<long long>(ca >> LOG_CPR) * p.Tc;
-        reinterpret_cast<uint32_t*>(p.codes + r * (HD / 2))[ca & (CPR - 1)] = wa;
-        if ((ca & (GS - 1)) == 0) p.scales[r * nblk + ((ca & (CPR - 1)) / GS)] = sa;
+#pragma unroll
+      for (int u = 0; u < kQPairs; ++u) {
+        if (c0 + u * 32 >= pairs) break;         // warp-uniform
+        const int c = c0 + u * 32 + lane;
+        float s = absmax16(ra[u], rb[u]);
+#pragma unroll
+        for (int o = 1; o < GS; o <<= 1) s = fmaxf(s, __shfl_xor_sync(0xffffffffu, s, o));
+        const float r = block_rcp(s);
+        const uint2 word = make_uint2(encode8_rep(ra[u], r, lane8), encode8_rep(rb[u], r, lane8));
+        if (c < pairs && in_range) {
+          const int cr = c & (PPR - 1);
+          const long long rr = orow + static_cast<long long>(c >> LOG_PPR) * p.Tc;
+          reinterpret_cast<uint2*>(p.codes + rr * (HD / 2))[cr] = word;
+          if ((c & (GS - 1)) == 0) p.scales[rr * nblk + cr / GS] = s;
+        }
       }
     }
   }
