@@ -118,12 +118,12 @@ size_t nqkv_decode_workspace_bytes(int B, int H, int hd, int Tc);
  *            (append-before-attend); 0 -> out[b] = 0
  * out        device fp32 [B][H][hd], 16-byte aligned
  * workspace  device, >= nqkv_decode_workspace_bytes(B,H,hd,Tc) bytes,
- *            16-byte aligned.  Its first 256 bytes (the work scheduler) must
- *            be ZERO before the first use; every completed call leaves them
- *            zero again.  Do not share one workspace between calls that may
- *            run concurrently (calls ordered on one stream may share it).
- * Launches: the decode kernel and, when Tc > 128, a small split-combine
- * kernel, both with programmatic dependent launch (PDL). */
+ *            16-byte aligned.  Its first 256 bytes (grid-barrier counters)
+ *            must be ZERO before the first use; every completed call leaves
+ *            them zero again.  Do not share one workspace between calls that
+ *            may run concurrently (calls ordered on one stream may share it).
+ * One cooperative launch (one CTA per SM) with programmatic dependent launch
+ * (PDL); split partials are merged in-kernel after a grid barrier. */
 int nqkv_decode_attention(const void* q, const uint8_t* k_codes, const float* k_scales,
                           const uint8_t* v_codes, const float* v_scales,
                           const int32_t* d_seq_lens, int B, int H, int hd, int blk, int Tc,

@@ -63,6 +63,7 @@ struct DecodeParams {
   float* out;
   float* ws_o;              // [B*H*max_segs][hd]  split partials
   float2* ws_ml;            // [B*H*max_segs]      (max, sum) per partial
+  int* grid_bar;            // [2] arrive / depart counters (zero between launches)
   int B, H, Tc, blk_shift, max_segs;
   float scale_log2;         // softmax_scale * log2(e)
   Levels lv;
@@ -552,6 +553,74 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const DecodeParams p
     if (consumed == 1) TRACE(5);
   }
   TRACE(6);
+
+  // ---- a7: merge the split partials in-kernel after one grid-wide barrier
+  // (cooperative launch: every CTA is resident).  One release/acquire pair per
+  // CTA instead of one per work item.
+  if (p.max_segs > 1) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      atomicAdd(p.grid_bar, 1);
+      int seen = 0;
+      do {
+        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(seen) : "l"(p.grid_bar) : "memory");
+      } while (seen < static_cast<int>(gridDim.x));
+    }
+    __syncthreads();
+    TRACE(7);
+    constexpr int DPL = HD / 32;        // output dims per lane
+    for (int r = gwarp; r < p.B * p.H; r += nwarps) {
+      const int len = s_len[r / p.H];
+      const int nseg = max(1, (len + kSeg - 1) / kSeg);
+      if (nseg <= 1) continue;
+      const long long base = static_cast<long long>(r) * p.max_segs;
+      float Mx = -INFINITY;
+      for (int i = lane; i < nseg; i += 32) Mx = fmaxf(Mx, __ldcg(&p.ws_ml[base + i].x));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) Mx = fmaxf(Mx, __shfl_xor_sync(0xffffffffu, Mx, o));
+      float den = 0.0f, acc[DPL];
+#pragma unroll
+      for (int d = 0; d < DPL; ++d) acc[d] = 0.0f;
+      for (int i0 = 0; i0 < nseg; i0 += 32) {
+        float f = 0.0f;
+        if (i0 + lane < nseg) {
+          const float2 ml = __ldcg(&p.ws_ml[base + i0 + lane]);
+          f = fast_exp2(ml.x - Mx);
+          den += f * ml.y;
+        }
+        const int cnt = min(32, nseg - i0);
+#pragma unroll 8
+        for (int i = 0; i < cnt; ++i) {
+          const float fi = __shfl_sync(0xffffffffu, f, i);
+          const float* src = p.ws_o + (base + i0 + i) * HD + lane * DPL;
+          if constexpr (DPL == 4) {
+            const float4 v = __ldcg(reinterpret_cast<const float4*>(src));
+            acc[0] += fi * v.x; acc[1] += fi * v.y; acc[2] += fi * v.z; acc[3] += fi * v.w;
+          } else {
+            const float2 v = __ldcg(reinterpret_cast<const float2*>(src));
+            acc[0] += fi * v.x; acc[1] += fi * v.y;
+          }
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) den += __shfl_xor_sync(0xffffffffu, den, o);
+      const float inv = 1.0f / den;
+      float* outp = p.out + static_cast<long long>(r) * HD + lane * DPL;
+      if constexpr (DPL == 4)
+        *reinterpret_cast<float4*>(outp) = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
+      else
+        *reinterpret_cast<float2*>(outp) = make_float2(acc[0] * inv, acc[1] * inv);
+    }
+    // leave the barrier counters zero for the next launch: the last CTA out resets
+    if (threadIdx.x == 0) {
+      const int d = atomicAdd(p.grid_bar + 1, 1);
+      if (d == static_cast<int>(gridDim.x) - 1) {
+        p.grid_bar[0] = 0;
+        p.grid_bar[1] = 0;
+      }
+    }
+  }
 }
 
 // ------------------------------------------------------- a7: split combine

@@ -116,32 +116,35 @@ int launch_decode(const DecodeParams& p, cudaStream_t st) {
       blocks_per_sm = n > 0 ? n : 1;
     }
   }
+  // exactly one resident CTA per SM (cooperative: the in-kernel split merge
+  // waits at a grid barrier)
   const unsigned blocks = static_cast<unsigned>(device_sms() * blocks_per_sm);
-  cudaError_t e = launch_pdl(kern, dim3(blocks), dim3(kDecodeWarps * 32),
-                             SmemLayout<HD, kDecodeWarps>::bytes(p.B), st, p);
-  if (e != cudaSuccess) return cuda_fail(e);
-  if (p.max_segs > 1) {   // some sequence may span several segments: merge partials
-    CombineParams c;
-    c.seq_lens = p.seq_lens; c.ws_o = p.ws_o; c.ws_ml = p.ws_ml; c.out = p.out;
-    c.B = p.B; c.H = p.H; c.Tc = p.Tc; c.max_segs = p.max_segs;
-    const long long threads = static_cast<long long>(p.B) * p.H * HD;
-    e = launch_pdl(combine_kernel<HD>, dim3(static_cast<unsigned>((threads + 255) / 256)), dim3(256),
-                   0, st, c);
-    if (e != cudaSuccess) return cuda_fail(e);
-  }
-  return NQKV_OK;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(kDecodeWarps * 32);
+  cfg.dynamicSmemBytes = SmemLayout<HD, kDecodeWarps>::bytes(p.B);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeCooperative;
+  attr[1].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, p);
+  return e == cudaSuccess ? NQKV_OK : cuda_fail(e);
 }
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct WsLayout {
-  size_t sched, ml, o, total;
+  size_t bar, ml, o, total;
 };
 
 WsLayout ws_layout(long long B, long long H, int hd, int Tc) {
   const long long ms = (Tc + kSeg - 1) / kSeg;
   WsLayout w;
-  w.sched = 0;
+  w.bar = 0;
   w.ml = 256;
   w.o = align_up(w.ml + static_cast<size_t>(B * H * ms) * sizeof(float2), 256);
   w.total = align_up(w.o + static_cast<size_t>(B * H * ms) * hd * sizeof(float), 256);
@@ -176,6 +179,7 @@ int decode_common(const void* q, const uint8_t* k_codes, const float* k_scales,
   p.v_new = static_cast<const __half*>(v_new);
   p.new_sb = new_sb; p.new_sh = new_sh;
   unsigned char* ws = static_cast<unsigned char*>(workspace);
+  p.grid_bar = reinterpret_cast<int*>(ws + w.bar);
   p.ws_ml = reinterpret_cast<float2*>(ws + w.ml);
   p.ws_o = reinterpret_cast<float*>(ws + w.o);
   p.max_segs = (Tc + kSeg - 1) / kSeg;

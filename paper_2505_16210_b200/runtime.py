@@ -159,8 +159,8 @@ class DecodeRunner:
         return int(toks * per_tok + self.B * self.Hl * self.hd * (2 + 4) + extra)
 
     def launches_per_step(self) -> int:
-        """Kernels this library launches per step: per layer the decode kernel
-        plus the split-combine kernel (always launched when Tc > 128), plus two
-        quantize launches when the append is not fused."""
-        per_layer = 1 + (1 if self.Tc > 128 else 0) + (0 if self.fused else 2)
+        """Kernels this library launches per step: per layer one decode kernel
+        (split partials merge in-kernel), plus two quantize launches when the
+        append is not fused."""
+        per_layer = 1 + (0 if self.fused else 2)
         return per_layer * self.L
