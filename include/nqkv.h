@@ -103,27 +103,35 @@ int nqkv_quantize(const void* x, int64_t stride_b, int64_t stride_t, int64_t str
 int nqkv_dequantize(const uint8_t* codes, const float* scales, int B, int H, int Tc, int hd,
                     int blk, int n_tokens, int out_dtype, void* out, void* stream);
 
-/* Bytes of workspace nqkv_decode_attention needs for this geometry. */
+/* Bytes of workspace nqkv_decode_attention / nqkv_decode_step need for this
+ * geometry (0 for an unsupported hd).  Layout: [0, nqkv_decode_counter_bytes)
+ * int32 per-(b, h) arrival counters that must be ZERO before the first call
+ * (every completed call leaves them zero again), then per-CTA split partials. */
 size_t nqkv_decode_workspace_bytes(int B, int H, int hd, int Tc);
+size_t nqkv_decode_counter_bytes(int B, int H);
 
 /* a4-a7. Fused decode attention over the 4-bit cache.
  * For every (b, h): out = softmax(softmax_scale * q . k_t) . v_t over
  * t < seq_lens[b], with k_t, v_t dequantised in registers (never written to
- * memory).  Split-K: the sequence is cut into fixed 128-token segments (a
- * function of seq_len only, so results do not depend on B, H or the GPU);
- * partial (max, sum, o) are merged in fixed segment order.  B <= 4096.
+ * memory).  Long sequences are split across CTAs (flash-decoding split-K)
+ * and their partial (max, sum, o) merged in-kernel (see below).
  * q          device fp16 [B][H][hd], 16-byte aligned
  * k_codes,…  the cache tensors described above
  * d_seq_lens device int32[B], 0..Tc, counting the token appended this step
  *            (append-before-attend); 0 -> out[b] = 0
  * out        device fp32 [B][H][hd], 16-byte aligned
  * workspace  device, >= nqkv_decode_workspace_bytes(B,H,hd,Tc) bytes,
- *            16-byte aligned.  Its first 256 bytes (grid-barrier counters)
- *            must be ZERO before the first use; every completed call leaves
- *            them zero again.  Do not share one workspace between calls that
- *            may run concurrently (calls ordered on one stream may share it).
- * One cooperative launch (one CTA per SM) with programmatic dependent launch
- * (PDL); split partials are merged in-kernel after a grid barrier. */
+ *            16-byte aligned.  Its first nqkv_decode_counter_bytes(B,H)
+ *            bytes must be ZERO before the first use; every completed call
+ *            leaves them zero again.  Do not share one workspace between calls
+ *            that may run concurrently (calls ordered on one stream may).
+ * One launch of one CTA per SM with programmatic dependent launch (PDL).  The
+ * (b, h, t) token list is cut into equal contiguous per-CTA ranges; a
+ * sequence split across CTAs is merged by the last of its CTAs to finish
+ * (per-(b, h) counter), in CTA order.  Results are bit-reproducible for a
+ * given (B, H, seq_lens, GPU); a different head shard of the same data may
+ * differ by fp32 reassociation only (reading R7).  B <= 1024 and
+ * B*H*Tc < 2^31. */
 int nqkv_decode_attention(const void* q, const uint8_t* k_codes, const float* k_scales,
                           const uint8_t* v_codes, const float* v_scales,
                           const int32_t* d_seq_lens, int B, int H, int hd, int blk, int Tc,

@@ -1,54 +1,68 @@
 // a4-a7: fused dequant-in-registers decode attention (+ optional fused
-// 1-token append) and the split-K combine kernel.
+// 1-token append).
 //
 // X' = dequantize_NF4(I); A = Softmax(t_Q X_K'^T); t_O = A X_V'
 // (the 1/sqrt(hd) factor is DESIGN.md reading R6).  The dequantised cache is
-// never written anywhere: packed codes stream from HBM into shared memory and
-// are turned into fp32 levels by shared-memory table lookups in registers.
+// never materialised: packed codes go from HBM straight into registers and
+// are turned into products by shared-memory table lookups.
 //
-// Work decomposition.  A work item is (b, h, 128-token segment); the
-// segmentation depends on seq_len only and partials are merged in segment
-// order, so results are independent of B, H, the grid and the GPU.  Items are
-// assigned statically (strided) to the warps of a persistent grid; each WARP
-// streams its items as one continuous sequence of stages (ST tokens of one
-// (b, h)):
-//   - lane 0 of the warp is the producer: it issues TMA bulk copies
-//     (cp.async.bulk, completion on an mbarrier) of a stage's K codes, V codes,
-//     K scales and V scales into a kStages-deep per-warp shared-memory ring,
-//     kStages-1 stages ahead of the consumer and across item boundaries;
-//   - all 32 lanes consume: each lane owns 16 consecutive head dims (8 packed
-//     bytes): LPT = hd/16 lanes cover a token row, G = 32/LPT token groups,
-//     kTPS = 4 tokens per lane per stage (ST = G*kTPS);
-//   - per-item q is prefetched with cp.async into a per-warp queue slot when the
-//     producer enters the item; item descriptors travel through the same queue.
+// Dequantisation by lookup:
+//  * K side -- a per-(b, h) q-table.  For head-dim pair j and code byte e
+//    (two 4-bit codes), T[e][j] = c * (q[2j] L[e & 15] + q[2j+1] L[e >> 4]),
+//    c = softmax_scale * log2(e), built in fp32 once per (b, h) piece.  A
+//    token's score is then sum_blocks s_blk * sum_{j in blk} T[byte_j][j]:
+//    ONE 4-byte shared load + one add per packed byte.  Row e of the table is
+//    256 B; a lane's 8 pairs are visited in a lane-rotated order so that the 32
+//    lanes of a warp always hit 32 distinct banks.
+//  * V side -- a constant fp32 pair table P[e] = (L[e & 15], L[e >> 4]),
+//    replicated per lane (lane l's copy in banks 2l, 2l+1): one 8-byte shared
+//    load + one fp32x2 FMA (weight p * s_blk) per packed byte.
+//  Both tables are addressed by ONE PRMT per byte (the code byte becomes
+//  address byte 1, i.e. row * 256; the lane/pair offset sits in byte 0) plus the
+//  load's immediate offset -- the dynamic shared window starts at 0x400
+//  (checked on device).
 //
-// Dequantisation.  A packed byte (two 4-bit codes) becomes the pair
-// (L[lo], L[hi]) through ONE shared-memory load from a 256-entry fp32-pair
-// table replicated per lane (64 KB, conflict-free: lane l reads bank pair 2l)
-// whose address is built by one PRMT (the table sits on a 64 KB boundary of
-// the shared window); the pair feeds one FFMA2.  Scores use fp32 levels with
-// the block scale applied once per 16 dims; values accumulate w*L with
-// w = p * scale.  The online softmax runs per token group (no cross-lane max
-// per stage); groups merge once per item.
+// Work decomposition.  The (b, h, t) token list of the launch (N tokens) is
+// cut into C equal contiguous ranges, one per CTA (C = min(grid, N /
+// min_tokens)); a range splits into "pieces" at (b, h) boundaries.
+// Warp specialisation inside the CTA:
+//  * NC consumer warps stream: stage s (ST tokens) of a piece goes to consumer
+//    s % NC.  Lane (g, sub) owns 16 head dims (8 packed bytes) of token g of
+//    each of the kTPS slots of a stage; loads run one stage ahead, across piece
+//    boundaries.  The online softmax keeps a warp-uniform running max.  At a
+//    piece end a consumer sums its token groups and publishes (m, l, o[hd]).
+//  * one producer warp builds the q-table of piece k into ring slot k % R
+//    (R = 4 for hd 64, 2 for hd 128) once every consumer has left piece k - R,
+//    and merges the consumers' states of each finished piece into the output.
+// Consumers therefore never wait on each other -- only on the producer's
+// "full" barrier of the next table, which is normally long complete.
+// A piece that does not cover a whole sequence (only a CTA's first and last
+// pieces can be partial) is written as an unnormalised partial (m, l, o);
+// the last of the sequence's CTAs to arrive (per-(b, h) counter) merges the
+// partials in CTA order.  Results depend on (B, H, seq_lens, grid) only: the
+// same call is bit-reproducible; a different head shard of the same data can
+// differ by fp32 reassociation (reading R7).
 #pragma once
 #include "common.cuh"
 
 namespace nqkv {
 
-constexpr int kSeg = 128;
-constexpr int kLutBytes = 256 * 32 * 8;
 constexpr int kMaxBatch = 1024;
+constexpr int kMaxGrid = 1024;         // partial slots in the workspace (>= CTAs per launch)
+constexpr int kMinTokensPerCta = 512;  // below this a CTA's table build would dominate
 #ifndef NQKV_DECODE_WARPS
-#define NQKV_DECODE_WARPS 16
+#define NQKV_DECODE_WARPS 16     // 15 consumers + 1 producer
 #endif
-#ifndef NQKV_STAGES
-#define NQKV_STAGES 3
+#ifndef NQKV_TPS
+#define NQKV_TPS 4
+#endif
+#ifndef NQKV_PF
+#define NQKV_PF 0                // L2 prefetch distance in a warp's own stages (0: off; measured no gain)
 #endif
 constexpr int kDecodeWarps = NQKV_DECODE_WARPS;
-constexpr int kStages = NQKV_STAGES;  // smem ring depth: TMA runs kStages-1 stages ahead
-constexpr int kQueue = 4;
-constexpr int kLaneDims = 16;         // head dims owned by one lane
-constexpr int kTPS = 4;               // tokens per lane per stage
+constexpr int kLaneDims = 16;          // head dims owned by one lane
+constexpr int kTPS = NQKV_TPS;         // token slots per lane per stage
+constexpr uint32_t kSmemWindow = 0x400;  // shared address of dynamic smem offset 0
 
 struct DecodeParams {
   const __half* q;
@@ -61,20 +75,19 @@ struct DecodeParams {
   const __half* v_new;
   long long new_sb, new_sh; // element strides of k_new / v_new ([B][H][hd])
   float* out;
-  float* ws_o;              // [B*H*max_segs][hd]  split partials
-  float2* ws_ml;            // [B*H*max_segs]      (max, sum) per partial
-  int* grid_bar;            // [2] arrive / depart counters (zero between launches)
-  int B, H, Tc, blk_shift, max_segs;
+  int* cnt;                 // [B*H] partial-arrival counters (zero between launches)
+  float* part;              // [kMaxGrid][2][hd + 2] partial (o[hd], m, l)
+  int B, H, Tc, blk_shift, min_tokens;
   float scale_log2;         // softmax_scale * log2(e)
   Levels lv;
   BucketTab tab;
-  unsigned long long* trace;   // debug builds (NQKV_TRACE): per-warp timestamps
+  unsigned long long* trace;   // NQKV_TRACE builds: per-warp globaltimer stamps [grid][NW][8]
 };
 
 #ifdef NQKV_TRACE
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
 #define TRACE(k) do { if (p.trace && lane == 0) p.trace[(blockIdx.x * NW + warp) * 8 + (k)] = gtimer(); } while (0)
@@ -83,59 +96,44 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #endif
 
 template <int HD>
-struct DecodeShape {
-  static constexpr int LPT = HD / kLaneDims;
-  static constexpr int G = 32 / LPT;
-  static constexpr int ST = G * kTPS;                     // tokens per stage (32 or 16)
-  static constexpr int kCodeBytes = ST * HD / 2;          // 1 KB per tensor per stage
-  static constexpr int kScaleBytes = ST * (HD / 32) * 4;  // room for blk = 32 (256 B)
-  static constexpr int kSlotBytes = 2 * kCodeBytes + 2 * kScaleBytes;
-  // per-warp block: ring | q queue (kQueue x hd fp16) | descriptors | mbarriers
-  static constexpr int kRingOff = 0;
-  static constexpr int kQOff = kStages * kSlotBytes;
-  static constexpr int kDescOff = kQOff + kQueue * HD * 2;
-  static constexpr int kMbarOff = kDescOff + kQueue * 8 * 4;
-  static constexpr int kWarpBytes = (kMbarOff + kStages * 8 + 15) / 16 * 16;
+struct Geo {
+  static constexpr int LPT = HD / kLaneDims;  // lanes per token row (4 / 8)
+  static constexpr int G = 32 / LPT;          // token groups per warp (8 / 4)
+  static constexpr int ST = G * kTPS;         // tokens per warp stage
+  static constexpr int R = HD == 64 ? 4 : 2;  // q-table ring depth
+  static constexpr int PPL = HD / 64;         // table pairs per producer lane (1 / 2)
 };
 
-// Shared-memory layout.  The pair LUT must start on a 64 KB boundary of the
-// shared window so that ONE PRMT can produce a complete LDS address
-// (byte 0 = lane*8, byte 1 = code byte, bytes 2-3 = LUT base >> 16): the
-// dynamic window starts at 0x400 (1 KB driver reserve), so the LUT goes at
-// dynamic offset kLutOff = 0xFC00 (checked on device; a mismatch traps).  Warp
-// blocks fill the space before the LUT first, the rest follow it.
-constexpr int kLutOff = 0xFC00;
+// Dynamic shared memory (offsets from the window start, shared address 0x400):
+//   [0, 64K)             V pair LUT: row e (256 B) = 32 lane copies of (L[lo], L[hi])
+//   [64K, 192K)          K q-table ring: row e of a table is 128 B (hd 64; two
+//                        tables share a 64 KB block of 256-B rows) or 256 B (hd 128)
+//   misc                 levels, bucket table, mbarriers, consumer states, lens/prefix
 template <int HD, int NW>
-struct SmemLayout {
-  static constexpr int kWB = DecodeShape<HD>::kWarpBytes;
-  static constexpr int kSmall = 512;                                 // bucket tab + levels
-  static constexpr int kPre = (kLutOff - kSmall) / kWB;              // warp blocks before the LUT
-  static constexpr int kBefore = kPre < NW ? kPre : NW;
-  static constexpr int kAfterOff = kLutOff + kLutBytes;
-  static constexpr int kTailOff = kAfterOff + (NW - kBefore) * kWB;   // prefix [B+1] + lens [B]
-  __host__ __device__ static constexpr int warp_off(int w) {
-    return w < kBefore ? kSmall + w * kWB : kAfterOff + (w - kBefore) * kWB;
-  }
-  __host__ __device__ static constexpr size_t bytes(int B) {
-    return static_cast<size_t>(kTailOff) + static_cast<size_t>(2 * B + 1) * sizeof(int);
-  }
+struct Smem {
+  static constexpr int NC = NW - 1;
+  static constexpr int R = Geo<HD>::R;
+  static constexpr uint32_t kV = 0;
+  static constexpr uint32_t kK = 0x10000;
+  static constexpr uint32_t kLv = kK + 0x20000;           // float[16]
+  static constexpr uint32_t kTab = kLv + 64;              // float2[kNumBuckets]
+  static constexpr uint32_t kMbar = kTab + 272;           // u64 full[R], done[R]
+  static constexpr uint32_t kMl = kMbar + 16 * R;         // float2 [R][NC]
+  static constexpr uint32_t kPc = (kMl + R * NC * 8 + 15) / 16 * 16;   // Piece [R] (producer)
+  static constexpr uint32_t kO = kPc + R * 32;            // float [R][NC][HD]
+  static constexpr uint32_t kPref = kO + R * NC * HD * 4; // int [kMaxBatch + 1]
+  static constexpr uint32_t kLen = kPref + (kMaxBatch + 1) * 4 + 12;  // int [kMaxBatch]
+  static constexpr uint32_t kBytes = kLen + kMaxBatch * 4;
+  static_assert(kBytes <= 227 * 1024, "decode smem over budget");
+  static_assert((kTab % 16) == 0 && (kMbar % 8) == 0 && (kO % 16) == 0, "alignment");
 };
 
-__device__ __forceinline__ void cp_async16(uint32_t smem_addr, const void* gptr) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(smem_addr), "l"(gptr) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait(int newer) {   // groups allowed to stay pending
-  if (newer <= 0) asm volatile("cp.async.wait_group 0;" ::: "memory");
-  else if (newer == 1) asm volatile("cp.async.wait_group 1;" ::: "memory");
-  else if (newer == 2) asm volatile("cp.async.wait_group 2;" ::: "memory");
-  else asm volatile("cp.async.wait_group 3;" ::: "memory");
-}
+// ------------------------------------------------------------ primitives
 __device__ __forceinline__ void mbar_init(uint32_t mbar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(mbar), "r"(count) : "memory");
 }
-__device__ __forceinline__ void mbar_expect_tx(uint32_t mbar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(mbar), "r"(bytes) : "memory");
+__device__ __forceinline__ void mbar_arrive(uint32_t mbar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(mbar) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
   asm volatile(
@@ -146,11 +144,44 @@ __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
       "@!p bra WAIT_%=;\n"
       "}\n" :: "r"(mbar), "r"(phase) : "memory");
 }
-// 1-D TMA bulk copy global -> shared, completion signalled on mbar.
-__device__ __forceinline__ void tma_load_1d(uint32_t dst, const void* src, uint32_t bytes, uint32_t mbar) {
-  asm volatile(
-      "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-      :: "r"(dst), "l"(src), "r"(bytes), "r"(mbar) : "memory");
+// K table entry (row/pair offset from one PRMT) -- immediate = table base
+__device__ __forceinline__ float lds_k(uint32_t off) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1+0x10400];" : "=f"(v) : "r"(off));
+  return v;
+}
+// V pair LUT entry
+__device__ __forceinline__ uint64_t lds_v(uint32_t off) {
+  uint64_t v;
+  asm volatile("ld.shared.b64 %0, [%1+0x400];" : "=l"(v) : "r"(off));
+  return v;
+}
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t s) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(s));
+  return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t shfl_xor64(uint64_t v, int o) {
+  const uint32_t lo = __shfl_xor_sync(0xffffffffu, static_cast<uint32_t>(v), o);
+  const uint32_t hi = __shfl_xor_sync(0xffffffffu, static_cast<uint32_t>(v >> 32), o);
+  return (static_cast<uint64_t>(hi) << 32) | lo;
+}
+// TMA bulk prefetch of [p, p + bytes) into L2 (no registers, no completion)
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  const uintptr_t a0 = a & ~static_cast<uintptr_t>(15);
+  const uint32_t n = static_cast<uint32_t>((a + bytes - a0 + 15) & ~static_cast<uintptr_t>(15));
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(a0), "r"(n) : "memory");
+}
+__device__ __forceinline__ float ldg_nc_f32(const float* p) {
+  float r;
+  asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(r) : "l"(p));
+  return r;
 }
 
 // Quantize this lane's 16 dims of the appended token (fp16) exactly as
@@ -180,142 +211,80 @@ __device__ __noinline__ NewTok quantize_new_token(const __half* kp, const __half
   return t;
 }
 
-// lane_sel: byte 0 = lane*8 (this lane's replica inside a 256-B LUT entry),
-// bytes 2-3 = the LUT's 64 KB-aligned shared address >> 16.  One PRMT splices
-// the code byte k of `word` in as byte 1 -> the full LDS address.
-__device__ __forceinline__ uint64_t lut_pair(uint32_t word, int k, uint32_t lane_sel) {
-  return lds64(__byte_perm(word, lane_sel, 0x7604 | (k << 4)));
-}
-__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
-  uint64_t d;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-__device__ __forceinline__ uint2 lds_u2(const uint8_t* p) { return *reinterpret_cast<const uint2*>(p); }
+// One CTA-contiguous run of tokens of one (b, h): tokens [t0, t1) of a
+// sequence of length len.  Walked identically by every warp.
+struct __align__(16) Piece {
+  long long gs;   // global (b, h, t) index of t0
+  int b, h, len, t0, t1, pad;
+};
 
-// One stage from a shared-memory slot: kTPS tokens per lane.  The online
-// softmax runs per token GROUP (the G groups see disjoint tokens; the LPT lanes
-// of a group hold identical scores), so no cross-lane max is needed here.
-template <int HD>
-__device__ __forceinline__ void compute_stage(const uint8_t* slot, int tok0, int end, int g, int sub,
-                                              int nblk, int sidx, const uint64_t (&q2)[8],
-                                              uint64_t (&o2)[8], float& m, float& l,
-                                              uint32_t lane_sel, float scale_log2) {
-  using Sh = DecodeShape<HD>;
-  constexpr int LPT = Sh::LPT, G = Sh::G;
-  const uint8_t* kb = slot;
-  const uint8_t* vb = slot + Sh::kCodeBytes;
-  const float* ksb = reinterpret_cast<const float*>(slot + 2 * Sh::kCodeBytes);
-  const float* vsb = reinterpret_cast<const float*>(slot + 2 * Sh::kCodeBytes + Sh::kScaleBytes);
-  float sc[kTPS];
-#pragma unroll
-  for (int i = 0; i < kTPS; ++i) {
-    const int r = i * G + g;
-    const uint2 kw = lds_u2(kb + r * (HD / 2) + sub * (kLaneDims / 2));
-    uint64_t a0 = 0, a1 = 0;   // two independent fp32x2 chains over 8 packed bytes
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      a0 = ffma2(q2[k], lut_pair(kw.x, k, lane_sel), a0);
-      a1 = ffma2(q2[4 + k], lut_pair(kw.y, k, lane_sel), a1);
-    }
-    const float2 a = unpack2(fadd2(a0, a1));
-    sc[i] = (a.x + a.y) * ksb[r * nblk + sidx];
-  }
-#pragma unroll
-  for (int o = 1; o < LPT; o <<= 1) {
-#pragma unroll
-    for (int i = 0; i < kTPS; ++i) sc[i] += __shfl_xor_sync(0xffffffffu, sc[i], o);
-  }
-  float mt = m;
-#pragma unroll
-  for (int i = 0; i < kTPS; ++i) {
-    sc[i] = (tok0 + i * G + g < end) ? sc[i] * scale_log2 : -INFINITY;
-    mt = fmaxf(mt, sc[i]);
-  }
-  // rescale unconditionally (corr = 1 when the group max did not move).  A
-  // group that has seen only masked tokens keeps m = -inf; subtracting the
-  // finite ms keeps every exponent -inf or finite (ex2(-inf) = 0, no NaN).
-  const float ms = fmaxf(mt, -3.0e38f);
-  const float corr = fast_exp2(m - ms);
-  m = mt;
-  l *= corr;
-  const uint64_t c2 = pack2(corr, corr);
-#pragma unroll
-  for (int j = 0; j < 8; ++j) o2[j] = fmul2(o2[j], c2);
-#pragma unroll
-  for (int i = 0; i < kTPS; ++i) {
-    const int r = i * G + g;
-    const uint2 vw = lds_u2(vb + r * (HD / 2) + sub * (kLaneDims / 2));
-    const float pr = fast_exp2(sc[i] - ms);
-    l += pr;
-    const float w = pr * vsb[r * nblk + sidx];
-    const uint64_t w2 = pack2(w, w);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      o2[k] = ffma2(lut_pair(vw.x, k, lane_sel), w2, o2[k]);
-      o2[4 + k] = ffma2(lut_pair(vw.y, k, lane_sel), w2, o2[4 + k]);
-    }
-  }
-}
-
-// Producer-side cursor (warp-uniform): walks items/stages kStages-1 ahead.
-struct LoadCursor {
-  int active;            // 1 while items remain
-  int q;                 // items entered so far (queue position of the next one)
-  int st, nst, start, end;
-  long long row0;
+// Registers of one stage: kTPS token slots of this lane.
+struct StageRegs {
+  uint2 k[kTPS], v[kTPS];
+  float ks[kTPS], vs[kTPS];
 };
 
 template <int HD, int NW>
 __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const DecodeParams p) {
-  using Sh = DecodeShape<HD>;
-  using Lay = SmemLayout<HD, NW>;
-  constexpr int LPT = Sh::LPT, G = Sh::G, ST = Sh::ST;
+  using Ge = Geo<HD>;
+  using Sm = Smem<HD, NW>;
+  constexpr int LPT = Ge::LPT, G = Ge::G, ST = Ge::ST, R = Ge::R;
+  constexpr int NT = NW * 32, NC = NW - 1;
   extern __shared__ __align__(16) unsigned char smem[];
-  float2* s_tab = reinterpret_cast<float2*>(smem);
-  float* s_lv = reinterpret_cast<float*>(smem + 384);
-  int* s_pref = reinterpret_cast<int*>(smem + Lay::kTailOff);           // [B+1]
-  int* s_len = s_pref + p.B + 1;                                        // [B]
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   TRACE(0);
-  unsigned char* wb = smem + Lay::warp_off(warp);
-  __half* qbuf = reinterpret_cast<__half*>(wb + Sh::kQOff);
-  int* desc = reinterpret_cast<int*>(wb + Sh::kDescOff);
-  const uint32_t ring = static_cast<uint32_t>(__cvta_generic_to_shared(wb + Sh::kRingOff));
-  const uint32_t mbar0 = static_cast<uint32_t>(__cvta_generic_to_shared(wb + Sh::kMbarOff));
+  if (static_cast<uint32_t>(__cvta_generic_to_shared(smem)) != kSmemWindow) __trap();
+  float* s_lv = reinterpret_cast<float*>(smem + Sm::kLv);
+  float2* s_tab = reinterpret_cast<float2*>(smem + Sm::kTab);
+  const uint32_t mb_full = kSmemWindow + Sm::kMbar;          // full[R]  (count 1: producer)
+  const uint32_t mb_done = kSmemWindow + Sm::kMbar + 8 * R;  // done[R]  (count NC)
+  float* s_o = reinterpret_cast<float*>(smem + Sm::kO);
+  float2* s_ml = reinterpret_cast<float2*>(smem + Sm::kMl);
+  Piece* s_pc = reinterpret_cast<Piece*>(smem + Sm::kPc);
+  int* s_pref = reinterpret_cast<int*>(smem + Sm::kPref);
+  int* s_len = reinterpret_cast<int*>(smem + Sm::kLen);
 
-  // ---- prologue independent of the previous kernel: tables, pair LUT, barriers
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int k = 0; k < 16; ++k) s_lv[k] = p.lv.v[k];
-  }
-  for (int i = threadIdx.x; i < kNumBuckets; i += blockDim.x) s_tab[i] = p.tab.e[i];
-  if (lane < kStages) mbar_init(mbar0 + lane * 8, 1);
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  __syncthreads();
-  {
-    float4* lut4 = reinterpret_cast<float4*>(smem + kLutOff);
-    for (int i = threadIdx.x; i < 256 * 16; i += blockDim.x) {
-      const int e = i >> 4;
-      const float lo = s_lv[e & 15], hi = s_lv[e >> 4];
-      lut4[i] = make_float4(lo, hi, lo, hi);
+  // ---- prologue independent of the previous kernel: levels, V LUT, barriers
+  if (tid < 16) s_lv[tid] = p.lv.v[tid];
+  if (tid < kNumBuckets) s_tab[tid] = p.tab.e[tid];
+  if (tid == 0) {
+    for (int r = 0; r < R; ++r) {
+      mbar_init(mb_full + 8 * r, 1);
+      mbar_init(mb_done + 8 * r, NC);
     }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  TRACE(1);
   pdl_trigger();
   pdl_wait();
-  TRACE(2);
-  // ---- per-batch lengths and item prefix: items(b) = H * max(1, ceil(len/kSeg))
+  TRACE(1);
+  // seq_lens (warp 0) in flight while the V LUT is written
+  int lens_r[kMaxBatch / 32];
+  if (warp == 0) {
+#pragma unroll
+    for (int u = 0; u < kMaxBatch / 32; ++u) {
+      const int b = u * 32 + lane;
+      lens_r[u] = (u * 32 < p.B && b < p.B) ? p.seq_lens[b] : 0;
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < 256 * 16; i += NT) {     // 16 B = two lane copies per store
+    const int e = i >> 4;
+    const float lo = s_lv[e & 15], hi = s_lv[e >> 4];
+    *reinterpret_cast<float4*>(smem + Sm::kV + e * 256 + (i & 15) * 16) = make_float4(lo, hi, lo, hi);
+  }
+  // ---- per-batch lengths and token prefix: tokens(b) = H * len_b
   if (warp == 0) {
     int carry = 0;
     if (lane == 0) s_pref[0] = 0;
-    for (int b0 = 0; b0 < p.B; b0 += 32) {
-      const int b = b0 + lane;
+#pragma unroll
+    for (int u = 0; u < kMaxBatch / 32; ++u) {
+      if (u * 32 >= p.B) break;
+      const int b = u * 32 + lane;
       int n = 0;
       if (b < p.B) {
-        const int len = min(max(p.seq_lens[b], 0), p.Tc);
+        const int len = min(max(lens_r[u], 0), p.Tc);
         s_len[b] = len;
-        n = p.H * max(1, (len + kSeg - 1) / kSeg);
+        n = p.H * len;
       }
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -327,340 +296,465 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const DecodeParams p
     }
   }
   __syncthreads();
-  const int total = s_pref[p.B];
-  TRACE(3);
-  const uint32_t lut = static_cast<uint32_t>(__cvta_generic_to_shared(smem + kLutOff));
-  if (lut & 0xFFFFu) __trap();        // the single-PRMT address needs a 64 KB-aligned LUT
-  const uint32_t lane_sel = (lut & 0xFFFF0000u) | (lane * 8u);
-  const uint32_t tab = static_cast<uint32_t>(__cvta_generic_to_shared(s_tab));
+  TRACE(2);
+  const long long N = s_pref[p.B];
+  // empty sequences: out = 0 (reading R12); strided over the grid
+  for (long long i = static_cast<long long>(blockIdx.x) * NT + tid; i < static_cast<long long>(p.B) * p.H * HD;
+       i += static_cast<long long>(gridDim.x) * NT) {
+    if (s_len[i / (static_cast<long long>(p.H) * HD)] == 0) p.out[i] = 0.0f;
+  }
+  if (N == 0) return;
+  const int C = static_cast<int>(min(static_cast<long long>(gridDim.x),
+                                     max(1ll, (N + p.min_tokens - 1) / p.min_tokens)));
+  if (static_cast<int>(blockIdx.x) >= C) return;
+  const int cta = blockIdx.x;
+  const long long g0 = static_cast<long long>(cta) * N / C;
+  const long long g1 = static_cast<long long>(cta + 1) * N / C;
+
+  // ---- piece walking (identical in every warp)
+  auto locate = [&](long long g, Piece& pc) {
+    int lo = 0, hi = p.B;                 // largest b with pref[b] <= g (pref[B] > g)
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (s_pref[mid] <= g) lo = mid; else hi = mid;
+    }
+    pc.b = lo;
+    pc.len = s_len[lo];
+    const long long off = g - s_pref[lo];
+    pc.h = static_cast<int>(off / pc.len);
+    pc.t0 = static_cast<int>(off - static_cast<long long>(pc.h) * pc.len);
+    pc.gs = g;
+    pc.t1 = static_cast<int>(min(static_cast<long long>(pc.len), pc.t0 + (g1 - g)));
+  };
+  auto next_piece = [&](Piece& pc) -> bool {
+    const long long g = pc.gs + (pc.t1 - pc.t0);
+    if (g >= g1) return false;
+    if (pc.h + 1 < p.H) {
+      ++pc.h;
+    } else {
+      do { ++pc.b; } while (s_len[pc.b] == 0);
+      pc.h = 0;
+      pc.len = s_len[pc.b];
+    }
+    pc.t0 = 0;
+    pc.gs = g;
+    pc.t1 = static_cast<int>(min(static_cast<long long>(pc.len), g1 - g));
+    return true;
+  };
+
+  // L2 prefetch of rows [r0, r1) of (b, h) -- codes and scales of K and V
+  const int nblk_ = HD >> p.blk_shift;
+  auto prefetch_rows = [&](long long bh, int r0, int r1) {
+    if (r1 <= r0) return;
+    const long long row = bh * p.Tc + r0;
+    const uint32_t n = static_cast<uint32_t>(r1 - r0);
+    prefetch_l2(p.kc + row * (HD / 2), n * (HD / 2));
+    prefetch_l2(p.vc + row * (HD / 2), n * (HD / 2));
+    prefetch_l2(p.ks + row * nblk_, n * nblk_ * 4);
+    prefetch_l2(p.vs + row * nblk_, n * nblk_ * 4);
+  };
+
+  // ---- table of piece 0, built by all threads (thread: pair quad tid % Q)
+  {
+    Piece p0;
+    locate(g0, p0);
+    constexpr int Q = HD / 8;
+    const long long bh = static_cast<long long>(p0.b) * p.H + p0.h;
+    const uint4 qraw = __ldg(reinterpret_cast<const uint4*>(p.q + bh * HD) + (tid % Q));
+    __half2 h2[4];
+    memcpy(h2, &qraw, 16);
+    float qa[8];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float2 f = __half22float2(h2[k]);
+      qa[2 * k] = f.x * p.scale_log2;
+      qa[2 * k + 1] = f.y * p.scale_log2;
+    }
+    for (int e = tid / Q; e < 256; e += NT / Q) {
+      const float lo = s_lv[e & 15], hi = s_lv[e >> 4];
+      *reinterpret_cast<float4*>(smem + Sm::kK + e * 256 + (tid % Q) * 16) =
+          make_float4(fmaf(qa[1], hi, qa[0] * lo), fmaf(qa[3], hi, qa[2] * lo),
+                      fmaf(qa[5], hi, qa[4] * lo), fmaf(qa[7], hi, qa[6] * lo));
+    }
+  }
+  __syncthreads();
+
+  if (warp == NC) {
+    // ================================================================ producer
+    // q-table slot r: hd 64 -> block r >> 1, half r & 1; hd 128 -> block r
+    auto build = [&](int slot, const float (&qa)[2 * Ge::PPL]) {
+#pragma unroll
+      for (int u = 0; u < Ge::PPL; ++u) {
+        const int j = lane + 32 * u;
+        const uint32_t base = Sm::kK + (HD == 64 ? (slot >> 1) * 0x10000 + (slot & 1) * 128
+                                                 : slot * 0x10000) + j * 4;
+        float A[16], Bv[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          A[c] = qa[2 * u] * s_lv[c];
+          Bv[c] = qa[2 * u + 1] * s_lv[c];
+        }
+        float* t = reinterpret_cast<float*>(smem + base);
+#pragma unroll
+        for (int e = 0; e < 256; ++e) t[e * 64] = A[e & 15] + Bv[e >> 4];
+      }
+    };
+    auto load_q = [&](const Piece& pc, float (&qa)[2 * Ge::PPL]) {
+      const long long bh = static_cast<long long>(pc.b) * p.H + pc.h;
+#pragma unroll
+      for (int u = 0; u < Ge::PPL; ++u) {
+        const __half2 h2 = __ldg(reinterpret_cast<const __half2*>(p.q + bh * HD) + lane + 32 * u);
+        const float2 f = __half22float2(h2);
+        qa[2 * u] = f.x * p.scale_log2;
+        qa[2 * u + 1] = f.y * p.scale_log2;
+      }
+    };
+    constexpr int DL = HD / 32;
+    // merge piece k's NC consumer states (ring slot k % R): output or partial
+    auto merge = [&](int k) {
+      const int slot = k % R;
+      const Piece pc = s_pc[slot];
+      float M = -INFINITY;
+      for (int w = 0; w < NC; ++w) M = fmaxf(M, s_ml[slot * NC + w].x);
+      float den = 0.0f, acc[DL];
+#pragma unroll
+      for (int d = 0; d < DL; ++d) acc[d] = 0.0f;
+      for (int w = 0; w < NC; ++w) {
+        const float2 ml = s_ml[slot * NC + w];
+        if (ml.x == -INFINITY) continue;                 // consumer saw no token
+        const float f = fast_exp2(ml.x - M);
+        den += f * ml.y;
+        const float* o = s_o + (slot * NC + w) * HD + lane * DL;
+#pragma unroll
+        for (int d = 0; d < DL; ++d) acc[d] = fmaf(f, o[d], acc[d]);
+      }
+      const long long bh = static_cast<long long>(pc.b) * p.H + pc.h;
+      if (pc.t0 == 0 && pc.t1 == pc.len) {
+        const float inv = 1.0f / den;
+#pragma unroll
+        for (int d = 0; d < DL; ++d) p.out[bh * HD + lane * DL + d] = acc[d] * inv;
+        return;
+      }
+      // partial piece: slot 0 = this CTA's first piece, 1 = its last
+      float* part = p.part + (static_cast<long long>(cta) * 2 + (k == 0 ? 0 : 1)) * (HD + 2);
+#pragma unroll
+      for (int d = 0; d < DL; ++d) part[lane * DL + d] = acc[d];
+      if (lane == 0) {
+        part[HD] = M;
+        part[HD + 1] = den;
+      }
+      __threadfence();
+      __syncwarp();
+      const long long st = pc.gs - pc.t0;                           // global index of token 0
+      const int ca = static_cast<int>(((st + 1) * C - 1) / N);
+      const int cb = static_cast<int>(((st + pc.len) * C - 1) / N);
+      int last = 0;
+      if (lane == 0) last = atomicAdd(p.cnt + bh, 1) == cb - ca;
+      last = __shfl_sync(0xffffffffu, last, 0);
+      if (!last) return;
+      __threadfence();
+      float Mx = -INFINITY;
+      for (int c = ca; c <= cb; ++c) {
+        const int sl = (c == ca && static_cast<long long>(c) * N / C != st) ? 1 : 0;
+        Mx = fmaxf(Mx, __ldcg(p.part + (static_cast<long long>(c) * 2 + sl) * (HD + 2) + HD));
+      }
+      float dsum = 0.0f, o[DL];
+#pragma unroll
+      for (int d = 0; d < DL; ++d) o[d] = 0.0f;
+      for (int c = ca; c <= cb; ++c) {
+        const int sl = (c == ca && static_cast<long long>(c) * N / C != st) ? 1 : 0;
+        const float* pp = p.part + (static_cast<long long>(c) * 2 + sl) * (HD + 2);
+        const float fc = fast_exp2(__ldcg(pp + HD) - Mx);
+        dsum += fc * __ldcg(pp + HD + 1);
+#pragma unroll
+        for (int d = 0; d < DL; ++d) o[d] = fmaf(fc, __ldcg(pp + lane * DL + d), o[d]);
+      }
+      const float inv = 1.0f / dsum;
+#pragma unroll
+      for (int d = 0; d < DL; ++d) p.out[bh * HD + lane * DL + d] = o[d] * inv;
+      if (lane == 0) p.cnt[bh] = 0;
+    };
+
+    Piece pc;
+    locate(g0, pc);
+    float qa[2 * Ge::PPL], qn[2 * Ge::PPL];
+#pragma unroll
+    for (int u = 0; u < 2 * Ge::PPL; ++u) qa[u] = 0.0f;
+    Piece nx = pc;
+    bool more = next_piece(nx);
+    if (more) load_q(nx, qn);
+    int k = 0;
+    for (;;) {
+      if (k >= R) {
+        mbar_wait(mb_done + 8 * ((k - R) % R), ((k - R) / R) & 1);
+        merge(k - R);
+      }
+      if (lane == 0) s_pc[k % R] = pc;
+      if (k > 0) {
+        build(k % R, qa);
+        // the first stage of every consumer in this piece: L2 prefetch
+        if (lane == 0)
+          prefetch_rows(static_cast<long long>(pc.b) * p.H + pc.h, pc.t0, min(pc.t1, pc.t0 + NC * ST));
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(mb_full + 8 * (k % R));
+      if (k == 0) TRACE(3);
+      if (!more) break;
+      pc = nx;
+      ++k;
+#pragma unroll
+      for (int u = 0; u < 2 * Ge::PPL; ++u) qa[u] = qn[u];
+      more = next_piece(nx);
+      if (more) load_q(nx, qn);
+    }
+    TRACE(5);
+    for (int j = max(0, k + 1 - R); j <= k; ++j) {
+      mbar_wait(mb_done + 8 * (j % R), (j / R) & 1);
+      merge(j);
+    }
+    TRACE(6);
+    return;
+  }
+
+  // ================================================================ consumers
   const int g = lane / LPT, sub = lane % LPT;
   const int nblk = HD >> p.blk_shift;
   const int sidx = (sub * kLaneDims) >> p.blk_shift;
-  const bool fused = p.k_new != nullptr;
   const int blk_lanes = (1 << p.blk_shift) / kLaneDims;
+  const int rho = (g + (HD == 128 ? 4 * (sub >> 2) : 0)) & 7;     // bank rotation
+  uint32_t rotA = 0, rotB = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    rotA |= static_cast<uint32_t>((i + rho) & 7) << (4 * i);
+    rotB |= static_cast<uint32_t>((i + 4 + rho) & 7) << (4 * i);
+  }
+  const uint32_t vsel = static_cast<uint32_t>(lane) * 8u;
+  const bool fused = p.k_new != nullptr;
+  const uint32_t tab = kSmemWindow + Sm::kTab;
+  auto nstages = [&](const Piece& pc) { return (pc.t1 - pc.t0 + ST - 1) / ST; };
 
-  // Static strided schedule: warp w takes items w, w + W, w + 2W, ...
-  const int gwarp = static_cast<int>(blockIdx.x) * NW + warp;
-  const int nwarps = static_cast<int>(gridDim.x) * NW;
-  int next_item = gwarp;
-
-  // ---- producer: enter the next scheduled item that has tokens (decode it,
-  // publish its descriptor, prefetch q).  Empty sequences are finished here
-  // (out = 0, reading R12).  Returns false when exhausted.
-  LoadCursor L;
-  L.q = 0;
-  auto enter_next = [&]() -> bool {
-    for (;;) {
-      const int item = next_item;
-      if (item >= total) return false;
-      next_item += nwarps;
-      int lo = 0, hi = p.B;
-      while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (s_pref[mid] <= item) lo = mid; else hi = mid;
-      }
-      const int b = lo;
-      const int len = s_len[b];
-      const int nseg = max(1, (len + kSeg - 1) / kSeg);
-      const int r = item - s_pref[b];
-      const int h = r / nseg, seg = r - h * nseg;
-      const int bh = b * p.H + h;
-      if (len == 0) {
-        for (int d = lane; d < HD; d += 32) p.out[static_cast<long long>(bh) * HD + d] = 0.0f;
-        continue;
-      }
-      const int start = seg * kSeg;
-      const int end = min(len, start + kSeg);
-      const int row_new = (fused && len - 1 >= start && len - 1 < end) ? len - 1 : -1;
-      const int slot = L.q & (kQueue - 1);
-      if (lane == 0) {
-        int* d = desc + slot * 8;
-        d[0] = bh; d[1] = start; d[2] = end; d[3] = nseg; d[4] = seg; d[5] = row_new; d[6] = b; d[7] = h;
-      }
-      constexpr int CH = HD * 2 / 16;       // 16-byte chunks per fp16 row (8 or 16)
-      const uint32_t qs = static_cast<uint32_t>(__cvta_generic_to_shared(qbuf + slot * HD));
-      if (lane < CH) cp_async16(qs + lane * 16, p.q + static_cast<long long>(bh) * HD + lane * 8);
-      cp_async_commit();
-      L.st = 0;
-      L.nst = (end - start + ST - 1) / ST;
-      L.start = start;
-      L.end = end;
-      L.row0 = static_cast<long long>(bh) * p.Tc;
-      ++L.q;
-      return true;
-    }
-  };
-  auto advance = [&]() {
-    if (++L.st >= L.nst) L.active = enter_next();
-  };
-  // TMA one stage (ST rows of one (b, h), clipped at Tc) into ring slot `pos % kStages`.
-  auto issue = [&](int pos) {
-    if (lane == 0) {
-      const int s = pos % kStages;
-      const uint32_t dst = ring + s * Sh::kSlotBytes;
-      const uint32_t mb = mbar0 + s * 8;
-      const int tok0 = L.start + L.st * ST;
-      const int rows = min(ST, p.Tc - tok0);
-      const long long row = L.row0 + tok0;
-      const uint32_t cb = rows * (HD / 2), sb = rows * nblk * 4;
-      mbar_expect_tx(mb, 2 * cb + 2 * sb);
-      tma_load_1d(dst, p.kc + row * (HD / 2), cb, mb);
-      tma_load_1d(dst + Sh::kCodeBytes, p.vc + row * (HD / 2), cb, mb);
-      tma_load_1d(dst + 2 * Sh::kCodeBytes, p.ks + row * nblk, sb, mb);
-      tma_load_1d(dst + 2 * Sh::kCodeBytes + Sh::kScaleBytes, p.vs + row * nblk, sb, mb);
-    }
+  uint32_t jsel[8];
+  auto set_jsel = [&](int slot) {
+    const uint32_t add = HD == 64 ? (static_cast<uint32_t>(slot >> 1) << 16) | ((slot & 1) * 128u)
+                                  : static_cast<uint32_t>(slot) << 16;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) jsel[k] = static_cast<uint32_t>(sub * 8 + ((k + rho) & 7)) * 4u + add;
   };
 
-  // ---- consumer state
-  int cq = 0, cst = 0, cnst = 0, cstart = 0, cend = 0, cbh = 0, cnseg = 1, cseg = 0, crow_new = -1;
-  int cb_ = 0, ch_ = 0;
-  bool copen = false;
-  uint64_t q2[8], o2[8];
+  uint64_t o2[8];
   float m = -INFINITY, l = 0.0f;
-
-  auto open_item = [&]() {
-    __syncwarp();
-    const int slot = cq & (kQueue - 1);
-    const int* d = desc + slot * 8;
-    cbh = d[0]; cstart = d[1]; cend = d[2]; cnseg = d[3]; cseg = d[4]; crow_new = d[5];
-    cb_ = d[6]; ch_ = d[7];
-    cnst = (cend - cstart + ST - 1) / ST;
-    cst = 0;
-    cp_async_wait(L.q - cq - 1);      // this item's q prefetch has landed
-    __syncwarp();
-    const uint4* qp = reinterpret_cast<const uint4*>(qbuf + slot * HD + sub * kLaneDims);
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const uint4 rq = qp[j];
-      const uint32_t w4[4] = {rq.x, rq.y, rq.z, rq.w};
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        __half2 h2;
-        memcpy(&h2, &w4[k], 4);
-        const float2 f = __half22float2(h2);
-        q2[j * 4 + k] = pack2(f.x, f.y);
-      }
-    }
+  bool any = false;            // this warp consumed a stage of the current piece
+  auto reset_state = [&]() {
 #pragma unroll
     for (int j = 0; j < 8; ++j) o2[j] = 0;
     m = -INFINITY;
     l = 0.0f;
-    copen = true;
+    any = false;
   };
 
-  auto close_item = [&]() {
-    // merge the G per-group softmax states: common max M, rescale, sum
-    float M = m;
-#pragma unroll
-    for (int o = LPT; o < 32; o <<= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-    const float f = fast_exp2(m - M);          // 0 for a group that saw no token
-    l *= f;
-    const uint64_t f2 = pack2(f, f);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) o2[j] = fmul2(o2[j], f2);
-#pragma unroll
-    for (int o = LPT; o < 32; o <<= 1) {
-      l += __shfl_xor_sync(0xffffffffu, l, o);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        float2 a = unpack2(o2[j]);
-        a.x += __shfl_xor_sync(0xffffffffu, a.x, o);
-        a.y += __shfl_xor_sync(0xffffffffu, a.y, o);
-        o2[j] = pack2(a.x, a.y);
+  auto load_stage = [&](StageRegs& Rg, const Piece& pc, int s) {
+    const long long bh = static_cast<long long>(pc.b) * p.H + pc.h;
+    const int tok0 = pc.t0 + s * ST;
+    if (NQKV_PF > 0 && lane == 0) {   // L2 prefetch NQKV_PF of this warp's stages ahead
+      const int first = s == warp ? 1 : NQKV_PF;
+      for (int d = first; d <= NQKV_PF; ++d) {
+        const int r0 = tok0 + d * NC * ST;
+        if (r0 >= pc.t1) break;
+        prefetch_rows(bh, r0, min(pc.t1, r0 + ST));
       }
     }
-    // every group now holds the full sums for its sub's 16 dims; group g
-    // writes dims [sub*16 + g*(16/G), +16/G)
-    constexpr int PER = kLaneDims / G;          // 2 (hd 64) or 4 (hd 128)
-    float res[PER];
+#ifdef NQKV_EXP_NOLOAD
 #pragma unroll
-    for (int d = 0; d < PER; ++d) {
-      const int idx = g * PER + d;              // 0..15 within the lane's 16 dims
-      float v = 0.0f;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const float2 a = unpack2(o2[j]);
-        if (idx == 2 * j) v = a.x;
-        if (idx == 2 * j + 1) v = a.y;
-      }
-      res[d] = v;
+    for (int i = 0; i < kTPS; ++i) {
+      Rg.k[i] = make_uint2(0x12345678u * (i + 1) + tok0, 0x9abcdef0u + lane);
+      Rg.v[i] = make_uint2(0x31415926u * (i + 3) + tok0, 0x27182818u + lane);
+      Rg.ks[i] = 1.0f;
+      Rg.vs[i] = 0.5f;
     }
-    float* dst;
-    if (cnseg == 1) {
-      const float inv = 1.0f / l;
+    return;
+#endif
 #pragma unroll
-      for (int d = 0; d < PER; ++d) res[d] *= inv;
-      dst = p.out + static_cast<long long>(cbh) * HD + sub * kLaneDims + g * PER;
-    } else {
-      const long long slot = static_cast<long long>(cbh) * p.max_segs + cseg;
-      dst = p.ws_o + slot * HD + sub * kLaneDims + g * PER;
-      if (lane == 0) p.ws_ml[slot] = make_float2(M, l);
+    for (int i = 0; i < kTPS; ++i) {
+      const int row = min(tok0 + i * G + g, pc.t1 - 1);     // clamp: masked rows read valid data
+      const long long r = bh * p.Tc + row;
+      Rg.k[i] = ldg_stream_64(p.kc + r * (HD / 2) + sub * 8);
+      Rg.v[i] = ldg_stream_64(p.vc + r * (HD / 2) + sub * 8);
+      Rg.ks[i] = ldg_nc_f32(p.ks + r * nblk + sidx);
+      Rg.vs[i] = ldg_nc_f32(p.vs + r * nblk + sidx);
     }
-    if constexpr (PER == 4) *reinterpret_cast<float4*>(dst) = make_float4(res[0], res[1], res[2], res[3]);
-    else *reinterpret_cast<float2*>(dst) = make_float2(res[0], res[1]);
-    ++cq;
-    copen = false;
   };
 
-  // Consume stage position `pos` (slot pos % kStages, parity (pos / kStages) & 1).
-  auto consume = [&](int pos) {
-    const int s = pos % kStages;
-    mbar_wait(mbar0 + s * 8, (pos / kStages) & 1);
-    uint8_t* slot = wb + Sh::kRingOff + s * Sh::kSlotBytes;
-    const int tok0 = cstart + cst * ST;
-    if (crow_new >= tok0 && crow_new < tok0 + ST) {   // warp-uniform: the stage holds the new token
-      const int r_new = crow_new - tok0;               // row inside the slot
-      const long long off = static_cast<long long>(cb_) * p.new_sb + static_cast<long long>(ch_) * p.new_sh +
-                            sub * kLaneDims;
-      const NewTok nt = quantize_new_token(p.k_new + off, p.v_new + off, blk_lanes, tab);
-      if (g == r_new % G) {
-        const long long row = static_cast<long long>(cbh) * p.Tc + crow_new;
-        const int cofs = sub * (kLaneDims / 2);
-        *reinterpret_cast<uint2*>(const_cast<uint8_t*>(p.kc) + row * (HD / 2) + cofs) = nt.k;
-        *reinterpret_cast<uint2*>(const_cast<uint8_t*>(p.vc) + row * (HD / 2) + cofs) = nt.v;
-        *reinterpret_cast<uint2*>(slot + r_new * (HD / 2) + cofs) = nt.k;
-        *reinterpret_cast<uint2*>(slot + Sh::kCodeBytes + r_new * (HD / 2) + cofs) = nt.v;
-        if (((sub * kLaneDims) & ((1 << p.blk_shift) - 1)) == 0) {
-          const_cast<float*>(p.ks)[row * nblk + sidx] = nt.ks;
-          const_cast<float*>(p.vs)[row * nblk + sidx] = nt.vs;
-          reinterpret_cast<float*>(slot + 2 * Sh::kCodeBytes)[r_new * nblk + sidx] = nt.ks;
-          reinterpret_cast<float*>(slot + 2 * Sh::kCodeBytes + Sh::kScaleBytes)[r_new * nblk + sidx] = nt.vs;
-        }
-      }
-      __syncwarp();
-    }
-    compute_stage<HD>(slot, tok0, cend, g, sub, nblk, sidx, q2, o2, m, l, lane_sel, p.scale_log2);
-    __syncwarp();                                      // slot reads done before it is refilled
-    if (++cst == cnst) close_item();
-  };
-
-  // ---- prime the pipeline: kStages-1 stages in flight
-  L.active = enter_next();
-  int issued = 0, consumed = 0;
-  for (int r = 0; r < kStages - 1 && L.active; ++r) {
-    issue(issued++);
-    advance();
-  }
-  TRACE(4);
-  // steady state: refill the slot consumed last, then consume the next stage
-  while (consumed < issued) {
-    if (L.active) {
-      issue(issued++);
-      advance();
-    }
-    if (!copen) open_item();
-    consume(consumed++);
-    if (consumed == 1) TRACE(5);
-  }
-  TRACE(6);
-
-  // ---- a7: merge the split partials in-kernel after one grid-wide barrier
-  // (cooperative launch: every CTA is resident).  One release/acquire pair per
-  // CTA instead of one per work item.
-  if (p.max_segs > 1) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      asm volatile("fence.acq_rel.gpu;" ::: "memory");
-      atomicAdd(p.grid_bar, 1);
-      int seen = 0;
-      do {
-        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(seen) : "l"(p.grid_bar) : "memory");
-      } while (seen < static_cast<int>(gridDim.x));
-    }
-    __syncthreads();
-    TRACE(7);
-    constexpr int DPL = HD / 32;        // output dims per lane
-    for (int r = gwarp; r < p.B * p.H; r += nwarps) {
-      const int len = s_len[r / p.H];
-      const int nseg = max(1, (len + kSeg - 1) / kSeg);
-      if (nseg <= 1) continue;
-      const long long base = static_cast<long long>(r) * p.max_segs;
-      float Mx = -INFINITY;
-      for (int i = lane; i < nseg; i += 32) Mx = fmaxf(Mx, __ldcg(&p.ws_ml[base + i].x));
+  auto consume = [&](StageRegs& Rg, const Piece& pc, int s) {
+    const int tok0 = pc.t0 + s * ST;
+    any = true;
+    if (fused) {
+      const int row_new = pc.len - 1;
+      if (row_new >= tok0 && row_new < tok0 + ST && row_new < pc.t1) {   // warp-uniform
+        const int rn = row_new - tok0, i_new = rn / G, g_new = rn % G;
+        const long long off = static_cast<long long>(pc.b) * p.new_sb +
+                              static_cast<long long>(pc.h) * p.new_sh + sub * kLaneDims;
+        const NewTok nt = quantize_new_token(p.k_new + off, p.v_new + off, blk_lanes, tab);
+        if (g == g_new) {
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) Mx = fmaxf(Mx, __shfl_xor_sync(0xffffffffu, Mx, o));
-      float den = 0.0f, acc[DPL];
-#pragma unroll
-      for (int d = 0; d < DPL; ++d) acc[d] = 0.0f;
-      for (int i0 = 0; i0 < nseg; i0 += 32) {
-        float f = 0.0f;
-        if (i0 + lane < nseg) {
-          const float2 ml = __ldcg(&p.ws_ml[base + i0 + lane]);
-          f = fast_exp2(ml.x - Mx);
-          den += f * ml.y;
-        }
-        const int cnt = min(32, nseg - i0);
-#pragma unroll 8
-        for (int i = 0; i < cnt; ++i) {
-          const float fi = __shfl_sync(0xffffffffu, f, i);
-          const float* src = p.ws_o + (base + i0 + i) * HD + lane * DPL;
-          if constexpr (DPL == 4) {
-            const float4 v = __ldcg(reinterpret_cast<const float4*>(src));
-            acc[0] += fi * v.x; acc[1] += fi * v.y; acc[2] += fi * v.z; acc[3] += fi * v.w;
-          } else {
-            const float2 v = __ldcg(reinterpret_cast<const float2*>(src));
-            acc[0] += fi * v.x; acc[1] += fi * v.y;
+          for (int i = 0; i < kTPS; ++i) {
+            if (i == i_new) {
+              Rg.k[i] = nt.k; Rg.v[i] = nt.v; Rg.ks[i] = nt.ks; Rg.vs[i] = nt.vs;
+            }
+          }
+          const long long r = (static_cast<long long>(pc.b) * p.H + pc.h) * p.Tc + row_new;
+          *reinterpret_cast<uint2*>(const_cast<uint8_t*>(p.kc) + r * (HD / 2) + sub * 8) = nt.k;
+          *reinterpret_cast<uint2*>(const_cast<uint8_t*>(p.vc) + r * (HD / 2) + sub * 8) = nt.v;
+          if (((sub * kLaneDims) & ((1 << p.blk_shift) - 1)) == 0) {
+            const_cast<float*>(p.ks)[r * nblk + sidx] = nt.ks;
+            const_cast<float*>(p.vs)[r * nblk + sidx] = nt.vs;
           }
         }
       }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) den += __shfl_xor_sync(0xffffffffu, den, o);
-      const float inv = 1.0f / den;
-      float* outp = p.out + static_cast<long long>(r) * HD + lane * DPL;
-      if constexpr (DPL == 4)
-        *reinterpret_cast<float4*>(outp) = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
-      else
-        *reinterpret_cast<float2*>(outp) = make_float2(acc[0] * inv, acc[1] * inv);
     }
-    // leave the barrier counters zero for the next launch: the last CTA out resets
-    if (threadIdx.x == 0) {
-      const int d = atomicAdd(p.grid_bar + 1, 1);
-      if (d == static_cast<int>(gridDim.x) - 1) {
-        p.grid_bar[0] = 0;
-        p.grid_bar[1] = 0;
+#ifdef NQKV_EXP_NOCOMPUTE
+    {
+      uint32_t x = 0;
+#pragma unroll
+      for (int i = 0; i < kTPS; ++i)
+        x ^= Rg.k[i].x ^ Rg.k[i].y ^ Rg.v[i].x ^ Rg.v[i].y ^ __float_as_uint(Rg.ks[i]) ^ __float_as_uint(Rg.vs[i]);
+      o2[0] ^= x;
+      l += 1.0f;
+      m = 0.0f;
+      return;
+    }
+#endif
+    // scores (log2 domain): this lane's 16 dims via the q-table
+    float sc[kTPS];
+#pragma unroll
+    for (int i = 0; i < kTPS; ++i) {
+      const uint32_t r0 = prmt(Rg.k[i].x, Rg.k[i].y, rotA);
+      const uint32_t r1 = prmt(Rg.k[i].x, Rg.k[i].y, rotB);
+      float a0 = lds_k(prmt(r0, jsel[0], 0x7604));
+      float a1 = lds_k(prmt(r0, jsel[1], 0x7614));
+      a0 += lds_k(prmt(r0, jsel[2], 0x7624));
+      a1 += lds_k(prmt(r0, jsel[3], 0x7634));
+      a0 += lds_k(prmt(r1, jsel[4], 0x7604));
+      a1 += lds_k(prmt(r1, jsel[5], 0x7614));
+      a0 += lds_k(prmt(r1, jsel[6], 0x7624));
+      a1 += lds_k(prmt(r1, jsel[7], 0x7634));
+      sc[i] = (a0 + a1) * Rg.ks[i];
+    }
+#pragma unroll
+    for (int o = 1; o < LPT; o <<= 1) {
+#pragma unroll
+      for (int i = 0; i < kTPS; ++i) sc[i] += __shfl_xor_sync(0xffffffffu, sc[i], o);
+    }
+    float mt = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < kTPS; ++i) {
+      sc[i] = (tok0 + i * G + g < pc.t1) ? sc[i] : -INFINITY;
+      mt = fmaxf(mt, sc[i]);
+    }
+#pragma unroll
+    for (int o = LPT; o < 32; o <<= 1) mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, o));
+    if (mt > m) {                     // warp-uniform; the stage has >= 1 valid token
+      const float corr = fast_exp2(m - mt);     // m = -inf -> 0
+      m = mt;
+      l *= corr;
+      const uint64_t c2 = pack2(corr, corr);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o2[j] = fmul2(o2[j], c2);
+    }
+#pragma unroll
+    for (int i = 0; i < kTPS; ++i) {
+      const float pr = fast_exp2(sc[i] - m);     // masked: exp2(-inf) = 0
+      l += pr;
+      const float w = pr * Rg.vs[i];
+      const uint64_t w2 = pack2(w, w);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        o2[k] = ffma2(lds_v(prmt(Rg.v[i].x, vsel, 0x7604 | (k << 4))), w2, o2[k]);
+        o2[4 + k] = ffma2(lds_v(prmt(Rg.v[i].y, vsel, 0x7604 | (k << 4))), w2, o2[4 + k]);
       }
     }
-  }
-}
+  };
 
-// ------------------------------------------------------- a7: split combine
-// out = sum_i e^(m_i - M) o_i / sum_i e^(m_i - M) l_i over the segments of
-// one (b, h), in segment order.  One warp per (b, h) with nseg > 1.
-struct CombineParams {
-  const int32_t* seq_lens;
-  const float* ws_o;
-  const float2* ws_ml;
-  float* out;
-  int B, H, Tc, max_segs;
-};
+  // end of piece k: sum the G token groups (common max), publish, arrive
+  auto end_piece = [&](int k) {
+    const int slot = k % R;
+    if (any) {
+#pragma unroll
+      for (int o = LPT; o < 32; o <<= 1) {
+        l += __shfl_xor_sync(0xffffffffu, l, o);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) o2[j] = fadd2(o2[j], shfl_xor64(o2[j], o));
+      }
+      if (g == 0) {
+        float* dst = s_o + (slot * NC + warp) * HD + sub * kLaneDims;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 a = unpack2(o2[2 * j]), b2 = unpack2(o2[2 * j + 1]);
+          *reinterpret_cast<float4*>(dst + 4 * j) = make_float4(a.x, a.y, b2.x, b2.y);
+        }
+      }
+    }
+    if (lane == 0) s_ml[slot * NC + warp] = make_float2(any ? m : -INFINITY, l);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(mb_done + 8 * slot);
+  };
 
-// One thread per (b, h, dim): independent loads over the segments, the
-// segment (max, sum) pairs are broadcast loads shared by the warp.
-template <int HD>
-__global__ void __launch_bounds__(256) combine_kernel(const CombineParams p) {
-  pdl_trigger();
-  pdl_wait();
-  const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const long long bh = t / HD;
-  const int d = static_cast<int>(t % HD);
-  if (bh >= static_cast<long long>(p.B) * p.H) return;
-  const int b = static_cast<int>(bh / p.H);
-  const int len = min(max(p.seq_lens[b], 0), p.Tc);
-  const int nseg = (len + kSeg - 1) / kSeg;
-  if (nseg <= 1) return;
-  const long long base = bh * p.max_segs;
-  float M = -INFINITY;
-#pragma unroll 8
-  for (int i = 0; i < nseg; ++i) M = fmaxf(M, p.ws_ml[base + i].x);
-  float den = 0.0f, acc = 0.0f;
-#pragma unroll 8
-  for (int i = 0; i < nseg; ++i) {
-    const float2 ml = p.ws_ml[base + i];
-    const float f = fast_exp2(ml.x - M);
-    den += f * ml.y;
-    acc += f * p.ws_o[(base + i) * HD + d];
+  // load cursor: (lp, ls) = next stage of this warp in piece order (index lpi)
+  Piece cp;
+  locate(g0, cp);
+  Piece lp = cp;
+  int ls = warp, lpi = 0;
+  bool lvalid = true;
+  while (ls >= nstages(lp)) {
+    if (!next_piece(lp)) { lvalid = false; break; }
+    ls = warp;
+    ++lpi;
   }
-  p.out[bh * HD + d] = acc / den;
+  StageRegs RA, RB;
+  if (lvalid) load_stage(RA, lp, ls);
+  int cpi = 0;
+  auto open_piece = [&]() {
+    set_jsel(cpi % R);
+    mbar_wait(mb_full + 8 * (cpi % R), (cpi / R) & 1);
+    reset_state();
+  };
+  open_piece();
+  TRACE(3);
+  auto step = [&](StageRegs& cur, StageRegs& nxt) -> bool {
+    // cur holds stage (lp, ls) of piece index lpi: advance the load cursor and
+    // issue the next stage's loads, then catch consumption up to cur's piece
+    const int cur_s = ls, cur_pi = lpi;
+    ls += NC;
+    while (ls >= nstages(lp)) {
+      if (!next_piece(lp)) { lvalid = false; break; }
+      ls = warp;
+      ++lpi;
+    }
+    if (lvalid) load_stage(nxt, lp, ls);
+    while (cpi < cur_pi) {
+      end_piece(cpi);
+      next_piece(cp);
+      ++cpi;
+      open_piece();
+    }
+    consume(cur, cp, cur_s);
+    return lvalid;
+  };
+  if (lvalid) {
+    for (;;) {
+      if (!step(RA, RB)) break;
+      TRACE(4);
+      if (!step(RB, RA)) break;
+    }
+  }
+  TRACE(5);
+  // close the current piece and any remaining ones (no stages of this warp)
+  for (;;) {
+    end_piece(cpi);
+    if (!next_piece(cp)) break;
+    ++cpi;
+    open_piece();
+  }
+  TRACE(6);
 }
 
 }  // namespace nqkv

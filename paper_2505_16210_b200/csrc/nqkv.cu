@@ -101,53 +101,40 @@ cudaError_t launch_pdl(void (*kern)(P), dim3 grid, dim3 block, size_t smem, cuda
 template <int HD>
 int launch_decode(const DecodeParams& p, cudaStream_t st) {
   auto kern = decode_kernel<HD, kDecodeWarps>;
-  const size_t smem_max = SmemLayout<HD, kDecodeWarps>::bytes(kMaxBatch);
-  static int blocks_per_sm = -1;
+  const size_t smem = Smem<HD, kDecodeWarps>::kBytes;
+  static bool attr_set = false;
   static std::mutex mu;
   {
     std::lock_guard<std::mutex> lk(mu);
-    if (blocks_per_sm < 0) {
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           static_cast<int>(smem_max));
+    if (!attr_set) {
+      const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 static_cast<int>(smem));
       if (e != cudaSuccess) return cuda_fail(e);
-      int n = 0;
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, kDecodeWarps * 32, smem_max);
-      if (e != cudaSuccess) return cuda_fail(e);
-      blocks_per_sm = n > 0 ? n : 1;
+      attr_set = true;
     }
   }
-  // exactly one resident CTA per SM (cooperative: the in-kernel split merge
-  // waits at a grid barrier)
-  const unsigned blocks = static_cast<unsigned>(device_sms() * blocks_per_sm);
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(blocks);
-  cfg.blockDim = dim3(kDecodeWarps * 32);
-  cfg.dynamicSmemBytes = SmemLayout<HD, kDecodeWarps>::bytes(p.B);
-  cfg.stream = st;
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  attr[1].id = cudaLaunchAttributeCooperative;
-  attr[1].val.cooperative = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 2;
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, p);
+  // one CTA per SM (the kernel needs ~140-215 KB of shared memory); CTAs
+  // beyond what the token count needs exit after the prologue
+  int sms = device_sms();
+  if (sms > kMaxGrid) sms = kMaxGrid;
+  const cudaError_t e = launch_pdl(kern, dim3(static_cast<unsigned>(sms)), dim3(kDecodeWarps * 32),
+                                   smem, st, p);
   return e == cudaSuccess ? NQKV_OK : cuda_fail(e);
 }
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
+// workspace: [B*H] int arrival counters (zero between launches) | partials
+// [kMaxGrid][2][hd + 2] fp32
 struct WsLayout {
-  size_t bar, ml, o, total;
+  size_t cnt, part, total;
 };
 
-WsLayout ws_layout(long long B, long long H, int hd, int Tc) {
-  const long long ms = (Tc + kSeg - 1) / kSeg;
+WsLayout ws_layout(long long B, long long H, int hd) {
   WsLayout w;
-  w.bar = 0;
-  w.ml = 256;
-  w.o = align_up(w.ml + static_cast<size_t>(B * H * ms) * sizeof(float2), 256);
-  w.total = align_up(w.o + static_cast<size_t>(B * H * ms) * hd * sizeof(float), 256);
+  w.cnt = 0;
+  w.part = align_up(static_cast<size_t>(B * H) * sizeof(int), 256);
+  w.total = align_up(w.part + static_cast<size_t>(kMaxGrid) * 2 * (hd + 2) * sizeof(float), 256);
   return w;
 }
 
@@ -160,13 +147,14 @@ int decode_common(const void* q, const uint8_t* k_codes, const float* k_scales,
     return NQKV_ERR_NULL;
   if (int s = check_geometry(hd, blk)) return s;
   if (B < 0 || H < 0 || Tc <= 0 || Tc % 64 || B > kMaxBatch) return NQKV_ERR_SHAPE;
+  if (static_cast<long long>(B) * H * Tc >= (1ll << 31)) return NQKV_ERR_SHAPE;
   if (!aligned16(q) || !aligned16(k_codes) || !aligned16(v_codes) || !aligned16(out) ||
-      !aligned16(k_scales) || !aligned16(v_scales))   // TMA bulk copies need 16-byte alignment
+      !aligned16(k_scales) || !aligned16(v_scales))
     return NQKV_ERR_ALIGN;
   if (k_new && (!aligned16(k_new) || !aligned16(v_new) || (new_sb % 8) || (new_sh % 8)))
     return NQKV_ERR_ALIGN;
   if (B == 0 || H == 0) return NQKV_OK;
-  const WsLayout w = ws_layout(B, H, hd, Tc);
+  const WsLayout w = ws_layout(B, H, hd);
   if (!workspace) return NQKV_ERR_NULL;
   if (!aligned16(workspace)) return NQKV_ERR_ALIGN;
   if (ws_bytes < w.total) return NQKV_ERR_WORKSPACE;
@@ -179,18 +167,18 @@ int decode_common(const void* q, const uint8_t* k_codes, const float* k_scales,
   p.v_new = static_cast<const __half*>(v_new);
   p.new_sb = new_sb; p.new_sh = new_sh;
   unsigned char* ws = static_cast<unsigned char*>(workspace);
-  p.grid_bar = reinterpret_cast<int*>(ws + w.bar);
-  p.ws_ml = reinterpret_cast<float2*>(ws + w.ml);
-  p.ws_o = reinterpret_cast<float*>(ws + w.o);
-  p.max_segs = (Tc + kSeg - 1) / kSeg;
+  p.cnt = reinterpret_cast<int*>(ws + w.cnt);
+  p.part = reinterpret_cast<float*>(ws + w.part);
   p.B = B; p.H = H; p.Tc = Tc;
   p.blk_shift = blk_shift_of(blk);
+  p.min_tokens = kMinTokensPerCta;
   p.scale_log2 = softmax_scale * 1.4426950408889634f;
   p.lv = make_levels();
   p.tab = make_bucket_tab();
   p.trace = nullptr;
 #ifdef NQKV_TRACE
-  if (const char* t = std::getenv("NQKV_TRACE_PTR")) p.trace = reinterpret_cast<unsigned long long*>(std::strtoull(t, nullptr, 0));
+  if (const char* t = std::getenv("NQKV_TRACE_PTR"))
+    p.trace = reinterpret_cast<unsigned long long*>(std::strtoull(t, nullptr, 0));
 #endif
   return hd == 64 ? launch_decode<64>(p, st) : launch_decode<128>(p, st);
 }
@@ -297,8 +285,13 @@ int nqkv_dequantize(const uint8_t* codes, const float* scales, int B, int H, int
 }
 
 size_t nqkv_decode_workspace_bytes(int B, int H, int hd, int Tc) {
-  if (B < 0 || H < 0 || Tc <= 0) return 0;
-  return ws_layout(B, H, hd, Tc).total;
+  if (B < 0 || H < 0 || Tc <= 0 || (hd != 64 && hd != 128)) return 0;
+  return ws_layout(B, H, hd).total;
+}
+
+size_t nqkv_decode_counter_bytes(int B, int H) {
+  if (B < 0 || H < 0) return 0;
+  return static_cast<size_t>(B) * H * sizeof(int);
 }
 
 int nqkv_decode_attention(const void* q, const uint8_t* k_codes, const float* k_scales,

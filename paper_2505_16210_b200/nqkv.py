@@ -35,6 +35,7 @@ _SIGS = {
                              _vp, _vp, _vp]),
     "nqkv_dequantize": (_i32, [_vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _vp]),
     "nqkv_decode_workspace_bytes": (_sz, [_i32, _i32, _i32, _i32]),
+    "nqkv_decode_counter_bytes": (_sz, [_i32, _i32]),
     "nqkv_decode_attention": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32,
                                      ctypes.c_float, _vp, _vp, _sz, _vp]),
     "nqkv_decode_step": (_i32, [_vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32,
@@ -94,6 +95,10 @@ def nqkv_thresholds() -> np.ndarray:
 
 def nqkv_decode_workspace_bytes(B: int, H: int, hd: int, Tc: int) -> int:
     return int(_lib.nqkv_decode_workspace_bytes(B, H, hd, Tc))
+
+
+def nqkv_decode_counter_bytes(B: int, H: int) -> int:
+    return int(_lib.nqkv_decode_counter_bytes(B, H))
 
 
 # --------------------------------------------------------------- device ----

@@ -90,7 +90,7 @@ def test_decode_step_argument_errors():
     assert f(*a) == -3
     a = list(args); a[18] = 8
     assert f(*a) == -5
-    a = list(args); a[10] = 5000                      # B > 4096
+    a = list(args); a[10] = 5000                      # B > kMaxBatch (1024)
     assert f(*a) == -2
 
 
@@ -105,11 +105,12 @@ def test_dequant_argument_errors():
 def test_workspace_size_grows_with_geometry():
     a = N.nqkv_decode_workspace_bytes(8, 32, 64, 2112)
     b = N.nqkv_decode_workspace_bytes(8, 32, 128, 2112)
-    c = N.nqkv_decode_workspace_bytes(8, 32, 64, 4096)
+    c = N.nqkv_decode_workspace_bytes(16, 32, 64, 2112)
     assert 0 < a < b and a < c and a % 256 == 0
-    # counters (B*H int) + ml (B*H*segs float2) + o (B*H*segs*hd float), 128-token segments
-    splits = -(-2112 // 128)
-    assert a >= 256 + 8 * 32 * splits * (8 + 64 * 4)
+    assert N.nqkv_decode_workspace_bytes(8, 32, 96, 2112) == 0        # unsupported hd
+    # per-(b, h) int32 counters first, then per-CTA split partials (o[hd], m, l)
+    assert N.nqkv_decode_counter_bytes(8, 32) == 8 * 32 * 4
+    assert a >= N.nqkv_decode_counter_bytes(8, 32) + 148 * 2 * (64 + 2) * 4
 
 
 def test_missing_library_fails_loudly(tmp_path):

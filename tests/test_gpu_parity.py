@@ -210,7 +210,7 @@ def _attn_case(N, B, H, hd, blk, lens, Tc, seed, outlier=True, dev_ws=None):
     out = N.nqkv_decode_attention(q.to(DEV), t(kc), t(ks), t(vc), t(vs),
                                   torch.tensor(lens, dtype=torch.int32, device=DEV), blk, ws)
     torch.cuda.synchronize()
-    assert torch.count_nonzero(ws[:256]) == 0                # scheduler reset
+    assert torch.count_nonzero(ws[:N.nqkv_decode_counter_bytes(B, H)]) == 0   # counters reset
     return out.cpu().numpy(), ref, (q, kc, ks, vc, vs)
 
 
@@ -258,7 +258,9 @@ def test_attention_closed_forms(N):
 
 
 def test_attention_invariances_bit_exact(N):
-    # output independent of Tc and of which heads are in the call; repeatable
+    # bit-identical across Tc and across repeated calls; a head shard of the
+    # same data is split over CTAs differently, so it may differ by fp32
+    # reassociation only (reading R7)
     B, H, hd, blk = 4, 6, 128, 64
     lens = [700, 64, 1000, 1]
     out1, ref, (q, kc, ks, vc, vs) = _attn_case(N, B, H, hd, blk, lens, 1024, seed=21)
@@ -274,7 +276,7 @@ def test_attention_invariances_bit_exact(N):
     ws3 = N.make_workspace(B, 3, hd, 1024, DEV)
     out3 = N.nqkv_decode_attention(q[:, 2:5].contiguous().to(DEV), t(kc[:, 2:5]), t(ks[:, 2:5]),
                                    t(vc[:, 2:5]), t(vs[:, 2:5]), L, blk, ws3)
-    assert np.array_equal(out1[:, 2:5], out3.cpu().numpy())
+    assert np.max(np.abs(out1[:, 2:5] - out3.cpu().numpy())) <= 1e-6
     for _ in range(3):
         again = N.nqkv_decode_attention(q.to(DEV), t(kc), t(ks), t(vc), t(vs), L, blk,
                                         N.make_workspace(B, H, hd, 1024, DEV))
@@ -365,7 +367,7 @@ def test_decode_step_fused_matches_separate_calls(N, hd, blk):
     assert np.array_equal(fk.cpu().numpy(), kc) and np.array_equal(fvs.cpu().numpy(), vs)
     ref = O.decode_attention(q.numpy(), kc, ks, vc, vs, [n + 1 for n in lens0], blk)
     assert np.max(np.abs(out_f.cpu().numpy() - ref)) <= ATOL
-    assert torch.count_nonzero(ws[:256]) == 0
+    assert torch.count_nonzero(ws[:N.nqkv_decode_counter_bytes(B, H)]) == 0
 
 
 def test_decode_runner_graph_matches_oracle(N):

@@ -1,40 +1,46 @@
-"""Debug: per-warp globaltimer trace of the decode kernel (NQKV_TRACE build)."""
+"""Debug: per-warp globaltimer trace of the decode kernel.  Builds an
+NQKV_TRACE variant of the library to /tmp and loads it via NQKV_LIB.
+    python tools/trace_decode.py [B H hd T]"""
 import os
 import sys
 
-import torch
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2505_16210_b200 import build as bld  # noqa: E402
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from synth import workloads as W  # noqa: E402
+lib = bld.build_variant("/tmp/libnqkv_trace.so", {"NQKV_TRACE": 1})
+os.environ["NQKV_LIB"] = lib
+import torch  # noqa: E402
 
-cfg = sys.argv[1] if len(sys.argv) > 1 else "c1"
-tr = torch.zeros(148 * 32 * 8, dtype=torch.int64, device="cuda")
+NW = 16
+tr = torch.zeros(148 * NW * 8, dtype=torch.int64, device="cuda")
 os.environ["NQKV_TRACE_PTR"] = str(tr.data_ptr())
 from paper_2505_16210_b200 import nqkv as N  # noqa: E402
 
-w = W.CONFIGS[cfg]
-H = 12 if cfg == "c5" else w.heads
-lens = W.seq_lens(w)
-T = int(lens.max())
-Tc = W.capacity(T + 1)
-K, V = W.layer_kv(w, 0, heads=range(H), tokens=T, device="cuda")
-cache = N.KVCache(w.batch, H, w.head_dim, Tc, w.blk, "cuda")
-z = torch.zeros(w.batch, dtype=torch.int32, device="cuda")
-cache.append(K, V, z)
-_, _, q = W.step_inputs(w, 0, 0, heads=range(H), device="cuda")
-L = (lens + 1).to("cuda")
-ws = N.make_workspace(w.batch, H, w.head_dim, Tc, "cuda")
-for _ in range(3):
+B, H, hd, T = (int(x) for x in sys.argv[1:5]) if len(sys.argv) > 4 else (8, 32, 64, 2049)
+Tc = -(-T // 64) * 64
+cache = N.KVCache(B, H, hd, Tc, 64, "cuda")
+cache.k_codes.random_(0, 256)
+cache.v_codes.random_(0, 256)
+cache.k_scales.uniform_(0.5, 2)
+cache.v_scales.uniform_(0.5, 2)
+q = torch.randn(B, H, hd, device="cuda").half()
+L = torch.full((B,), T, dtype=torch.int32, device="cuda")
+ws = N.make_workspace(B, H, hd, Tc, "cuda")
+for _ in range(5):
     tr.zero_()
+    torch.cuda._sleep(100000)
     cache.attend(q, L, ws)
     torch.cuda.synchronize()
-t = tr.view(-1, 8).cpu()
-t = t[t[:, 0] > 0]
-t0 = t[:, 0].min()
-rel = (t - t0).double() / 1000.0
-names = ["entry", "lut+sync", "pdl_wait", "prefix", "primed", "1st stage", "exit"]
-for k, n in enumerate(names):
-    col = rel[:, k]
-    col = col[t[:, k] > 0]
-    if len(col):
-        print(f"{n:10s} min {col.min():8.2f} med {col.median():8.2f} max {col.max():8.2f} us (n={len(col)})")
+t = tr.view(148, NW, 8).cpu()
+t0 = t[:, :, 0][t[:, :, 0] > 0].min()
+names = ["entry", "pdl_wait", "prefix", "tab0/full0", "1st step", "loop end", "exit"]
+for role, sl in (("consumer", slice(0, NW - 1)), ("producer", slice(NW - 1, NW))):
+    x = t[:, sl, :].reshape(-1, 8)
+    x = x[x[:, 0] > 0]
+    for k, n in enumerate(names):
+        col = x[:, k]
+        col = col[col > 0]
+        if len(col):
+            r = (col - t0).double() / 1000.0
+            print(f"{role:9s} {n:11s} min {r.min():8.2f} med {r.median():8.2f} max {r.max():8.2f} us (n={len(col)})")
