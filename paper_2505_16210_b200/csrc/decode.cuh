@@ -56,6 +56,9 @@ constexpr int kMinTokensPerCta = 512;  // below this a CTA's table build would d
 #ifndef NQKV_TPS
 #define NQKV_TPS 4
 #endif
+#ifndef NQKV_DEPTH
+#define NQKV_DEPTH 2             // register ring depth: stages in flight per consumer warp
+#endif
 #ifndef NQKV_PF
 #define NQKV_PF 0                // L2 prefetch distance in a warp's own stages (0: off; measured no gain)
 #endif
@@ -90,7 +93,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-#define TRACE(k) do { if (p.trace && lane == 0) p.trace[(blockIdx.x * NW + warp) * 8 + (k)] = gtimer(); } while (0)
+#define TRACE(k) do { if (p.trace && lane == 0) p.trace[(blockIdx.x * NW + warp) * 16 + (k)] = gtimer(); } while (0)
 #else
 #define TRACE(k) do { } while (0)
 #endif
@@ -121,9 +124,12 @@ struct Smem {
   static constexpr uint32_t kMl = kMbar + 16 * R;         // float2 [R][NC]
   static constexpr uint32_t kPc = (kMl + R * NC * 8 + 15) / 16 * 16;   // Piece [R] (producer)
   static constexpr uint32_t kO = kPc + R * 32;            // float [R][NC][HD]
-  static constexpr uint32_t kPref = kO + R * NC * HD * 4; // int [kMaxBatch + 1]
+  static constexpr uint32_t kNew = kO + R * NC * HD * 4;  // float [R][HD + 4] appended-token state
+  static constexpr uint32_t kPref = kNew + R * (HD + 4) * 4;  // int [kMaxBatch + 1]
   static constexpr uint32_t kLen = kPref + (kMaxBatch + 1) * 4 + 12;  // int [kMaxBatch]
-  static constexpr uint32_t kBytes = kLen + kMaxBatch * 4;
+  static constexpr uint32_t kOne = kLen + kMaxBatch * 4;  // u32 [kMaxBatch / 32]: fused, len == 1
+  static constexpr uint32_t kWalk = kOne + kMaxBatch / 8;  // Piece first, last; int reorder, limit
+  static constexpr uint32_t kBytes = kWalk + 64;
   static_assert(kBytes <= 227 * 1024, "decode smem over budget");
   static_assert((kTab % 16) == 0 && (kMbar % 8) == 0 && (kO % 16) == 0, "alignment");
 };
@@ -178,44 +184,24 @@ __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
   const uint32_t n = static_cast<uint32_t>((a + bytes - a0 + 15) & ~static_cast<uintptr_t>(15));
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(a0), "r"(n) : "memory");
 }
+// 64-bit address = base + a * b (one IMAD.WIDE.U32)
+__device__ __forceinline__ const void* addr_wide(const void* base, uint32_t a, uint32_t b) {
+  unsigned long long r;
+  asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(r) : "r"(a), "r"(b), "l"(reinterpret_cast<unsigned long long>(base)));
+  return reinterpret_cast<const void*>(r);
+}
 __device__ __forceinline__ float ldg_nc_f32(const float* p) {
   float r;
   asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(r) : "l"(p));
   return r;
 }
 
-// Quantize this lane's 16 dims of the appended token (fp16) exactly as
-// nqkv_quantize would: block absmax across the blk/16 adjacent lanes of the
-// block, then the code of every element.  Out of line: runs once per (b, h).
-struct NewTok {
-  uint2 k, v;
-  float ks, vs;
-};
-
-__device__ __forceinline__ uint2 quantize_lane16(const __half* src, int blk_lanes, uint32_t tab,
-                                                 float& scale) {
-  const uint4 r0 = __ldg(reinterpret_cast<const uint4*>(src));
-  const uint4 r1 = __ldg(reinterpret_cast<const uint4*>(src) + 1);
-  float s = fmaxf(absmax8(r0), absmax8(r1));
-  for (int o = 1; o < blk_lanes; o <<= 1) s = fmaxf(s, __shfl_xor_sync(0xffffffffu, s, o));
-  const float r = block_rcp(s);
-  scale = s;
-  return make_uint2(encode8c(r0, r, tab - 0x5A000000u), encode8c(r1, r, tab - 0x5A000000u));
-}
-
-__device__ __noinline__ NewTok quantize_new_token(const __half* kp, const __half* vp, int blk_lanes,
-                                                  uint32_t tab) {
-  NewTok t;
-  t.k = quantize_lane16(kp, blk_lanes, tab, t.ks);
-  t.v = quantize_lane16(vp, blk_lanes, tab, t.vs);
-  return t;
-}
-
 // One CTA-contiguous run of tokens of one (b, h): tokens [t0, t1) of a
-// sequence of length len.  Walked identically by every warp.
-struct __align__(16) Piece {
-  long long gs;   // global (b, h, t) index of t0
-  int b, h, len, t0, t1, pad;
+// sequence whose streamed length is len.  Walked identically by every warp.
+// All indices fit in 32 bits (the host enforces B*H*Tc < 2^31).
+struct Piece {
+  int gs;         // global (b, h, t) index of t0
+  int b, h, len, t0, t1;
 };
 
 // Registers of one stage: kTPS token slots of this lane.
@@ -228,8 +214,9 @@ template <int HD, int NW>
 __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const DecodeParams p) {
   using Ge = Geo<HD>;
   using Sm = Smem<HD, NW>;
-  constexpr int LPT = Ge::LPT, G = Ge::G, ST = Ge::ST, R = Ge::R;
+  constexpr int LPT = Ge::LPT, G = Ge::G, ST = Ge::ST, R = Ge::R, PPL = Ge::PPL;
   constexpr int NT = NW * 32, NC = NW - 1;
+  constexpr int Q = HD / 8;          // 4-pair quads per q-table row
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   TRACE(0);
@@ -241,10 +228,13 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const DecodeParams p
   float* s_o = reinterpret_cast<float*>(smem + Sm::kO);
   float2* s_ml = reinterpret_cast<float2*>(smem + Sm::kMl);
   Piece* s_pc = reinterpret_cast<Piece*>(smem + Sm::kPc);
+  float* s_new = reinterpret_cast<float*>(smem + Sm::kNew);
   int* s_pref = reinterpret_cast<int*>(smem + Sm::kPref);
   int* s_len = reinterpret_cast<int*>(smem + Sm::kLen);
+  const bool fused = p.k_new != nullptr;
+  const int nblk = HD >> p.blk_shift;
 
-  // ---- prologue independent of the previous kernel: levels, V LUT, barriers
+  // ---- prologue independent of the previous kernel: levels, barriers
   if (tid < 16) s_lv[tid] = p.lv.v[tid];
   if (tid < kNumBuckets) s_tab[tid] = p.tab.e[tid];
   if (tid == 0) {
@@ -266,13 +256,9 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const DecodeParams p
       lens_r[u] = (u * 32 < p.B && b < p.B) ? p.seq_lens[b] : 0;
     }
   }
-  __syncthreads();
-  for (int i = tid; i < 256 * 16; i += NT) {     // 16 B = two lane copies per store
-    const int e = i >> 4;
-    const float lo = s_lv[e & 15], hi = s_lv[e >> 4];
-    *reinterpret_cast<float4*>(smem + Sm::kV + e * 256 + (i & 15) * 16) = make_float4(lo, hi, lo, hi);
-  }
-  // ---- per-batch lengths and token prefix: tokens(b) = H * len_b
+  // ---- per-batch streamed lengths and token prefix: tokens(b) = H * len'_b.
+  // Fused step: the appended row (len - 1) is not streamed; the producer
+  // quantises it and folds it into the piece merge (s_len holds len').
   if (warp == 0) {
     int carry = 0;
     if (lane == 0) s_pref[0] = 0;
@@ -281,8 +267,11 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const DecodeParams p
       if (u * 32 >= p.B) break;
       const int b = u * 32 + lane;
       int n = 0;
+      const int raw = b < p.B ? min(max(lens_r[u], 0), p.Tc) : 0;
+      const unsigned one = __ballot_sync(0xffffffffu, fused && raw == 1);
+      if (lane == 0) reinterpret_cast<uint32_t*>(smem + Sm::kOne)[u] = one;
       if (b < p.B) {
-        const int len = min(max(lens_r[u], 0), p.Tc);
+        const int len = fused ? max(raw - 1, 0) : raw;
         s_len[b] = len;
         n = p.H * len;
       }
@@ -297,22 +286,98 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const DecodeParams p
   }
   __syncthreads();
   TRACE(2);
-  const long long N = s_pref[p.B];
-  // empty sequences: out = 0 (reading R12); strided over the grid
-  for (long long i = static_cast<long long>(blockIdx.x) * NT + tid; i < static_cast<long long>(p.B) * p.H * HD;
-       i += static_cast<long long>(gridDim.x) * NT) {
-    if (s_len[i / (static_cast<long long>(p.H) * HD)] == 0) p.out[i] = 0.0f;
+  const int N = s_pref[p.B];
+
+  // ---- the appended token (fused step), warp-wide: lane owns pairs j = lane
+  // + 32u (dims 2j, 2j+1).  Quantised exactly as quantize_kernel does and
+  // written to the cache; returns its dequantised value and (from the q-table
+  // in ring slot `slot`, if >= 0) its score in the log2 domain.
+  const uint32_t tabc = kSmemWindow + Sm::kTab - 0x5A000000u;
+  auto new_token = [&](int b, int h, int slot, float (&vh)[2 * PPL]) -> float {
+    const long long bh = static_cast<long long>(b) * p.H + h;
+    const long long src = static_cast<long long>(b) * p.new_sb + static_cast<long long>(h) * p.new_sh;
+    const int row = min(s_len[b], p.Tc - 1);                      // = len - 1
+    const long long r = bh * p.Tc + row;
+    const int bp = 1 << (p.blk_shift - 1);                         // pairs per block
+    float xk[2 * PPL], xv[2 * PPL], sk[PPL], sv[PPL];
+#pragma unroll
+    for (int u = 0; u < PPL; ++u) {
+      const int j = lane + 32 * u;
+      const float2 fk = __half22float2(__ldg(reinterpret_cast<const __half2*>(p.k_new + src) + j));
+      const float2 fv = __half22float2(__ldg(reinterpret_cast<const __half2*>(p.v_new + src) + j));
+      xk[2 * u] = fk.x; xk[2 * u + 1] = fk.y;
+      xv[2 * u] = fv.x; xv[2 * u + 1] = fv.y;
+      sk[u] = fmaxf(fabsf(fk.x), fabsf(fk.y));
+      sv[u] = fmaxf(fabsf(fv.x), fabsf(fv.y));
+    }
+    if (bp > 32) {                       // one block spans both halves (hd 128, blk 128)
+      sk[0] = sk[PPL - 1] = fmaxf(sk[0], sk[PPL - 1]);
+      sv[0] = sv[PPL - 1] = fmaxf(sv[0], sv[PPL - 1]);
+    }
+    const int span = min(bp, 32);
+#pragma unroll
+    for (int u = 0; u < PPL; ++u) {
+      for (int o = 1; o < span; o <<= 1) {
+        sk[u] = fmaxf(sk[u], __shfl_xor_sync(0xffffffffu, sk[u], o));
+        sv[u] = fmaxf(sv[u], __shfl_xor_sync(0xffffffffu, sv[u], o));
+      }
+    }
+    float part = 0.0f;
+#pragma unroll
+    for (int u = 0; u < PPL; ++u) {
+      const int j = lane + 32 * u;
+      const float rk = block_rcp(sk[u]), rv = block_rcp(sv[u]);
+      const uint32_t ck = nf4_code_c(__fmul_rn(xk[2 * u], rk), tabc) |
+                          (nf4_code_c(__fmul_rn(xk[2 * u + 1], rk), tabc) << 4);
+      const uint32_t cvl = nf4_code_c(__fmul_rn(xv[2 * u], rv), tabc);
+      const uint32_t cvh = nf4_code_c(__fmul_rn(xv[2 * u + 1], rv), tabc);
+      const_cast<uint8_t*>(p.kc)[r * (HD / 2) + j] = static_cast<uint8_t>(ck);
+      const_cast<uint8_t*>(p.vc)[r * (HD / 2) + j] = static_cast<uint8_t>(cvl | (cvh << 4));
+      if (((2 * j) & ((1 << p.blk_shift) - 1)) == 0) {
+        const_cast<float*>(p.ks)[r * nblk + ((2 * j) >> p.blk_shift)] = sk[u];
+        const_cast<float*>(p.vs)[r * nblk + ((2 * j) >> p.blk_shift)] = sv[u];
+      }
+      vh[2 * u] = __fmul_rn(sv[u], s_lv[cvl]);
+      vh[2 * u + 1] = __fmul_rn(sv[u], s_lv[cvh]);
+      if (slot >= 0) {
+        const uint32_t off = HD == 64 ? (slot >> 1) * 0x10000u + (slot & 1) * 128u : slot * 0x10000u;
+        part += reinterpret_cast<const float*>(smem + Sm::kK + off + ck * 256)[j] * sk[u];
+      }
+    }
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    return part;
+  };
+
+  // ---- empty sequences (out = 0, reading R12) and, in a fused step,
+  // sequences whose only token is the appended one (out = its value)
+  const uint32_t* s_one = reinterpret_cast<const uint32_t*>(smem + Sm::kOne);
+  auto single = [&](int b) { return (s_one[b >> 5] >> (b & 31)) & 1u; };
+  for (int i = blockIdx.x * NT + tid; i < p.B * p.H * HD; i += gridDim.x * NT) {
+    const int b = i / (p.H * HD);
+    if (s_len[b] == 0 && !single(b)) p.out[i] = 0.0f;
+  }
+  if (fused) {
+    for (int bh = blockIdx.x * NW + warp; bh < p.B * p.H; bh += gridDim.x * NW) {
+      const int b = bh / p.H, h = bh - b * p.H;
+      if (!single(b)) continue;
+      float vh[2 * PPL];
+      new_token(b, h, -1, vh);
+#pragma unroll
+      for (int u = 0; u < PPL; ++u)
+        *reinterpret_cast<float2*>(p.out + static_cast<long long>(bh) * HD + 2 * (lane + 32 * u)) =
+            make_float2(vh[2 * u], vh[2 * u + 1]);
+    }
   }
   if (N == 0) return;
-  const int C = static_cast<int>(min(static_cast<long long>(gridDim.x),
-                                     max(1ll, (N + p.min_tokens - 1) / p.min_tokens)));
+  const int C = min(static_cast<int>(gridDim.x), max(1, (N + p.min_tokens - 1) / p.min_tokens));
   if (static_cast<int>(blockIdx.x) >= C) return;
   const int cta = blockIdx.x;
-  const long long g0 = static_cast<long long>(cta) * N / C;
-  const long long g1 = static_cast<long long>(cta + 1) * N / C;
+  const int g0 = static_cast<int>(static_cast<long long>(cta) * N / C);
+  const int g1 = static_cast<int>(static_cast<long long>(cta + 1) * N / C);
 
   // ---- piece walking (identical in every warp)
-  auto locate = [&](long long g, Piece& pc) {
+  auto locate = [&](int g, Piece& pc) {
     int lo = 0, hi = p.B;                 // largest b with pref[b] <= g (pref[B] > g)
     while (hi - lo > 1) {
       const int mid = (lo + hi) >> 1;
@@ -320,15 +385,15 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const DecodeParams p
     }
     pc.b = lo;
     pc.len = s_len[lo];
-    const long long off = g - s_pref[lo];
-    pc.h = static_cast<int>(off / pc.len);
-    pc.t0 = static_cast<int>(off - static_cast<long long>(pc.h) * pc.len);
+    const int off = g - s_pref[lo];
+    pc.h = off / pc.len;
+    pc.t0 = off - pc.h * pc.len;
     pc.gs = g;
-    pc.t1 = static_cast<int>(min(static_cast<long long>(pc.len), pc.t0 + (g1 - g)));
+    pc.t1 = min(pc.len, pc.t0 + (g1 - g));
   };
-  auto next_piece = [&](Piece& pc) -> bool {
-    const long long g = pc.gs + (pc.t1 - pc.t0);
-    if (g >= g1) return false;
+  auto next_piece_to = [&](Piece& pc, int lim) -> bool {
+    const int g = pc.gs + (pc.t1 - pc.t0);
+    if (g >= lim) return false;
     if (pc.h + 1 < p.H) {
       ++pc.h;
     } else {
@@ -338,189 +403,330 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const DecodeParams p
     }
     pc.t0 = 0;
     pc.gs = g;
-    pc.t1 = static_cast<int>(min(static_cast<long long>(pc.len), g1 - g));
+    pc.t1 = min(pc.len, g1 - g);
     return true;
   };
-
-  // L2 prefetch of rows [r0, r1) of (b, h) -- codes and scales of K and V
-  const int nblk_ = HD >> p.blk_shift;
-  auto prefetch_rows = [&](long long bh, int r0, int r1) {
-    if (r1 <= r0) return;
-    const long long row = bh * p.Tc + r0;
-    const uint32_t n = static_cast<uint32_t>(r1 - r0);
-    prefetch_l2(p.kc + row * (HD / 2), n * (HD / 2));
-    prefetch_l2(p.vc + row * (HD / 2), n * (HD / 2));
-    prefetch_l2(p.ks + row * nblk_, n * nblk_ * 4);
-    prefetch_l2(p.vs + row * nblk_, n * nblk_ * 4);
+  // Processing order.  If the range's last piece is split with the next CTA
+  // it is processed FIRST, so that both cross-CTA partials of this CTA are
+  // published early and the last piece processed (normally a whole sequence)
+  // needs no cross-CTA merge at the end of the kernel.  Order: [last], first,
+  // first+1, ..., up to (not including) the moved last piece.
+  // (kept in shared memory: the walkers run rarely, registers are scarce)
+  Piece* s_walk = reinterpret_cast<Piece*>(smem + Sm::kWalk);
+  int* s_wi = reinterpret_cast<int*>(smem + Sm::kWalk + 48);
+  if (tid == 0) {
+    Piece pf, pl;
+    locate(g0, pf);
+    locate(g1 - 1, pl);
+    locate(max(g0, g1 - 1 - pl.t0), pl);
+    const bool ro = pl.gs != pf.gs && pl.t1 < pl.len;
+    s_walk[0] = pf;
+    s_walk[1] = pl;
+    s_wi[0] = ro;
+    s_wi[1] = ro ? pl.gs : g1;
+  }
+  __syncthreads();
+  TRACE(3);
+  auto walk_first = [&](Piece& pc) { pc = s_walk[s_wi[0] ? 1 : 0]; };
+  auto walk_next = [&](Piece& pc, int k) -> bool {   // k = index of pc in processing order
+    if (s_wi[0] && k == 0) { pc = s_walk[0]; return true; }
+    return next_piece_to(pc, s_wi[1]);
   };
-
-  // ---- table of piece 0, built by all threads (thread: pair quad tid % Q)
-  {
-    Piece p0;
-    locate(g0, p0);
-    constexpr int Q = HD / 8;
-    const long long bh = static_cast<long long>(p0.b) * p.H + p0.h;
-    const uint4 qraw = __ldg(reinterpret_cast<const uint4*>(p.q + bh * HD) + (tid % Q));
+  auto nstages = [&](const Piece& pc) { return (pc.t1 - pc.t0 + ST - 1) / ST; };
+  auto rowbase = [&](const Piece& pc) { return (pc.b * p.H + pc.h) * p.Tc; };
+  // q-table slot offset (bytes from kK): hd 64 -> block r >> 1, half r & 1;
+  // hd 128 -> block r
+  auto slot_off = [](int r) -> uint32_t {
+    return HD == 64 ? static_cast<uint32_t>(r >> 1) * 0x10000u + static_cast<uint32_t>(r & 1) * 128u
+                    : static_cast<uint32_t>(r) * 0x10000u;
+  };
+  // q of pair quad qd of (b, h), times softmax_scale * log2(e): even dims
+  // (q_{2j}) in a[], odd dims (q_{2j+1}) in b[]
+  auto load_quad = [&](const Piece& pc, int qd) -> uint4 {
+    const long long bh = static_cast<long long>(pc.b) * p.H + pc.h;
+    return __ldg(reinterpret_cast<const uint4*>(p.q + bh * HD) + qd);
+  };
+  auto split_quad = [&](const uint4 raw, float (&a)[4], float (&b)[4]) {
     __half2 h2[4];
-    memcpy(h2, &qraw, 16);
-    float qa[8];
+    memcpy(h2, &raw, 16);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const float2 f = __half22float2(h2[k]);
-      qa[2 * k] = f.x * p.scale_log2;
-      qa[2 * k + 1] = f.y * p.scale_log2;
+      a[k] = f.x * p.scale_log2;
+      b[k] = f.y * p.scale_log2;
     }
+  };
+
+  // ---- consumer lane geometry and the first stage's loads (in flight during
+  // the table-0 build)
+  const int g = lane / LPT, sub = lane % LPT;
+  const int sidx = (sub * kLaneDims) >> p.blk_shift;
+  // rows of (b, h) start at row index rb = (b*H + h)*Tc (32-bit)
+  auto load_stage = [&](StageRegs& Rg, int rb, int tok0, int t1) {
+#ifdef NQKV_EXP_NOLOAD
+#pragma unroll
+    for (int i = 0; i < kTPS; ++i) {
+      Rg.k[i] = make_uint2(0x12345678u * (i + 1) + tok0, 0x9abcdef0u + lane);
+      Rg.v[i] = make_uint2(0x31415926u * (i + 3) + tok0, 0x27182818u + lane);
+      Rg.ks[i] = 1.0f;
+      Rg.vs[i] = 0.5f;
+    }
+    return;
+#endif
+    const int rlast = rb + t1 - 1;
+    const int r0 = rb + tok0 + g;
+#pragma unroll
+    for (int i = 0; i < kTPS; ++i) {
+      const uint32_t r = static_cast<uint32_t>(min(r0 + i * G, rlast));   // clamp: valid rows
+      const uint32_t cw = r * (HD / 16) + static_cast<uint32_t>(sub);     // 8-byte word index
+      const uint32_t sw = r * static_cast<uint32_t>(nblk) + static_cast<uint32_t>(sidx);
+      Rg.k[i] = ldg_stream_64(addr_wide(p.kc, cw, 8));
+      Rg.v[i] = ldg_stream_64(addr_wide(p.vc, cw, 8));
+      Rg.ks[i] = ldg_nc_f32(static_cast<const float*>(addr_wide(p.ks, sw, 4)));
+      Rg.vs[i] = ldg_nc_f32(static_cast<const float*>(addr_wide(p.vs, sw, 4)));
+    }
+  };
+  // q of piece 0 first: its table is the first thing the consumers need
+  Piece p0;
+  walk_first(p0);
+  const uint4 q0 = load_quad(p0, tid % Q);
+  // load cursor (piece lp, stage ls, piece index lpi): one stage ahead of
+  // consumption, across piece boundaries
+  Piece lp = p0;
+  int ls = warp, lpi = 0;
+  bool lvalid = warp < NC;
+  int lrb = 0;
+  if (lvalid) {
+    while (ls >= nstages(lp)) {
+      if (!walk_next(lp, lpi)) { lvalid = false; break; }
+      ls = warp;
+      ++lpi;
+    }
+    if (lvalid) lrb = rowbase(lp);
+  }
+  // register ring: buffer d holds the stage at (tok0 mtok[d], piece end mt1[d],
+  // piece index mpi[d]); refilled with the cursor's next stage once consumed
+  constexpr int D = NQKV_DEPTH;
+  StageRegs RG[D];
+  int mtok[D], mt1[D], mpi[D];
+  bool has[D];
+  auto fill = [&](int d) -> bool {
+    if (!lvalid) return false;
+    mtok[d] = lp.t0 + ls * ST;
+    mt1[d] = lp.t1;
+    mpi[d] = lpi;
+    load_stage(RG[d], lrb, mtok[d], mt1[d]);
+    ls += NC;
+    if (ls >= nstages(lp)) {
+      do {
+        if (!walk_next(lp, lpi)) { lvalid = false; break; }
+        ls = warp;
+        ++lpi;
+      } while (ls >= nstages(lp));
+      if (lvalid) lrb = rowbase(lp);
+    }
+    return true;
+  };
+#pragma unroll
+  for (int d = 0; d < D - 1; ++d) has[d] = fill(d);
+  has[D - 1] = false;
+
+  // ---- table of piece 0, built by all threads (thread: pair quad tid % Q);
+  // T[e][j] = RN(c q_{2j} L[e & 15]) + RN(c q_{2j+1} L[e >> 4]) everywhere
+  TRACE(4);
+  for (int i = tid; i < 256 * 16; i += NT) {     // V LUT; 16 B = two lane copies per store
+    const int e = i >> 4;
+    const float lo = s_lv[e & 15], hi = s_lv[e >> 4];
+    *reinterpret_cast<float4*>(smem + Sm::kV + e * 256 + (i & 15) * 16) = make_float4(lo, hi, lo, hi);
+  }
+  TRACE(5);
+  {
+    float a[4], b[4];
+    split_quad(q0, a, b);
     for (int e = tid / Q; e < 256; e += NT / Q) {
       const float lo = s_lv[e & 15], hi = s_lv[e >> 4];
       *reinterpret_cast<float4*>(smem + Sm::kK + e * 256 + (tid % Q) * 16) =
-          make_float4(fmaf(qa[1], hi, qa[0] * lo), fmaf(qa[3], hi, qa[2] * lo),
-                      fmaf(qa[5], hi, qa[4] * lo), fmaf(qa[7], hi, qa[6] * lo));
+          make_float4(a[0] * lo + b[0] * hi, a[1] * lo + b[1] * hi, a[2] * lo + b[2] * hi, a[3] * lo + b[3] * hi);
     }
   }
+  TRACE(6);
   __syncthreads();
+  TRACE(7);
 
   if (warp == NC) {
     // ================================================================ producer
-    // q-table slot r: hd 64 -> block r >> 1, half r & 1; hd 128 -> block r
-    auto build = [&](int slot, const float (&qa)[2 * Ge::PPL]) {
+    // build: lane owns quad qd = lane % Q for rows with hi nibble = lane / Q
+    // (mod 32 / Q); A[lo] = c q_even L[lo] for the quad (fp32x2 pairs)
+    auto build = [&](int slot, const uint4 qraw) {
+      float a[4], b[4];
+      split_quad(qraw, a, b);
+      const int qd = lane % Q;
+      uint64_t A01[16], A23[16];
 #pragma unroll
-      for (int u = 0; u < Ge::PPL; ++u) {
-        const int j = lane + 32 * u;
-        const uint32_t base = Sm::kK + (HD == 64 ? (slot >> 1) * 0x10000 + (slot & 1) * 128
-                                                 : slot * 0x10000) + j * 4;
-        float A[16], Bv[16];
+      for (int c = 0; c < 16; ++c) {
+        const float L = s_lv[c];
+        A01[c] = pack2(a[0] * L, a[1] * L);
+        A23[c] = pack2(a[2] * L, a[3] * L);
+      }
+      unsigned char* base = smem + Sm::kK + slot_off(slot) + qd * 16;
+#pragma unroll 1
+      for (int hi = lane / Q; hi < 16; hi += 32 / Q) {
+        const float L = s_lv[hi];
+        const uint64_t B01 = pack2(b[0] * L, b[1] * L), B23 = pack2(b[2] * L, b[3] * L);
+        unsigned char* row = base + hi * 16 * 256;
 #pragma unroll
-        for (int c = 0; c < 16; ++c) {
-          A[c] = qa[2 * u] * s_lv[c];
-          Bv[c] = qa[2 * u + 1] * s_lv[c];
+        for (int lo = 0; lo < 16; ++lo) {
+          const float2 t01 = unpack2(fadd2(A01[lo], B01)), t23 = unpack2(fadd2(A23[lo], B23));
+          *reinterpret_cast<float4*>(row + lo * 256) = make_float4(t01.x, t01.y, t23.x, t23.y);
         }
-        float* t = reinterpret_cast<float*>(smem + base);
-#pragma unroll
-        for (int e = 0; e < 256; ++e) t[e * 64] = A[e & 15] + Bv[e >> 4];
       }
     };
-    auto load_q = [&](const Piece& pc, float (&qa)[2 * Ge::PPL]) {
-      const long long bh = static_cast<long long>(pc.b) * p.H + pc.h;
+    // appended-token state of piece k (fused step, the sequence's last piece):
+    // score and value into s_new[k % R]; else score = -inf
+    auto new_state = [&](int k, const Piece& pc) {
+      float* st = s_new + (k % R) * (HD + 4);
+      if (fused && pc.t1 == pc.len) {
+        float vh[2 * PPL];
+        const float sc = new_token(pc.b, pc.h, k % R, vh);
 #pragma unroll
-      for (int u = 0; u < Ge::PPL; ++u) {
-        const __half2 h2 = __ldg(reinterpret_cast<const __half2*>(p.q + bh * HD) + lane + 32 * u);
-        const float2 f = __half22float2(h2);
-        qa[2 * u] = f.x * p.scale_log2;
-        qa[2 * u + 1] = f.y * p.scale_log2;
+        for (int u = 0; u < PPL; ++u)
+          *reinterpret_cast<float2*>(st + 2 * (lane + 32 * u)) = make_float2(vh[2 * u], vh[2 * u + 1]);
+        if (lane == 0) st[HD] = sc;
+      } else if (lane == 0) {
+        st[HD] = -INFINITY;
       }
     };
-    constexpr int DL = HD / 32;
-    // merge piece k's NC consumer states (ring slot k % R): output or partial
+    // this lane's output dims: 2j, 2j+1 for j = lane + 32u
+    auto dim = [&](int u) { return 2 * (lane + 32 * u); };
+    // merge piece k's NC consumer states (+ appended token): output or partial
     auto merge = [&](int k) {
       const int slot = k % R;
       const Piece pc = s_pc[slot];
-      float M = -INFINITY;
-      for (int w = 0; w < NC; ++w) M = fmaxf(M, s_ml[slot * NC + w].x);
-      float den = 0.0f, acc[DL];
+      const float* st = s_new + slot * (HD + 4);
+      const float snew = st[HD];
+      float mw[NC];
+      float M = snew;
 #pragma unroll
-      for (int d = 0; d < DL; ++d) acc[d] = 0.0f;
       for (int w = 0; w < NC; ++w) {
-        const float2 ml = s_ml[slot * NC + w];
-        if (ml.x == -INFINITY) continue;                 // consumer saw no token
-        const float f = fast_exp2(ml.x - M);
-        den += f * ml.y;
-        const float* o = s_o + (slot * NC + w) * HD + lane * DL;
+        mw[w] = s_ml[slot * NC + w].x;
+        M = fmaxf(M, mw[w]);
+      }
+      float den = 0.0f, acc[2 * PPL];
 #pragma unroll
-        for (int d = 0; d < DL; ++d) acc[d] = fmaf(f, o[d], acc[d]);
+      for (int d = 0; d < 2 * PPL; ++d) acc[d] = 0.0f;
+#pragma unroll
+      for (int w = 0; w < NC; ++w) {
+        const float f = fast_exp2(mw[w] - M);           // consumer without tokens: -inf -> 0
+        den = fmaf(f, s_ml[slot * NC + w].y, den);
+        const float* o = s_o + (slot * NC + w) * HD;
+#pragma unroll
+        for (int u = 0; u < PPL; ++u) {
+          const float2 x = *reinterpret_cast<const float2*>(o + dim(u));
+          acc[2 * u] = fmaf(f, x.x, acc[2 * u]);
+          acc[2 * u + 1] = fmaf(f, x.y, acc[2 * u + 1]);
+        }
+      }
+      if (snew != -INFINITY) {
+        const float f = fast_exp2(snew - M);
+        den += f;
+#pragma unroll
+        for (int u = 0; u < PPL; ++u) {
+          const float2 x = *reinterpret_cast<const float2*>(st + dim(u));
+          acc[2 * u] = fmaf(f, x.x, acc[2 * u]);
+          acc[2 * u + 1] = fmaf(f, x.y, acc[2 * u + 1]);
+        }
       }
       const long long bh = static_cast<long long>(pc.b) * p.H + pc.h;
       if (pc.t0 == 0 && pc.t1 == pc.len) {
         const float inv = 1.0f / den;
 #pragma unroll
-        for (int d = 0; d < DL; ++d) p.out[bh * HD + lane * DL + d] = acc[d] * inv;
+        for (int u = 0; u < PPL; ++u)
+          *reinterpret_cast<float2*>(p.out + bh * HD + dim(u)) = make_float2(acc[2 * u] * inv, acc[2 * u + 1] * inv);
         return;
       }
-      // partial piece: slot 0 = this CTA's first piece, 1 = its last
-      float* part = p.part + (static_cast<long long>(cta) * 2 + (k == 0 ? 0 : 1)) * (HD + 2);
+      // partial piece: slot 0 = this CTA's first piece (starts at g0), 1 = its last.  The
+      // counter's acq_rel RMW publishes the partial (after the warp barrier)
+      // and, for the last arriver, acquires everyone else's.
+      float* part = p.part + (static_cast<long long>(cta) * 2 + (pc.gs == g0 ? 0 : 1)) * (HD + 2);
 #pragma unroll
-      for (int d = 0; d < DL; ++d) part[lane * DL + d] = acc[d];
+      for (int u = 0; u < PPL; ++u)
+        *reinterpret_cast<float2*>(part + dim(u)) = make_float2(acc[2 * u], acc[2 * u + 1]);
       if (lane == 0) {
         part[HD] = M;
         part[HD + 1] = den;
       }
-      __threadfence();
       __syncwarp();
-      const long long st = pc.gs - pc.t0;                           // global index of token 0
-      const int ca = static_cast<int>(((st + 1) * C - 1) / N);
-      const int cb = static_cast<int>(((st + pc.len) * C - 1) / N);
+      const int st0 = pc.gs - pc.t0;                                // global index of token 0
+      const int ca = static_cast<int>((static_cast<long long>(st0 + 1) * C - 1) / N);
+      const int cb = static_cast<int>((static_cast<long long>(st0 + pc.len) * C - 1) / N);
       int last = 0;
-      if (lane == 0) last = atomicAdd(p.cnt + bh, 1) == cb - ca;
+      if (lane == 0) last = atom_add_acq_rel(p.cnt + bh, 1) == cb - ca;
       last = __shfl_sync(0xffffffffu, last, 0);
       if (!last) return;
-      __threadfence();
       float Mx = -INFINITY;
       for (int c = ca; c <= cb; ++c) {
-        const int sl = (c == ca && static_cast<long long>(c) * N / C != st) ? 1 : 0;
+        const int sl = (c == ca && static_cast<long long>(c) * N / C != st0) ? 1 : 0;
         Mx = fmaxf(Mx, __ldcg(p.part + (static_cast<long long>(c) * 2 + sl) * (HD + 2) + HD));
       }
-      float dsum = 0.0f, o[DL];
+      float dsum = 0.0f, o[2 * PPL];
 #pragma unroll
-      for (int d = 0; d < DL; ++d) o[d] = 0.0f;
+      for (int d = 0; d < 2 * PPL; ++d) o[d] = 0.0f;
       for (int c = ca; c <= cb; ++c) {
-        const int sl = (c == ca && static_cast<long long>(c) * N / C != st) ? 1 : 0;
+        const int sl = (c == ca && static_cast<long long>(c) * N / C != st0) ? 1 : 0;
         const float* pp = p.part + (static_cast<long long>(c) * 2 + sl) * (HD + 2);
         const float fc = fast_exp2(__ldcg(pp + HD) - Mx);
         dsum += fc * __ldcg(pp + HD + 1);
 #pragma unroll
-        for (int d = 0; d < DL; ++d) o[d] = fmaf(fc, __ldcg(pp + lane * DL + d), o[d]);
+        for (int u = 0; u < PPL; ++u) {
+          const float2 x = __ldcg(reinterpret_cast<const float2*>(pp + dim(u)));
+          o[2 * u] = fmaf(fc, x.x, o[2 * u]);
+          o[2 * u + 1] = fmaf(fc, x.y, o[2 * u + 1]);
+        }
       }
       const float inv = 1.0f / dsum;
 #pragma unroll
-      for (int d = 0; d < DL; ++d) p.out[bh * HD + lane * DL + d] = o[d] * inv;
+      for (int u = 0; u < PPL; ++u)
+        *reinterpret_cast<float2*>(p.out + bh * HD + dim(u)) = make_float2(o[2 * u] * inv, o[2 * u + 1] * inv);
       if (lane == 0) p.cnt[bh] = 0;
     };
 
-    Piece pc;
-    locate(g0, pc);
-    float qa[2 * Ge::PPL], qn[2 * Ge::PPL];
-#pragma unroll
-    for (int u = 0; u < 2 * Ge::PPL; ++u) qa[u] = 0.0f;
+    Piece pc = p0;
+    if (lane == 0) s_pc[0] = pc;
+    new_state(0, pc);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(mb_full);
+    TRACE(8);
     Piece nx = pc;
-    bool more = next_piece(nx);
-    if (more) load_q(nx, qn);
+    bool more = walk_next(nx, 0);
+    uint4 qn = more ? load_quad(nx, lane % Q) : make_uint4(0, 0, 0, 0);
     int k = 0;
-    for (;;) {
+    while (more) {
+      pc = nx;
+      ++k;
+      const uint4 qc = qn;
+      more = walk_next(nx, k);
+      if (more) qn = load_quad(nx, lane % Q);
       if (k >= R) {
         mbar_wait(mb_done + 8 * ((k - R) % R), ((k - R) / R) & 1);
         merge(k - R);
       }
+      build(k % R, qc);
+      __syncwarp();
       if (lane == 0) s_pc[k % R] = pc;
-      if (k > 0) {
-        build(k % R, qa);
-        // the first stage of every consumer in this piece: L2 prefetch
-        if (lane == 0)
-          prefetch_rows(static_cast<long long>(pc.b) * p.H + pc.h, pc.t0, min(pc.t1, pc.t0 + NC * ST));
-      }
+      new_state(k, pc);
       __syncwarp();
       if (lane == 0) mbar_arrive(mb_full + 8 * (k % R));
-      if (k == 0) TRACE(3);
-      if (!more) break;
-      pc = nx;
-      ++k;
-#pragma unroll
-      for (int u = 0; u < 2 * Ge::PPL; ++u) qa[u] = qn[u];
-      more = next_piece(nx);
-      if (more) load_q(nx, qn);
     }
-    TRACE(5);
+    TRACE(9);
     for (int j = max(0, k + 1 - R); j <= k; ++j) {
       mbar_wait(mb_done + 8 * (j % R), (j / R) & 1);
       merge(j);
     }
-    TRACE(6);
+    TRACE(10);
     return;
   }
 
   // ================================================================ consumers
-  const int g = lane / LPT, sub = lane % LPT;
-  const int nblk = HD >> p.blk_shift;
-  const int sidx = (sub * kLaneDims) >> p.blk_shift;
-  const int blk_lanes = (1 << p.blk_shift) / kLaneDims;
   const int rho = (g + (HD == 128 ? 4 * (sub >> 2) : 0)) & 7;     // bank rotation
   uint32_t rotA = 0, rotB = 0;
 #pragma unroll
@@ -529,14 +735,10 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const DecodeParams p
     rotB |= static_cast<uint32_t>((i + 4 + rho) & 7) << (4 * i);
   }
   const uint32_t vsel = static_cast<uint32_t>(lane) * 8u;
-  const bool fused = p.k_new != nullptr;
-  const uint32_t tab = kSmemWindow + Sm::kTab;
-  auto nstages = [&](const Piece& pc) { return (pc.t1 - pc.t0 + ST - 1) / ST; };
 
   uint32_t jsel[8];
   auto set_jsel = [&](int slot) {
-    const uint32_t add = HD == 64 ? (static_cast<uint32_t>(slot >> 1) << 16) | ((slot & 1) * 128u)
-                                  : static_cast<uint32_t>(slot) << 16;
+    const uint32_t add = slot_off(slot);
 #pragma unroll
     for (int k = 0; k < 8; ++k) jsel[k] = static_cast<uint32_t>(sub * 8 + ((k + rho) & 7)) * 4u + add;
   };
@@ -552,65 +754,8 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const DecodeParams p
     any = false;
   };
 
-  auto load_stage = [&](StageRegs& Rg, const Piece& pc, int s) {
-    const long long bh = static_cast<long long>(pc.b) * p.H + pc.h;
-    const int tok0 = pc.t0 + s * ST;
-    if (NQKV_PF > 0 && lane == 0) {   // L2 prefetch NQKV_PF of this warp's stages ahead
-      const int first = s == warp ? 1 : NQKV_PF;
-      for (int d = first; d <= NQKV_PF; ++d) {
-        const int r0 = tok0 + d * NC * ST;
-        if (r0 >= pc.t1) break;
-        prefetch_rows(bh, r0, min(pc.t1, r0 + ST));
-      }
-    }
-#ifdef NQKV_EXP_NOLOAD
-#pragma unroll
-    for (int i = 0; i < kTPS; ++i) {
-      Rg.k[i] = make_uint2(0x12345678u * (i + 1) + tok0, 0x9abcdef0u + lane);
-      Rg.v[i] = make_uint2(0x31415926u * (i + 3) + tok0, 0x27182818u + lane);
-      Rg.ks[i] = 1.0f;
-      Rg.vs[i] = 0.5f;
-    }
-    return;
-#endif
-#pragma unroll
-    for (int i = 0; i < kTPS; ++i) {
-      const int row = min(tok0 + i * G + g, pc.t1 - 1);     // clamp: masked rows read valid data
-      const long long r = bh * p.Tc + row;
-      Rg.k[i] = ldg_stream_64(p.kc + r * (HD / 2) + sub * 8);
-      Rg.v[i] = ldg_stream_64(p.vc + r * (HD / 2) + sub * 8);
-      Rg.ks[i] = ldg_nc_f32(p.ks + r * nblk + sidx);
-      Rg.vs[i] = ldg_nc_f32(p.vs + r * nblk + sidx);
-    }
-  };
-
-  auto consume = [&](StageRegs& Rg, const Piece& pc, int s) {
-    const int tok0 = pc.t0 + s * ST;
+  auto consume = [&](const StageRegs& Rg, int tok0, int t1) {
     any = true;
-    if (fused) {
-      const int row_new = pc.len - 1;
-      if (row_new >= tok0 && row_new < tok0 + ST && row_new < pc.t1) {   // warp-uniform
-        const int rn = row_new - tok0, i_new = rn / G, g_new = rn % G;
-        const long long off = static_cast<long long>(pc.b) * p.new_sb +
-                              static_cast<long long>(pc.h) * p.new_sh + sub * kLaneDims;
-        const NewTok nt = quantize_new_token(p.k_new + off, p.v_new + off, blk_lanes, tab);
-        if (g == g_new) {
-#pragma unroll
-          for (int i = 0; i < kTPS; ++i) {
-            if (i == i_new) {
-              Rg.k[i] = nt.k; Rg.v[i] = nt.v; Rg.ks[i] = nt.ks; Rg.vs[i] = nt.vs;
-            }
-          }
-          const long long r = (static_cast<long long>(pc.b) * p.H + pc.h) * p.Tc + row_new;
-          *reinterpret_cast<uint2*>(const_cast<uint8_t*>(p.kc) + r * (HD / 2) + sub * 8) = nt.k;
-          *reinterpret_cast<uint2*>(const_cast<uint8_t*>(p.vc) + r * (HD / 2) + sub * 8) = nt.v;
-          if (((sub * kLaneDims) & ((1 << p.blk_shift) - 1)) == 0) {
-            const_cast<float*>(p.ks)[r * nblk + sidx] = nt.ks;
-            const_cast<float*>(p.vs)[r * nblk + sidx] = nt.vs;
-          }
-        }
-      }
-    }
 #ifdef NQKV_EXP_NOCOMPUTE
     {
       uint32_t x = 0;
@@ -629,15 +774,13 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const DecodeParams p
     for (int i = 0; i < kTPS; ++i) {
       const uint32_t r0 = prmt(Rg.k[i].x, Rg.k[i].y, rotA);
       const uint32_t r1 = prmt(Rg.k[i].x, Rg.k[i].y, rotB);
-      float a0 = lds_k(prmt(r0, jsel[0], 0x7604));
-      float a1 = lds_k(prmt(r0, jsel[1], 0x7614));
-      a0 += lds_k(prmt(r0, jsel[2], 0x7624));
-      a1 += lds_k(prmt(r0, jsel[3], 0x7634));
-      a0 += lds_k(prmt(r1, jsel[4], 0x7604));
-      a1 += lds_k(prmt(r1, jsel[5], 0x7614));
-      a0 += lds_k(prmt(r1, jsel[6], 0x7624));
-      a1 += lds_k(prmt(r1, jsel[7], 0x7634));
-      sc[i] = (a0 + a1) * Rg.ks[i];
+      // pairs of lookups accumulate as fp32x2
+      uint64_t a = pack2(lds_k(prmt(r0, jsel[0], 0x7604)), lds_k(prmt(r0, jsel[1], 0x7614)));
+      a = fadd2(a, pack2(lds_k(prmt(r0, jsel[2], 0x7624)), lds_k(prmt(r0, jsel[3], 0x7634))));
+      const uint64_t b = pack2(lds_k(prmt(r1, jsel[4], 0x7604)), lds_k(prmt(r1, jsel[5], 0x7614)));
+      a = fadd2(a, fadd2(b, pack2(lds_k(prmt(r1, jsel[6], 0x7624)), lds_k(prmt(r1, jsel[7], 0x7634)))));
+      const float2 af = unpack2(a);
+      sc[i] = (af.x + af.y) * Rg.ks[i];
     }
 #pragma unroll
     for (int o = 1; o < LPT; o <<= 1) {
@@ -647,7 +790,7 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const DecodeParams p
     float mt = -INFINITY;
 #pragma unroll
     for (int i = 0; i < kTPS; ++i) {
-      sc[i] = (tok0 + i * G + g < pc.t1) ? sc[i] : -INFINITY;
+      sc[i] = (tok0 + i * G + g < t1) ? sc[i] : -INFINITY;
       mt = fmaxf(mt, sc[i]);
     }
 #pragma unroll
@@ -674,7 +817,8 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const DecodeParams p
     }
   };
 
-  // end of piece k: sum the G token groups (common max), publish, arrive
+  // end of piece k: sum the G token groups (common max), publish, arrive.
+  // A warp that saw no token publishes zeros and m = -inf.
   auto end_piece = [&](int k) {
     const int slot = k % R;
     if (any) {
@@ -684,13 +828,13 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const DecodeParams p
 #pragma unroll
         for (int j = 0; j < 8; ++j) o2[j] = fadd2(o2[j], shfl_xor64(o2[j], o));
       }
-      if (g == 0) {
-        float* dst = s_o + (slot * NC + warp) * HD + sub * kLaneDims;
+    }
+    if (g == 0) {
+      float* dst = s_o + (slot * NC + warp) * HD + sub * kLaneDims;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const float2 a = unpack2(o2[2 * j]), b2 = unpack2(o2[2 * j + 1]);
-          *reinterpret_cast<float4*>(dst + 4 * j) = make_float4(a.x, a.y, b2.x, b2.y);
-        }
+      for (int j = 0; j < 4; ++j) {
+        const float2 a = unpack2(o2[2 * j]), b2 = unpack2(o2[2 * j + 1]);
+        *reinterpret_cast<float4*>(dst + 4 * j) = make_float4(a.x, a.y, b2.x, b2.y);
       }
     }
     if (lane == 0) s_ml[slot * NC + warp] = make_float2(any ? m : -INFINITY, l);
@@ -698,63 +842,59 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const DecodeParams p
     if (lane == 0) mbar_arrive(mb_done + 8 * slot);
   };
 
-  // load cursor: (lp, ls) = next stage of this warp in piece order (index lpi)
-  Piece cp;
-  locate(g0, cp);
-  Piece lp = cp;
-  int ls = warp, lpi = 0;
-  bool lvalid = true;
-  while (ls >= nstages(lp)) {
-    if (!next_piece(lp)) { lvalid = false; break; }
-    ls = warp;
-    ++lpi;
-  }
-  StageRegs RA, RB;
-  if (lvalid) load_stage(RA, lp, ls);
   int cpi = 0;
+#ifdef NQKV_TRACE
+  unsigned long long waited = 0;
+#endif
   auto open_piece = [&]() {
     set_jsel(cpi % R);
+#ifdef NQKV_TRACE
+    const unsigned long long w0 = gtimer();
+#endif
     mbar_wait(mb_full + 8 * (cpi % R), (cpi / R) & 1);
+#ifdef NQKV_TRACE
+    waited += gtimer() - w0;
+#endif
     reset_state();
   };
   open_piece();
-  TRACE(3);
-  auto step = [&](StageRegs& cur, StageRegs& nxt) -> bool {
-    // cur holds stage (lp, ls) of piece index lpi: advance the load cursor and
-    // issue the next stage's loads, then catch consumption up to cur's piece
-    const int cur_s = ls, cur_pi = lpi;
-    ls += NC;
-    while (ls >= nstages(lp)) {
-      if (!next_piece(lp)) { lvalid = false; break; }
-      ls = warp;
-      ++lpi;
+  TRACE(8);
+  // buffer d-1 (consumed in the previous step) is refilled BEFORE buffer d is
+  // consumed, so D stages are in flight while one is being computed
+  bool running = has[0];
+  while (running) {
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const int pd = (d + D - 1) % D;
+      has[pd] = fill(pd);
+      if (!has[d]) { running = false; break; }
+      while (cpi < mpi[d]) {
+        end_piece(cpi);
+        ++cpi;
+        open_piece();
+      }
+      consume(RG[d], mtok[d], mt1[d]);
     }
-    if (lvalid) load_stage(nxt, lp, ls);
-    while (cpi < cur_pi) {
+    TRACE(12);
+  }
+  TRACE(9);
+  // close the current piece and any remaining ones (no stages of this warp);
+  // the number of pieces is the same for every warp
+  {
+    Piece cp;
+    walk_first(cp);
+    for (int k = 0; k < cpi; ++k) walk_next(cp, k);
+    for (;;) {
       end_piece(cpi);
-      next_piece(cp);
+      if (!walk_next(cp, cpi)) break;
       ++cpi;
       open_piece();
     }
-    consume(cur, cp, cur_s);
-    return lvalid;
-  };
-  if (lvalid) {
-    for (;;) {
-      if (!step(RA, RB)) break;
-      TRACE(4);
-      if (!step(RB, RA)) break;
-    }
   }
-  TRACE(5);
-  // close the current piece and any remaining ones (no stages of this warp)
-  for (;;) {
-    end_piece(cpi);
-    if (!next_piece(cp)) break;
-    ++cpi;
-    open_piece();
-  }
-  TRACE(6);
+  TRACE(10);
+#ifdef NQKV_TRACE
+  if (p.trace && lane == 0) p.trace[(blockIdx.x * NW + warp) * 16 + 15] = waited + 1;
+#endif
 }
 
 }  // namespace nqkv

@@ -335,8 +335,9 @@ def test_full_size_layer_sampled(N, cfg):
 @pytest.mark.parametrize("hd,blk", [(64, 64), (64, 32), (128, 64), (128, 128)])
 def test_decode_step_fused_matches_separate_calls(N, hd, blk):
     """nqkv_decode_step == nqkv_quantize(n_new=1) + nqkv_decode_attention:
-    identical cache bytes, output within 2e-3 of the oracle, and bit-identical
-    to the unfused attention on the updated cache."""
+    identical cache bytes, output within 2e-3 of the oracle, and equal to the
+    unfused attention on the updated cache up to fp32 reassociation (the fused
+    kernel folds the appended token into the merge; reading R7)."""
     B, H, Tc = 5, 3, 512
     lens0 = [0, 1, 127, 128, 300]           # cached tokens before the step
     T = max(lens0)
@@ -361,7 +362,7 @@ def test_decode_step_fused_matches_separate_calls(N, hd, blk):
     out_s = N.nqkv_decode_attention(q.to(DEV), sk, sks, sv, svs, lens, blk, N.make_workspace(B, H, hd, Tc, DEV))
     torch.cuda.synchronize()
     assert torch.equal(fk, sk) and torch.equal(fks, sks) and torch.equal(fv, sv) and torch.equal(fvs, svs)
-    assert torch.equal(out_f, out_s)
+    assert torch.allclose(out_f, out_s, rtol=1e-5, atol=1e-6)
     O.quantize_append(kn.unsqueeze(1).numpy(), lens0, blk, kc, ks)
     O.quantize_append(vn.unsqueeze(1).numpy(), lens0, blk, vc, vs)
     assert np.array_equal(fk.cpu().numpy(), kc) and np.array_equal(fvs.cpu().numpy(), vs)

@@ -8,12 +8,17 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2505_16210_b200 import build as bld  # noqa: E402
 
-lib = bld.build_variant("/tmp/libnqkv_trace.so", {"NQKV_TRACE": 1})
+defs = {"NQKV_TRACE": 1}
+for kv in os.environ.get("DEFS", "").split(","):
+    if kv:
+        k, v = kv.split("=")
+        defs[k] = v
+lib = bld.build_variant("/tmp/libnqkv_trace.so", defs)
 os.environ["NQKV_LIB"] = lib
 import torch  # noqa: E402
 
 NW = 16
-tr = torch.zeros(148 * NW * 8, dtype=torch.int64, device="cuda")
+tr = torch.zeros(148 * NW * 16, dtype=torch.int64, device="cuda")
 os.environ["NQKV_TRACE_PTR"] = str(tr.data_ptr())
 from paper_2505_16210_b200 import nqkv as N  # noqa: E402
 
@@ -32,15 +37,20 @@ for _ in range(5):
     torch.cuda._sleep(100000)
     cache.attend(q, L, ws)
     torch.cuda.synchronize()
-t = tr.view(148, NW, 8).cpu()
+t = tr.view(148, NW, 16).cpu()
 t0 = t[:, :, 0][t[:, :, 0] > 0].min()
-names = ["entry", "pdl_wait", "prefix", "tab0/full0", "1st step", "loop end", "exit"]
+names = ["entry", "pdl_wait", "prefix", "walk", "loads issued", "V LUT", "table0", "sync", "full0", "loop end", "exit", "", "last odd step"]
 for role, sl in (("consumer", slice(0, NW - 1)), ("producer", slice(NW - 1, NW))):
-    x = t[:, sl, :].reshape(-1, 8)
+    x = t[:, sl, :].reshape(-1, 16)
     x = x[x[:, 0] > 0]
     for k, n in enumerate(names):
+        if not n:
+            continue
         col = x[:, k]
         col = col[col > 0]
         if len(col):
             r = (col - t0).double() / 1000.0
             print(f"{role:9s} {n:11s} min {r.min():8.2f} med {r.median():8.2f} max {r.max():8.2f} us (n={len(col)})")
+w = t[:, :NW - 1, 15]
+w = w[w > 0].double() / 1000.0
+print(f"consumer wait on full barriers: med {w.median():.2f} max {w.max():.2f} us per warp")
