@@ -210,8 +210,241 @@ struct StageRegs {
   float ks[kTPS], vs[kTPS];
 };
 
+// Launch-wide scheduling constants: C CTAs own equal contiguous ranges of
+// the N-token (b, h, t) list; range c = [bnd(c), bnd(c + 1)).
+struct Sched {
+  int N, C, q, r;        // N = q*C + r
+  __device__ __forceinline__ int bnd(int c) const { return c * q + (c * r) / C; }   // floor(c*N/C)
+  __device__ int cta_of(int g) const {                                             // bnd(c) <= g < bnd(c+1)
+    int lo = 0, hi = C;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (bnd(mid) <= g) lo = mid; else hi = mid;
+    }
+    return lo;
+  }
+};
+
+// q-table slot offset (bytes from Smem::kK): hd 64 -> 64 KB block r >> 1,
+// 128-B half r & 1 of each 256-B row; hd 128 -> block r
+template <int HD>
+__device__ __forceinline__ uint32_t slot_off(int r) {
+  return HD == 64 ? static_cast<uint32_t>(r >> 1) * 0x10000u + static_cast<uint32_t>(r & 1) * 128u
+                  : static_cast<uint32_t>(r) * 0x10000u;
+}
+
+// ---------------------------------------------------------------- producer
+// Out of line (run once per piece by one warp): keeps the kernel's hot code
+// compact in the instruction cache.
+
+// The appended token of a fused step, warp-wide: lane owns pairs j = lane +
+// 32u (dims 2j, 2j+1).  Quantised exactly as quantize_kernel does, written to
+// the cache row `row` of (b, h); vh gets its dequantised values and the return
+// value is its score (log2 domain) from the q-table in `slot` (slot < 0: 0).
 template <int HD, int NW>
-__global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const DecodeParams p) {
+__device__ __noinline__ float new_token_fn(const DecodeParams& p, unsigned char* smem, int b, int h,
+                                           int row, int slot, float* vh) {
+  using Sm = Smem<HD, NW>;
+  constexpr int PPL = Geo<HD>::PPL;
+  const int lane = threadIdx.x & 31;
+  const float* s_lv = reinterpret_cast<const float*>(smem + Sm::kLv);
+  const uint32_t tabc = kSmemWindow + Sm::kTab - 0x5A000000u;
+  const int nblk = HD >> p.blk_shift;
+  const long long bh = static_cast<long long>(b) * p.H + h;
+  const long long src = static_cast<long long>(b) * p.new_sb + static_cast<long long>(h) * p.new_sh;
+  const long long r = bh * p.Tc + row;
+  const int bp = 1 << (p.blk_shift - 1);                         // pairs per block
+  float xk[2 * PPL], xv[2 * PPL], sk[PPL], sv[PPL];
+#pragma unroll
+  for (int u = 0; u < PPL; ++u) {
+    const int j = lane + 32 * u;
+    const float2 fk = __half22float2(__ldg(reinterpret_cast<const __half2*>(p.k_new + src) + j));
+    const float2 fv = __half22float2(__ldg(reinterpret_cast<const __half2*>(p.v_new + src) + j));
+    xk[2 * u] = fk.x; xk[2 * u + 1] = fk.y;
+    xv[2 * u] = fv.x; xv[2 * u + 1] = fv.y;
+    sk[u] = fmaxf(fabsf(fk.x), fabsf(fk.y));
+    sv[u] = fmaxf(fabsf(fv.x), fabsf(fv.y));
+  }
+  if (bp > 32) {                       // one block spans both halves (hd 128, blk 128)
+    sk[0] = sk[PPL - 1] = fmaxf(sk[0], sk[PPL - 1]);
+    sv[0] = sv[PPL - 1] = fmaxf(sv[0], sv[PPL - 1]);
+  }
+  const int span = min(bp, 32);
+#pragma unroll
+  for (int u = 0; u < PPL; ++u) {
+    for (int o = 1; o < span; o <<= 1) {
+      sk[u] = fmaxf(sk[u], __shfl_xor_sync(0xffffffffu, sk[u], o));
+      sv[u] = fmaxf(sv[u], __shfl_xor_sync(0xffffffffu, sv[u], o));
+    }
+  }
+  float part = 0.0f;
+#pragma unroll
+  for (int u = 0; u < PPL; ++u) {
+    const int j = lane + 32 * u;
+    const float rk = block_rcp(sk[u]), rv = block_rcp(sv[u]);
+    const uint32_t ck = nf4_code_c(__fmul_rn(xk[2 * u], rk), tabc) |
+                        (nf4_code_c(__fmul_rn(xk[2 * u + 1], rk), tabc) << 4);
+    const uint32_t cvl = nf4_code_c(__fmul_rn(xv[2 * u], rv), tabc);
+    const uint32_t cvh = nf4_code_c(__fmul_rn(xv[2 * u + 1], rv), tabc);
+    const_cast<uint8_t*>(p.kc)[r * (HD / 2) + j] = static_cast<uint8_t>(ck);
+    const_cast<uint8_t*>(p.vc)[r * (HD / 2) + j] = static_cast<uint8_t>(cvl | (cvh << 4));
+    if (((2 * j) & ((1 << p.blk_shift) - 1)) == 0) {
+      const_cast<float*>(p.ks)[r * nblk + ((2 * j) >> p.blk_shift)] = sk[u];
+      const_cast<float*>(p.vs)[r * nblk + ((2 * j) >> p.blk_shift)] = sv[u];
+    }
+    vh[2 * u] = __fmul_rn(sv[u], s_lv[cvl]);
+    vh[2 * u + 1] = __fmul_rn(sv[u], s_lv[cvh]);
+    if (slot >= 0)
+      part += reinterpret_cast<const float*>(smem + Sm::kK + slot_off<HD>(slot) + ck * 256)[j] * sk[u];
+  }
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+  return part;
+}
+
+// q-table of one piece into ring slot `slot`: lane owns pair quad qd = lane %
+// Q for rows whose high nibble is lane / Q (mod 32 / Q).  T[e][j] =
+// RN(c q_{2j} L[e & 15]) + RN(c q_{2j+1} L[e >> 4]) (the same formula as the
+// cooperative table-0 build).
+template <int HD, int NW>
+__device__ __noinline__ void build_fn(unsigned char* smem, int slot, uint4 qraw, float scale_log2) {
+  using Sm = Smem<HD, NW>;
+  constexpr int Q = HD / 8;
+  const int lane = threadIdx.x & 31;
+  const float* s_lv = reinterpret_cast<const float*>(smem + Sm::kLv);
+  __half2 h2[4];
+  memcpy(h2, &qraw, 16);
+  float a[4], b[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float2 f = __half22float2(h2[k]);
+    a[k] = f.x * scale_log2;
+    b[k] = f.y * scale_log2;
+  }
+  const int qd = lane % Q;
+  uint64_t A01[16], A23[16];
+#pragma unroll
+  for (int c = 0; c < 16; ++c) {
+    const float L = s_lv[c];
+    A01[c] = pack2(a[0] * L, a[1] * L);
+    A23[c] = pack2(a[2] * L, a[3] * L);
+  }
+  unsigned char* base = smem + Sm::kK + slot_off<HD>(slot) + qd * 16;
+#pragma unroll 1
+  for (int hi = lane / Q; hi < 16; hi += 32 / Q) {
+    const float L = s_lv[hi];
+    const uint64_t B01 = pack2(b[0] * L, b[1] * L), B23 = pack2(b[2] * L, b[3] * L);
+    unsigned char* row = base + hi * 16 * 256;
+#pragma unroll
+    for (int lo = 0; lo < 16; ++lo) {
+      const float2 t01 = unpack2(fadd2(A01[lo], B01)), t23 = unpack2(fadd2(A23[lo], B23));
+      *reinterpret_cast<float4*>(row + lo * 256) = make_float4(t01.x, t01.y, t23.x, t23.y);
+    }
+  }
+}
+
+// Merge piece k's NC consumer states (ring slot k % R) and, in a fused step,
+// the appended token's state: write the output, or a partial (+ the
+// last-arriver merge of the sequence's partials across CTAs).
+template <int HD, int NW>
+__device__ __noinline__ void merge_fn(const DecodeParams& p, unsigned char* smem, int k, Sched sc,
+                                      int cta, int g0) {
+  using Sm = Smem<HD, NW>;
+  constexpr int PPL = Geo<HD>::PPL, R = Geo<HD>::R, NC = NW - 1;
+  const int lane = threadIdx.x & 31;
+  const int slot = k % R;
+  const Piece pc = reinterpret_cast<const Piece*>(smem + Sm::kPc)[slot];
+  const float* st = reinterpret_cast<const float*>(smem + Sm::kNew) + slot * (HD + 4);
+  const float2* s_ml = reinterpret_cast<const float2*>(smem + Sm::kMl) + slot * NC;
+  const float* s_o = reinterpret_cast<const float*>(smem + Sm::kO) + slot * NC * HD;
+  auto dim = [&](int u) { return 2 * (lane + 32 * u); };
+  const float snew = st[HD];
+  float mw[NC];
+  float M = snew;
+#pragma unroll
+  for (int w = 0; w < NC; ++w) {
+    mw[w] = s_ml[w].x;
+    M = fmaxf(M, mw[w]);
+  }
+  float den = 0.0f, acc[2 * PPL];
+#pragma unroll
+  for (int d = 0; d < 2 * PPL; ++d) acc[d] = 0.0f;
+#pragma unroll
+  for (int w = 0; w < NC; ++w) {
+    const float f = fast_exp2(mw[w] - M);           // consumer without tokens: -inf -> 0
+    den = fmaf(f, s_ml[w].y, den);
+#pragma unroll
+    for (int u = 0; u < PPL; ++u) {
+      const float2 x = *reinterpret_cast<const float2*>(s_o + w * HD + dim(u));
+      acc[2 * u] = fmaf(f, x.x, acc[2 * u]);
+      acc[2 * u + 1] = fmaf(f, x.y, acc[2 * u + 1]);
+    }
+  }
+  if (snew != -INFINITY) {
+    const float f = fast_exp2(snew - M);
+    den += f;
+#pragma unroll
+    for (int u = 0; u < PPL; ++u) {
+      const float2 x = *reinterpret_cast<const float2*>(st + dim(u));
+      acc[2 * u] = fmaf(f, x.x, acc[2 * u]);
+      acc[2 * u + 1] = fmaf(f, x.y, acc[2 * u + 1]);
+    }
+  }
+  const long long bh = static_cast<long long>(pc.b) * p.H + pc.h;
+  if (pc.t0 == 0 && pc.t1 == pc.len) {
+    const float inv = 1.0f / den;
+#pragma unroll
+    for (int u = 0; u < PPL; ++u)
+      *reinterpret_cast<float2*>(p.out + bh * HD + dim(u)) = make_float2(acc[2 * u] * inv, acc[2 * u + 1] * inv);
+    return;
+  }
+  // partial piece: slot 0 = this CTA's first piece (starts at g0), 1 = its
+  // last.  The counter's acq_rel RMW publishes the partial (after the warp
+  // barrier) and, for the last arriver, acquires everyone else's.
+  float* part = p.part + (static_cast<long long>(cta) * 2 + (pc.gs == g0 ? 0 : 1)) * (HD + 2);
+#pragma unroll
+  for (int u = 0; u < PPL; ++u)
+    *reinterpret_cast<float2*>(part + dim(u)) = make_float2(acc[2 * u], acc[2 * u + 1]);
+  if (lane == 0) {
+    part[HD] = M;
+    part[HD + 1] = den;
+  }
+  __syncwarp();
+  const int st0 = pc.gs - pc.t0;                                // global index of token 0
+  const int ca = sc.cta_of(st0), cb = sc.cta_of(st0 + pc.len - 1);
+  int last = 0;
+  if (lane == 0) last = atom_add_acq_rel(p.cnt + bh, 1) == cb - ca;
+  last = __shfl_sync(0xffffffffu, last, 0);
+  if (!last) return;
+  float Mx = -INFINITY;
+  for (int c = ca; c <= cb; ++c) {
+    const int sl = (c == ca && sc.bnd(c) != st0) ? 1 : 0;
+    Mx = fmaxf(Mx, __ldcg(p.part + (static_cast<long long>(c) * 2 + sl) * (HD + 2) + HD));
+  }
+  float dsum = 0.0f, o[2 * PPL];
+#pragma unroll
+  for (int d = 0; d < 2 * PPL; ++d) o[d] = 0.0f;
+  for (int c = ca; c <= cb; ++c) {
+    const int sl = (c == ca && sc.bnd(c) != st0) ? 1 : 0;
+    const float* pp = p.part + (static_cast<long long>(c) * 2 + sl) * (HD + 2);
+    const float fc = fast_exp2(__ldcg(pp + HD) - Mx);
+    dsum += fc * __ldcg(pp + HD + 1);
+#pragma unroll
+    for (int u = 0; u < PPL; ++u) {
+      const float2 x = __ldcg(reinterpret_cast<const float2*>(pp + dim(u)));
+      o[2 * u] = fmaf(fc, x.x, o[2 * u]);
+      o[2 * u + 1] = fmaf(fc, x.y, o[2 * u + 1]);
+    }
+  }
+  const float inv = 1.0f / dsum;
+#pragma unroll
+  for (int u = 0; u < PPL; ++u)
+    *reinterpret_cast<float2*>(p.out + bh * HD + dim(u)) = make_float2(o[2 * u] * inv, o[2 * u + 1] * inv);
+  if (lane == 0) p.cnt[bh] = 0;
+}
+
+template <int HD, int NW>
+__global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constant__ DecodeParams p) {
   using Ge = Geo<HD>;
   using Sm = Smem<HD, NW>;
   constexpr int LPT = Ge::LPT, G = Ge::G, ST = Ge::ST, R = Ge::R, PPL = Ge::PPL;
@@ -247,29 +480,18 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const DecodeParams p
   pdl_trigger();
   pdl_wait();
   TRACE(1);
-  // seq_lens (warp 0) in flight while the V LUT is written
-  int lens_r[kMaxBatch / 32];
-  if (warp == 0) {
-#pragma unroll
-    for (int u = 0; u < kMaxBatch / 32; ++u) {
-      const int b = u * 32 + lane;
-      lens_r[u] = (u * 32 < p.B && b < p.B) ? p.seq_lens[b] : 0;
-    }
-  }
   // ---- per-batch streamed lengths and token prefix: tokens(b) = H * len'_b.
   // Fused step: the appended row (len - 1) is not streamed; the producer
   // quantises it and folds it into the piece merge (s_len holds len').
   if (warp == 0) {
     int carry = 0;
     if (lane == 0) s_pref[0] = 0;
-#pragma unroll
-    for (int u = 0; u < kMaxBatch / 32; ++u) {
-      if (u * 32 >= p.B) break;
-      const int b = u * 32 + lane;
-      int n = 0;
-      const int raw = b < p.B ? min(max(lens_r[u], 0), p.Tc) : 0;
+    for (int b0 = 0; b0 < p.B; b0 += 32) {
+      const int b = b0 + lane;
+      const int raw = b < p.B ? min(max(p.seq_lens[b], 0), p.Tc) : 0;
       const unsigned one = __ballot_sync(0xffffffffu, fused && raw == 1);
-      if (lane == 0) reinterpret_cast<uint32_t*>(smem + Sm::kOne)[u] = one;
+      if (lane == 0) reinterpret_cast<uint32_t*>(smem + Sm::kOne)[b0 >> 5] = one;
+      int n = 0;
       if (b < p.B) {
         const int len = fused ? max(raw - 1, 0) : raw;
         s_len[b] = len;
@@ -286,95 +508,43 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const DecodeParams p
   }
   __syncthreads();
   TRACE(2);
-  const int N = s_pref[p.B];
-
-  // ---- the appended token (fused step), warp-wide: lane owns pairs j = lane
-  // + 32u (dims 2j, 2j+1).  Quantised exactly as quantize_kernel does and
-  // written to the cache; returns its dequantised value and (from the q-table
-  // in ring slot `slot`, if >= 0) its score in the log2 domain.
-  const uint32_t tabc = kSmemWindow + Sm::kTab - 0x5A000000u;
-  auto new_token = [&](int b, int h, int slot, float (&vh)[2 * PPL]) -> float {
-    const long long bh = static_cast<long long>(b) * p.H + h;
-    const long long src = static_cast<long long>(b) * p.new_sb + static_cast<long long>(h) * p.new_sh;
-    const int row = min(s_len[b], p.Tc - 1);                      // = len - 1
-    const long long r = bh * p.Tc + row;
-    const int bp = 1 << (p.blk_shift - 1);                         // pairs per block
-    float xk[2 * PPL], xv[2 * PPL], sk[PPL], sv[PPL];
-#pragma unroll
-    for (int u = 0; u < PPL; ++u) {
-      const int j = lane + 32 * u;
-      const float2 fk = __half22float2(__ldg(reinterpret_cast<const __half2*>(p.k_new + src) + j));
-      const float2 fv = __half22float2(__ldg(reinterpret_cast<const __half2*>(p.v_new + src) + j));
-      xk[2 * u] = fk.x; xk[2 * u + 1] = fk.y;
-      xv[2 * u] = fv.x; xv[2 * u + 1] = fv.y;
-      sk[u] = fmaxf(fabsf(fk.x), fabsf(fk.y));
-      sv[u] = fmaxf(fabsf(fv.x), fabsf(fv.y));
-    }
-    if (bp > 32) {                       // one block spans both halves (hd 128, blk 128)
-      sk[0] = sk[PPL - 1] = fmaxf(sk[0], sk[PPL - 1]);
-      sv[0] = sv[PPL - 1] = fmaxf(sv[0], sv[PPL - 1]);
-    }
-    const int span = min(bp, 32);
-#pragma unroll
-    for (int u = 0; u < PPL; ++u) {
-      for (int o = 1; o < span; o <<= 1) {
-        sk[u] = fmaxf(sk[u], __shfl_xor_sync(0xffffffffu, sk[u], o));
-        sv[u] = fmaxf(sv[u], __shfl_xor_sync(0xffffffffu, sv[u], o));
-      }
-    }
-    float part = 0.0f;
-#pragma unroll
-    for (int u = 0; u < PPL; ++u) {
-      const int j = lane + 32 * u;
-      const float rk = block_rcp(sk[u]), rv = block_rcp(sv[u]);
-      const uint32_t ck = nf4_code_c(__fmul_rn(xk[2 * u], rk), tabc) |
-                          (nf4_code_c(__fmul_rn(xk[2 * u + 1], rk), tabc) << 4);
-      const uint32_t cvl = nf4_code_c(__fmul_rn(xv[2 * u], rv), tabc);
-      const uint32_t cvh = nf4_code_c(__fmul_rn(xv[2 * u + 1], rv), tabc);
-      const_cast<uint8_t*>(p.kc)[r * (HD / 2) + j] = static_cast<uint8_t>(ck);
-      const_cast<uint8_t*>(p.vc)[r * (HD / 2) + j] = static_cast<uint8_t>(cvl | (cvh << 4));
-      if (((2 * j) & ((1 << p.blk_shift) - 1)) == 0) {
-        const_cast<float*>(p.ks)[r * nblk + ((2 * j) >> p.blk_shift)] = sk[u];
-        const_cast<float*>(p.vs)[r * nblk + ((2 * j) >> p.blk_shift)] = sv[u];
-      }
-      vh[2 * u] = __fmul_rn(sv[u], s_lv[cvl]);
-      vh[2 * u + 1] = __fmul_rn(sv[u], s_lv[cvh]);
-      if (slot >= 0) {
-        const uint32_t off = HD == 64 ? (slot >> 1) * 0x10000u + (slot & 1) * 128u : slot * 0x10000u;
-        part += reinterpret_cast<const float*>(smem + Sm::kK + off + ck * 256)[j] * sk[u];
-      }
-    }
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-    return part;
-  };
+  Sched sc;
+  sc.N = s_pref[p.B];
 
   // ---- empty sequences (out = 0, reading R12) and, in a fused step,
-  // sequences whose only token is the appended one (out = its value)
+  // sequences whose only token is the appended one (out = its value).  Off
+  // the critical path: done by the producer warps after table 0 (or here by
+  // every CTA when there is no token to stream at all).
   const uint32_t* s_one = reinterpret_cast<const uint32_t*>(smem + Sm::kOne);
-  auto single = [&](int b) { return (s_one[b >> 5] >> (b & 31)) & 1u; };
-  for (int i = blockIdx.x * NT + tid; i < p.B * p.H * HD; i += gridDim.x * NT) {
-    const int b = i / (p.H * HD);
-    if (s_len[b] == 0 && !single(b)) p.out[i] = 0.0f;
-  }
-  if (fused) {
-    for (int bh = blockIdx.x * NW + warp; bh < p.B * p.H; bh += gridDim.x * NW) {
+  auto empties = [&](int wid, int nwarps) {
+    for (int i = wid * 32 + lane; i < p.B * p.H * HD; i += nwarps * 32) {
+      const int b = i / (p.H * HD);
+      if (s_len[b] == 0 && !((s_one[b >> 5] >> (b & 31)) & 1u)) p.out[i] = 0.0f;
+    }
+    if (!fused) return;
+    for (int bh = wid; bh < p.B * p.H; bh += nwarps) {
       const int b = bh / p.H, h = bh - b * p.H;
-      if (!single(b)) continue;
+      if (!((s_one[b >> 5] >> (b & 31)) & 1u)) continue;
       float vh[2 * PPL];
-      new_token(b, h, -1, vh);
+      new_token_fn<HD, NW>(p, smem, b, h, 0, -1, vh);
 #pragma unroll
       for (int u = 0; u < PPL; ++u)
         *reinterpret_cast<float2*>(p.out + static_cast<long long>(bh) * HD + 2 * (lane + 32 * u)) =
             make_float2(vh[2 * u], vh[2 * u + 1]);
     }
+  };
+  if (sc.N == 0) {
+    empties(blockIdx.x * NW + warp, gridDim.x * NW);
+    return;
   }
-  if (N == 0) return;
-  const int C = min(static_cast<int>(gridDim.x), max(1, (N + p.min_tokens - 1) / p.min_tokens));
-  if (static_cast<int>(blockIdx.x) >= C) return;
+  TRACE(11);
+  sc.C = min(static_cast<int>(gridDim.x), max(1, (sc.N + p.min_tokens - 1) / p.min_tokens));
+  if (static_cast<int>(blockIdx.x) >= sc.C) return;
+  sc.q = sc.N / sc.C;
+  sc.r = sc.N - sc.q * sc.C;
   const int cta = blockIdx.x;
-  const int g0 = static_cast<int>(static_cast<long long>(cta) * N / C);
-  const int g1 = static_cast<int>(static_cast<long long>(cta + 1) * N / C);
+  const int g0 = sc.bnd(cta), g1 = sc.bnd(cta + 1);
+  TRACE(13);
 
   // ---- piece walking (identical in every warp)
   auto locate = [&](int g, Piece& pc) {
@@ -425,6 +595,7 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const DecodeParams p
     s_wi[0] = ro;
     s_wi[1] = ro ? pl.gs : g1;
   }
+  TRACE(14);
   __syncthreads();
   TRACE(3);
   auto walk_first = [&](Piece& pc) { pc = s_walk[s_wi[0] ? 1 : 0]; };
@@ -434,31 +605,16 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const DecodeParams p
   };
   auto nstages = [&](const Piece& pc) { return (pc.t1 - pc.t0 + ST - 1) / ST; };
   auto rowbase = [&](const Piece& pc) { return (pc.b * p.H + pc.h) * p.Tc; };
-  // q-table slot offset (bytes from kK): hd 64 -> block r >> 1, half r & 1;
-  // hd 128 -> block r
-  auto slot_off = [](int r) -> uint32_t {
-    return HD == 64 ? static_cast<uint32_t>(r >> 1) * 0x10000u + static_cast<uint32_t>(r & 1) * 128u
-                    : static_cast<uint32_t>(r) * 0x10000u;
-  };
-  // q of pair quad qd of (b, h), times softmax_scale * log2(e): even dims
-  // (q_{2j}) in a[], odd dims (q_{2j+1}) in b[]
   auto load_quad = [&](const Piece& pc, int qd) -> uint4 {
     const long long bh = static_cast<long long>(pc.b) * p.H + pc.h;
     return __ldg(reinterpret_cast<const uint4*>(p.q + bh * HD) + qd);
   };
-  auto split_quad = [&](const uint4 raw, float (&a)[4], float (&b)[4]) {
-    __half2 h2[4];
-    memcpy(h2, &raw, 16);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const float2 f = __half22float2(h2[k]);
-      a[k] = f.x * p.scale_log2;
-      b[k] = f.y * p.scale_log2;
-    }
-  };
 
-  // ---- consumer lane geometry and the first stage's loads (in flight during
-  // the table-0 build)
+  // ---- q of piece 0 first (its table is the first thing the consumers
+  // need), then the consumers' first stage loads
+  Piece p0;
+  walk_first(p0);
+  const uint4 q0 = load_quad(p0, tid % Q);
   const int g = lane / LPT, sub = lane % LPT;
   const int sidx = (sub * kLaneDims) >> p.blk_shift;
   // rows of (b, h) start at row index rb = (b*H + h)*Tc (32-bit)
@@ -486,11 +642,7 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const DecodeParams p
       Rg.vs[i] = ldg_nc_f32(static_cast<const float*>(addr_wide(p.vs, sw, 4)));
     }
   };
-  // q of piece 0 first: its table is the first thing the consumers need
-  Piece p0;
-  walk_first(p0);
-  const uint4 q0 = load_quad(p0, tid % Q);
-  // load cursor (piece lp, stage ls, piece index lpi): one stage ahead of
+  // load cursor (piece lp, stage ls, piece index lpi): D stages ahead of
   // consumption, across piece boundaries
   Piece lp = p0;
   int ls = warp, lpi = 0;
@@ -530,10 +682,10 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const DecodeParams p
 #pragma unroll
   for (int d = 0; d < D - 1; ++d) has[d] = fill(d);
   has[D - 1] = false;
-
-  // ---- table of piece 0, built by all threads (thread: pair quad tid % Q);
-  // T[e][j] = RN(c q_{2j} L[e & 15]) + RN(c q_{2j+1} L[e >> 4]) everywhere
   TRACE(4);
+
+  // ---- V LUT and the table of piece 0, built by all threads (thread: pair
+  // quad tid % Q); T[e][j] = RN(c q_{2j} L[e & 15]) + RN(c q_{2j+1} L[e >> 4])
   for (int i = tid; i < 256 * 16; i += NT) {     // V LUT; 16 B = two lane copies per store
     const int e = i >> 4;
     const float lo = s_lv[e & 15], hi = s_lv[e >> 4];
@@ -541,8 +693,15 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const DecodeParams p
   }
   TRACE(5);
   {
+    __half2 h2[4];
+    memcpy(h2, &q0, 16);
     float a[4], b[4];
-    split_quad(q0, a, b);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float2 f = __half22float2(h2[k]);
+      a[k] = f.x * p.scale_log2;
+      b[k] = f.y * p.scale_log2;
+    }
     for (int e = tid / Q; e < 256; e += NT / Q) {
       const float lo = s_lv[e & 15], hi = s_lv[e >> 4];
       *reinterpret_cast<float4*>(smem + Sm::kK + e * 256 + (tid % Q) * 16) =
@@ -555,147 +714,27 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const DecodeParams p
 
   if (warp == NC) {
     // ================================================================ producer
-    // build: lane owns quad qd = lane % Q for rows with hi nibble = lane / Q
-    // (mod 32 / Q); A[lo] = c q_even L[lo] for the quad (fp32x2 pairs)
-    auto build = [&](int slot, const uint4 qraw) {
-      float a[4], b[4];
-      split_quad(qraw, a, b);
-      const int qd = lane % Q;
-      uint64_t A01[16], A23[16];
-#pragma unroll
-      for (int c = 0; c < 16; ++c) {
-        const float L = s_lv[c];
-        A01[c] = pack2(a[0] * L, a[1] * L);
-        A23[c] = pack2(a[2] * L, a[3] * L);
-      }
-      unsigned char* base = smem + Sm::kK + slot_off(slot) + qd * 16;
-#pragma unroll 1
-      for (int hi = lane / Q; hi < 16; hi += 32 / Q) {
-        const float L = s_lv[hi];
-        const uint64_t B01 = pack2(b[0] * L, b[1] * L), B23 = pack2(b[2] * L, b[3] * L);
-        unsigned char* row = base + hi * 16 * 256;
-#pragma unroll
-        for (int lo = 0; lo < 16; ++lo) {
-          const float2 t01 = unpack2(fadd2(A01[lo], B01)), t23 = unpack2(fadd2(A23[lo], B23));
-          *reinterpret_cast<float4*>(row + lo * 256) = make_float4(t01.x, t01.y, t23.x, t23.y);
-        }
-      }
-    };
-    // appended-token state of piece k (fused step, the sequence's last piece):
-    // score and value into s_new[k % R]; else score = -inf
+    // appended-token state of piece k (fused step, the sequence's last piece)
     auto new_state = [&](int k, const Piece& pc) {
       float* st = s_new + (k % R) * (HD + 4);
       if (fused && pc.t1 == pc.len) {
         float vh[2 * PPL];
-        const float sc = new_token(pc.b, pc.h, k % R, vh);
+        const float sco = new_token_fn<HD, NW>(p, smem, pc.b, pc.h, min(pc.len, p.Tc - 1), k % R, vh);
 #pragma unroll
         for (int u = 0; u < PPL; ++u)
           *reinterpret_cast<float2*>(st + 2 * (lane + 32 * u)) = make_float2(vh[2 * u], vh[2 * u + 1]);
-        if (lane == 0) st[HD] = sc;
+        if (lane == 0) st[HD] = sco;
       } else if (lane == 0) {
         st[HD] = -INFINITY;
       }
     };
-    // this lane's output dims: 2j, 2j+1 for j = lane + 32u
-    auto dim = [&](int u) { return 2 * (lane + 32 * u); };
-    // merge piece k's NC consumer states (+ appended token): output or partial
-    auto merge = [&](int k) {
-      const int slot = k % R;
-      const Piece pc = s_pc[slot];
-      const float* st = s_new + slot * (HD + 4);
-      const float snew = st[HD];
-      float mw[NC];
-      float M = snew;
-#pragma unroll
-      for (int w = 0; w < NC; ++w) {
-        mw[w] = s_ml[slot * NC + w].x;
-        M = fmaxf(M, mw[w]);
-      }
-      float den = 0.0f, acc[2 * PPL];
-#pragma unroll
-      for (int d = 0; d < 2 * PPL; ++d) acc[d] = 0.0f;
-#pragma unroll
-      for (int w = 0; w < NC; ++w) {
-        const float f = fast_exp2(mw[w] - M);           // consumer without tokens: -inf -> 0
-        den = fmaf(f, s_ml[slot * NC + w].y, den);
-        const float* o = s_o + (slot * NC + w) * HD;
-#pragma unroll
-        for (int u = 0; u < PPL; ++u) {
-          const float2 x = *reinterpret_cast<const float2*>(o + dim(u));
-          acc[2 * u] = fmaf(f, x.x, acc[2 * u]);
-          acc[2 * u + 1] = fmaf(f, x.y, acc[2 * u + 1]);
-        }
-      }
-      if (snew != -INFINITY) {
-        const float f = fast_exp2(snew - M);
-        den += f;
-#pragma unroll
-        for (int u = 0; u < PPL; ++u) {
-          const float2 x = *reinterpret_cast<const float2*>(st + dim(u));
-          acc[2 * u] = fmaf(f, x.x, acc[2 * u]);
-          acc[2 * u + 1] = fmaf(f, x.y, acc[2 * u + 1]);
-        }
-      }
-      const long long bh = static_cast<long long>(pc.b) * p.H + pc.h;
-      if (pc.t0 == 0 && pc.t1 == pc.len) {
-        const float inv = 1.0f / den;
-#pragma unroll
-        for (int u = 0; u < PPL; ++u)
-          *reinterpret_cast<float2*>(p.out + bh * HD + dim(u)) = make_float2(acc[2 * u] * inv, acc[2 * u + 1] * inv);
-        return;
-      }
-      // partial piece: slot 0 = this CTA's first piece (starts at g0), 1 = its last.  The
-      // counter's acq_rel RMW publishes the partial (after the warp barrier)
-      // and, for the last arriver, acquires everyone else's.
-      float* part = p.part + (static_cast<long long>(cta) * 2 + (pc.gs == g0 ? 0 : 1)) * (HD + 2);
-#pragma unroll
-      for (int u = 0; u < PPL; ++u)
-        *reinterpret_cast<float2*>(part + dim(u)) = make_float2(acc[2 * u], acc[2 * u + 1]);
-      if (lane == 0) {
-        part[HD] = M;
-        part[HD + 1] = den;
-      }
-      __syncwarp();
-      const int st0 = pc.gs - pc.t0;                                // global index of token 0
-      const int ca = static_cast<int>((static_cast<long long>(st0 + 1) * C - 1) / N);
-      const int cb = static_cast<int>((static_cast<long long>(st0 + pc.len) * C - 1) / N);
-      int last = 0;
-      if (lane == 0) last = atom_add_acq_rel(p.cnt + bh, 1) == cb - ca;
-      last = __shfl_sync(0xffffffffu, last, 0);
-      if (!last) return;
-      float Mx = -INFINITY;
-      for (int c = ca; c <= cb; ++c) {
-        const int sl = (c == ca && static_cast<long long>(c) * N / C != st0) ? 1 : 0;
-        Mx = fmaxf(Mx, __ldcg(p.part + (static_cast<long long>(c) * 2 + sl) * (HD + 2) + HD));
-      }
-      float dsum = 0.0f, o[2 * PPL];
-#pragma unroll
-      for (int d = 0; d < 2 * PPL; ++d) o[d] = 0.0f;
-      for (int c = ca; c <= cb; ++c) {
-        const int sl = (c == ca && static_cast<long long>(c) * N / C != st0) ? 1 : 0;
-        const float* pp = p.part + (static_cast<long long>(c) * 2 + sl) * (HD + 2);
-        const float fc = fast_exp2(__ldcg(pp + HD) - Mx);
-        dsum += fc * __ldcg(pp + HD + 1);
-#pragma unroll
-        for (int u = 0; u < PPL; ++u) {
-          const float2 x = __ldcg(reinterpret_cast<const float2*>(pp + dim(u)));
-          o[2 * u] = fmaf(fc, x.x, o[2 * u]);
-          o[2 * u + 1] = fmaf(fc, x.y, o[2 * u + 1]);
-        }
-      }
-      const float inv = 1.0f / dsum;
-#pragma unroll
-      for (int u = 0; u < PPL; ++u)
-        *reinterpret_cast<float2*>(p.out + bh * HD + dim(u)) = make_float2(o[2 * u] * inv, o[2 * u + 1] * inv);
-      if (lane == 0) p.cnt[bh] = 0;
-    };
-
     Piece pc = p0;
     if (lane == 0) s_pc[0] = pc;
     new_state(0, pc);
     __syncwarp();
     if (lane == 0) mbar_arrive(mb_full);
     TRACE(8);
+    empties(cta, sc.C);
     Piece nx = pc;
     bool more = walk_next(nx, 0);
     uint4 qn = more ? load_quad(nx, lane % Q) : make_uint4(0, 0, 0, 0);
@@ -708,9 +747,9 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const DecodeParams p
       if (more) qn = load_quad(nx, lane % Q);
       if (k >= R) {
         mbar_wait(mb_done + 8 * ((k - R) % R), ((k - R) / R) & 1);
-        merge(k - R);
+        merge_fn<HD, NW>(p, smem, k - R, sc, cta, g0);
       }
-      build(k % R, qc);
+      build_fn<HD, NW>(smem, k % R, qc, p.scale_log2);
       __syncwarp();
       if (lane == 0) s_pc[k % R] = pc;
       new_state(k, pc);
@@ -720,7 +759,7 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const DecodeParams p
     TRACE(9);
     for (int j = max(0, k + 1 - R); j <= k; ++j) {
       mbar_wait(mb_done + 8 * (j % R), (j / R) & 1);
-      merge(j);
+      merge_fn<HD, NW>(p, smem, j, sc, cta, g0);
     }
     TRACE(10);
     return;
@@ -738,7 +777,7 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const DecodeParams p
 
   uint32_t jsel[8];
   auto set_jsel = [&](int slot) {
-    const uint32_t add = slot_off(slot);
+    const uint32_t add = slot_off<HD>(slot);
 #pragma unroll
     for (int k = 0; k < 8; ++k) jsel[k] = static_cast<uint32_t>(sub * 8 + ((k + rho) & 7)) * 4u + add;
   };
@@ -769,7 +808,7 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const DecodeParams p
     }
 #endif
     // scores (log2 domain): this lane's 16 dims via the q-table
-    float sc[kTPS];
+    float s[kTPS];
 #pragma unroll
     for (int i = 0; i < kTPS; ++i) {
       const uint32_t r0 = prmt(Rg.k[i].x, Rg.k[i].y, rotA);
@@ -780,18 +819,18 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const DecodeParams p
       const uint64_t b = pack2(lds_k(prmt(r1, jsel[4], 0x7604)), lds_k(prmt(r1, jsel[5], 0x7614)));
       a = fadd2(a, fadd2(b, pack2(lds_k(prmt(r1, jsel[6], 0x7624)), lds_k(prmt(r1, jsel[7], 0x7634)))));
       const float2 af = unpack2(a);
-      sc[i] = (af.x + af.y) * Rg.ks[i];
+      s[i] = (af.x + af.y) * Rg.ks[i];
     }
 #pragma unroll
     for (int o = 1; o < LPT; o <<= 1) {
 #pragma unroll
-      for (int i = 0; i < kTPS; ++i) sc[i] += __shfl_xor_sync(0xffffffffu, sc[i], o);
+      for (int i = 0; i < kTPS; ++i) s[i] += __shfl_xor_sync(0xffffffffu, s[i], o);
     }
     float mt = -INFINITY;
 #pragma unroll
     for (int i = 0; i < kTPS; ++i) {
-      sc[i] = (tok0 + i * G + g < t1) ? sc[i] : -INFINITY;
-      mt = fmaxf(mt, sc[i]);
+      s[i] = (tok0 + i * G + g < t1) ? s[i] : -INFINITY;
+      mt = fmaxf(mt, s[i]);
     }
 #pragma unroll
     for (int o = LPT; o < 32; o <<= 1) mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, o));
@@ -805,7 +844,7 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const DecodeParams p
     }
 #pragma unroll
     for (int i = 0; i < kTPS; ++i) {
-      const float pr = fast_exp2(sc[i] - m);     // masked: exp2(-inf) = 0
+      const float pr = fast_exp2(s[i] - m);     // masked: exp2(-inf) = 0
       l += pr;
       const float w = pr * Rg.vs[i];
       const uint64_t w2 = pack2(w, w);
