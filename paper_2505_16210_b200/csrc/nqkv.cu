@@ -234,25 +234,35 @@ int nqkv_quantize(const void* x, int64_t stride_b, int64_t stride_t, int64_t str
   if (tables_status() != 0) return NQKV_ERR_INTERNAL;
   const long long rows = static_cast<long long>(B) * n_new;   // token rows (b, t)
   if (rows == 0 || H == 0) return NQKV_OK;
-  if (rows >= (1ll << 31)) return NQKV_ERR_SHAPE;
+  const long long chunks = rows * H * (hd / 16);               // 16-element chunks
+  if (chunks >= (1ll << 31)) return NQKV_ERR_SHAPE;
   QuantParams p;
   p.x = static_cast<const __half*>(x);
   p.sb = stride_b; p.st = stride_t; p.sh = stride_h;
   p.pos = d_pos; p.codes = codes; p.scales = scales;
   p.B = B; p.n_new = n_new; p.H = H; p.Tc = Tc;
   p.blk_shift = blk_shift_of(blk);
+  p.total = static_cast<uint32_t>(chunks);
+  p.v256 = ((reinterpret_cast<uintptr_t>(x) & 31u) == 0 && stride_b % 16 == 0 && stride_t % 16 == 0 &&
+            stride_h % 16 == 0) ? 1 : 0;
+  if (stride_h == hd && stride_t == static_cast<int64_t>(H) * hd &&
+      (B == 1 || stride_b == static_cast<int64_t>(n_new) * H * hd))
+    p.v256 |= 2;
+  p.cpr = make_fastdiv(static_cast<uint32_t>(H * (hd / 16)));
+  p.nnew = make_fastdiv(static_cast<uint32_t>(n_new));
   p.tab = make_bucket_tab();
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const dim3 grid(static_cast<unsigned>(grid_for(rows * 32, 256, 8)));
+  // one warp per 64-chunk unit, grid-strided: up to 8 CTAs of 8 warps per SM
+  const dim3 grid(static_cast<unsigned>(grid_for((chunks + 1) / 2, 256, 8)));
   cudaError_t e;
   const size_t sm = kQuantSmem;
   if (hd == 64) {
-    e = blk == 32 ? launch_pdl(quantize_kernel<64, 2>, grid, dim3(256), sm, st, p)
-                  : launch_pdl(quantize_kernel<64, 4>, grid, dim3(256), sm, st, p);
+    e = blk == 32 ? launch_pdl(quantize_kernel<64, 32>, grid, dim3(256), sm, st, p)
+                  : launch_pdl(quantize_kernel<64, 64>, grid, dim3(256), sm, st, p);
   } else {
-    e = blk == 32   ? launch_pdl(quantize_kernel<128, 2>, grid, dim3(256), sm, st, p)
-        : blk == 64 ? launch_pdl(quantize_kernel<128, 4>, grid, dim3(256), sm, st, p)
-                    : launch_pdl(quantize_kernel<128, 8>, grid, dim3(256), sm, st, p);
+    e = blk == 32   ? launch_pdl(quantize_kernel<128, 32>, grid, dim3(256), sm, st, p)
+        : blk == 64 ? launch_pdl(quantize_kernel<128, 64>, grid, dim3(256), sm, st, p)
+                    : launch_pdl(quantize_kernel<128, 128>, grid, dim3(256), sm, st, p);
   }
   return e == cudaSuccess ? NQKV_OK : cuda_fail(e);
 }
