@@ -443,7 +443,7 @@ __device__ __noinline__ void merge_fn(const DecodeParams& p, unsigned char* smem
   if (lane == 0) p.cnt[bh] = 0;
 }
 
-template <int HD, int NW>
+template <int HD, int BLK, int NW>
 __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constant__ DecodeParams p) {
   using Ge = Geo<HD>;
   using Sm = Smem<HD, NW>;
@@ -616,8 +616,18 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
   walk_first(p0);
   const uint4 q0 = load_quad(p0, tid % Q);
   const int g = lane / LPT, sub = lane % LPT;
-  const int sidx = (sub * kLaneDims) >> p.blk_shift;
-  // rows of (b, h) start at row index rb = (b*H + h)*Tc (32-bit)
+  constexpr int NBLK = HD / BLK;
+  const int sidx = (sub * kLaneDims) / BLK;
+  // Per-lane 32-bit byte offsets (codes, scales) of the load cursor: this
+  // lane's bytes of the stage to load next (token tok0 + g of its (b, h));
+  // slot i is at the immediate offset i*G rows.  Advanced by NC*ST rows per
+  // stage.  (The host guarantees each codes tensor is < 4 GB.)
+  uint32_t loff_c = 0, loff_s = 0;
+  auto set_ptrs = [&](int rb, int tok0) {
+    const uint32_t r = static_cast<uint32_t>(rb + tok0 + g);
+    loff_c = r * (HD / 2) + sub * 8;
+    loff_s = (r * NBLK + sidx) * 4;
+  };
   auto load_stage = [&](StageRegs& Rg, int rb, int tok0, int t1) {
 #ifdef NQKV_EXP_NOLOAD
 #pragma unroll
@@ -629,17 +639,17 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
     }
     return;
 #endif
-    const int rlast = rb + t1 - 1;
-    const int r0 = rb + tok0 + g;
+    (void)rb;
+    // rows >= t1 are not loaded: the slot keeps earlier (finite) data and is
+    // masked in consume
 #pragma unroll
     for (int i = 0; i < kTPS; ++i) {
-      const uint32_t r = static_cast<uint32_t>(min(r0 + i * G, rlast));   // clamp: valid rows
-      const uint32_t cw = r * (HD / 16) + static_cast<uint32_t>(sub);     // 8-byte word index
-      const uint32_t sw = r * static_cast<uint32_t>(nblk) + static_cast<uint32_t>(sidx);
-      Rg.k[i] = ldg_stream_64(addr_wide(p.kc, cw, 8));
-      Rg.v[i] = ldg_stream_64(addr_wide(p.vc, cw, 8));
-      Rg.ks[i] = ldg_nc_f32(static_cast<const float*>(addr_wide(p.ks, sw, 4)));
-      Rg.vs[i] = ldg_nc_f32(static_cast<const float*>(addr_wide(p.vs, sw, 4)));
+      if (tok0 + i * G + g < t1) {
+        Rg.k[i] = ldg_stream_64(p.kc + loff_c + i * G * (HD / 2));
+        Rg.v[i] = ldg_stream_64(p.vc + loff_c + i * G * (HD / 2));
+        Rg.ks[i] = ldg_nc_f32(reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(p.ks) + loff_s) + i * G * NBLK);
+        Rg.vs[i] = ldg_nc_f32(reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(p.vs) + loff_s) + i * G * NBLK);
+      }
     }
   };
   // load cursor (piece lp, stage ls, piece index lpi): D stages ahead of
@@ -654,12 +664,23 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
       ls = warp;
       ++lpi;
     }
-    if (lvalid) lrb = rowbase(lp);
+    if (lvalid) {
+      lrb = rowbase(lp);
+      set_ptrs(lrb, lp.t0 + ls * ST);
+    }
   }
   // register ring: buffer d holds the stage at (tok0 mtok[d], piece end mt1[d],
   // piece index mpi[d]); refilled with the cursor's next stage once consumed
   constexpr int D = NQKV_DEPTH;
   StageRegs RG[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+#pragma unroll
+    for (int i = 0; i < kTPS; ++i) {
+      RG[d].k[i] = RG[d].v[i] = make_uint2(0, 0);
+      RG[d].ks[i] = RG[d].vs[i] = 0.0f;
+    }
+  }
   int mtok[D], mt1[D], mpi[D];
   bool has[D];
   auto fill = [&](int d) -> bool {
@@ -675,7 +696,13 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
         ls = warp;
         ++lpi;
       } while (ls >= nstages(lp));
-      if (lvalid) lrb = rowbase(lp);
+      if (lvalid) {
+        lrb = rowbase(lp);
+        set_ptrs(lrb, lp.t0 + ls * ST);
+      }
+    } else {
+      loff_c += NC * ST * (HD / 2);
+      loff_s += NC * ST * NBLK * 4;
     }
     return true;
   };
@@ -826,12 +853,13 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
 #pragma unroll
       for (int i = 0; i < kTPS; ++i) s[i] += __shfl_xor_sync(0xffffffffu, s[i], o);
     }
-    float mt = -INFINITY;
+    if (tok0 + ST > t1) {             // warp-uniform: only a piece's last stage is partial
 #pragma unroll
-    for (int i = 0; i < kTPS; ++i) {
-      s[i] = (tok0 + i * G + g < t1) ? s[i] : -INFINITY;
-      mt = fmaxf(mt, s[i]);
+      for (int i = 0; i < kTPS; ++i) s[i] = (tok0 + i * G + g < t1) ? s[i] : -INFINITY;
     }
+    float mt = s[0];
+#pragma unroll
+    for (int i = 1; i < kTPS; ++i) mt = fmaxf(mt, s[i]);
 #pragma unroll
     for (int o = LPT; o < 32; o <<= 1) mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, o));
     if (mt > m) {                     // warp-uniform; the stage has >= 1 valid token

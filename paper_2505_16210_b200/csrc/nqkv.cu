@@ -98,9 +98,9 @@ cudaError_t launch_pdl(void (*kern)(P), dim3 grid, dim3 block, size_t smem, cuda
   return cudaLaunchKernelEx(&cfg, kern, prm);
 }
 
-template <int HD>
-int launch_decode(const DecodeParams& p, cudaStream_t st) {
-  auto kern = decode_kernel<HD, kDecodeWarps>;
+template <int HD, int BLK>
+int launch_decode_blk(const DecodeParams& p, cudaStream_t st) {
+  auto kern = decode_kernel<HD, BLK, kDecodeWarps>;
   const size_t smem = Smem<HD, kDecodeWarps>::kBytes;
   static bool attr_set = false;
   static std::mutex mu;
@@ -113,13 +113,22 @@ int launch_decode(const DecodeParams& p, cudaStream_t st) {
       attr_set = true;
     }
   }
-  // one CTA per SM (the kernel needs ~140-215 KB of shared memory); CTAs
+  // one CTA per SM (the kernel needs ~150-225 KB of shared memory); CTAs
   // beyond what the token count needs exit after the prologue
   int sms = device_sms();
   if (sms > kMaxGrid) sms = kMaxGrid;
   const cudaError_t e = launch_pdl(kern, dim3(static_cast<unsigned>(sms)), dim3(kDecodeWarps * 32),
                                    smem, st, p);
   return e == cudaSuccess ? NQKV_OK : cuda_fail(e);
+}
+
+template <int HD>
+int launch_decode(const DecodeParams& p, cudaStream_t st) {
+  switch (p.blk_shift) {
+    case 5: return launch_decode_blk<HD, 32>(p, st);
+    case 6: return launch_decode_blk<HD, 64>(p, st);
+    default: return HD == 128 ? launch_decode_blk<HD, 128>(p, st) : NQKV_ERR_UNSUPPORTED;
+  }
 }
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
@@ -148,6 +157,7 @@ int decode_common(const void* q, const uint8_t* k_codes, const float* k_scales,
   if (int s = check_geometry(hd, blk)) return s;
   if (B < 0 || H < 0 || Tc <= 0 || Tc % 64 || B > kMaxBatch) return NQKV_ERR_SHAPE;
   if (static_cast<long long>(B) * H * Tc >= (1ll << 31)) return NQKV_ERR_SHAPE;
+  if (static_cast<long long>(B) * H * Tc * (hd / 2) >= (1ll << 32)) return NQKV_ERR_SHAPE;  // 32-bit offsets
   if (!aligned16(q) || !aligned16(k_codes) || !aligned16(v_codes) || !aligned16(out) ||
       !aligned16(k_scales) || !aligned16(v_scales))
     return NQKV_ERR_ALIGN;

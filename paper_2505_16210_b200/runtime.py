@@ -77,7 +77,7 @@ class DecodeRunner:
             K, V = K.to(self.dev), V.to(self.dev)
             for x, codes, scales in ((K, c.k_codes, c.k_scales), (V, c.v_codes, c.v_scales)):
                 if flush is not None:
-                    flush.add_(1)
+                    flush.sum()         # read-only L2 sweep: evicts without dirty write-backs
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
                 e0.record()

@@ -18,7 +18,7 @@ from synth import workloads as W  # noqa: E402
 def timeit(fn, flush, reps=10):
     ts = []
     for _ in range(reps):
-        flush.add_(1)
+        flush.sum()                 # read-only L2 sweep: evicts without leaving dirty lines
         torch.cuda._sleep(200000)       # keep the GPU busy while the host enqueues
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)

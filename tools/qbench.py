@@ -20,7 +20,7 @@ for (B, T, H, hd) in [(8, 2048, 32, 64), (32, 1988, 32, 128), (4, 8192, 40, 128)
     z = torch.zeros(B, dtype=torch.int32, device="cuda")
     ts = []
     for i in range(12):
-        flush.add_(1)
+        flush.sum()                 # read-only L2 sweep: evicts without leaving dirty lines
         torch.cuda._sleep(100000)
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)

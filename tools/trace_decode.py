@@ -35,7 +35,7 @@ ws = N.make_workspace(B, H, hd, Tc, "cuda")
 flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
 warm = os.environ.get("WARM") == "1"    # trace the 2nd of two back-to-back launches (no flush between)
 for _ in range(5):
-    flush.add_(1)                       # evict the cache from L2: HBM-honest timing
+    flush.sum()                         # read-only L2 sweep (no dirty lines): HBM-honest timing
     torch.cuda._sleep(100000)
     if warm:
         cache.attend(q, L, ws)
