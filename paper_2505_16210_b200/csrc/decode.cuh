@@ -537,7 +537,6 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
     empties(blockIdx.x * NW + warp, gridDim.x * NW);
     return;
   }
-  TRACE(11);
   sc.C = min(static_cast<int>(gridDim.x), max(1, (sc.N + p.min_tokens - 1) / p.min_tokens));
   if (static_cast<int>(blockIdx.x) >= sc.C) return;
   sc.q = sc.N / sc.C;
@@ -786,6 +785,7 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
     TRACE(9);
     for (int j = max(0, k + 1 - R); j <= k; ++j) {
       mbar_wait(mb_done + 8 * (j % R), (j / R) & 1);
+      if (j == k) TRACE(11);
       merge_fn<HD, NW>(p, smem, j, sc, cta, g0);
     }
     TRACE(10);

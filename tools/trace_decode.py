@@ -46,7 +46,7 @@ for _ in range(5):
     torch.cuda.synchronize()
 t = tr.view(148, NW, 16).cpu()
 t0 = t[:, :, 0][t[:, :, 0] > 0].min()
-names = ["entry", "pdl_wait", "prefix", "walk", "loads issued", "V LUT", "table0", "sync", "full0", "loop end", "exit", "zero-fill", "last odd step", "g0/g1", "walk-computed"]
+names = ["entry", "pdl_wait", "prefix", "walk", "loads issued", "V LUT", "table0", "sync", "full0", "loop end", "exit", "prod: last done", "last odd step", "g0/g1", "walk-computed"]
 for role, sl in (("consumer", slice(0, NW - 1)), ("producer", slice(NW - 1, NW))):
     x = t[:, sl, :].reshape(-1, 16)
     x = x[x[:, 0] > 0]
@@ -61,3 +61,24 @@ for role, sl in (("consumer", slice(0, NW - 1)), ("producer", slice(NW - 1, NW))
 w = t[:, :NW - 1, 15]
 w = w[w > 0].double() / 1000.0
 print(f"consumer wait on full barriers: med {w.median():.2f} max {w.max():.2f} us per warp")
+
+# per-CTA: slowest consumer loop end vs number of pieces in the CTA's range
+import numpy as np  # noqa: E402
+lens_h = [T] * B
+N = B * H * T
+C = min(148, max(1, -(-N // 512)))
+pref = np.cumsum([0] + [H * n for n in lens_h])
+ends = (t[:, :NW - 1, 9].double() - t0.double()) / 1000.0
+rows = []
+for c in range(C):
+    g0, g1 = c * N // C, (c + 1) * N // C
+    starts = [int(pref[b] + h * lens_h[b]) for b in range(B) for h in range(H)]
+    inner = sum(1 for s0 in starts if g0 < s0 < g1)
+    e = ends[c][ends[c] > 0]
+    rows.append((inner + 1, float(e.max()) if len(e) else 0.0, float(e.min()) if len(e) else 0.0))
+for npc in sorted(set(r[0] for r in rows)):
+    sel = [r for r in rows if r[0] == npc]
+    print(f"pieces={npc}: CTAs {len(sel)} loop-end max med {np.median([r[1] for r in sel]):.2f} "
+          f"min-warp med {np.median([r[2] for r in sel]):.2f} us")
+order = sorted(rows, key=lambda r: r[1])
+print("fastest CTAs", [(r[0], round(r[1], 1)) for r in order[:5]], "slowest", [(r[0], round(r[1], 1)) for r in order[-5:]])
