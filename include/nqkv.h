@@ -155,6 +155,30 @@ int nqkv_decode_step(const void* k_new, const void* v_new, int64_t new_stride_b,
                      int hd, int blk, int Tc, float softmax_scale, float* out, void* workspace,
                      size_t ws_bytes, void* stream);
 
+/* Per-step schedule (optional).  Every layer of a decode step shares
+ * (B, H, Tc, seq_lens): nqkv_decode_plan computes the launch's work
+ * partition once -- streamed lengths, token prefix, CTA count and each CTA's
+ * first/last piece -- into `plan` (device, >= nqkv_decode_plan_bytes() bytes,
+ * 16-byte aligned, caller-owned), so that each layer's decode kernel starts
+ * streaming without rebuilding it.  fused = 1 for nqkv_decode_step_planned
+ * (the appended row is not streamed), 0 for nqkv_decode_attention_planned.
+ * The plan must be recomputed whenever seq_lens, B, H, Tc or fused change;
+ * results are bit-identical to the unplanned calls. */
+size_t nqkv_decode_plan_bytes(void);
+int nqkv_decode_plan(const int32_t* d_seq_lens, int B, int H, int Tc, int fused, void* plan,
+                     size_t plan_bytes, void* stream);
+int nqkv_decode_attention_planned(const void* q, const uint8_t* k_codes, const float* k_scales,
+                                  const uint8_t* v_codes, const float* v_scales,
+                                  const int32_t* d_seq_lens, int B, int H, int hd, int blk, int Tc,
+                                  float softmax_scale, float* out, void* workspace,
+                                  size_t ws_bytes, const void* plan, void* stream);
+int nqkv_decode_step_planned(const void* k_new, const void* v_new, int64_t new_stride_b,
+                             int64_t new_stride_h, const void* q, uint8_t* k_codes,
+                             float* k_scales, uint8_t* v_codes, float* v_scales,
+                             const int32_t* d_seq_lens, int B, int H, int hd, int blk, int Tc,
+                             float softmax_scale, float* out, void* workspace, size_t ws_bytes,
+                             const void* plan, void* stream);
+
 /* Test hook: the kernels' code function on fp32 inputs already normalised
  * to [-1, 1] (values outside are clamped).  d_n device float[count],
  * d_codes device uint8[count]. */

@@ -84,7 +84,8 @@ struct DecodeParams {
   float scale_log2;         // softmax_scale * log2(e)
   Levels lv;
   BucketTab tab;
-  unsigned long long* trace;   // NQKV_TRACE builds: per-warp globaltimer stamps [grid][NW][8]
+  const int* plan;             // optional per-step schedule (nqkv_decode_plan); nullptr: computed here
+  unsigned long long* trace;   // NQKV_TRACE builds: per-warp globaltimer stamps [grid][NW][16]
 };
 
 #ifdef NQKV_TRACE
@@ -231,6 +232,111 @@ template <int HD>
 __device__ __forceinline__ uint32_t slot_off(int r) {
   return HD == 64 ? static_cast<uint32_t>(r >> 1) * 0x10000u + static_cast<uint32_t>(r & 1) * 128u
                   : static_cast<uint32_t>(r) * 0x10000u;
+}
+
+// ------------------------------------------------------------------- plan
+// A decode step's schedule depends only on (B, H, Tc, seq_lens, fused, grid),
+// which every layer of the step shares: nqkv_decode_plan computes it once
+// (decode_plan_kernel) and each layer's decode kernel reads its CTA's entry
+// instead of rebuilding it on its own serial prologue path.
+// Layout (int32): header [0, 8) = {N, C, q, r, B, H, fused, Tc};
+// per-CTA entries [8, 8 + 16 kMaxGrid) = {first piece (6), last piece (6),
+// reorder, limit, g0, g1}; then len'[kMaxBatch], prefix[kMaxBatch + 1] and
+// the fused single-token mask[kMaxBatch / 32].
+constexpr int kPlanHdr = 8;
+constexpr int kPlanEntry = 16;
+constexpr int kPlanLen = kPlanHdr + kPlanEntry * kMaxGrid;
+constexpr int kPlanPref = kPlanLen + kMaxBatch;
+constexpr int kPlanOne = kPlanPref + kMaxBatch + 1;
+constexpr int kPlanInts = kPlanOne + kMaxBatch / 32;
+
+// The piece of the range [g, g1) that starts at global token g.
+__device__ __forceinline__ void locate_piece(const int* pref, const int* len, int B, int H, int g, int g1,
+                                             Piece& pc) {
+  int lo = 0, hi = B;                   // largest b with pref[b] <= g (pref[B] > g)
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (pref[mid] <= g) lo = mid; else hi = mid;
+  }
+  pc.b = lo;
+  pc.len = len[lo];
+  const int off = g - pref[lo];
+  pc.h = off / pc.len;
+  pc.t0 = off - pc.h * pc.len;
+  pc.gs = g;
+  pc.t1 = min(pc.len, pc.t0 + (g1 - g));
+}
+
+// Range [g0, g1) of a CTA -> its first piece, its last piece, and whether the
+// last piece (split with the next CTA) is processed first.
+__device__ __forceinline__ void cta_walk(const int* pref, const int* len, int B, int H, int g0, int g1,
+                                         Piece& pf, Piece& pl, int& reorder, int& limit) {
+  locate_piece(pref, len, B, H, g0, g1, pf);
+  locate_piece(pref, len, B, H, g1 - 1, g1, pl);
+  locate_piece(pref, len, B, H, max(g0, g1 - 1 - pl.t0), g1, pl);
+  reorder = pl.gs != pf.gs && pl.t1 < pl.len;
+  limit = reorder ? pl.gs : g1;
+}
+
+__global__ void __launch_bounds__(1024) decode_plan_kernel(const int32_t* seq_lens, int B, int H, int Tc,
+                                                           int fused, int G, int min_tokens, int* plan) {
+  __shared__ int s_len[kMaxBatch], s_pref[kMaxBatch + 1], s_wsum[32];
+  pdl_trigger();
+  pdl_wait();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int raw = tid < B ? min(max(seq_lens[tid], 0), Tc) : 0;
+  const unsigned one = __ballot_sync(0xffffffffu, fused && raw == 1);
+  if (lane == 0 && warp * 32 < B) plan[kPlanOne + warp] = static_cast<int>(one);
+  const int len = fused ? max(raw - 1, 0) : raw;
+  int n = H * len;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, n, o);
+    if (lane >= o) n += v;
+  }
+  if (lane == 31) s_wsum[warp] = n;
+  __syncthreads();
+  if (warp == 0) {
+    int w = s_wsum[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += v;
+    }
+    s_wsum[lane] = w;                    // inclusive prefix of the warp totals
+  }
+  __syncthreads();
+  if (tid < B) {
+    const int incl = n + (warp ? s_wsum[warp - 1] : 0);
+    s_len[tid] = len;
+    s_pref[tid + 1] = incl;
+    plan[kPlanLen + tid] = len;
+    plan[kPlanPref + tid + 1] = incl;
+  }
+  if (tid == 0) {
+    s_pref[0] = 0;
+    plan[kPlanPref] = 0;
+  }
+  __syncthreads();
+  Sched sc;
+  sc.N = s_pref[B];
+  sc.C = min(G, max(1, (sc.N + min_tokens - 1) / min_tokens));
+  sc.q = sc.N / sc.C;
+  sc.r = sc.N - sc.q * sc.C;
+  if (tid == 0) {
+    plan[0] = sc.N; plan[1] = sc.C; plan[2] = sc.q; plan[3] = sc.r;
+    plan[4] = B; plan[5] = H; plan[6] = fused; plan[7] = Tc;
+  }
+  if (sc.N > 0 && tid < sc.C) {
+    const int g0 = sc.bnd(tid), g1 = sc.bnd(tid + 1);
+    Piece pf, pl;
+    int ro, lim;
+    cta_walk(s_pref, s_len, B, H, g0, g1, pf, pl, ro, lim);
+    int* e = plan + kPlanHdr + tid * kPlanEntry;
+    e[0] = pf.gs; e[1] = pf.b; e[2] = pf.h; e[3] = pf.len; e[4] = pf.t0; e[5] = pf.t1;
+    e[6] = pl.gs; e[7] = pl.b; e[8] = pl.h; e[9] = pl.len; e[10] = pl.t0; e[11] = pl.t1;
+    e[12] = ro; e[13] = lim; e[14] = g0; e[15] = g1;
+  }
 }
 
 // ---------------------------------------------------------------- producer
@@ -467,7 +573,14 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
   const bool fused = p.k_new != nullptr;
   const int nblk = HD >> p.blk_shift;
 
-  // ---- prologue independent of the previous kernel: levels, barriers
+  // ---- prologue independent of the previous kernel.  Warm the constant
+  // cache: one lane per 64-byte line of the parameter block, all in parallel
+  // (otherwise each first use of a parameter line on the serial prologue path
+  // is a separate cold miss).
+  if (warp == 1 && lane * 16 < static_cast<int>(sizeof(DecodeParams) / 4)) {
+    const uint32_t w = reinterpret_cast<const uint32_t*>(&p)[lane * 16];
+    if (w == 0x9E3779B9u && lane == 31) s_tab[0].x = 0.0f;   // keeps the load; never true in practice
+  }
   if (tid < 16) s_lv[tid] = p.lv.v[tid];
   if (tid < kNumBuckets) s_tab[tid] = p.tab.e[tid];
   if (tid == 0) {
@@ -480,42 +593,106 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
   pdl_trigger();
   pdl_wait();
   TRACE(1);
-  // ---- per-batch streamed lengths and token prefix: tokens(b) = H * len'_b.
-  // Fused step: the appended row (len - 1) is not streamed; the producer
-  // quantises it and folds it into the piece merge (s_len holds len').
-  if (warp == 0) {
-    int carry = 0;
-    if (lane == 0) s_pref[0] = 0;
-    for (int b0 = 0; b0 < p.B; b0 += 32) {
-      const int b = b0 + lane;
-      const int raw = b < p.B ? min(max(p.seq_lens[b], 0), p.Tc) : 0;
-      const unsigned one = __ballot_sync(0xffffffffu, fused && raw == 1);
-      if (lane == 0) reinterpret_cast<uint32_t*>(smem + Sm::kOne)[b0 >> 5] = one;
-      int n = 0;
-      if (b < p.B) {
-        const int len = fused ? max(raw - 1, 0) : raw;
-        s_len[b] = len;
-        n = p.H * len;
-      }
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_up_sync(0xffffffffu, n, o);
-        if (lane >= o) n += v;
-      }
-      if (b < p.B) s_pref[b + 1] = carry + n;
-      carry += __shfl_sync(0xffffffffu, n, 31);
-    }
-  }
-  __syncthreads();
-  TRACE(2);
+  const uint32_t* s_one = reinterpret_cast<const uint32_t*>(smem + Sm::kOne);
+  Piece* s_walk = reinterpret_cast<Piece*>(smem + Sm::kWalk);
+  int* s_wi = reinterpret_cast<int*>(smem + Sm::kWalk + 48);
+  const int cta = blockIdx.x;
   Sched sc;
-  sc.N = s_pref[p.B];
+  int g0 = 0, g1 = 0;
+  Piece p0;                    // first piece in processing order
+  // per-batch arrays into shared memory: from the plan, or computed here
+  auto copy_plan_arrays = [&]() {
+    for (int i = tid; i < p.B; i += NT) s_len[i] = __ldcg(p.plan + kPlanLen + i);
+    for (int i = tid; i <= p.B; i += NT) s_pref[i] = __ldcg(p.plan + kPlanPref + i);
+    for (int i = tid; i < (p.B + 31) / 32; i += NT)
+      reinterpret_cast<uint32_t*>(smem + Sm::kOne)[i] = __ldcg(p.plan + kPlanOne + i);
+  };
+  if (p.plan) {
+    const int4 hdr = __ldcg(reinterpret_cast<const int4*>(p.plan));
+    sc.N = hdr.x; sc.C = hdr.y; sc.q = hdr.z; sc.r = hdr.w;
+    if (sc.N == 0 || cta >= sc.C) {
+      if (sc.N == 0) copy_plan_arrays();
+      __syncthreads();
+    } else {
+      const int4* e4 = reinterpret_cast<const int4*>(p.plan + kPlanHdr + cta * kPlanEntry);
+      const int4 a = __ldcg(e4), b = __ldcg(e4 + 1), c = __ldcg(e4 + 2), d = __ldcg(e4 + 3);
+      Piece pf, pl;
+      pf.gs = a.x; pf.b = a.y; pf.h = a.z; pf.len = a.w; pf.t0 = b.x; pf.t1 = b.y;
+      pl.gs = b.z; pl.b = b.w; pl.h = c.x; pl.len = c.y; pl.t0 = c.z; pl.t1 = c.w;
+      g0 = d.z;
+      g1 = d.w;
+      p0 = d.x ? pl : pf;
+      if (tid == 0) {
+        s_walk[0] = pf;
+        s_walk[1] = pl;
+        s_wi[0] = d.x;
+        s_wi[1] = d.y;
+        reinterpret_cast<int*>(smem + Sm::kWalk + 56)[0] = 0;
+      }
+    }
+  } else {
+    // ---- per-batch streamed lengths and token prefix: tokens(b) = H * len'_b.
+    // Fused step: the appended row (len - 1) is not streamed; the producer
+    // quantises it and folds it into the piece merge (s_len holds len').
+    if (warp == 0) {
+      int carry = 0;
+      if (lane == 0) s_pref[0] = 0;
+      for (int b0 = 0; b0 < p.B; b0 += 32) {
+        const int b = b0 + lane;
+        const int raw = b < p.B ? min(max(p.seq_lens[b], 0), p.Tc) : 0;
+        const unsigned one = __ballot_sync(0xffffffffu, fused && raw == 1);
+        if (lane == 0) reinterpret_cast<uint32_t*>(smem + Sm::kOne)[b0 >> 5] = one;
+        int n = 0;
+        if (b < p.B) {
+          const int len = fused ? max(raw - 1, 0) : raw;
+          s_len[b] = len;
+          n = p.H * len;
+        }
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int v = __shfl_up_sync(0xffffffffu, n, o);
+          if (lane >= o) n += v;
+        }
+        if (b < p.B) s_pref[b + 1] = carry + n;
+        carry += __shfl_sync(0xffffffffu, n, 31);
+      }
+    }
+    __syncthreads();
+    sc.N = s_pref[p.B];
+    if (sc.N > 0) {
+      sc.C = min(static_cast<int>(gridDim.x), max(1, (sc.N + p.min_tokens - 1) / p.min_tokens));
+      sc.q = sc.N / sc.C;
+      sc.r = sc.N - sc.q * sc.C;
+      if (cta < sc.C) {
+        g0 = sc.bnd(cta);
+        g1 = sc.bnd(cta + 1);
+        // Processing order.  If the range's last piece is split with the next
+        // CTA it is processed FIRST, so that both cross-CTA partials of this CTA
+        // are published early and the last piece processed (normally a whole
+        // sequence) needs no cross-CTA merge at the end of the kernel.  Order:
+        // [last], first, first+1, ..., up to (not including) the moved last
+        // piece.  (Kept in shared memory: the walkers run rarely.)
+        if (tid == 0) {
+          Piece pf, pl;
+          int ro, lim;
+          cta_walk(s_pref, s_len, p.B, p.H, g0, g1, pf, pl, ro, lim);
+          s_walk[0] = pf;
+          s_walk[1] = pl;
+          s_wi[0] = ro;
+          s_wi[1] = lim;
+          reinterpret_cast<int*>(smem + Sm::kWalk + 56)[0] = 0;
+        }
+      }
+    }
+    __syncthreads();
+    if (sc.N > 0 && cta < sc.C) p0 = s_walk[s_wi[0] ? 1 : 0];
+  }
+  TRACE(2);
 
   // ---- empty sequences (out = 0, reading R12) and, in a fused step,
   // sequences whose only token is the appended one (out = its value).  Off
   // the critical path: done by the producer warps after table 0 (or here by
   // every CTA when there is no token to stream at all).
-  const uint32_t* s_one = reinterpret_cast<const uint32_t*>(smem + Sm::kOne);
   auto empties = [&](int wid, int nwarps) {
     for (int i = wid * 32 + lane; i < p.B * p.H * HD; i += nwarps * 32) {
       const int b = i / (p.H * HD);
@@ -537,29 +714,10 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
     empties(blockIdx.x * NW + warp, gridDim.x * NW);
     return;
   }
-  sc.C = min(static_cast<int>(gridDim.x), max(1, (sc.N + p.min_tokens - 1) / p.min_tokens));
-  if (static_cast<int>(blockIdx.x) >= sc.C) return;
-  sc.q = sc.N / sc.C;
-  sc.r = sc.N - sc.q * sc.C;
-  const int cta = blockIdx.x;
-  const int g0 = sc.bnd(cta), g1 = sc.bnd(cta + 1);
+  if (cta >= sc.C) return;
   TRACE(13);
 
-  // ---- piece walking (identical in every warp)
-  auto locate = [&](int g, Piece& pc) {
-    int lo = 0, hi = p.B;                 // largest b with pref[b] <= g (pref[B] > g)
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (s_pref[mid] <= g) lo = mid; else hi = mid;
-    }
-    pc.b = lo;
-    pc.len = s_len[lo];
-    const int off = g - s_pref[lo];
-    pc.h = off / pc.len;
-    pc.t0 = off - pc.h * pc.len;
-    pc.gs = g;
-    pc.t1 = min(pc.len, pc.t0 + (g1 - g));
-  };
+  // ---- piece walking (identical in every warp; needs s_len / s_pref)
   auto next_piece_to = [&](Piece& pc, int lim) -> bool {
     const int g = pc.gs + (pc.t1 - pc.t0);
     if (g >= lim) return false;
@@ -575,28 +733,6 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
     pc.t1 = min(pc.len, g1 - g);
     return true;
   };
-  // Processing order.  If the range's last piece is split with the next CTA
-  // it is processed FIRST, so that both cross-CTA partials of this CTA are
-  // published early and the last piece processed (normally a whole sequence)
-  // needs no cross-CTA merge at the end of the kernel.  Order: [last], first,
-  // first+1, ..., up to (not including) the moved last piece.
-  // (kept in shared memory: the walkers run rarely, registers are scarce)
-  Piece* s_walk = reinterpret_cast<Piece*>(smem + Sm::kWalk);
-  int* s_wi = reinterpret_cast<int*>(smem + Sm::kWalk + 48);
-  if (tid == 0) {
-    Piece pf, pl;
-    locate(g0, pf);
-    locate(g1 - 1, pl);
-    locate(max(g0, g1 - 1 - pl.t0), pl);
-    const bool ro = pl.gs != pf.gs && pl.t1 < pl.len;
-    s_walk[0] = pf;
-    s_walk[1] = pl;
-    s_wi[0] = ro;
-    s_wi[1] = ro ? pl.gs : g1;
-  }
-  TRACE(14);
-  __syncthreads();
-  TRACE(3);
   auto walk_first = [&](Piece& pc) { pc = s_walk[s_wi[0] ? 1 : 0]; };
   auto walk_next = [&](Piece& pc, int k) -> bool {   // k = index of pc in processing order
     if (s_wi[0] && k == 0) { pc = s_walk[0]; return true; }
@@ -611,8 +747,6 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
 
   // ---- q of piece 0 first (its table is the first thing the consumers
   // need), then the consumers' first stage loads
-  Piece p0;
-  walk_first(p0);
   const uint4 q0 = load_quad(p0, tid % Q);
   const int g = lane / LPT, sub = lane % LPT;
   constexpr int NBLK = HD / BLK;
@@ -651,23 +785,16 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
       }
     }
   };
-  // load cursor (piece lp, stage ls, piece index lpi): D stages ahead of
-  // consumption, across piece boundaries
+  // Load cursor (piece lp, stage ls, piece index lpi): D - 1 stages ahead of
+  // consumption, across piece boundaries.  It advances lazily (at the next
+  // fill), so a warp whose first stage lies in piece 0 issues that load before
+  // any piece walking -- in plan mode before the per-batch arrays are in
+  // shared memory.
   Piece lp = p0;
   int ls = warp, lpi = 0;
-  bool lvalid = warp < NC;
-  int lrb = 0;
-  if (lvalid) {
-    while (ls >= nstages(lp)) {
-      if (!walk_next(lp, lpi)) { lvalid = false; break; }
-      ls = warp;
-      ++lpi;
-    }
-    if (lvalid) {
-      lrb = rowbase(lp);
-      set_ptrs(lrb, lp.t0 + ls * ST);
-    }
-  }
+  bool lvalid = warp < NC, ladv = false;
+  int lrb = rowbase(p0);
+  set_ptrs(lrb, p0.t0 + warp * ST);
   // register ring: buffer d holds the stage at (tok0 mtok[d], piece end mt1[d],
   // piece index mpi[d]); refilled with the cursor's next stage once consumed
   constexpr int D = NQKV_DEPTH;
@@ -684,32 +811,34 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
   bool has[D];
   auto fill = [&](int d) -> bool {
     if (!lvalid) return false;
+    if (ladv) {
+      ls += NC;
+      loff_c += NC * ST * (HD / 2);
+      loff_s += NC * ST * NBLK * 4;
+    }
+    ladv = true;
+    if (ls >= nstages(lp)) {
+      do {
+        if (!walk_next(lp, lpi)) { lvalid = false; return false; }
+        ls = warp;
+        ++lpi;
+      } while (ls >= nstages(lp));
+      lrb = rowbase(lp);
+      set_ptrs(lrb, lp.t0 + ls * ST);
+    }
     mtok[d] = lp.t0 + ls * ST;
     mt1[d] = lp.t1;
     mpi[d] = lpi;
     load_stage(RG[d], lrb, mtok[d], mt1[d]);
-    ls += NC;
-    if (ls >= nstages(lp)) {
-      do {
-        if (!walk_next(lp, lpi)) { lvalid = false; break; }
-        ls = warp;
-        ++lpi;
-      } while (ls >= nstages(lp));
-      if (lvalid) {
-        lrb = rowbase(lp);
-        set_ptrs(lrb, lp.t0 + ls * ST);
-      }
-    } else {
-      loff_c += NC * ST * (HD / 2);
-      loff_s += NC * ST * NBLK * 4;
-    }
     return true;
   };
 #pragma unroll
-  for (int d = 0; d < D - 1; ++d) has[d] = fill(d);
-  has[D - 1] = false;
+  for (int d = 0; d < D; ++d) has[d] = false;
+  // first stage now if it needs no walking (and the arrays are present)
+  const bool early = !p.plan || warp < nstages(p0);
+  if (early) has[0] = fill(0);
+  if (p.plan) copy_plan_arrays();
   TRACE(4);
-
   // ---- V LUT and the table of piece 0, built by all threads (thread: pair
   // quad tid % Q); T[e][j] = RN(c q_{2j} L[e & 15]) + RN(c q_{2j+1} L[e >> 4])
   for (int i = tid; i < 256 * 16; i += NT) {     // V LUT; 16 B = two lane copies per store
@@ -737,6 +866,9 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
   TRACE(6);
   __syncthreads();
   TRACE(7);
+  if (!early) has[0] = fill(0);
+#pragma unroll
+  for (int d = 1; d < D - 1; ++d) has[d] = fill(d);
 
   if (warp == NC) {
     // ================================================================ producer

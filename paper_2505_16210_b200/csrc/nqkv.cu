@@ -72,6 +72,11 @@ int device_sms() {
   return sms > 0 ? sms : 148;
 }
 
+int decode_grid() {
+  const int sms = device_sms();
+  return sms > kMaxGrid ? kMaxGrid : sms;
+}
+
 long long grid_for(long long work, int threads, int per_sm) {
   long long blocks = (work + threads - 1) / threads;
   const long long cap = static_cast<long long>(device_sms()) * per_sm;
@@ -82,6 +87,22 @@ long long grid_for(long long work, int threads, int per_sm) {
 // Launch with programmatic stream serialization (PDL) so the kernel's
 // prologue overlaps the previous kernel's tail; device code waits with
 // griddepcontrol.wait before reading anything the previous kernel wrote.
+template <typename... Args, typename... Actual>
+cudaError_t launch_pdl_n(void (*kern)(Args...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                         Actual... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 template <typename P>
 cudaError_t launch_pdl(void (*kern)(P), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                        const P& prm) {
@@ -115,10 +136,8 @@ int launch_decode_blk(const DecodeParams& p, cudaStream_t st) {
   }
   // one CTA per SM (the kernel needs ~150-225 KB of shared memory); CTAs
   // beyond what the token count needs exit after the prologue
-  int sms = device_sms();
-  if (sms > kMaxGrid) sms = kMaxGrid;
-  const cudaError_t e = launch_pdl(kern, dim3(static_cast<unsigned>(sms)), dim3(kDecodeWarps * 32),
-                                   smem, st, p);
+  const cudaError_t e = launch_pdl(kern, dim3(static_cast<unsigned>(decode_grid())),
+                                   dim3(kDecodeWarps * 32), smem, st, p);
   return e == cudaSuccess ? NQKV_OK : cuda_fail(e);
 }
 
@@ -151,7 +170,7 @@ int decode_common(const void* q, const uint8_t* k_codes, const float* k_scales,
                   const uint8_t* v_codes, const float* v_scales, const int32_t* d_seq_lens,
                   const void* k_new, const void* v_new, int64_t new_sb, int64_t new_sh, int B,
                   int H, int hd, int blk, int Tc, float softmax_scale, float* out, void* workspace,
-                  size_t ws_bytes, cudaStream_t st) {
+                  size_t ws_bytes, const void* plan, cudaStream_t st) {
   if (!q || !k_codes || !k_scales || !v_codes || !v_scales || !d_seq_lens || !out)
     return NQKV_ERR_NULL;
   if (int s = check_geometry(hd, blk)) return s;
@@ -185,6 +204,7 @@ int decode_common(const void* q, const uint8_t* k_codes, const float* k_scales,
   p.scale_log2 = softmax_scale * 1.4426950408889634f;
   p.lv = make_levels();
   p.tab = make_bucket_tab();
+  p.plan = static_cast<const int*>(plan);
   p.trace = nullptr;
 #ifdef NQKV_TRACE
   if (const char* t = std::getenv("NQKV_TRACE_PTR"))
@@ -320,7 +340,34 @@ int nqkv_decode_attention(const void* q, const uint8_t* k_codes, const float* k_
                           float softmax_scale, float* out, void* workspace, size_t ws_bytes,
                           void* stream) {
   return decode_common(q, k_codes, k_scales, v_codes, v_scales, d_seq_lens, nullptr, nullptr, 0,
-                       0, B, H, hd, blk, Tc, softmax_scale, out, workspace, ws_bytes,
+                       0, B, H, hd, blk, Tc, softmax_scale, out, workspace, ws_bytes, nullptr,
+                       static_cast<cudaStream_t>(stream));
+}
+
+size_t nqkv_decode_plan_bytes(void) { return static_cast<size_t>(kPlanInts) * sizeof(int); }
+
+int nqkv_decode_plan(const int32_t* d_seq_lens, int B, int H, int Tc, int fused, void* plan,
+                     size_t plan_bytes, void* stream) {
+  if (!d_seq_lens || !plan) return NQKV_ERR_NULL;
+  if (B < 0 || H <= 0 || Tc <= 0 || Tc % 64 || B > kMaxBatch) return NQKV_ERR_SHAPE;
+  if (static_cast<long long>(B) * H * Tc >= (1ll << 31)) return NQKV_ERR_SHAPE;
+  if (!aligned16(plan)) return NQKV_ERR_ALIGN;
+  if (plan_bytes < nqkv_decode_plan_bytes()) return NQKV_ERR_WORKSPACE;
+  const cudaError_t e = launch_pdl_n(decode_plan_kernel, dim3(1), dim3(1024), 0,
+                                   static_cast<cudaStream_t>(stream), d_seq_lens, B, H, Tc,
+                                   fused ? 1 : 0, decode_grid(), kMinTokensPerCta,
+                                   static_cast<int*>(plan));
+  return e == cudaSuccess ? NQKV_OK : cuda_fail(e);
+}
+
+int nqkv_decode_attention_planned(const void* q, const uint8_t* k_codes, const float* k_scales,
+                                  const uint8_t* v_codes, const float* v_scales,
+                                  const int32_t* d_seq_lens, int B, int H, int hd, int blk, int Tc,
+                                  float softmax_scale, float* out, void* workspace,
+                                  size_t ws_bytes, const void* plan, void* stream) {
+  if (!plan) return NQKV_ERR_NULL;
+  return decode_common(q, k_codes, k_scales, v_codes, v_scales, d_seq_lens, nullptr, nullptr, 0,
+                       0, B, H, hd, blk, Tc, softmax_scale, out, workspace, ws_bytes, plan,
                        static_cast<cudaStream_t>(stream));
 }
 
@@ -332,7 +379,19 @@ int nqkv_decode_step(const void* k_new, const void* v_new, int64_t new_stride_b,
   if (!k_new || !v_new) return NQKV_ERR_NULL;
   return decode_common(q, k_codes, k_scales, v_codes, v_scales, d_seq_lens, k_new, v_new,
                        new_stride_b, new_stride_h, B, H, hd, blk, Tc, softmax_scale, out,
-                       workspace, ws_bytes, static_cast<cudaStream_t>(stream));
+                       workspace, ws_bytes, nullptr, static_cast<cudaStream_t>(stream));
+}
+
+int nqkv_decode_step_planned(const void* k_new, const void* v_new, int64_t new_stride_b,
+                             int64_t new_stride_h, const void* q, uint8_t* k_codes,
+                             float* k_scales, uint8_t* v_codes, float* v_scales,
+                             const int32_t* d_seq_lens, int B, int H, int hd, int blk, int Tc,
+                             float softmax_scale, float* out, void* workspace, size_t ws_bytes,
+                             const void* plan, void* stream) {
+  if (!k_new || !v_new || !plan) return NQKV_ERR_NULL;
+  return decode_common(q, k_codes, k_scales, v_codes, v_scales, d_seq_lens, k_new, v_new,
+                       new_stride_b, new_stride_h, B, H, hd, blk, Tc, softmax_scale, out,
+                       workspace, ws_bytes, plan, static_cast<cudaStream_t>(stream));
 }
 
 int nqkv_encode_normalized(const float* d_n, int64_t count, uint8_t* d_codes, void* stream) {

@@ -41,6 +41,13 @@ _SIGS = {
     "nqkv_decode_step": (_i32, [_vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32,
                                 _i32, _i32, _i32, ctypes.c_float, _vp, _vp, _sz, _vp]),
     "nqkv_encode_normalized": (_i32, [_vp, _i64, _vp, _vp]),
+    "nqkv_decode_plan_bytes": (_sz, []),
+    "nqkv_decode_plan": (_i32, [_vp, _i32, _i32, _i32, _i32, _vp, _sz, _vp]),
+    "nqkv_decode_attention_planned": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32,
+                                             _i32, ctypes.c_float, _vp, _vp, _sz, _vp, _vp]),
+    "nqkv_decode_step_planned": (_i32, [_vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _i32,
+                                        _i32, _i32, _i32, _i32, ctypes.c_float, _vp, _vp, _sz,
+                                        _vp, _vp]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -179,6 +186,57 @@ def nqkv_decode_step(k_new: torch.Tensor, v_new: torch.Tensor, q: torch.Tensor,
     return out
 
 
+def make_plan(device="cuda") -> torch.Tensor:
+    """Buffer for nqkv_decode_plan (device, caller-owned)."""
+    return torch.zeros(int(_lib.nqkv_decode_plan_bytes()), dtype=torch.uint8, device=device)
+
+
+def nqkv_decode_plan(seq_lens: torch.Tensor, H: int, Tc: int, fused: bool, plan: torch.Tensor,
+                     stream=None) -> torch.Tensor:
+    """Per-step schedule shared by every layer's planned decode call."""
+    assert seq_lens.dtype == torch.int32
+    _check(_lib.nqkv_decode_plan(_ptr(seq_lens), seq_lens.numel(), H, Tc, int(bool(fused)),
+                                 _ptr(plan), plan.numel() * plan.element_size(), _stream(stream)),
+           "nqkv_decode_plan")
+    return plan
+
+
+def nqkv_decode_attention_planned(q, k_codes, k_scales, v_codes, v_scales, seq_lens, blk,
+                                  workspace, plan, softmax_scale=None, out=None, stream=None):
+    B, H, hd = q.shape
+    Tc = k_codes.shape[2]
+    if softmax_scale is None:
+        softmax_scale = 1.0 / math.sqrt(hd)
+    if out is None:
+        out = torch.empty((B, H, hd), dtype=torch.float32, device=q.device)
+    assert q.dtype == torch.float16 and q.is_contiguous() and out.is_contiguous()
+    _check(_lib.nqkv_decode_attention_planned(
+        _ptr(q), _ptr(k_codes), _ptr(k_scales), _ptr(v_codes), _ptr(v_scales), _ptr(seq_lens), B, H,
+        hd, blk, Tc, float(softmax_scale), _ptr(out), _ptr(workspace),
+        workspace.numel() * workspace.element_size(), _ptr(plan), _stream(stream)),
+        "nqkv_decode_attention_planned")
+    return out
+
+
+def nqkv_decode_step_planned(k_new, v_new, q, k_codes, k_scales, v_codes, v_scales, seq_lens, blk,
+                             workspace, plan, softmax_scale=None, out=None, stream=None):
+    B, H, hd = q.shape
+    Tc = k_codes.shape[2]
+    if softmax_scale is None:
+        softmax_scale = 1.0 / math.sqrt(hd)
+    if out is None:
+        out = torch.empty((B, H, hd), dtype=torch.float32, device=q.device)
+    assert k_new.shape == (B, H, hd) and v_new.shape == (B, H, hd)
+    assert k_new.stride() == v_new.stride() and k_new.stride(2) == 1
+    assert q.dtype == torch.float16 and q.is_contiguous() and out.is_contiguous()
+    _check(_lib.nqkv_decode_step_planned(
+        _ptr(k_new), _ptr(v_new), k_new.stride(0), k_new.stride(1), _ptr(q), _ptr(k_codes),
+        _ptr(k_scales), _ptr(v_codes), _ptr(v_scales), _ptr(seq_lens), B, H, hd, blk, Tc,
+        float(softmax_scale), _ptr(out), _ptr(workspace), workspace.numel() * workspace.element_size(),
+        _ptr(plan), _stream(stream)), "nqkv_decode_step_planned")
+    return out
+
+
 def nqkv_encode_normalized(n: torch.Tensor, stream=None) -> torch.Tensor:
     assert n.dtype == torch.float32 and n.is_contiguous()
     codes = torch.empty(n.shape, dtype=torch.uint8, device=n.device)
@@ -219,6 +277,17 @@ class KVCache:
         """Fused append + attend (seq_lens counts the appended token)."""
         return nqkv_decode_step(k_new, v_new, q, self.k_codes, self.k_scales, self.v_codes,
                                 self.v_scales, seq_lens, self.blk, workspace, out=out, stream=stream)
+
+    def attend_planned(self, q, seq_lens, workspace, plan, out=None, stream=None):
+        return nqkv_decode_attention_planned(q, self.k_codes, self.k_scales, self.v_codes,
+                                             self.v_scales, seq_lens, self.blk, workspace, plan,
+                                             out=out, stream=stream)
+
+    def step_planned(self, k_new, v_new, q, seq_lens, workspace, plan, out=None, stream=None):
+        """Fused append + attend with a per-step plan (nqkv_decode_plan, fused=True)."""
+        return nqkv_decode_step_planned(k_new, v_new, q, self.k_codes, self.k_scales,
+                                        self.v_codes, self.v_scales, seq_lens, self.blk,
+                                        workspace, plan, out=out, stream=stream)
 
     def nbytes(self) -> int:
         return sum(t.numel() * t.element_size()

@@ -26,9 +26,11 @@ from . import sharding
 class DecodeRunner:
     def __init__(self, w: W.Workload, heads: range, device, group=None, world: int = 1,
                  step_slots: int | None = None, layers: int | None = None, fused: bool = True,
-                 gen_device=None):
+                 gen_device=None, planned: bool = True):
         self.w = w
         self.fused = fused
+        # one nqkv_decode_plan per step, shared by every layer's decode launch
+        self.planned = planned
         self.heads = heads
         self.dev = torch.device(device)
         # where the seeded synthetic inputs are drawn (CPU and CUDA generators
@@ -44,6 +46,7 @@ class DecodeRunner:
         self.caches = [N.KVCache(self.B, self.Hl, self.hd, self.Tc, self.blk, self.dev)
                        for _ in range(self.L)]
         self.ws = N.make_workspace(self.B, self.Hl, self.hd, self.Tc, self.dev)
+        self.plan = N.make_plan(self.dev)
         self.out = torch.zeros((self.L, self.B, self.Hl, self.hd), dtype=torch.float32, device=self.dev)
         steps = torch.arange(self.S, dtype=torch.int32)[:, None]
         self.pos = (lens0[None, :] + steps).to(torch.int32).to(self.dev)          # [S, B]
@@ -93,13 +96,19 @@ class DecodeRunner:
         x = self.inputs[s]
         pos, lens = self.pos[s], self.attn_lens[s]
         cur = torch.cuda.current_stream()
+        if self.planned:
+            N.nqkv_decode_plan(lens, self.Hl, self.Tc, self.fused, self.plan)
         for l, c in enumerate(self.caches):
             if not self.fused:
                 c.append(x[l, 0].unsqueeze(1), x[l, 1].unsqueeze(1), pos)   # [B, 1, H, hd] views
             if events is not None:
                 events[l][0].record()
-            if self.fused:
+            if self.fused and self.planned:
+                c.step_planned(x[l, 0], x[l, 1], x[l, 2], lens, self.ws, self.plan, out=self.out[l])
+            elif self.fused:
                 c.step(x[l, 0], x[l, 1], x[l, 2], lens, self.ws, out=self.out[l])
+            elif self.planned:
+                c.attend_planned(x[l, 2], lens, self.ws, self.plan, out=self.out[l])
             else:
                 c.attend(x[l, 2], lens, self.ws, out=self.out[l])
             if events is not None:
@@ -161,6 +170,6 @@ class DecodeRunner:
     def launches_per_step(self) -> int:
         """Kernels this library launches per step: per layer one decode kernel
         (split partials merge in-kernel), plus two quantize launches when the
-        append is not fused."""
+        append is not fused; plus one plan kernel per step when planned."""
         per_layer = 1 + (0 if self.fused else 2)
-        return per_layer * self.L
+        return per_layer * self.L + (1 if self.planned else 0)

@@ -398,3 +398,45 @@ def test_decode_runner_graph_matches_oracle(N):
         ref = O.decode_attention(q.numpy(), kc, ks, vc, vs, [n + 3 for n in lens], w.blk)
         assert np.max(np.abs(run.out[l].cpu().numpy() - ref)) <= ATOL
     assert all(t > 0 for t in run.decode_kernel_ms())
+
+
+# ------------------------------------------------------ per-step plan API
+@pytest.mark.parametrize("hd,blk", [(64, 64), (128, 64), (128, 32)])
+def test_planned_calls_match_unplanned_bit_exact(N, hd, blk):
+    """nqkv_decode_plan + *_planned calls give bit-identical results to the
+    unplanned calls (same schedule), for plain and fused steps, with empty,
+    single-token and ragged sequences."""
+    B, H, Tc = 6, 5, 1024
+    lens0 = [0, 1, 63, 300, 777, 1000]
+    T = max(lens0)
+    x = _rand_kv(B, T, H, hd, seed=51)
+    y = _rand_kv(B, T, H, hd, seed=52, outlier=False)
+    kn = _rand_kv(B, 1, H, hd, seed=53)[:, 0].to(DEV)
+    vn = _rand_kv(B, 1, H, hd, seed=54, outlier=False)[:, 0].to(DEV)
+    q = torch.randn(B, H, hd, generator=torch.Generator().manual_seed(55)).to(torch.float16).to(DEV)
+    kc, ks = _oracle_cache(x, [0] * B, blk, Tc)
+    vc, vs = _oracle_cache(y, [0] * B, blk, Tc)
+    t = lambda a: torch.from_numpy(a.copy()).to(DEV)
+    L = torch.tensor(lens0, dtype=torch.int32, device=DEV)
+    plan = N.make_plan(DEV)
+    # plain attention
+    N.nqkv_decode_plan(L, H, Tc, False, plan)
+    o1 = N.nqkv_decode_attention(q, t(kc), t(ks), t(vc), t(vs), L, blk, N.make_workspace(B, H, hd, Tc, DEV))
+    o2 = N.nqkv_decode_attention_planned(q, t(kc), t(ks), t(vc), t(vs), L, blk,
+                                         N.make_workspace(B, H, hd, Tc, DEV), plan)
+    torch.cuda.synchronize()
+    assert torch.equal(o1, o2)
+    # fused step (lens after the append)
+    L1 = L + 1
+    N.nqkv_decode_plan(L1, H, Tc, True, plan)
+    a = [t(z) for z in (kc, ks, vc, vs)]
+    b = [t(z) for z in (kc, ks, vc, vs)]
+    f1 = N.nqkv_decode_step(kn, vn, q, *a, L1, blk, N.make_workspace(B, H, hd, Tc, DEV))
+    f2 = N.nqkv_decode_step_planned(kn, vn, q, *b, L1, blk, N.make_workspace(B, H, hd, Tc, DEV), plan)
+    torch.cuda.synchronize()
+    assert torch.equal(f1, f2)
+    assert all(torch.equal(u, v) for u, v in zip(a, b))
+    O.quantize_append(kn.unsqueeze(1).cpu().numpy(), lens0, blk, kc, ks)
+    O.quantize_append(vn.unsqueeze(1).cpu().numpy(), lens0, blk, vc, vs)
+    ref = O.decode_attention(q.cpu().numpy(), kc, ks, vc, vs, [n + 1 for n in lens0], blk)
+    assert np.max(np.abs(f2.cpu().numpy() - ref)) <= ATOL

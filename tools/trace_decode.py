@@ -34,6 +34,11 @@ L = torch.full((B,), T, dtype=torch.int32, device="cuda")
 ws = N.make_workspace(B, H, hd, Tc, "cuda")
 flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
 warm = os.environ.get("WARM") == "1"    # trace the 2nd of two back-to-back launches (no flush between)
+planned = os.environ.get("PLAN") == "1"
+plan = N.make_plan("cuda")
+N.nqkv_decode_plan(L, H, Tc, False, plan)
+if planned:
+    cache.attend = lambda q_, L_, ws_: cache.attend_planned(q_, L_, ws_, plan)
 for _ in range(5):
     flush.sum()                         # read-only L2 sweep (no dirty lines): HBM-honest timing
     torch.cuda._sleep(100000)
