@@ -105,8 +105,9 @@ int nqkv_dequantize(const uint8_t* codes, const float* scales, int B, int H, int
 
 /* Bytes of workspace nqkv_decode_attention / nqkv_decode_step need for this
  * geometry (0 for an unsupported hd).  Layout: [0, nqkv_decode_counter_bytes)
- * int32 per-(b, h) arrival counters that must be ZERO before the first call
- * (every completed call leaves them zero again), then per-CTA split partials. */
+ * int32 per-(b, h) arrival counters, then per-CTA split-partial records of
+ * tagged 64-bit words (value | valid << 32).  The WHOLE workspace must be
+ * ZERO before the first call; every completed call leaves it zero again. */
 size_t nqkv_decode_workspace_bytes(int B, int H, int hd, int Tc);
 size_t nqkv_decode_counter_bytes(int B, int H);
 
@@ -121,14 +122,14 @@ size_t nqkv_decode_counter_bytes(int B, int H);
  *            (append-before-attend); 0 -> out[b] = 0
  * out        device fp32 [B][H][hd], 16-byte aligned
  * workspace  device, >= nqkv_decode_workspace_bytes(B,H,hd,Tc) bytes,
- *            16-byte aligned.  Its first nqkv_decode_counter_bytes(B,H)
- *            bytes must be ZERO before the first use; every completed call
- *            leaves them zero again.  Do not share one workspace between calls
+ *            16-byte aligned, ALL ZERO before the first use; every
+ *            completed call leaves it zero again.  Do not share one workspace between calls
  *            that may run concurrently (calls ordered on one stream may).
  * One launch of one CTA per SM with programmatic dependent launch (PDL).  The
  * (b, h, t) token list is cut into equal contiguous per-CTA ranges; a
- * sequence split across CTAs is merged by the last of its CTAs to finish
- * (per-(b, h) counter), in CTA order.  Results are bit-reproducible for a
+ * sequence split across CTAs is merged by the last of its CTAs to arrive
+ * (per-(b, h) relaxed counter; the others publish tagged partial records
+ * that the last one polls), in CTA order.  Results are bit-reproducible for a
  * given (B, H, seq_lens, GPU); a different head shard of the same data may
  * differ by fp32 reassociation only (reading R7).  B <= 1024 and
  * B*H*Tc < 2^31. */

@@ -59,14 +59,31 @@ __device__ __forceinline__ float fast_exp2(float x) {  // ex2.approx(-inf) = +0
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-// Programmatic dependent launch: let the next kernel in the stream start its
-// prologue early; wait for the previous kernel before touching its outputs.
+// Programmatic dependent launch: wait for the previous kernel before touching
+// its outputs, then let the next kernel in the stream start its prologue.
+// Every kernel here triggers only AFTER its own wait, so a kernel that runs
+// knows that all kernels before its immediate predecessor have completed.
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ int atom_add_acq_rel(int* p, int v) {
+__device__ __forceinline__ void pdl_enter() {
+  pdl_wait();
+  pdl_trigger();
+}
+__device__ __forceinline__ int atom_add_relaxed(int* p, int v) {
   int r;
-  asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(r) : "l"(p), "r"(v) : "memory");
+  asm volatile("atom.relaxed.gpu.global.add.s32 %0, [%1], %2;" : "=r"(r) : "l"(p), "r"(v) : "memory");
   return r;
+}
+// Tagged 64-bit words (value bits | tag << 32): an aligned 64-bit relaxed
+// access is single-copy atomic, so a reader that sees the tag also sees the
+// value written with it -- no fence or acquire needed.
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
 }
 
 // Fast unsigned division by a runtime constant (n < 2^31).

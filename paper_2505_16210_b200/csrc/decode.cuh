@@ -60,7 +60,7 @@ constexpr int kMinTokensPerCta = 512;  // below this a CTA's table build would d
 #define NQKV_DEPTH 2             // register ring depth: stages in flight per consumer warp
 #endif
 #ifndef NQKV_PF
-#define NQKV_PF 0                // L2 prefetch distance in a warp's own stages (0: off; measured no gain)
+#define NQKV_PF -1               // L2 prefetch distance in a warp's own stages (-1: per head_dim default)
 #endif
 constexpr int kDecodeWarps = NQKV_DECODE_WARPS;
 constexpr int kLaneDims = 16;          // head dims owned by one lane
@@ -79,7 +79,8 @@ struct DecodeParams {
   long long new_sb, new_sh; // element strides of k_new / v_new ([B][H][hd])
   float* out;
   int* cnt;                 // [B*H] partial-arrival counters (zero between launches)
-  float* part;              // [kMaxGrid][2][hd + 2] partial (o[hd], m, l)
+  unsigned long long* part; // [kMaxGrid][2][hd + 2] tagged partial words (o[hd], m, l);
+                            // zero (= no partial) between launches
   int B, H, Tc, blk_shift, min_tokens;
   float scale_log2;         // softmax_scale * log2(e)
   Levels lv;
@@ -88,12 +89,12 @@ struct DecodeParams {
   unsigned long long* trace;   // NQKV_TRACE builds: per-warp globaltimer stamps [grid][NW][16]
 };
 
-#ifdef NQKV_TRACE
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+#ifdef NQKV_TRACE
 #define TRACE(k) do { if (p.trace && lane == 0) p.trace[(blockIdx.x * NW + warp) * 16 + (k)] = gtimer(); } while (0)
 #else
 #define TRACE(k) do { } while (0)
@@ -184,6 +185,22 @@ __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
   const uintptr_t a0 = a & ~static_cast<uintptr_t>(15);
   const uint32_t n = static_cast<uint32_t>((a + bytes - a0 + 15) & ~static_cast<uintptr_t>(15));
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(a0), "r"(n) : "memory");
+}
+// L2 prefetch of the cache rows [r0, r1) of one stage (r = (b*H + h)*Tc + t):
+// one instruction per warp; lanes 0-8 / 9-17 take the K / V code lines,
+// 18-19 / 20-21 the K / V scale lines (only lines holding bytes of the rows,
+// so every address is inside the cache tensors).  A prefetch is a hint: it
+// never changes what a load returns, so it may run before the PDL wait.
+template <int HD, int NBLK, typename P>
+__device__ __forceinline__ void prefetch_rows_l2(const P& p, int lane, long long r0, long long r1) {
+  const bool sc = lane >= 18;
+  const bool isv = sc ? lane >= 20 : lane >= 9;
+  const int li = lane - (sc ? (isv ? 20 : 18) : (isv ? 9 : 0));
+  const long long w = sc ? NBLK * 4 : HD / 2;
+  const long long f = (r0 * w) >> 7, l = (r1 * w - 1) >> 7;
+  const unsigned char* base = sc ? reinterpret_cast<const unsigned char*>(isv ? p.vs : p.ks)
+                                 : (isv ? p.vc : p.kc);
+  if (lane < 22 && f + li <= l) asm volatile("prefetch.global.L2 [%0];" :: "l"(base + ((f + li) << 7)));
 }
 // 64-bit address = base + a * b (one IMAD.WIDE.U32)
 __device__ __forceinline__ const void* addr_wide(const void* base, uint32_t a, uint32_t b) {
@@ -281,8 +298,7 @@ __device__ __forceinline__ void cta_walk(const int* pref, const int* len, int B,
 __global__ void __launch_bounds__(1024) decode_plan_kernel(const int32_t* seq_lens, int B, int H, int Tc,
                                                            int fused, int G, int min_tokens, int* plan) {
   __shared__ int s_len[kMaxBatch], s_pref[kMaxBatch + 1], s_wsum[32];
-  pdl_trigger();
-  pdl_wait();
+  pdl_enter();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int raw = tid < B ? min(max(seq_lens[tid], 0), Tc) : 0;
   const unsigned one = __ballot_sync(0xffffffffu, fused && raw == 1);
@@ -504,43 +520,102 @@ __device__ __noinline__ void merge_fn(const DecodeParams& p, unsigned char* smem
       *reinterpret_cast<float2*>(p.out + bh * HD + dim(u)) = make_float2(acc[2 * u] * inv, acc[2 * u + 1] * inv);
     return;
   }
-  // partial piece: slot 0 = this CTA's first piece (starts at g0), 1 = its
-  // last.  The counter's acq_rel RMW publishes the partial (after the warp
-  // barrier) and, for the last arriver, acquires everyone else's.
-  float* part = p.part + (static_cast<long long>(cta) * 2 + (pc.gs == g0 ? 0 : 1)) * (HD + 2);
-#pragma unroll
-  for (int u = 0; u < PPL; ++u)
-    *reinterpret_cast<float2*>(part + dim(u)) = make_float2(acc[2 * u], acc[2 * u + 1]);
-  if (lane == 0) {
-    part[HD] = M;
-    part[HD + 1] = den;
-  }
-  __syncwarp();
+  // Partial piece.  Record slot 0 = this CTA's first piece (starts at g0),
+  // 1 = its last.  Arrive first (relaxed counter): a CTA that is not the
+  // last arriver publishes its partial as tagged words and leaves; the last
+  // one polls the others' records -- every one of them was, or is about to
+  // be, stored by a CTA that has already arrived and never waits on anyone,
+  // so the poll terminates -- merges all of them in CTA order, and clears
+  // the records and the counter for the next launch.  Two L2 round trips on
+  // the critical path (atomic, poll), no fence.
   const int st0 = pc.gs - pc.t0;                                // global index of token 0
   const int ca = sc.cta_of(st0), cb = sc.cta_of(st0 + pc.len - 1);
   int last = 0;
-  if (lane == 0) last = atom_add_acq_rel(p.cnt + bh, 1) == cb - ca;
+  if (lane == 0) last = atom_add_relaxed(p.cnt + bh, 1) == cb - ca;
   last = __shfl_sync(0xffffffffu, last, 0);
-  if (!last) return;
-  float Mx = -INFINITY;
-  for (int c = ca; c <= cb; ++c) {
-    const int sl = (c == ca && sc.bnd(c) != st0) ? 1 : 0;
-    Mx = fmaxf(Mx, __ldcg(p.part + (static_cast<long long>(c) * 2 + sl) * (HD + 2) + HD));
-  }
-  float dsum = 0.0f, o[2 * PPL];
-#pragma unroll
-  for (int d = 0; d < 2 * PPL; ++d) o[d] = 0.0f;
-  for (int c = ca; c <= cb; ++c) {
-    const int sl = (c == ca && sc.bnd(c) != st0) ? 1 : 0;
-    const float* pp = p.part + (static_cast<long long>(c) * 2 + sl) * (HD + 2);
-    const float fc = fast_exp2(__ldcg(pp + HD) - Mx);
-    dsum += fc * __ldcg(pp + HD + 1);
+  auto rec = [&](int c, int sl) { return p.part + (static_cast<long long>(c) * 2 + sl) * (HD + 2); };
+  auto tag = [](float v) {
+    return static_cast<unsigned long long>(__float_as_uint(v)) | (1ull << 32);
+  };
+  if (!last) {
+    unsigned long long* r = rec(cta, pc.gs == g0 ? 0 : 1);
 #pragma unroll
     for (int u = 0; u < PPL; ++u) {
-      const float2 x = __ldcg(reinterpret_cast<const float2*>(pp + dim(u)));
-      o[2 * u] = fmaf(fc, x.x, o[2 * u]);
-      o[2 * u + 1] = fmaf(fc, x.y, o[2 * u + 1]);
+      st_relaxed_u64(r + dim(u), tag(acc[2 * u]));
+      st_relaxed_u64(r + dim(u) + 1, tag(acc[2 * u + 1]));
     }
+    if (lane == 0) {
+      st_relaxed_u64(r + HD, tag(M));
+      st_relaxed_u64(r + HD + 1, tag(den));
+    }
+    return;
+  }
+  constexpr int MAXC = 4;                     // records merged per pass (registers)
+  float Mx = -INFINITY, dsum = 0.0f, o[2 * PPL];
+#pragma unroll
+  for (int d = 0; d < 2 * PPL; ++d) o[d] = 0.0f;
+  for (int c0 = ca; c0 <= cb; c0 += MAXC) {
+    float rm[MAXC], rl[MAXC], ro[MAXC][2 * PPL];
+    const int nc = min(MAXC, cb - c0 + 1);
+#pragma unroll
+    for (int i = 0; i < MAXC; ++i) {
+      if (i >= nc) break;
+      const int c = c0 + i;
+      if (c == cta) {
+        rm[i] = M; rl[i] = den;
+#pragma unroll
+        for (int d = 0; d < 2 * PPL; ++d) ro[i][d] = acc[d];
+        continue;
+      }
+      const unsigned long long* r = rec(c, (c == ca && sc.bnd(c) != st0) ? 1 : 0);
+      unsigned long long wm, wl, wo[2 * PPL];
+      for (;;) {
+        wm = ld_relaxed_u64(r + HD);
+        wl = ld_relaxed_u64(r + HD + 1);
+        bool ok = (wm >> 32) && (wl >> 32);
+#pragma unroll
+        for (int u = 0; u < PPL; ++u) {
+          wo[2 * u] = ld_relaxed_u64(r + dim(u));
+          wo[2 * u + 1] = ld_relaxed_u64(r + dim(u) + 1);
+          ok = ok && (wo[2 * u] >> 32) && (wo[2 * u + 1] >> 32);
+        }
+        if (__all_sync(0xffffffffu, ok)) break;
+      }
+      rm[i] = __uint_as_float(static_cast<uint32_t>(wm));
+      rl[i] = __uint_as_float(static_cast<uint32_t>(wl));
+#pragma unroll
+      for (int d = 0; d < 2 * PPL; ++d) ro[i][d] = __uint_as_float(static_cast<uint32_t>(wo[d]));
+      unsigned long long* rw = const_cast<unsigned long long*>(r);  // clear for the next launch
+#pragma unroll
+      for (int u = 0; u < PPL; ++u) {
+        st_relaxed_u64(rw + dim(u), 0ull);
+        st_relaxed_u64(rw + dim(u) + 1, 0ull);
+      }
+      if (lane == 0) {
+        st_relaxed_u64(rw + HD, 0ull);
+        st_relaxed_u64(rw + HD + 1, 0ull);
+      }
+    }
+    // merge in CTA order: batch max first, the running sum rescaled only
+    // when a batch raises it (one batch -- the usual case -- is a plain
+    // two-pass softmax merge)
+    float Mn = Mx;
+#pragma unroll
+    for (int i = 0; i < MAXC; ++i)
+      if (i < nc) Mn = fmaxf(Mn, rm[i]);
+    const float fa = fast_exp2(Mx - Mn);      // Mx = -inf on the first batch: 0
+    dsum *= fa;
+#pragma unroll
+    for (int d = 0; d < 2 * PPL; ++d) o[d] *= fa;
+#pragma unroll
+    for (int i = 0; i < MAXC; ++i) {
+      if (i >= nc) break;
+      const float fc = fast_exp2(rm[i] - Mn);
+      dsum = fmaf(fc, rl[i], dsum);
+#pragma unroll
+      for (int d = 0; d < 2 * PPL; ++d) o[d] = fmaf(fc, ro[i][d], o[d]);
+    }
+    Mx = Mn;
   }
   const float inv = 1.0f / dsum;
 #pragma unroll
@@ -590,9 +665,14 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  pdl_trigger();
-  pdl_wait();
-  TRACE(1);
+  // V LUT (independent of the previous kernel); levels via shared memory
+  // (a divergent constant-bank index would serialise)
+  __syncthreads();
+  for (int i = tid; i < 256 * 16; i += NT) {     // 16 B = two lane copies per store
+    const int e = i >> 4;
+    const float lo = s_lv[e & 15], hi = s_lv[e >> 4];
+    *reinterpret_cast<float4*>(smem + Sm::kV + e * 256 + (i & 15) * 16) = make_float4(lo, hi, lo, hi);
+  }
   const uint32_t* s_one = reinterpret_cast<const uint32_t*>(smem + Sm::kOne);
   Piece* s_walk = reinterpret_cast<Piece*>(smem + Sm::kWalk);
   int* s_wi = reinterpret_cast<int*>(smem + Sm::kWalk + 48);
@@ -607,14 +687,14 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
     for (int i = tid; i < (p.B + 31) / 32; i += NT)
       reinterpret_cast<uint32_t*>(smem + Sm::kOne)[i] = __ldcg(p.plan + kPlanOne + i);
   };
-  if (p.plan) {
+  auto read_plan = [&]() {
+    const int4* e4 = reinterpret_cast<const int4*>(p.plan + kPlanHdr + cta * kPlanEntry);
     const int4 hdr = __ldcg(reinterpret_cast<const int4*>(p.plan));
     sc.N = hdr.x; sc.C = hdr.y; sc.q = hdr.z; sc.r = hdr.w;
     if (sc.N == 0 || cta >= sc.C) {
       if (sc.N == 0) copy_plan_arrays();
       __syncthreads();
     } else {
-      const int4* e4 = reinterpret_cast<const int4*>(p.plan + kPlanHdr + cta * kPlanEntry);
       const int4 a = __ldcg(e4), b = __ldcg(e4 + 1), c = __ldcg(e4 + 2), d = __ldcg(e4 + 3);
       Piece pf, pl;
       pf.gs = a.x; pf.b = a.y; pf.h = a.z; pf.len = a.w; pf.t0 = b.x; pf.t1 = b.y;
@@ -630,6 +710,11 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
         reinterpret_cast<int*>(smem + Sm::kWalk + 56)[0] = 0;
       }
     }
+  };
+  pdl_enter();
+  TRACE(1);
+  if (p.plan) {
+    read_plan();
   } else {
     // ---- per-batch streamed lengths and token prefix: tokens(b) = H * len'_b.
     // Fused step: the appended row (len - 1) is not streamed; the producer
@@ -798,6 +883,9 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
   // register ring: buffer d holds the stage at (tok0 mtok[d], piece end mt1[d],
   // piece index mpi[d]); refilled with the cursor's next stage once consumed
   constexpr int D = NQKV_DEPTH;
+  // L2 prefetch distance (own stages): +11% steady state at hd 128, none at
+  // hd 64 (tools/run_var.sh)
+  constexpr int PF = NQKV_PF >= 0 ? NQKV_PF : (HD == 128 ? 2 : 0);
   StageRegs RG[D];
 #pragma unroll
   for (int d = 0; d < D; ++d) {
@@ -830,6 +918,12 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
     mt1[d] = lp.t1;
     mpi[d] = lpi;
     load_stage(RG[d], lrb, mtok[d], mt1[d]);
+    // L2 prefetch of this warp's stage PF ahead in the same piece
+    if (PF > 0 && ls + PF * NC < nstages(lp)) {
+      const int t = lp.t0 + (ls + PF * NC) * ST;
+      prefetch_rows_l2<HD, NBLK>(p, lane, static_cast<long long>(lrb) + t,
+                                 static_cast<long long>(lrb) + min(t + ST, lp.t1));
+    }
     return true;
   };
 #pragma unroll
@@ -839,13 +933,8 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
   if (early) has[0] = fill(0);
   if (p.plan) copy_plan_arrays();
   TRACE(4);
-  // ---- V LUT and the table of piece 0, built by all threads (thread: pair
-  // quad tid % Q); T[e][j] = RN(c q_{2j} L[e & 15]) + RN(c q_{2j+1} L[e >> 4])
-  for (int i = tid; i < 256 * 16; i += NT) {     // V LUT; 16 B = two lane copies per store
-    const int e = i >> 4;
-    const float lo = s_lv[e & 15], hi = s_lv[e >> 4];
-    *reinterpret_cast<float4*>(smem + Sm::kV + e * 256 + (i & 15) * 16) = make_float4(lo, hi, lo, hi);
-  }
+  // ---- the table of piece 0, built by all threads (thread: pair quad
+  // tid % Q); T[e][j] = RN(c q_{2j} L[e & 15]) + RN(c q_{2j+1} L[e >> 4])
   TRACE(5);
   {
     __half2 h2[4];

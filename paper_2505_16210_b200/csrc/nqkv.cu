@@ -162,7 +162,7 @@ WsLayout ws_layout(long long B, long long H, int hd) {
   WsLayout w;
   w.cnt = 0;
   w.part = align_up(static_cast<size_t>(B * H) * sizeof(int), 256);
-  w.total = align_up(w.part + static_cast<size_t>(kMaxGrid) * 2 * (hd + 2) * sizeof(float), 256);
+  w.total = align_up(w.part + static_cast<size_t>(kMaxGrid) * 2 * (hd + 2) * sizeof(unsigned long long), 256);
   return w;
 }
 
@@ -197,7 +197,7 @@ int decode_common(const void* q, const uint8_t* k_codes, const float* k_scales,
   p.new_sb = new_sb; p.new_sh = new_sh;
   unsigned char* ws = static_cast<unsigned char*>(workspace);
   p.cnt = reinterpret_cast<int*>(ws + w.cnt);
-  p.part = reinterpret_cast<float*>(ws + w.part);
+  p.part = reinterpret_cast<unsigned long long*>(ws + w.part);
   p.B = B; p.H = H; p.Tc = Tc;
   p.blk_shift = blk_shift_of(blk);
   p.min_tokens = kMinTokensPerCta;

@@ -85,9 +85,8 @@ __global__ void __launch_bounds__(256) quantize_kernel(const __grid_constant__ Q
   for (int i = threadIdx.x; i < kNumBuckets * 32; i += blockDim.x)
     reinterpret_cast<float2*>(qsmem)[i] = p.tab.e[i >> 5];
   if (static_cast<uint32_t>(__cvta_generic_to_shared(qsmem)) != 0x400u) __trap();
-  pdl_trigger();
   __syncthreads();
-  pdl_wait();
+  pdl_enter();                       // wait, then trigger: see common.cuh
   const int lane = threadIdx.x & 31;
   const uint32_t lane8 = lane * 8u;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
@@ -182,9 +181,8 @@ __global__ void __launch_bounds__(256) dequant_kernel(const DequantParams p) {
 #pragma unroll
     for (int k = 0; k < 16; ++k) s_lv[k] = p.lv.v[k];
   }
-  pdl_trigger();
   __syncthreads();
-  pdl_wait();
+  pdl_enter();                       // wait, then trigger: see common.cuh
   const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
   for (long long c = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
        c < p.total_chunks; c += stride) {

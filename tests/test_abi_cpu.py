@@ -110,7 +110,7 @@ def test_workspace_size_grows_with_geometry():
     assert N.nqkv_decode_workspace_bytes(8, 32, 96, 2112) == 0        # unsupported hd
     # per-(b, h) int32 counters first, then per-CTA split partials (o[hd], m, l)
     assert N.nqkv_decode_counter_bytes(8, 32) == 8 * 32 * 4
-    assert a >= N.nqkv_decode_counter_bytes(8, 32) + 148 * 2 * (64 + 2) * 4
+    assert a >= N.nqkv_decode_counter_bytes(8, 32) + 148 * 2 * (64 + 2) * 8     # tagged 64-bit words
 
 
 def test_missing_library_fails_loudly(tmp_path):
