@@ -223,9 +223,12 @@ struct Piece {
 };
 
 // Registers of one stage: kTPS token slots of this lane.
-struct StageRegs {
+// RS (reduce-scatter, BLK = 16*kTPS): one K and one V scale per lane -- the
+// scale of token slot sub % kTPS of its block -- instead of one per slot.
+template <bool RS>
+struct StageRegsT {
   uint2 k[kTPS], v[kTPS];
-  float ks[kTPS], vs[kTPS];
+  float ks[RS ? 1 : kTPS], vs[RS ? 1 : kTPS];
 };
 
 // Launch-wide scheduling constants: C CTAs own equal contiguous ranges of
@@ -836,6 +839,13 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
   const int g = lane / LPT, sub = lane % LPT;
   constexpr int NBLK = HD / BLK;
   const int sidx = (sub * kLaneDims) / BLK;
+  // Reduce-scatter layout (BLK = 16 * kTPS, i.e. blk 64): the kTPS lanes of a
+  // block each own one token slot j = sub % kTPS of the stage: they load its
+  // K / V scale, finish its score, exponentiate it, and hand its weight
+  // p_j * vs_j to the other lanes of the block.  1 scale load, 1 exp2 per lane
+  // and stage instead of kTPS.
+  constexpr bool RS = BLK == kLaneDims * kTPS && kTPS == 4;
+  const uint32_t soff_rs = RS ? static_cast<uint32_t>((sub & 3) * G * NBLK * 4) : 0u;
   // Per-lane 32-bit byte offsets (codes, scales) of the load cursor: this
   // lane's bytes of the stage to load next (token tok0 + g of its (b, h));
   // slot i is at the immediate offset i*G rows.  Advanced by NC*ST rows per
@@ -846,12 +856,16 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
     loff_c = r * (HD / 2) + sub * 8;
     loff_s = (r * NBLK + sidx) * 4;
   };
+  using StageRegs = StageRegsT<RS>;
   auto load_stage = [&](StageRegs& Rg, int rb, int tok0, int t1) {
 #ifdef NQKV_EXP_NOLOAD
 #pragma unroll
     for (int i = 0; i < kTPS; ++i) {
       Rg.k[i] = make_uint2(0x12345678u * (i + 1) + tok0, 0x9abcdef0u + lane);
       Rg.v[i] = make_uint2(0x31415926u * (i + 3) + tok0, 0x27182818u + lane);
+    }
+#pragma unroll
+    for (int i = 0; i < (RS ? 1 : kTPS); ++i) {
       Rg.ks[i] = 1.0f;
       Rg.vs[i] = 0.5f;
     }
@@ -865,8 +879,16 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
       if (tok0 + i * G + g < t1) {
         Rg.k[i] = ldg_stream_64(p.kc + loff_c + i * G * (HD / 2));
         Rg.v[i] = ldg_stream_64(p.vc + loff_c + i * G * (HD / 2));
-        Rg.ks[i] = ldg_nc_f32(reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(p.ks) + loff_s) + i * G * NBLK);
-        Rg.vs[i] = ldg_nc_f32(reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(p.vs) + loff_s) + i * G * NBLK);
+        if constexpr (!RS) {
+          Rg.ks[i] = ldg_nc_f32(reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(p.ks) + loff_s) + i * G * NBLK);
+          Rg.vs[i] = ldg_nc_f32(reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(p.vs) + loff_s) + i * G * NBLK);
+        }
+      }
+    }
+    if constexpr (RS) {
+      if (tok0 + (sub & 3) * G + g < t1) {
+        Rg.ks[0] = ldg_nc_f32(reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(p.ks) + loff_s + soff_rs));
+        Rg.vs[0] = ldg_nc_f32(reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(p.vs) + loff_s + soff_rs));
       }
     }
   };
@@ -1048,7 +1070,8 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
       uint32_t x = 0;
 #pragma unroll
       for (int i = 0; i < kTPS; ++i)
-        x ^= Rg.k[i].x ^ Rg.k[i].y ^ Rg.v[i].x ^ Rg.v[i].y ^ __float_as_uint(Rg.ks[i]) ^ __float_as_uint(Rg.vs[i]);
+        x ^= Rg.k[i].x ^ Rg.k[i].y ^ Rg.v[i].x ^ Rg.v[i].y ^ __float_as_uint(Rg.ks[RS ? 0 : i]) ^
+             __float_as_uint(Rg.vs[RS ? 0 : i]);
       o2[0] ^= x;
       l += 1.0f;
       m = 0.0f;
@@ -1067,36 +1090,72 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
       const uint64_t b = pack2(lds_k(prmt(r1, jsel[4], 0x7604)), lds_k(prmt(r1, jsel[5], 0x7614)));
       a = fadd2(a, fadd2(b, pack2(lds_k(prmt(r1, jsel[6], 0x7624)), lds_k(prmt(r1, jsel[7], 0x7634)))));
       const float2 af = unpack2(a);
-      s[i] = (af.x + af.y) * Rg.ks[i];
+      s[i] = RS ? af.x + af.y : (af.x + af.y) * Rg.ks[i];
     }
+    float wv[kTPS];                   // V weight p_i * vs_i of each token slot
+    if constexpr (RS) {
+      // reduce-scatter over the 4 lanes of the block: lane j = sub % 4 ends
+      // with the block sum of slot j (xor 2 keeps the pair holding j, xor 1
+      // the element), scales it, then (hd 128) adds the other block's half
+      const bool b1 = (lane >> 1) & 1, b0 = lane & 1;
+      const float x0 = __shfl_xor_sync(0xffffffffu, b1 ? s[0] : s[2], 2);
+      const float x1 = __shfl_xor_sync(0xffffffffu, b1 ? s[1] : s[3], 2);
+      const float k0 = (b1 ? s[2] : s[0]) + x0, k1 = (b1 ? s[3] : s[1]) + x1;
+      float sj = (b0 ? k1 : k0) + __shfl_xor_sync(0xffffffffu, b0 ? k0 : k1, 1);
+      sj *= Rg.ks[0];
+      if (LPT == 8) sj += __shfl_xor_sync(0xffffffffu, sj, 4);
+      if (tok0 + ST > t1)             // warp-uniform: only a piece's last stage is partial
+        sj = (tok0 + (sub & 3) * G + g < t1) ? sj : -INFINITY;
+      float mt = sj;
 #pragma unroll
-    for (int o = 1; o < LPT; o <<= 1) {
+      for (int o = 1; o < 32; o <<= 1)
+        if (!(LPT == 8 && o == 4)) mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, o));
+      if (mt > m) {                   // warp-uniform; the stage has >= 1 valid token
+        const float corr = fast_exp2(m - mt);   // m = -inf -> 0
+        m = mt;
+        l *= corr;
+        const uint64_t c2 = pack2(corr, corr);
 #pragma unroll
-      for (int i = 0; i < kTPS; ++i) s[i] += __shfl_xor_sync(0xffffffffu, s[i], o);
-    }
-    if (tok0 + ST > t1) {             // warp-uniform: only a piece's last stage is partial
+        for (int j = 0; j < 8; ++j) o2[j] = fmul2(o2[j], c2);
+      }
+      const float pr = fast_exp2(sj - m);       // masked: exp2(-inf) = 0
+      l += pr;                        // this lane's slot only (reduced in end_piece)
+      const float w = pr * Rg.vs[0];
 #pragma unroll
-      for (int i = 0; i < kTPS; ++i) s[i] = (tok0 + i * G + g < t1) ? s[i] : -INFINITY;
-    }
-    float mt = s[0];
+      for (int i = 0; i < kTPS; ++i) wv[i] = __shfl_sync(0xffffffffu, w, (lane & ~3) | i);
+    } else {
 #pragma unroll
-    for (int i = 1; i < kTPS; ++i) mt = fmaxf(mt, s[i]);
+      for (int o = 1; o < LPT; o <<= 1) {
 #pragma unroll
-    for (int o = LPT; o < 32; o <<= 1) mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, o));
-    if (mt > m) {                     // warp-uniform; the stage has >= 1 valid token
-      const float corr = fast_exp2(m - mt);     // m = -inf -> 0
-      m = mt;
-      l *= corr;
-      const uint64_t c2 = pack2(corr, corr);
+        for (int i = 0; i < kTPS; ++i) s[i] += __shfl_xor_sync(0xffffffffu, s[i], o);
+      }
+      if (tok0 + ST > t1) {           // warp-uniform: only a piece's last stage is partial
 #pragma unroll
-      for (int j = 0; j < 8; ++j) o2[j] = fmul2(o2[j], c2);
+        for (int i = 0; i < kTPS; ++i) s[i] = (tok0 + i * G + g < t1) ? s[i] : -INFINITY;
+      }
+      float mt = s[0];
+#pragma unroll
+      for (int i = 1; i < kTPS; ++i) mt = fmaxf(mt, s[i]);
+#pragma unroll
+      for (int o = LPT; o < 32; o <<= 1) mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, o));
+      if (mt > m) {                   // warp-uniform; the stage has >= 1 valid token
+        const float corr = fast_exp2(m - mt);   // m = -inf -> 0
+        m = mt;
+        l *= corr;
+        const uint64_t c2 = pack2(corr, corr);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) o2[j] = fmul2(o2[j], c2);
+      }
+#pragma unroll
+      for (int i = 0; i < kTPS; ++i) {
+        const float pr = fast_exp2(s[i] - m);   // masked: exp2(-inf) = 0
+        l += pr;
+        wv[i] = pr * Rg.vs[i];
+      }
     }
 #pragma unroll
     for (int i = 0; i < kTPS; ++i) {
-      const float pr = fast_exp2(s[i] - m);     // masked: exp2(-inf) = 0
-      l += pr;
-      const float w = pr * Rg.vs[i];
-      const uint64_t w2 = pack2(w, w);
+      const uint64_t w2 = pack2(wv[i], wv[i]);
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         o2[k] = ffma2(lds_v(prmt(Rg.v[i].x, vsel, 0x7604 | (k << 4))), w2, o2[k]);
@@ -1110,6 +1169,11 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
   auto end_piece = [&](int k) {
     const int slot = k % R;
     if (any) {
+      if constexpr (RS) {             // l: one slot per lane (hd 128: lanes sub, sub ^ 4 alike)
+#pragma unroll
+        for (int o = 1; o < LPT; o <<= 1)
+          if (o != 4) l += __shfl_xor_sync(0xffffffffu, l, o);
+      }
 #pragma unroll
       for (int o = LPT; o < 32; o <<= 1) {
         l += __shfl_xor_sync(0xffffffffu, l, o);
