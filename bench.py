@@ -288,11 +288,16 @@ def run_ours(args, w, rank, world, local_rank):
     if rank != 0:
         return 0
     # roofline for the dominant kernel (decode attention): algorithmic bytes
-    # per launch / mean launch time (events inside the graphs, last replay of
-    # each slot, all within the timed region)
+    # per launch / average launch duration.  The launches of a step are
+    # PDL-chained (each one's prologue overlaps its predecessor's tail), so the
+    # average duration is the device-timed step time over the decode launches
+    # of a step -- conservative: the per-step plan kernel is charged to them.
+    # The isolated duration (CUDA events around each launch, which break the
+    # chaining) is reported beside it.
     bytes_per_launch = runner.decode_bytes(0)
     dec_mean_ms = statistics.mean(dec_ms) if dec_ms else float("nan")
-    achieved = bytes_per_launch / (dec_mean_ms * 1e-3) / 1e9
+    chained_ms = (ms / args.steps) / w.layers
+    achieved = bytes_per_launch / (chained_ms * 1e-3) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
@@ -323,11 +328,15 @@ def run_ours(args, w, rank, world, local_rank):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": "decode_kernel (nqkv_decode_attention)",
-                     "bytes_per_launch": bytes_per_launch, "mean_launch_us": dec_mean_ms * 1e3,
-                     "launches_timed": len(dec_ms), "peak_source": peak_src,
-                     "timing": "CUDA events around every layer's launch in step slot 0's graph "
-                               "(its last replay inside the timed region; no PDL overlap there)",
-                     "decode_share_of_step": (dec_mean_ms * w.layers) / (ms / args.steps)},
+                     "bytes_per_launch": bytes_per_launch, "mean_launch_us": chained_ms * 1e3,
+                     "launches_timed": args.steps * w.layers, "peak_source": peak_src,
+                     "timing": "device-timed step (CUDA events around the timed region) / decode "
+                               "launches per step; launches PDL-chained inside the step graph; the "
+                               "per-step plan kernel is charged to them",
+                     "isolated_launch_us": dec_mean_ms * 1e3,
+                     "isolated_timing": "CUDA events around every layer's launch in step slot "
+                                        "0's graph (its last replay inside the timed region; "
+                                        "the events break the PDL chaining)"},
         "quantize_roofline": {"bound": "hbm", "achieved": statistics.median(q_gbs), "peak": peak,
                               "unit": "GB/s", "frac": statistics.median(q_gbs) / peak,
                               "kernel": "quantize_kernel (nqkv_quantize, bulk prefill, L2 flushed)",
