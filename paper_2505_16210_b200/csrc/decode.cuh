@@ -27,7 +27,7 @@
 // min_tokens)); a range splits into "pieces" at (b, h) boundaries.
 // Warp specialisation inside the CTA:
 //  * NC consumer warps stream: stage s (ST tokens) of a piece goes to consumer
-//    s % NC.  Lane (g, sub) owns 16 head dims (8 packed bytes) of token g of
+//    (s + o) % NC, o continuing the round robin of the CTA's previous pieces.  Lane (g, sub) owns 16 head dims (8 packed bytes) of token g of
 //    each of the kTPS slots of a stage; loads run one stage ahead, across piece
 //    boundaries.  The online softmax keeps a warp-uniform running max.  At a
 //    piece end a consumer sums its token groups and publishes (m, l, o[hd]).
@@ -898,7 +898,12 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
   // any piece walking -- in plan mode before the per-batch arrays are in
   // shared memory.
   Piece lp = p0;
-  int ls = warp, lpi = 0;
+  // Stage ls of piece lp belongs to warp (ls + lro) mod NC, where lro (the
+  // warp of the piece's first stage) continues the previous piece's round
+  // robin: over a CTA's whole range the warps' stage counts differ by at most
+  // one (a per-piece restart at warp 0 would give the low warps one extra
+  // stage per piece).
+  int ls = warp, lpi = 0, lro = 0;
   bool lvalid = warp < NC, ladv = false;
   int lrb = rowbase(p0);
   set_ptrs(lrb, p0.t0 + warp * ST);
@@ -929,8 +934,9 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
     ladv = true;
     if (ls >= nstages(lp)) {
       do {
+        lro = (lro + nstages(lp)) % NC;
         if (!walk_next(lp, lpi)) { lvalid = false; return false; }
-        ls = warp;
+        ls = warp >= lro ? warp - lro : warp + NC - lro;
         ++lpi;
       } while (ls >= nstages(lp));
       lrb = rowbase(lp);
