@@ -1004,6 +1004,7 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
       }
     };
     Piece pc = p0;
+    TRACE(3);
     if (lane == 0) s_pc[0] = pc;
     new_state(0, pc);
     __syncwarp();
@@ -1196,6 +1197,7 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
       }
     }
     if (lane == 0) s_ml[slot * NC + warp] = make_float2(any ? m : -INFINITY, l);
+    if (k == 0) mbar_wait(mb_full, 0);    // phase 0 of full[0] (see open_piece)
     __syncwarp();
     if (lane == 0) mbar_arrive(mb_done + 8 * slot);
   };
@@ -1209,7 +1211,12 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
 #ifdef NQKV_TRACE
     const unsigned long long w0 = gtimer();
 #endif
-    mbar_wait(mb_full + 8 * (cpi % R), (cpi / R) & 1);
+    // Table 0 was built by the whole CTA before the __syncthreads, so piece
+    // 0 needs no wait (the producer's arrival on full[0] can lag by ~1 us);
+    // its phase 0 is consumed in end_piece(0), before this warp's done(0)
+    // arrival -- phase 1 cannot complete before that (the producer waits
+    // for done(0) before refilling slot 0), so the parity wait is unambiguous.
+    if (cpi != 0) mbar_wait(mb_full + 8 * (cpi % R), (cpi / R) & 1);
 #ifdef NQKV_TRACE
     waited += gtimer() - w0;
 #endif

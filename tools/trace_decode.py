@@ -51,7 +51,7 @@ for _ in range(5):
     torch.cuda.synchronize()
 t = tr.view(148, NW, 16).cpu()
 t0 = t[:, :, 0][t[:, :, 0] > 0].min()
-names = ["entry", "pdl_wait", "prefix", "walk", "loads issued", "V LUT", "table0", "sync", "full0", "loop end", "exit", "prod: last done", "last odd step", "g0/g1", "walk-computed"]
+names = ["entry", "pdl_wait", "prefix", "prod: start", "loads issued", "V LUT", "table0", "sync", "full0", "loop end", "exit", "prod: last done", "last odd step", "g0/g1", "prod: new0 done"]
 for role, sl in (("consumer", slice(0, NW - 1)), ("producer", slice(NW - 1, NW))):
     x = t[:, sl, :].reshape(-1, 16)
     x = x[x[:, 0] > 0]
