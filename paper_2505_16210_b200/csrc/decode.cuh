@@ -131,9 +131,10 @@ struct Smem {
   static constexpr uint32_t kLen = kPref + (kMaxBatch + 1) * 4 + 12;  // int [kMaxBatch]
   static constexpr uint32_t kOne = kLen + kMaxBatch * 4;  // u32 [kMaxBatch / 32]: fused, len == 1
   static constexpr uint32_t kWalk = kOne + kMaxBatch / 8;  // Piece first, last; int reorder, limit
-  static constexpr uint32_t kBytes = kWalk + 64;
+  static constexpr uint32_t kBytes = kWalk + 80;   // + int4 next pieces at kWalk + 64
   static_assert(kBytes <= 227 * 1024, "decode smem over budget");
-  static_assert((kTab % 16) == 0 && (kMbar % 8) == 0 && (kO % 16) == 0, "alignment");
+  static_assert((kTab % 16) == 0 && (kMbar % 8) == 0 && (kO % 16) == 0 && (kWalk % 16) == 0,
+                "alignment");
 };
 
 // ------------------------------------------------------------ primitives
@@ -260,11 +261,12 @@ __device__ __forceinline__ uint32_t slot_off(int r) {
 // (decode_plan_kernel) and each layer's decode kernel reads its CTA's entry
 // instead of rebuilding it on its own serial prologue path.
 // Layout (int32): header [0, 8) = {N, C, q, r, B, H, fused, Tc};
-// per-CTA entries [8, 8 + 16 kMaxGrid) = {first piece (6), last piece (6),
-// reorder, limit, g0, g1}; then len'[kMaxBatch], prefix[kMaxBatch + 1] and
+// per-CTA entries [8, 8 + 20 kMaxGrid) = {first piece (6), last piece (6),
+// reorder, limit, g0, g1, b*H + h of pieces 1..3 in processing order (-1:
+// none), min(4, #pieces)}; then len'[kMaxBatch], prefix[kMaxBatch + 1] and
 // the fused single-token mask[kMaxBatch / 32].
 constexpr int kPlanHdr = 8;
-constexpr int kPlanEntry = 16;
+constexpr int kPlanEntry = 20;
 constexpr int kPlanLen = kPlanHdr + kPlanEntry * kMaxGrid;
 constexpr int kPlanPref = kPlanLen + kMaxBatch;
 constexpr int kPlanOne = kPlanPref + kMaxBatch + 1;
@@ -296,6 +298,36 @@ __device__ __forceinline__ void cta_walk(const int* pref, const int* len, int B,
   locate_piece(pref, len, B, H, max(g0, g1 - 1 - pl.t0), g1, pl);
   reorder = pl.gs != pf.gs && pl.t1 < pl.len;
   limit = reorder ? pl.gs : g1;
+}
+
+// b*H + h of pieces 1..3 in processing order ([last if reordered], first,
+// first+1, ... below limit; -1: none) and min(4, #pieces).
+__device__ __forceinline__ int4 next_pieces(const int* len, int H, int g1, const Piece& pf,
+                                            const Piece& pl, int ro, int lim) {
+  int bh[3] = {-1, -1, -1};
+  Piece x = ro ? pl : pf;
+  int n = 1;
+  for (int k = 1; k < 4; ++k) {
+    if (ro && k == 1) {
+      x = pf;
+    } else {
+      const int g = x.gs + (x.t1 - x.t0);
+      if (g >= lim) break;
+      if (x.h + 1 < H) {
+        ++x.h;
+      } else {
+        do { ++x.b; } while (len[x.b] == 0);
+        x.h = 0;
+        x.len = len[x.b];
+      }
+      x.t0 = 0;
+      x.gs = g;
+      x.t1 = min(x.len, g1 - g);
+    }
+    bh[k - 1] = x.b * H + x.h;
+    ++n;
+  }
+  return make_int4(bh[0], bh[1], bh[2], n);
 }
 
 __global__ void __launch_bounds__(1024) decode_plan_kernel(const int32_t* seq_lens, int B, int H, int Tc,
@@ -355,6 +387,8 @@ __global__ void __launch_bounds__(1024) decode_plan_kernel(const int32_t* seq_le
     e[0] = pf.gs; e[1] = pf.b; e[2] = pf.h; e[3] = pf.len; e[4] = pf.t0; e[5] = pf.t1;
     e[6] = pl.gs; e[7] = pl.b; e[8] = pl.h; e[9] = pl.len; e[10] = pl.t0; e[11] = pl.t1;
     e[12] = ro; e[13] = lim; e[14] = g0; e[15] = g1;
+    const int4 nx = next_pieces(s_len, H, g1, pf, pl, ro, lim);
+    e[16] = nx.x; e[17] = nx.y; e[18] = nx.z; e[19] = nx.w;
   }
 }
 
@@ -637,6 +671,13 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   TRACE(0);
+#ifdef NQKV_TRACE
+  if (p.trace && lane == 0 && warp == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    p.trace[(blockIdx.x * NW + warp) * 16 + 14] = smid + 1;
+  }
+#endif
   if (static_cast<uint32_t>(__cvta_generic_to_shared(smem)) != kSmemWindow) __trap();
   float* s_lv = reinterpret_cast<float*>(smem + Sm::kLv);
   float2* s_tab = reinterpret_cast<float2*>(smem + Sm::kTab);
@@ -682,6 +723,11 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
   const int cta = blockIdx.x;
   Sched sc;
   int g0 = 0, g1 = 0;
+  // pieces 0..R0-1 (processing order) get their q-tables built by the whole
+  // CTA before the consumers start (plan mode: up to R; else piece 0 only),
+  // so short leading pieces never leave consumers waiting on the producer
+  int R0 = 1;
+  int4 pbh = make_int4(-1, -1, -1, 1);     // b*H + h of pieces 1..3, #pieces (<= 4)
   Piece p0;                    // first piece in processing order
   // per-batch arrays into shared memory: from the plan, or computed here
   auto copy_plan_arrays = [&]() {
@@ -699,6 +745,8 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
       __syncthreads();
     } else {
       const int4 a = __ldcg(e4), b = __ldcg(e4 + 1), c = __ldcg(e4 + 2), d = __ldcg(e4 + 3);
+      pbh = __ldcg(e4 + 4);
+      R0 = min(R, pbh.w);
       Piece pf, pl;
       pf.gs = a.x; pf.b = a.y; pf.h = a.z; pf.len = a.w; pf.t0 = b.x; pf.t1 = b.y;
       pl.gs = b.z; pl.b = b.w; pl.h = c.x; pl.len = c.y; pl.t0 = c.z; pl.t1 = c.w;
@@ -769,11 +817,16 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
           s_wi[0] = ro;
           s_wi[1] = lim;
           reinterpret_cast<int*>(smem + Sm::kWalk + 56)[0] = 0;
+          *reinterpret_cast<int4*>(smem + Sm::kWalk + 64) = next_pieces(s_len, p.H, g1, pf, pl, ro, lim);
         }
       }
     }
     __syncthreads();
-    if (sc.N > 0 && cta < sc.C) p0 = s_walk[s_wi[0] ? 1 : 0];
+    if (sc.N > 0 && cta < sc.C) {
+      p0 = s_walk[s_wi[0] ? 1 : 0];
+      pbh = *reinterpret_cast<const int4*>(smem + Sm::kWalk + 64);
+      R0 = min(R, pbh.w);
+    }
   }
   TRACE(2);
 
@@ -836,6 +889,11 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
   // ---- q of piece 0 first (its table is the first thing the consumers
   // need), then the consumers' first stage loads
   const uint4 q0 = load_quad(p0, tid % Q);
+  uint4 qx[R > 1 ? R - 1 : 1];               // q quads of the other prebuilt pieces
+#pragma unroll
+  for (int k = 1; k < R; ++k)
+    if (k < R0)
+      qx[k - 1] = __ldg(reinterpret_cast<const uint4*>(p.q + static_cast<long long>(k == 1 ? pbh.x : k == 2 ? pbh.y : pbh.z) * HD) + tid % Q);
   const int g = lane / LPT, sub = lane % LPT;
   constexpr int NBLK = HD / BLK;
   const int sidx = (sub * kLaneDims) / BLK;
@@ -964,20 +1022,28 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
   // ---- the table of piece 0, built by all threads (thread: pair quad
   // tid % Q); T[e][j] = RN(c q_{2j} L[e & 15]) + RN(c q_{2j+1} L[e >> 4])
   TRACE(5);
-  {
+  // T[e][j] = RN(RN(c q_{2j} L[e & 15]) + RN(c q_{2j+1} L[e >> 4])), exactly
+  // as build_fn rounds it (thread: pair quad tid % Q of rows e = tid / Q + ...)
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    if (k >= R0) break;
     __half2 h2[4];
-    memcpy(h2, &q0, 16);
+    memcpy(h2, k == 0 ? &q0 : &qx[k > 0 ? k - 1 : 0], 16);
     float a[4], b[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const float2 f = __half22float2(h2[k]);
-      a[k] = f.x * p.scale_log2;
-      b[k] = f.y * p.scale_log2;
+    for (int i = 0; i < 4; ++i) {
+      const float2 f = __half22float2(h2[i]);
+      a[i] = f.x * p.scale_log2;
+      b[i] = f.y * p.scale_log2;
     }
+    unsigned char* base = smem + Sm::kK + slot_off<HD>(k) + (tid % Q) * 16;
     for (int e = tid / Q; e < 256; e += NT / Q) {
       const float lo = s_lv[e & 15], hi = s_lv[e >> 4];
-      *reinterpret_cast<float4*>(smem + Sm::kK + e * 256 + (tid % Q) * 16) =
-          make_float4(a[0] * lo + b[0] * hi, a[1] * lo + b[1] * hi, a[2] * lo + b[2] * hi, a[3] * lo + b[3] * hi);
+      *reinterpret_cast<float4*>(base + e * 256) =
+          make_float4(__fadd_rn(__fmul_rn(a[0], lo), __fmul_rn(b[0], hi)),
+                      __fadd_rn(__fmul_rn(a[1], lo), __fmul_rn(b[1], hi)),
+                      __fadd_rn(__fmul_rn(a[2], lo), __fmul_rn(b[2], hi)),
+                      __fadd_rn(__fmul_rn(a[3], lo), __fmul_rn(b[3], hi)));
     }
   }
   TRACE(6);
@@ -1025,7 +1091,7 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
         mbar_wait(mb_done + 8 * ((k - R) % R), ((k - R) / R) & 1);
         merge_fn<HD, NW>(p, smem, k - R, sc, cta, g0);
       }
-      build_fn<HD, NW>(smem, k % R, qc, p.scale_log2);
+      if (k >= R0) build_fn<HD, NW>(smem, k % R, qc, p.scale_log2);
       __syncwarp();
       if (lane == 0) s_pc[k % R] = pc;
       new_state(k, pc);
@@ -1197,7 +1263,7 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
       }
     }
     if (lane == 0) s_ml[slot * NC + warp] = make_float2(any ? m : -INFINITY, l);
-    if (k == 0) mbar_wait(mb_full, 0);    // phase 0 of full[0] (see open_piece)
+    if (k < R0) mbar_wait(mb_full + 8 * k, 0);   // phase 0 of a prebuilt slot (see open_piece)
     __syncwarp();
     if (lane == 0) mbar_arrive(mb_done + 8 * slot);
   };
@@ -1211,12 +1277,12 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
 #ifdef NQKV_TRACE
     const unsigned long long w0 = gtimer();
 #endif
-    // Table 0 was built by the whole CTA before the __syncthreads, so piece
-    // 0 needs no wait (the producer's arrival on full[0] can lag by ~1 us);
-    // its phase 0 is consumed in end_piece(0), before this warp's done(0)
-    // arrival -- phase 1 cannot complete before that (the producer waits
-    // for done(0) before refilling slot 0), so the parity wait is unambiguous.
-    if (cpi != 0) mbar_wait(mb_full + 8 * (cpi % R), (cpi / R) & 1);
+    // Tables 0..R0-1 were built by the whole CTA before the __syncthreads, so
+    // those pieces need no wait (the producer's arrivals can lag by ~1 us);
+    // their phase 0 is consumed in end_piece(k), before this warp's done(k)
+    // arrival -- phase 1 cannot complete before that (the producer waits for
+    // done(k) before refilling slot k), so the parity wait is unambiguous.
+    if (cpi >= R0) mbar_wait(mb_full + 8 * (cpi % R), (cpi / R) & 1);
 #ifdef NQKV_TRACE
     waited += gtimer() - w0;
 #endif

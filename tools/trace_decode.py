@@ -51,7 +51,7 @@ for _ in range(5):
     torch.cuda.synchronize()
 t = tr.view(148, NW, 16).cpu()
 t0 = t[:, :, 0][t[:, :, 0] > 0].min()
-names = ["entry", "pdl_wait", "prefix", "prod: start", "loads issued", "V LUT", "table0", "sync", "full0", "loop end", "exit", "prod: last done", "last odd step", "g0/g1", "prod: new0 done"]
+names = ["entry", "pdl_wait", "prefix", "prod: start", "loads issued", "V LUT", "table0", "sync", "full0", "loop end", "exit", "prod: last done", "last odd step", "g0/g1", ""]
 for role, sl in (("consumer", slice(0, NW - 1)), ("producer", slice(NW - 1, NW))):
     x = t[:, sl, :].reshape(-1, 16)
     x = x[x[:, 0] > 0]
@@ -87,3 +87,16 @@ for npc in sorted(set(r[0] for r in rows)):
           f"min-warp med {np.median([r[2] for r in sel]):.2f} us")
 order = sorted(rows, key=lambda r: r[1])
 print("fastest CTAs", [(r[0], round(r[1], 1)) for r in order[:5]], "slowest", [(r[0], round(r[1], 1)) for r in order[-5:]])
+
+# per-CTA streaming time vs SM id (stamp 14 of warp 0 = smid + 1)
+sm = t[:, 0, 14].long() - 1
+f0 = (t[:, :NW - 1, 8].double() - t0.double()) / 1000.0
+dur = [float(ends[c][ends[c] > 0].max() - f0[c][f0[c] > 0].min()) for c in range(C)]
+rows2 = sorted(((int(sm[c]), dur[c], rows[c][0]) for c in range(C)), key=lambda r: r[0])
+print("smid:dur(us):pieces  " + " ".join(f"{a}:{b:.1f}:{c}" for a, b, c in rows2))
+tpc = {}
+for a, b, c in rows2:
+    tpc.setdefault(a // 2, []).append(b)
+import statistics as st_  # noqa: E402
+print("slowest SMs", sorted(rows2, key=lambda r: -r[1])[:12])
+print("fastest SMs", sorted(rows2, key=lambda r: r[1])[:12])
