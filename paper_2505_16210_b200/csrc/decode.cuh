@@ -133,6 +133,7 @@ struct Smem {
   static constexpr uint32_t kWalk = kOne + kMaxBatch / 8;  // Piece first, last; int reorder, limit
   static constexpr uint32_t kBytes = kWalk + 80;   // + int4 next pieces at kWalk + 64
   static_assert(kBytes <= 227 * 1024, "decode smem over budget");
+  static_assert(kMaxBatch <= 2 * NW * 32, "per-batch arrays: two entries per thread");
   static_assert((kTab % 16) == 0 && (kMbar % 8) == 0 && (kO % 16) == 0 && (kWalk % 16) == 0,
                 "alignment");
 };
@@ -1017,7 +1018,19 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
   // first stage now if it needs no walking (and the arrays are present)
   const bool early = !p.plan || warp < nstages(p0);
   if (early) has[0] = fill(0);
-  if (p.plan) copy_plan_arrays();
+  // per-batch arrays (plan mode): loaded now, stored to shared memory after
+  // the table build, so their latency overlaps the q loads' instead of
+  // stalling the builders (they are first read after the barrier below)
+  int pa_len[2], pa_pref[2], pa_one = 0;
+  if (p.plan) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int b = tid + i * NT;
+      pa_len[i] = b < p.B ? __ldcg(p.plan + kPlanLen + b) : 0;
+      pa_pref[i] = b < p.B ? __ldcg(p.plan + kPlanPref + b) : 0;   // pref[B] = N (header)
+    }
+    if (tid < (p.B + 31) / 32) pa_one = __ldcg(p.plan + kPlanOne + tid);
+  }
   TRACE(4);
   // ---- the table of piece 0, built by all threads (thread: pair quad
   // tid % Q); T[e][j] = RN(c q_{2j} L[e & 15]) + RN(c q_{2j+1} L[e >> 4])
@@ -1045,6 +1058,18 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
                       __fadd_rn(__fmul_rn(a[2], lo), __fmul_rn(b[2], hi)),
                       __fadd_rn(__fmul_rn(a[3], lo), __fmul_rn(b[3], hi)));
     }
+  }
+  if (p.plan) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int b = tid + i * NT;
+      if (b < p.B) {
+        s_len[b] = pa_len[i];
+        s_pref[b] = pa_pref[i];
+      }
+    }
+    if (tid == 0) s_pref[p.B] = sc.N;
+    if (tid < (p.B + 31) / 32) reinterpret_cast<uint32_t*>(smem + Sm::kOne)[tid] = pa_one;
   }
   TRACE(6);
   __syncthreads();
