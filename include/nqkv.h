@@ -164,7 +164,19 @@ int nqkv_decode_step(const void* k_new, const void* v_new, int64_t new_stride_b,
  * streaming without rebuilding it.  fused = 1 for nqkv_decode_step_planned
  * (the appended row is not streamed), 0 for nqkv_decode_attention_planned.
  * The plan must be recomputed whenever seq_lens, B, H, Tc or fused change;
- * results are bit-identical to the unplanned calls. */
+ * results are bit-identical to the unplanned calls.
+ *
+ * flags (the *_planned calls): 0, or NQKV_EARLY_START when neither the plan
+ * nor the cache tensors passed to the call are written by the kernel
+ * launched immediately before it on the same stream -- e.g. layers 1.. of a
+ * decode step whose plan was computed before layer 0.  Every kernel of this
+ * library waits for its predecessor (programmatic dependent launch) before
+ * it lets its successor start, so such a plan and cache are complete when
+ * the call starts, and the kernel reads the plan and issues its first cache
+ * loads before that wait, overlapping the predecessor's tail.  q, k_new,
+ * v_new, seq_lens, out and the workspace are always accessed after the wait.
+ * Results do not depend on flags. */
+#define NQKV_EARLY_START 1
 size_t nqkv_decode_plan_bytes(void);
 int nqkv_decode_plan(const int32_t* d_seq_lens, int B, int H, int Tc, int fused, void* plan,
                      size_t plan_bytes, void* stream);
@@ -172,13 +184,13 @@ int nqkv_decode_attention_planned(const void* q, const uint8_t* k_codes, const f
                                   const uint8_t* v_codes, const float* v_scales,
                                   const int32_t* d_seq_lens, int B, int H, int hd, int blk, int Tc,
                                   float softmax_scale, float* out, void* workspace,
-                                  size_t ws_bytes, const void* plan, void* stream);
+                                  size_t ws_bytes, const void* plan, int flags, void* stream);
 int nqkv_decode_step_planned(const void* k_new, const void* v_new, int64_t new_stride_b,
                              int64_t new_stride_h, const void* q, uint8_t* k_codes,
                              float* k_scales, uint8_t* v_codes, float* v_scales,
                              const int32_t* d_seq_lens, int B, int H, int hd, int blk, int Tc,
                              float softmax_scale, float* out, void* workspace, size_t ws_bytes,
-                             const void* plan, void* stream);
+                             const void* plan, int flags, void* stream);
 
 /* Test hook: the kernels' code function on fp32 inputs already normalised
  * to [-1, 1] (values outside are clamped).  d_n device float[count],

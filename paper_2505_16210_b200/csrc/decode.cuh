@@ -86,6 +86,7 @@ struct DecodeParams {
   Levels lv;
   BucketTab tab;
   const int* plan;             // optional per-step schedule (nqkv_decode_plan); nullptr: computed here
+  int early;                   // NQKV_EARLY_START: plan and cache readable before the PDL wait
   unsigned long long* trace;   // NQKV_TRACE builds: per-warp globaltimer stamps [grid][NW][16]
 };
 
@@ -763,8 +764,16 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
       }
     }
   };
-  pdl_enter();
-  TRACE(1);
+  // NQKV_EARLY_START (planned calls): neither the plan nor the cache is
+  // written by the kernel launched just before this one, and every kernel of
+  // the library triggers its successor only after its own wait, so both are
+  // complete: read the plan and issue the first cache loads before the PDL
+  // wait; everything else (q, k_new / v_new, out, workspace) after it.
+  const bool pre = p.plan != nullptr && p.early != 0;
+  if (!pre) {
+    pdl_enter();
+    TRACE(1);
+  }
   if (p.plan) {
     read_plan();
   } else {
@@ -852,11 +861,11 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
             make_float2(vh[2 * u], vh[2 * u + 1]);
     }
   };
-  if (sc.N == 0) {
-    empties(blockIdx.x * NW + warp, gridDim.x * NW);
+  if (sc.N == 0 || cta >= sc.C) {
+    if (pre) pdl_enter();                     // empties read k_new / write out
+    if (sc.N == 0) empties(blockIdx.x * NW + warp, gridDim.x * NW);
     return;
   }
-  if (cta >= sc.C) return;
   TRACE(13);
 
   // ---- piece walking (identical in every warp; needs s_len / s_pref)
@@ -889,12 +898,7 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
 
   // ---- q of piece 0 first (its table is the first thing the consumers
   // need), then the consumers' first stage loads
-  const uint4 q0 = load_quad(p0, tid % Q);
-  uint4 qx[R > 1 ? R - 1 : 1];               // q quads of the other prebuilt pieces
-#pragma unroll
-  for (int k = 1; k < R; ++k)
-    if (k < R0)
-      qx[k - 1] = __ldg(reinterpret_cast<const uint4*>(p.q + static_cast<long long>(k == 1 ? pbh.x : k == 2 ? pbh.y : pbh.z) * HD) + tid % Q);
+  uint4 q0, qx[R > 1 ? R - 1 : 1];          // q quads of the prebuilt pieces (loaded below)
   const int g = lane / LPT, sub = lane % LPT;
   constexpr int NBLK = HD / BLK;
   const int sidx = (sub * kLaneDims) / BLK;
@@ -1031,6 +1035,15 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
     }
     if (tid < (p.B + 31) / 32) pa_one = __ldcg(p.plan + kPlanOne + tid);
   }
+  if (pre) {
+    pdl_enter();
+    TRACE(1);
+  }
+  q0 = load_quad(p0, tid % Q);
+#pragma unroll
+  for (int k = 1; k < R; ++k)
+    if (k < R0)
+      qx[k - 1] = __ldg(reinterpret_cast<const uint4*>(p.q + static_cast<long long>(k == 1 ? pbh.x : k == 2 ? pbh.y : pbh.z) * HD) + tid % Q);
   TRACE(4);
   // ---- the table of piece 0, built by all threads (thread: pair quad
   // tid % Q); T[e][j] = RN(c q_{2j} L[e & 15]) + RN(c q_{2j+1} L[e >> 4])

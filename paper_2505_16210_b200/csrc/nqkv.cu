@@ -170,7 +170,7 @@ int decode_common(const void* q, const uint8_t* k_codes, const float* k_scales,
                   const uint8_t* v_codes, const float* v_scales, const int32_t* d_seq_lens,
                   const void* k_new, const void* v_new, int64_t new_sb, int64_t new_sh, int B,
                   int H, int hd, int blk, int Tc, float softmax_scale, float* out, void* workspace,
-                  size_t ws_bytes, const void* plan, cudaStream_t st) {
+                  size_t ws_bytes, const void* plan, int flags, cudaStream_t st) {
   if (!q || !k_codes || !k_scales || !v_codes || !v_scales || !d_seq_lens || !out)
     return NQKV_ERR_NULL;
   if (int s = check_geometry(hd, blk)) return s;
@@ -205,6 +205,7 @@ int decode_common(const void* q, const uint8_t* k_codes, const float* k_scales,
   p.lv = make_levels();
   p.tab = make_bucket_tab();
   p.plan = static_cast<const int*>(plan);
+  p.early = plan && (flags & NQKV_EARLY_START) ? 1 : 0;
   p.trace = nullptr;
 #ifdef NQKV_TRACE
   if (const char* t = std::getenv("NQKV_TRACE_PTR"))
@@ -340,7 +341,7 @@ int nqkv_decode_attention(const void* q, const uint8_t* k_codes, const float* k_
                           float softmax_scale, float* out, void* workspace, size_t ws_bytes,
                           void* stream) {
   return decode_common(q, k_codes, k_scales, v_codes, v_scales, d_seq_lens, nullptr, nullptr, 0,
-                       0, B, H, hd, blk, Tc, softmax_scale, out, workspace, ws_bytes, nullptr,
+                       0, B, H, hd, blk, Tc, softmax_scale, out, workspace, ws_bytes, nullptr, 0,
                        static_cast<cudaStream_t>(stream));
 }
 
@@ -364,11 +365,11 @@ int nqkv_decode_attention_planned(const void* q, const uint8_t* k_codes, const f
                                   const uint8_t* v_codes, const float* v_scales,
                                   const int32_t* d_seq_lens, int B, int H, int hd, int blk, int Tc,
                                   float softmax_scale, float* out, void* workspace,
-                                  size_t ws_bytes, const void* plan, void* stream) {
+                                  size_t ws_bytes, const void* plan, int flags, void* stream) {
   if (!plan) return NQKV_ERR_NULL;
   return decode_common(q, k_codes, k_scales, v_codes, v_scales, d_seq_lens, nullptr, nullptr, 0,
                        0, B, H, hd, blk, Tc, softmax_scale, out, workspace, ws_bytes, plan,
-                       static_cast<cudaStream_t>(stream));
+                       flags, static_cast<cudaStream_t>(stream));
 }
 
 int nqkv_decode_step(const void* k_new, const void* v_new, int64_t new_stride_b,
@@ -379,7 +380,7 @@ int nqkv_decode_step(const void* k_new, const void* v_new, int64_t new_stride_b,
   if (!k_new || !v_new) return NQKV_ERR_NULL;
   return decode_common(q, k_codes, k_scales, v_codes, v_scales, d_seq_lens, k_new, v_new,
                        new_stride_b, new_stride_h, B, H, hd, blk, Tc, softmax_scale, out,
-                       workspace, ws_bytes, nullptr, static_cast<cudaStream_t>(stream));
+                       workspace, ws_bytes, nullptr, 0, static_cast<cudaStream_t>(stream));
 }
 
 int nqkv_decode_step_planned(const void* k_new, const void* v_new, int64_t new_stride_b,
@@ -387,11 +388,11 @@ int nqkv_decode_step_planned(const void* k_new, const void* v_new, int64_t new_s
                              float* k_scales, uint8_t* v_codes, float* v_scales,
                              const int32_t* d_seq_lens, int B, int H, int hd, int blk, int Tc,
                              float softmax_scale, float* out, void* workspace, size_t ws_bytes,
-                             const void* plan, void* stream) {
+                             const void* plan, int flags, void* stream) {
   if (!k_new || !v_new || !plan) return NQKV_ERR_NULL;
   return decode_common(q, k_codes, k_scales, v_codes, v_scales, d_seq_lens, k_new, v_new,
                        new_stride_b, new_stride_h, B, H, hd, blk, Tc, softmax_scale, out,
-                       workspace, ws_bytes, plan, static_cast<cudaStream_t>(stream));
+                       workspace, ws_bytes, plan, flags, static_cast<cudaStream_t>(stream));
 }
 
 int nqkv_encode_normalized(const float* d_n, int64_t count, uint8_t* d_codes, void* stream) {

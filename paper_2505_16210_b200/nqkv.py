@@ -44,10 +44,10 @@ _SIGS = {
     "nqkv_decode_plan_bytes": (_sz, []),
     "nqkv_decode_plan": (_i32, [_vp, _i32, _i32, _i32, _i32, _vp, _sz, _vp]),
     "nqkv_decode_attention_planned": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32,
-                                             _i32, ctypes.c_float, _vp, _vp, _sz, _vp, _vp]),
+                                             _i32, ctypes.c_float, _vp, _vp, _sz, _vp, _i32, _vp]),
     "nqkv_decode_step_planned": (_i32, [_vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _i32,
                                         _i32, _i32, _i32, _i32, ctypes.c_float, _vp, _vp, _sz,
-                                        _vp, _vp]),
+                                        _vp, _i32, _vp]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -58,6 +58,8 @@ EXPORTED = tuple(_SIGS)
 ABI_VERSION = 1
 if _lib.nqkv_abi_version() != ABI_VERSION:
     raise ImportError("libnqkv.so ABI version mismatch; rebuild")
+
+EARLY_START = 1     # NQKV_EARLY_START: plan and cache not written by the kernel just before
 
 STATUS = {0: "NQKV_OK", -1: "NQKV_ERR_NULL", -2: "NQKV_ERR_SHAPE", -3: "NQKV_ERR_UNSUPPORTED",
           -4: "NQKV_ERR_ALIGN", -5: "NQKV_ERR_WORKSPACE", -6: "NQKV_ERR_CUDA",
@@ -202,7 +204,8 @@ def nqkv_decode_plan(seq_lens: torch.Tensor, H: int, Tc: int, fused: bool, plan:
 
 
 def nqkv_decode_attention_planned(q, k_codes, k_scales, v_codes, v_scales, seq_lens, blk,
-                                  workspace, plan, softmax_scale=None, out=None, stream=None):
+                                  workspace, plan, softmax_scale=None, out=None, stream=None,
+                                  flags=0):
     B, H, hd = q.shape
     Tc = k_codes.shape[2]
     if softmax_scale is None:
@@ -213,13 +216,13 @@ def nqkv_decode_attention_planned(q, k_codes, k_scales, v_codes, v_scales, seq_l
     _check(_lib.nqkv_decode_attention_planned(
         _ptr(q), _ptr(k_codes), _ptr(k_scales), _ptr(v_codes), _ptr(v_scales), _ptr(seq_lens), B, H,
         hd, blk, Tc, float(softmax_scale), _ptr(out), _ptr(workspace),
-        workspace.numel() * workspace.element_size(), _ptr(plan), _stream(stream)),
+        workspace.numel() * workspace.element_size(), _ptr(plan), int(flags), _stream(stream)),
         "nqkv_decode_attention_planned")
     return out
 
 
 def nqkv_decode_step_planned(k_new, v_new, q, k_codes, k_scales, v_codes, v_scales, seq_lens, blk,
-                             workspace, plan, softmax_scale=None, out=None, stream=None):
+                             workspace, plan, softmax_scale=None, out=None, stream=None, flags=0):
     B, H, hd = q.shape
     Tc = k_codes.shape[2]
     if softmax_scale is None:
@@ -233,7 +236,7 @@ def nqkv_decode_step_planned(k_new, v_new, q, k_codes, k_scales, v_codes, v_scal
         _ptr(k_new), _ptr(v_new), k_new.stride(0), k_new.stride(1), _ptr(q), _ptr(k_codes),
         _ptr(k_scales), _ptr(v_codes), _ptr(v_scales), _ptr(seq_lens), B, H, hd, blk, Tc,
         float(softmax_scale), _ptr(out), _ptr(workspace), workspace.numel() * workspace.element_size(),
-        _ptr(plan), _stream(stream)), "nqkv_decode_step_planned")
+        _ptr(plan), int(flags), _stream(stream)), "nqkv_decode_step_planned")
     return out
 
 
@@ -278,16 +281,17 @@ class KVCache:
         return nqkv_decode_step(k_new, v_new, q, self.k_codes, self.k_scales, self.v_codes,
                                 self.v_scales, seq_lens, self.blk, workspace, out=out, stream=stream)
 
-    def attend_planned(self, q, seq_lens, workspace, plan, out=None, stream=None):
+    def attend_planned(self, q, seq_lens, workspace, plan, out=None, stream=None, flags=0):
         return nqkv_decode_attention_planned(q, self.k_codes, self.k_scales, self.v_codes,
                                              self.v_scales, seq_lens, self.blk, workspace, plan,
-                                             out=out, stream=stream)
+                                             out=out, stream=stream, flags=flags)
 
-    def step_planned(self, k_new, v_new, q, seq_lens, workspace, plan, out=None, stream=None):
+    def step_planned(self, k_new, v_new, q, seq_lens, workspace, plan, out=None, stream=None,
+                     flags=0):
         """Fused append + attend with a per-step plan (nqkv_decode_plan, fused=True)."""
         return nqkv_decode_step_planned(k_new, v_new, q, self.k_codes, self.k_scales,
                                         self.v_codes, self.v_scales, seq_lens, self.blk,
-                                        workspace, plan, out=out, stream=stream)
+                                        workspace, plan, out=out, stream=stream, flags=flags)
 
     def nbytes(self) -> int:
         return sum(t.numel() * t.element_size()

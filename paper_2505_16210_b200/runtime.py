@@ -15,12 +15,16 @@ libnqkv.so; this module only owns buffers, streams and graphs.
 """
 from __future__ import annotations
 
+import os
+
 import torch
 
 from synth import workloads as W
 
 from . import nqkv as N
 from . import sharding
+
+_EARLY = os.environ.get("NQKV_EARLY_START", "1") != "0"   # A/B switch for measurements
 
 
 class DecodeRunner:
@@ -103,8 +107,12 @@ class DecodeRunner:
                 c.append(x[l, 0].unsqueeze(1), x[l, 1].unsqueeze(1), pos)   # [B, 1, H, hd] views
             if events is not None:
                 events[l][0].record()
+            # layers 1.. of a fused step: the kernel just before is the previous
+            # layer's decode, which writes neither the plan nor this cache
+            early = N.EARLY_START if (self.fused and l > 0 and _EARLY) else 0
             if self.fused and self.planned:
-                c.step_planned(x[l, 0], x[l, 1], x[l, 2], lens, self.ws, self.plan, out=self.out[l])
+                c.step_planned(x[l, 0], x[l, 1], x[l, 2], lens, self.ws, self.plan, out=self.out[l],
+                               flags=early)
             elif self.fused:
                 c.step(x[l, 0], x[l, 1], x[l, 2], lens, self.ws, out=self.out[l])
             elif self.planned:

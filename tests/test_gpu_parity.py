@@ -424,18 +424,26 @@ def test_planned_calls_match_unplanned_bit_exact(N, hd, blk):
     o1 = N.nqkv_decode_attention(q, t(kc), t(ks), t(vc), t(vs), L, blk, N.make_workspace(B, H, hd, Tc, DEV))
     o2 = N.nqkv_decode_attention_planned(q, t(kc), t(ks), t(vc), t(vs), L, blk,
                                          N.make_workspace(B, H, hd, Tc, DEV), plan)
+    # plan and first cache loads before the PDL wait (the kernel just before
+    # writes neither: it is torch's workspace fill)
+    o3 = N.nqkv_decode_attention_planned(q, t(kc), t(ks), t(vc), t(vs), L, blk,
+                                         N.make_workspace(B, H, hd, Tc, DEV), plan,
+                                         flags=N.EARLY_START)
     torch.cuda.synchronize()
-    assert torch.equal(o1, o2)
+    assert torch.equal(o1, o2) and torch.equal(o1, o3)
     # fused step (lens after the append)
     L1 = L + 1
     N.nqkv_decode_plan(L1, H, Tc, True, plan)
     a = [t(z) for z in (kc, ks, vc, vs)]
     b = [t(z) for z in (kc, ks, vc, vs)]
     f1 = N.nqkv_decode_step(kn, vn, q, *a, L1, blk, N.make_workspace(B, H, hd, Tc, DEV))
+    c = [t(z) for z in (kc, ks, vc, vs)]
     f2 = N.nqkv_decode_step_planned(kn, vn, q, *b, L1, blk, N.make_workspace(B, H, hd, Tc, DEV), plan)
+    f3 = N.nqkv_decode_step_planned(kn, vn, q, *c, L1, blk, N.make_workspace(B, H, hd, Tc, DEV), plan,
+                                    flags=N.EARLY_START)
     torch.cuda.synchronize()
-    assert torch.equal(f1, f2)
-    assert all(torch.equal(u, v) for u, v in zip(a, b))
+    assert torch.equal(f1, f2) and torch.equal(f1, f3)
+    assert all(torch.equal(u, v) and torch.equal(u, w) for u, v, w in zip(a, b, c))
     O.quantize_append(kn.unsqueeze(1).cpu().numpy(), lens0, blk, kc, ks)
     O.quantize_append(vn.unsqueeze(1).cpu().numpy(), lens0, blk, vc, vs)
     ref = O.decode_attention(q.cpu().numpy(), kc, ks, vc, vs, [n + 1 for n in lens0], blk)

@@ -46,7 +46,7 @@ def chain(traced):
     N.nqkv_decode_plan(lens, H, Tc, True, plan)
     for i in range(L):
         os.environ["NQKV_TRACE_PTR"] = str(tr[i].data_ptr() if traced else 0)
-        kw = {"plan_flags": N.PLAN_EARLY if i > 0 and EARLY else 0} if hasattr(N, "PLAN_EARLY") else {}
+        kw = {"flags": N.EARLY_START if i > 0 and EARLY else 0} if hasattr(N, "EARLY_START") else {}
         caches[i].step_planned(kn[i], vn[i], q[i], lens, ws, plan, out=out[i], **kw)
 
 
