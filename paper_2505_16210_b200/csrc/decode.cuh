@@ -59,6 +59,9 @@ constexpr int kMinTokensPerCta = 512;  // below this a CTA's table build would d
 #ifndef NQKV_DEPTH
 #define NQKV_DEPTH 2             // register ring depth: stages in flight per consumer warp
 #endif
+#ifndef NQKV_SPLIT
+#define NQKV_SPLIT -1            // split K/V ring: 1 on, 0 off, -1 hd 64 only (measured)
+#endif
 #ifndef NQKV_PF
 #define NQKV_PF -1               // L2 prefetch distance in a warp's own stages (-1: per head_dim default)
 #endif
@@ -1017,11 +1020,85 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
     }
     return true;
   };
+  constexpr bool SPL = NQKV_SPLIT > 0 || (NQKV_SPLIT < 0 && HD == 64);
+  // Split ring (D = 2, SPL): a stage's K half is consumed before its V half, so
+  // K slot d is refilled with stage k + 2 right after stage k's scores and V
+  // slot d with stage k + 1... one step later: K loads get ~1.5 steps and V
+  // loads ~1.5 steps to land instead of one, with the same registers.
+  static_assert(!SPL || D == 2, "split ring needs D = 2");
+  uint32_t voff_c[D], voff_s[D];
+  auto fill_k = [&](int d) -> bool {
+    if (!lvalid) return false;
+    if (ladv) {
+      ls += NC;
+      loff_c += NC * ST * (HD / 2);
+      loff_s += NC * ST * NBLK * 4;
+    }
+    ladv = true;
+    if (ls >= nstages(lp)) {
+      do {
+        lro = (lro + nstages(lp)) % NC;
+        if (!walk_next(lp, lpi)) { lvalid = false; return false; }
+        ls = warp >= lro ? warp - lro : warp + NC - lro;
+        ++lpi;
+      } while (ls >= nstages(lp));
+      lrb = rowbase(lp);
+      set_ptrs(lrb, lp.t0 + ls * ST);
+    }
+    const int tok0 = lp.t0 + ls * ST, t1 = lp.t1;
+    mtok[d] = tok0;
+    mt1[d] = t1;
+    mpi[d] = lpi;
+    voff_c[d] = loff_c;
+    voff_s[d] = loff_s;
+    StageRegs& Rg = RG[d];
+#pragma unroll
+    for (int i = 0; i < kTPS; ++i) {
+      if (tok0 + i * G + g < t1) {
+        Rg.k[i] = ldg_stream_64(p.kc + loff_c + i * G * (HD / 2));
+        if constexpr (!RS)
+          Rg.ks[i] = ldg_nc_f32(reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(p.ks) + loff_s) + i * G * NBLK);
+      }
+    }
+    if constexpr (RS) {
+      if (tok0 + (sub & 3) * G + g < t1)
+        Rg.ks[0] = ldg_nc_f32(reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(p.ks) + loff_s + soff_rs));
+    }
+    if (PF > 0 && ls + PF * NC < nstages(lp)) {
+      const int t = lp.t0 + (ls + PF * NC) * ST;
+      prefetch_rows_l2<HD, NBLK>(p, lane, static_cast<long long>(lrb) + t,
+                                 static_cast<long long>(lrb) + min(t + ST, lp.t1));
+    }
+    return true;
+  };
+  auto fill_v = [&](int d) {
+    const int tok0 = mtok[d], t1 = mt1[d];
+    StageRegs& Rg = RG[d];
+#pragma unroll
+    for (int i = 0; i < kTPS; ++i) {
+      if (tok0 + i * G + g < t1) {
+        Rg.v[i] = ldg_stream_64(p.vc + voff_c[d] + i * G * (HD / 2));
+        if constexpr (!RS)
+          Rg.vs[i] = ldg_nc_f32(reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(p.vs) + voff_s[d]) + i * G * NBLK);
+      }
+    }
+    if constexpr (RS) {
+      if (tok0 + (sub & 3) * G + g < t1)
+        Rg.vs[0] = ldg_nc_f32(reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(p.vs) + voff_s[d] + soff_rs));
+    }
+  };
 #pragma unroll
   for (int d = 0; d < D; ++d) has[d] = false;
   // first stage now if it needs no walking (and the arrays are present)
   const bool early = !p.plan || warp < nstages(p0);
-  if (early) has[0] = fill(0);
+  if (early) {
+    if constexpr (SPL) {
+      has[0] = fill_k(0);
+      if (has[0]) fill_v(0);
+    } else {
+      has[0] = fill(0);
+    }
+  }
   // per-batch arrays (plan mode): loaded now, stored to shared memory after
   // the table build, so their latency overlaps the q loads' instead of
   // stalling the builders (they are first read after the barrier below)
@@ -1087,9 +1164,17 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
   TRACE(6);
   __syncthreads();
   TRACE(7);
-  if (!early) has[0] = fill(0);
+  if constexpr (SPL) {
+    if (!early) {
+      has[0] = fill_k(0);
+      if (has[0]) fill_v(0);
+    }
+    has[1] = has[0] && fill_k(1);
+  } else {
+    if (!early) has[0] = fill(0);
 #pragma unroll
-  for (int d = 1; d < D - 1; ++d) has[d] = fill(d);
+    for (int d = 1; d < D - 1; ++d) has[d] = fill(d);
+  }
 
   if (warp == NC) {
     // ================================================================ producer
@@ -1174,7 +1259,8 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
     any = false;
   };
 
-  auto consume = [&](const StageRegs& Rg, int tok0, int t1) {
+  // scores, online-softmax update and the V weights of one stage ...
+  auto consume_s = [&](const StageRegs& Rg, int tok0, int t1, float (&wv)[kTPS]) {
     any = true;
 #ifdef NQKV_EXP_NOCOMPUTE
     {
@@ -1186,6 +1272,8 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
       o2[0] ^= x;
       l += 1.0f;
       m = 0.0f;
+#pragma unroll
+      for (int i = 0; i < kTPS; ++i) wv[i] = 0.0f;
       return;
     }
 #endif
@@ -1203,7 +1291,6 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
       const float2 af = unpack2(a);
       s[i] = RS ? af.x + af.y : (af.x + af.y) * Rg.ks[i];
     }
-    float wv[kTPS];                   // V weight p_i * vs_i of each token slot
     if constexpr (RS) {
       // reduce-scatter over the 4 lanes of the block: lane j = sub % 4 ends
       // with the block sum of slot j (xor 2 keeps the pair holding j, xor 1
@@ -1264,6 +1351,12 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
         wv[i] = pr * Rg.vs[i];
       }
     }
+  };
+  // ... and its P.V accumulation
+  auto consume_v = [&](const StageRegs& Rg, const float (&wv)[kTPS]) {
+#ifdef NQKV_EXP_NOCOMPUTE
+    return;
+#endif
 #pragma unroll
     for (int i = 0; i < kTPS; ++i) {
       const uint64_t w2 = pack2(wv[i], wv[i]);
@@ -1334,15 +1427,32 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
   while (running) {
 #pragma unroll
     for (int d = 0; d < D; ++d) {
-      const int pd = (d + D - 1) % D;
-      has[pd] = fill(pd);
-      if (!has[d]) { running = false; break; }
-      while (cpi < mpi[d]) {
-        end_piece(cpi);
-        ++cpi;
-        open_piece();
+      if constexpr (SPL) {
+        // slot d: K and V of stage k; slot 1 - d: K of stage k + 1
+        if (!has[d]) { running = false; break; }
+        if (has[1 - d]) fill_v((d + 1) % D);
+        while (cpi < mpi[d]) {
+          end_piece(cpi);
+          ++cpi;
+          open_piece();
+        }
+        float wv[kTPS];
+        consume_s(RG[d], mtok[d], mt1[d], wv);
+        has[d] = fill_k(d);                    // K of stage k + 2
+        consume_v(RG[d], wv);
+      } else {
+        const int pd = (d + D - 1) % D;
+        has[pd] = fill(pd);
+        if (!has[d]) { running = false; break; }
+        while (cpi < mpi[d]) {
+          end_piece(cpi);
+          ++cpi;
+          open_piece();
+        }
+        float wv[kTPS];
+        consume_s(RG[d], mtok[d], mt1[d], wv);
+        consume_v(RG[d], wv);
       }
-      consume(RG[d], mtok[d], mt1[d]);
     }
     TRACE(12);
   }
