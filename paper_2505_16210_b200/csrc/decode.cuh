@@ -1304,19 +1304,24 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
       if (LPT == 8) sj += __shfl_xor_sync(0xffffffffu, sj, 4);
       if (tok0 + ST > t1)             // warp-uniform: only a piece's last stage is partial
         sj = (tok0 + (sub & 3) * G + g < t1) ? sj : -INFINITY;
+      // running max per token row group g (its 4 / 8 lanes share the V
+      // weights, so they must share the max): 2 shuffle rounds, not 4-5;
+      // groups are brought to a common max once per piece in end_piece
       float mt = sj;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1)
-        if (!(LPT == 8 && o == 4)) mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, o));
-      if (mt > m) {                   // warp-uniform; the stage has >= 1 valid token
-        const float corr = fast_exp2(m - mt);   // m = -inf -> 0
-        m = mt;
+      mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, 1));
+      mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, 2));
+      const bool up = mt > m;         // uniform within the group
+      if (__any_sync(0xffffffffu, up)) {
+        const float corr = up ? fast_exp2(m - mt) : 1.0f;   // m = -inf -> 0
+        m = up ? mt : m;
         l *= corr;
         const uint64_t c2 = pack2(corr, corr);
 #pragma unroll
         for (int j = 0; j < 8; ++j) o2[j] = fmul2(o2[j], c2);
       }
-      const float pr = fast_exp2(sj - m);       // masked: exp2(-inf) = 0
+      // masked: exp2(-inf) = 0 (a group that has seen only masked slots keeps
+      // m = -inf: subtract 0 there, not -inf)
+      const float pr = fast_exp2(sj - (m == -INFINITY ? 0.0f : m));
       l += pr;                        // this lane's slot only (reduced in end_piece)
       const float w = pr * Rg.vs[0];
 #pragma unroll
@@ -1377,6 +1382,17 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
 #pragma unroll
         for (int o = 1; o < LPT; o <<= 1)
           if (o != 4) l += __shfl_xor_sync(0xffffffffu, l, o);
+        // bring the row groups to the warp max (a group that saw no token has
+        // m = -inf, l = 0, o = 0: its factor is 0)
+        float M = m;
+#pragma unroll
+        for (int o = LPT; o < 32; o <<= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+        const float f = m == -INFINITY ? 0.0f : fast_exp2(m - M);
+        l *= f;
+        const uint64_t f2 = pack2(f, f);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) o2[j] = fmul2(o2[j], f2);
+        m = M;
       }
 #pragma unroll
       for (int o = LPT; o < 32; o <<= 1) {
