@@ -159,12 +159,14 @@ int nqkv_decode_step(const void* k_new, const void* v_new, int64_t new_stride_b,
 /* Per-step schedule (optional).  Every layer of a decode step shares
  * (B, H, Tc, seq_lens): nqkv_decode_plan computes the launch's work
  * partition once -- streamed lengths, token prefix, CTA count and each CTA's
- * first/last piece -- into `plan` (device, >= nqkv_decode_plan_bytes() bytes,
+ * piece order -- into `plan` (device, >= nqkv_decode_plan_bytes() bytes,
  * 16-byte aligned, caller-owned), so that each layer's decode kernel starts
- * streaming without rebuilding it.  fused = 1 for nqkv_decode_step_planned
+ * streaming without rebuilding it.  hd (64 or 128, else
+ * NQKV_ERR_UNSUPPORTED) is the head_dim of the calls that will use the plan
+ * (the piece order depends on it).  fused = 1 for nqkv_decode_step_planned
  * (the appended row is not streamed), 0 for nqkv_decode_attention_planned.
- * The plan must be recomputed whenever seq_lens, B, H, Tc or fused change;
- * results are bit-identical to the unplanned calls.
+ * The plan must be recomputed whenever seq_lens, B, H, hd, Tc or fused
+ * change; results are bit-identical to the unplanned calls.
  *
  * flags (the *_planned calls): 0, or NQKV_EARLY_START when neither the plan
  * nor the cache tensors passed to the call are written by the kernel
@@ -178,7 +180,7 @@ int nqkv_decode_step(const void* k_new, const void* v_new, int64_t new_stride_b,
  * Results do not depend on flags. */
 #define NQKV_EARLY_START 1
 size_t nqkv_decode_plan_bytes(void);
-int nqkv_decode_plan(const int32_t* d_seq_lens, int B, int H, int Tc, int fused, void* plan,
+int nqkv_decode_plan(const int32_t* d_seq_lens, int B, int H, int hd, int Tc, int fused, void* plan,
                      size_t plan_bytes, void* stream);
 int nqkv_decode_attention_planned(const void* q, const uint8_t* k_codes, const float* k_scales,
                                   const uint8_t* v_codes, const float* v_scales,

@@ -134,8 +134,8 @@ struct Smem {
   static constexpr uint32_t kPref = kNew + R * (HD + 4) * 4;  // int [kMaxBatch + 1]
   static constexpr uint32_t kLen = kPref + (kMaxBatch + 1) * 4 + 12;  // int [kMaxBatch]
   static constexpr uint32_t kOne = kLen + kMaxBatch * 4;  // u32 [kMaxBatch / 32]: fused, len == 1
-  static constexpr uint32_t kWalk = kOne + kMaxBatch / 8;  // Piece first, last; int reorder, limit
-  static constexpr uint32_t kBytes = kWalk + 80;   // + int4 next pieces at kWalk + 64
+  static constexpr uint32_t kWalk = kOne + kMaxBatch / 8;  // WalkState (80 B)
+  static constexpr uint32_t kBytes = kWalk + 96;   // + int4 next pieces at kWalk + 80
   static_assert(kBytes <= 227 * 1024, "decode smem over budget");
   static_assert(kMaxBatch <= 2 * NW * 32, "per-batch arrays: two entries per thread");
   static_assert((kTab % 16) == 0 && (kMbar % 8) == 0 && (kO % 16) == 0 && (kWalk % 16) == 0,
@@ -266,12 +266,13 @@ __device__ __forceinline__ uint32_t slot_off(int r) {
 // (decode_plan_kernel) and each layer's decode kernel reads its CTA's entry
 // instead of rebuilding it on its own serial prologue path.
 // Layout (int32): header [0, 8) = {N, C, q, r, B, H, fused, Tc};
-// per-CTA entries [8, 8 + 20 kMaxGrid) = {first piece (6), last piece (6),
-// reorder, limit, g0, g1, b*H + h of pieces 1..3 in processing order (-1:
-// none), min(4, #pieces)}; then len'[kMaxBatch], prefix[kMaxBatch + 1] and
-// the fused single-token mask[kMaxBatch / 32].
+// per-CTA entries [8, 8 + 28 kMaxGrid) = {first piece (6), last piece (6),
+// order flags, limit, g0, g1, b*H + h of pieces 1..3 in processing order (-1:
+// none), min(4, #pieces), first middle piece (6), 0, 0} (WalkState); then
+// len'[kMaxBatch], prefix[kMaxBatch + 1] and the fused single-token
+// mask[kMaxBatch / 32].
 constexpr int kPlanHdr = 8;
-constexpr int kPlanEntry = 20;
+constexpr int kPlanEntry = 28;
 constexpr int kPlanLen = kPlanHdr + kPlanEntry * kMaxGrid;
 constexpr int kPlanPref = kPlanLen + kMaxBatch;
 constexpr int kPlanOne = kPlanPref + kMaxBatch + 1;
@@ -294,41 +295,80 @@ __device__ __forceinline__ void locate_piece(const int* pref, const int* len, in
   pc.t1 = min(pc.len, pc.t0 + (g1 - g));
 }
 
-// Range [g0, g1) of a CTA -> its first piece, its last piece, and whether the
-// last piece (split with the next CTA) is processed first.
-__device__ __forceinline__ void cta_walk(const int* pref, const int* len, int B, int H, int g0, int g1,
-                                         Piece& pf, Piece& pl, int& reorder, int& limit) {
-  locate_piece(pref, len, B, H, g0, g1, pf);
-  locate_piece(pref, len, B, H, g1 - 1, g1, pl);
-  locate_piece(pref, len, B, H, max(g0, g1 - 1 - pl.t0), g1, pl);
-  reorder = pl.gs != pf.gs && pl.t1 < pl.len;
-  limit = reorder ? pl.gs : g1;
+// Processing order of a CTA's pieces (range [g0, g1)):
+//   [pl if split with the next CTA ("reorder": its partial is published
+//   early)], then either pf, pf+1, ... or -- "defer", when pf continues the
+//   previous CTA's sequence, a middle piece exists and the CTA has more
+//   pieces than prebuilt q-table slots R -- pm = pf+1, ..., the last middle,
+//   and pf last, so that no short split piece precedes a producer-built table.
+struct WalkState {
+  Piece pf, pl, pm;
+  int flags;                 // bit 0: reorder, bit 1: defer
+  int limit;                 // end of the sequential run (pl.gs if reorder, else g1)
+};
+
+// piece after pc in token order, if it starts below lim (len: per-batch streamed lengths)
+__device__ __forceinline__ bool next_in_order(const int* len, int H, int g1, int lim, Piece& pc) {
+  const int g = pc.gs + (pc.t1 - pc.t0);
+  if (g >= lim) return false;
+  if (pc.h + 1 < H) {
+    ++pc.h;
+  } else {
+    do { ++pc.b; } while (len[pc.b] == 0);
+    pc.h = 0;
+    pc.len = len[pc.b];
+  }
+  pc.t0 = 0;
+  pc.gs = g;
+  pc.t1 = min(pc.len, g1 - g);
+  return true;
+}
+__device__ __forceinline__ Piece walk_first_ws(const WalkState& w) {
+  return (w.flags & 1) ? w.pl : (w.flags & 2) ? w.pm : w.pf;
+}
+// pc = piece k of the order -> piece k + 1 (false: none)
+__device__ __forceinline__ bool walk_next_ws(const WalkState& w, const int* len, int H, int g1, Piece& pc,
+                                             int k) {
+  const bool defer = (w.flags & 2) != 0;
+  if ((w.flags & 1) && k == 0) {
+    pc = defer ? w.pm : w.pf;
+    return true;
+  }
+  if (defer && pc.gs == w.pf.gs) return false;      // the deferred first piece was last
+  if (next_in_order(len, H, g1, w.limit, pc)) return true;
+  if (defer) {
+    pc = w.pf;
+    return true;
+  }
+  return false;
 }
 
-// b*H + h of pieces 1..3 in processing order ([last if reordered], first,
-// first+1, ... below limit; -1: none) and min(4, #pieces).
-__device__ __forceinline__ int4 next_pieces(const int* len, int H, int g1, const Piece& pf,
-                                            const Piece& pl, int ro, int lim) {
+__device__ __forceinline__ void cta_walk(const int* pref, const int* len, int B, int H, int g0, int g1,
+                                         int R, WalkState& w) {
+  locate_piece(pref, len, B, H, g0, g1, w.pf);
+  locate_piece(pref, len, B, H, g1 - 1, g1, w.pl);
+  locate_piece(pref, len, B, H, max(g0, g1 - 1 - w.pl.t0), g1, w.pl);
+  const bool reorder = w.pl.gs != w.pf.gs && w.pl.t1 < w.pl.len;
+  w.limit = reorder ? w.pl.gs : g1;
+  w.pm = w.pf;
+  const bool middle = next_in_order(len, H, g1, w.limit, w.pm);
+  bool defer = false;
+  if (middle && w.pf.t0 > 0) {              // count pieces (up to R + 1)
+    int n = 1 + (reorder ? 1 : 0);
+    Piece x = w.pf;
+    while (n <= R && next_in_order(len, H, g1, w.limit, x)) ++n;
+    defer = n > R;
+  }
+  w.flags = (reorder ? 1 : 0) | (defer ? 2 : 0);
+}
+
+// b*H + h of pieces 1..3 in processing order (-1: none) and min(4, #pieces).
+__device__ __forceinline__ int4 next_pieces(const WalkState& w, const int* len, int H, int g1) {
   int bh[3] = {-1, -1, -1};
-  Piece x = ro ? pl : pf;
+  Piece x = walk_first_ws(w);
   int n = 1;
   for (int k = 1; k < 4; ++k) {
-    if (ro && k == 1) {
-      x = pf;
-    } else {
-      const int g = x.gs + (x.t1 - x.t0);
-      if (g >= lim) break;
-      if (x.h + 1 < H) {
-        ++x.h;
-      } else {
-        do { ++x.b; } while (len[x.b] == 0);
-        x.h = 0;
-        x.len = len[x.b];
-      }
-      x.t0 = 0;
-      x.gs = g;
-      x.t1 = min(x.len, g1 - g);
-    }
+    if (!walk_next_ws(w, len, H, g1, x, k - 1)) break;
     bh[k - 1] = x.b * H + x.h;
     ++n;
   }
@@ -336,7 +376,8 @@ __device__ __forceinline__ int4 next_pieces(const int* len, int H, int g1, const
 }
 
 __global__ void __launch_bounds__(1024) decode_plan_kernel(const int32_t* seq_lens, int B, int H, int Tc,
-                                                           int fused, int G, int min_tokens, int* plan) {
+                                                           int fused, int G, int min_tokens, int R,
+                                                           int* plan) {
   __shared__ int s_len[kMaxBatch], s_pref[kMaxBatch + 1], s_wsum[32];
   pdl_enter();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -385,15 +426,19 @@ __global__ void __launch_bounds__(1024) decode_plan_kernel(const int32_t* seq_le
   }
   if (sc.N > 0 && tid < sc.C) {
     const int g0 = sc.bnd(tid), g1 = sc.bnd(tid + 1);
-    Piece pf, pl;
-    int ro, lim;
-    cta_walk(s_pref, s_len, B, H, g0, g1, pf, pl, ro, lim);
+    WalkState w;
+    cta_walk(s_pref, s_len, B, H, g0, g1, R, w);
     int* e = plan + kPlanHdr + tid * kPlanEntry;
+    const Piece& pf = w.pf;
+    const Piece& pl = w.pl;
+    const Piece& pm = w.pm;
     e[0] = pf.gs; e[1] = pf.b; e[2] = pf.h; e[3] = pf.len; e[4] = pf.t0; e[5] = pf.t1;
     e[6] = pl.gs; e[7] = pl.b; e[8] = pl.h; e[9] = pl.len; e[10] = pl.t0; e[11] = pl.t1;
-    e[12] = ro; e[13] = lim; e[14] = g0; e[15] = g1;
-    const int4 nx = next_pieces(s_len, H, g1, pf, pl, ro, lim);
+    e[12] = w.flags; e[13] = w.limit; e[14] = g0; e[15] = g1;
+    const int4 nx = next_pieces(w, s_len, H, g1);
     e[16] = nx.x; e[17] = nx.y; e[18] = nx.z; e[19] = nx.w;
+    e[20] = pm.gs; e[21] = pm.b; e[22] = pm.h; e[23] = pm.len; e[24] = pm.t0; e[25] = pm.t1;
+    e[26] = e[27] = 0;
   }
 }
 
@@ -723,8 +768,8 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
     *reinterpret_cast<float4*>(smem + Sm::kV + e * 256 + (i & 15) * 16) = make_float4(lo, hi, lo, hi);
   }
   const uint32_t* s_one = reinterpret_cast<const uint32_t*>(smem + Sm::kOne);
-  Piece* s_walk = reinterpret_cast<Piece*>(smem + Sm::kWalk);
-  int* s_wi = reinterpret_cast<int*>(smem + Sm::kWalk + 48);
+  WalkState* s_ws = reinterpret_cast<WalkState*>(smem + Sm::kWalk);
+  static_assert(sizeof(WalkState) == 80, "walk state layout");
   const int cta = blockIdx.x;
   Sched sc;
   int g0 = 0, g1 = 0;
@@ -751,20 +796,18 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
     } else {
       const int4 a = __ldcg(e4), b = __ldcg(e4 + 1), c = __ldcg(e4 + 2), d = __ldcg(e4 + 3);
       pbh = __ldcg(e4 + 4);
+      const int4 f = __ldcg(e4 + 5), h2 = __ldcg(e4 + 6);
       R0 = min(R, pbh.w);
-      Piece pf, pl;
-      pf.gs = a.x; pf.b = a.y; pf.h = a.z; pf.len = a.w; pf.t0 = b.x; pf.t1 = b.y;
-      pl.gs = b.z; pl.b = b.w; pl.h = c.x; pl.len = c.y; pl.t0 = c.z; pl.t1 = c.w;
+      WalkState w;
+      w.pf.gs = a.x; w.pf.b = a.y; w.pf.h = a.z; w.pf.len = a.w; w.pf.t0 = b.x; w.pf.t1 = b.y;
+      w.pl.gs = b.z; w.pl.b = b.w; w.pl.h = c.x; w.pl.len = c.y; w.pl.t0 = c.z; w.pl.t1 = c.w;
+      w.pm.gs = f.x; w.pm.b = f.y; w.pm.h = f.z; w.pm.len = f.w; w.pm.t0 = h2.x; w.pm.t1 = h2.y;
+      w.flags = d.x;
+      w.limit = d.y;
       g0 = d.z;
       g1 = d.w;
-      p0 = d.x ? pl : pf;
-      if (tid == 0) {
-        s_walk[0] = pf;
-        s_walk[1] = pl;
-        s_wi[0] = d.x;
-        s_wi[1] = d.y;
-        reinterpret_cast<int*>(smem + Sm::kWalk + 56)[0] = 0;
-      }
+      p0 = walk_first_ws(w);
+      if (tid == 0) *s_ws = w;
     }
   };
   // NQKV_EARLY_START (planned calls): neither the plan nor the cache is
@@ -817,27 +860,20 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
         g1 = sc.bnd(cta + 1);
         // Processing order.  If the range's last piece is split with the next
         // CTA it is processed FIRST, so that both cross-CTA partials of this CTA
-        // are published early and the last piece processed (normally a whole
-        // sequence) needs no cross-CTA merge at the end of the kernel.  Order:
-        // [last], first, first+1, ..., up to (not including) the moved last
-        // piece.  (Kept in shared memory: the walkers run rarely.)
+        // are published early (WalkState: full order).  Kept in shared memory:
+        // the walkers run rarely.
         if (tid == 0) {
-          Piece pf, pl;
-          int ro, lim;
-          cta_walk(s_pref, s_len, p.B, p.H, g0, g1, pf, pl, ro, lim);
-          s_walk[0] = pf;
-          s_walk[1] = pl;
-          s_wi[0] = ro;
-          s_wi[1] = lim;
-          reinterpret_cast<int*>(smem + Sm::kWalk + 56)[0] = 0;
-          *reinterpret_cast<int4*>(smem + Sm::kWalk + 64) = next_pieces(s_len, p.H, g1, pf, pl, ro, lim);
+          WalkState w;
+          cta_walk(s_pref, s_len, p.B, p.H, g0, g1, R, w);
+          *s_ws = w;
+          *reinterpret_cast<int4*>(smem + Sm::kWalk + 80) = next_pieces(w, s_len, p.H, g1);
         }
       }
     }
     __syncthreads();
     if (sc.N > 0 && cta < sc.C) {
-      p0 = s_walk[s_wi[0] ? 1 : 0];
-      pbh = *reinterpret_cast<const int4*>(smem + Sm::kWalk + 64);
+      p0 = walk_first_ws(*s_ws);
+      pbh = *reinterpret_cast<const int4*>(smem + Sm::kWalk + 80);
       R0 = min(R, pbh.w);
     }
   }
@@ -872,25 +908,9 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
   TRACE(13);
 
   // ---- piece walking (identical in every warp; needs s_len / s_pref)
-  auto next_piece_to = [&](Piece& pc, int lim) -> bool {
-    const int g = pc.gs + (pc.t1 - pc.t0);
-    if (g >= lim) return false;
-    if (pc.h + 1 < p.H) {
-      ++pc.h;
-    } else {
-      do { ++pc.b; } while (s_len[pc.b] == 0);
-      pc.h = 0;
-      pc.len = s_len[pc.b];
-    }
-    pc.t0 = 0;
-    pc.gs = g;
-    pc.t1 = min(pc.len, g1 - g);
-    return true;
-  };
-  auto walk_first = [&](Piece& pc) { pc = s_walk[s_wi[0] ? 1 : 0]; };
+  auto walk_first = [&](Piece& pc) { pc = walk_first_ws(*s_ws); };
   auto walk_next = [&](Piece& pc, int k) -> bool {   // k = index of pc in processing order
-    if (s_wi[0] && k == 0) { pc = s_walk[0]; return true; }
-    return next_piece_to(pc, s_wi[1]);
+    return walk_next_ws(*s_ws, s_len, p.H, g1, pc, k);
   };
   auto nstages = [&](const Piece& pc) { return (pc.t1 - pc.t0 + ST - 1) / ST; };
   auto rowbase = [&](const Piece& pc) { return (pc.b * p.H + pc.h) * p.Tc; };

@@ -347,9 +347,10 @@ int nqkv_decode_attention(const void* q, const uint8_t* k_codes, const float* k_
 
 size_t nqkv_decode_plan_bytes(void) { return static_cast<size_t>(kPlanInts) * sizeof(int); }
 
-int nqkv_decode_plan(const int32_t* d_seq_lens, int B, int H, int Tc, int fused, void* plan,
+int nqkv_decode_plan(const int32_t* d_seq_lens, int B, int H, int hd, int Tc, int fused, void* plan,
                      size_t plan_bytes, void* stream) {
   if (!d_seq_lens || !plan) return NQKV_ERR_NULL;
+  if (hd != 64 && hd != 128) return NQKV_ERR_UNSUPPORTED;
   if (B < 0 || H <= 0 || Tc <= 0 || Tc % 64 || B > kMaxBatch) return NQKV_ERR_SHAPE;
   if (static_cast<long long>(B) * H * Tc >= (1ll << 31)) return NQKV_ERR_SHAPE;
   if (!aligned16(plan)) return NQKV_ERR_ALIGN;
@@ -357,7 +358,7 @@ int nqkv_decode_plan(const int32_t* d_seq_lens, int B, int H, int Tc, int fused,
   const cudaError_t e = launch_pdl_n(decode_plan_kernel, dim3(1), dim3(1024), 0,
                                    static_cast<cudaStream_t>(stream), d_seq_lens, B, H, Tc,
                                    fused ? 1 : 0, decode_grid(), kMinTokensPerCta,
-                                   static_cast<int*>(plan));
+                                   hd == 64 ? Geo<64>::R : Geo<128>::R, static_cast<int*>(plan));
   return e == cudaSuccess ? NQKV_OK : cuda_fail(e);
 }
 

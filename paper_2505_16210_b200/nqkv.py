@@ -42,7 +42,7 @@ _SIGS = {
                                 _i32, _i32, _i32, ctypes.c_float, _vp, _vp, _sz, _vp]),
     "nqkv_encode_normalized": (_i32, [_vp, _i64, _vp, _vp]),
     "nqkv_decode_plan_bytes": (_sz, []),
-    "nqkv_decode_plan": (_i32, [_vp, _i32, _i32, _i32, _i32, _vp, _sz, _vp]),
+    "nqkv_decode_plan": (_i32, [_vp, _i32, _i32, _i32, _i32, _i32, _vp, _sz, _vp]),
     "nqkv_decode_attention_planned": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32,
                                              _i32, ctypes.c_float, _vp, _vp, _sz, _vp, _i32, _vp]),
     "nqkv_decode_step_planned": (_i32, [_vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _i32,
@@ -194,10 +194,10 @@ def make_plan(device="cuda") -> torch.Tensor:
 
 
 def nqkv_decode_plan(seq_lens: torch.Tensor, H: int, Tc: int, fused: bool, plan: torch.Tensor,
-                     stream=None) -> torch.Tensor:
+                     stream=None, hd: int = 64) -> torch.Tensor:
     """Per-step schedule shared by every layer's planned decode call."""
     assert seq_lens.dtype == torch.int32
-    _check(_lib.nqkv_decode_plan(_ptr(seq_lens), seq_lens.numel(), H, Tc, int(bool(fused)),
+    _check(_lib.nqkv_decode_plan(_ptr(seq_lens), seq_lens.numel(), H, hd, Tc, int(bool(fused)),
                                  _ptr(plan), plan.numel() * plan.element_size(), _stream(stream)),
            "nqkv_decode_plan")
     return plan

@@ -101,7 +101,7 @@ class DecodeRunner:
         pos, lens = self.pos[s], self.attn_lens[s]
         cur = torch.cuda.current_stream()
         if self.planned:
-            N.nqkv_decode_plan(lens, self.Hl, self.Tc, self.fused, self.plan)
+            N.nqkv_decode_plan(lens, self.Hl, self.Tc, self.fused, self.plan, hd=self.hd)
         for l, c in enumerate(self.caches):
             if not self.fused:
                 c.append(x[l, 0].unsqueeze(1), x[l, 1].unsqueeze(1), pos)   # [B, 1, H, hd] views

@@ -124,3 +124,13 @@ def test_missing_library_fails_loudly(tmp_path):
     (pkg / "nqkv.py").write_text(open(N.__file__).read())
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True)
     assert r.returncode != 0 and "not built" in r.stderr
+
+
+def test_plan_argument_errors():
+    f = N._lib.nqkv_decode_plan
+    nb = N._lib.nqkv_decode_plan_bytes()
+    assert f(None, 4, 8, 64, 256, 0, FAKE, nb, None) == -1
+    assert f(FAKE, 4, 8, 96, 256, 0, FAKE, nb, None) == -3        # unsupported head_dim
+    assert f(FAKE, 4, 8, 64, 100, 0, FAKE, nb, None) == -2        # Tc not a multiple of 64
+    assert f(FAKE, 4, 8, 64, 256, 0, FAKE + 4, nb, None) == -4    # misaligned plan
+    assert f(FAKE, 4, 8, 64, 256, 0, FAKE, nb - 16, None) == -5   # plan buffer too small

@@ -420,7 +420,7 @@ def test_planned_calls_match_unplanned_bit_exact(N, hd, blk):
     L = torch.tensor(lens0, dtype=torch.int32, device=DEV)
     plan = N.make_plan(DEV)
     # plain attention
-    N.nqkv_decode_plan(L, H, Tc, False, plan)
+    N.nqkv_decode_plan(L, H, Tc, False, plan, hd=hd)
     o1 = N.nqkv_decode_attention(q, t(kc), t(ks), t(vc), t(vs), L, blk, N.make_workspace(B, H, hd, Tc, DEV))
     o2 = N.nqkv_decode_attention_planned(q, t(kc), t(ks), t(vc), t(vs), L, blk,
                                          N.make_workspace(B, H, hd, Tc, DEV), plan)
@@ -433,7 +433,7 @@ def test_planned_calls_match_unplanned_bit_exact(N, hd, blk):
     assert torch.equal(o1, o2) and torch.equal(o1, o3)
     # fused step (lens after the append)
     L1 = L + 1
-    N.nqkv_decode_plan(L1, H, Tc, True, plan)
+    N.nqkv_decode_plan(L1, H, Tc, True, plan, hd=hd)
     a = [t(z) for z in (kc, ks, vc, vs)]
     b = [t(z) for z in (kc, ks, vc, vs)]
     f1 = N.nqkv_decode_step(kn, vn, q, *a, L1, blk, N.make_workspace(B, H, hd, Tc, DEV))
@@ -448,3 +448,30 @@ def test_planned_calls_match_unplanned_bit_exact(N, hd, blk):
     O.quantize_append(vn.unsqueeze(1).cpu().numpy(), lens0, blk, vc, vs)
     ref = O.decode_attention(q.cpu().numpy(), kc, ks, vc, vs, [n + 1 for n in lens0], blk)
     assert np.max(np.abs(f2.cpu().numpy() - ref)) <= ATOL
+
+
+@pytest.mark.parametrize("hd", [64, 128])
+def test_planned_many_pieces_deferred_order(N, hd):
+    """CTAs holding more pieces than prebuilt q-table slots process a split
+    first piece last (WalkState "defer"): planned == unplanned bit for bit,
+    and both match the oracle."""
+    blk = 64
+    lens0 = [(37 * i) % 190 + 3 for i in range(40)]
+    B, H, T = len(lens0), 6, max(lens0)
+    Tc = -(-T // 64) * 64
+    x = _rand_kv(B, T, H, hd, seed=61)
+    y = _rand_kv(B, T, H, hd, seed=62, outlier=False)
+    q = torch.randn(B, H, hd, generator=torch.Generator().manual_seed(63)).to(torch.float16).to(DEV)
+    kc, ks = _oracle_cache(x, [0] * B, blk, Tc)
+    vc, vs = _oracle_cache(y, [0] * B, blk, Tc)
+    t = lambda a: torch.from_numpy(a.copy()).to(DEV)
+    L = torch.tensor(lens0, dtype=torch.int32, device=DEV)
+    plan = N.make_plan(DEV)
+    N.nqkv_decode_plan(L, H, Tc, False, plan, hd=hd)
+    o1 = N.nqkv_decode_attention(q, t(kc), t(ks), t(vc), t(vs), L, blk, N.make_workspace(B, H, hd, Tc, DEV))
+    o2 = N.nqkv_decode_attention_planned(q, t(kc), t(ks), t(vc), t(vs), L, blk,
+                                         N.make_workspace(B, H, hd, Tc, DEV), plan)
+    torch.cuda.synchronize()
+    assert torch.equal(o1, o2)
+    ref = O.decode_attention(q.cpu().numpy(), kc, ks, vc, vs, lens0, blk)
+    assert np.max(np.abs(o2.cpu().numpy() - ref)) <= ATOL

@@ -43,7 +43,7 @@ flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
 
 
 def chain(traced):
-    N.nqkv_decode_plan(lens, H, Tc, True, plan)
+    N.nqkv_decode_plan(lens, H, Tc, True, plan, hd=hd)
     for i in range(L):
         os.environ["NQKV_TRACE_PTR"] = str(tr[i].data_ptr() if traced else 0)
         kw = {"flags": N.EARLY_START if i > 0 and EARLY else 0} if hasattr(N, "EARLY_START") else {}

@@ -36,7 +36,7 @@ flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
 warm = os.environ.get("WARM") == "1"    # trace the 2nd of two back-to-back launches (no flush between)
 planned = os.environ.get("PLAN") == "1"
 plan = N.make_plan("cuda")
-N.nqkv_decode_plan(L, H, Tc, False, plan)
+N.nqkv_decode_plan(L, H, Tc, False, plan, hd=hd)
 if planned:
     cache.attend = lambda q_, L_, ws_: cache.attend_planned(q_, L_, ws_, plan)
 for _ in range(5):
@@ -100,3 +100,8 @@ for a, b, c in rows2:
 import statistics as st_  # noqa: E402
 print("slowest SMs", sorted(rows2, key=lambda r: -r[1])[:12])
 print("fastest SMs", sorted(rows2, key=lambda r: r[1])[:12])
+# per-warp-index medians of (loop end - full0): SM sub-partition (warp % 4) balance
+le = (t[:, :NW - 1, 9].double() - t0.double()) / 1000.0
+f0w = (t[:, :NW - 1, 8].double() - t0.double()) / 1000.0
+dd = le - f0w
+print("warp: median stream time (us) " + " ".join(f"{w}:{float(dd[:, w].median()):.2f}" for w in range(NW - 1)))
