@@ -475,3 +475,33 @@ def test_planned_many_pieces_deferred_order(N, hd):
     assert torch.equal(o1, o2)
     ref = O.decode_attention(q.cpu().numpy(), kc, ks, vc, vs, lens0, blk)
     assert np.max(np.abs(o2.cpu().numpy() - ref)) <= ATOL
+
+
+def test_planned_large_batch_arrays(N):
+    """B > 512: the per-batch arrays take two entries per thread in the
+    planned prologue (and pref[B] comes from the plan header)."""
+    blk, hd, H = 64, 64, 2
+    B = 700
+    lens0 = [(i * 7919) % 97 for i in range(B)]          # includes empty sequences
+    T = max(lens0)
+    Tc = -(-T // 64) * 64
+    x = _rand_kv(B, T, H, hd, seed=71)
+    y = _rand_kv(B, T, H, hd, seed=72, outlier=False)
+    q = torch.randn(B, H, hd, generator=torch.Generator().manual_seed(73)).to(torch.float16).to(DEV)
+    kc, ks = _oracle_cache(x, [0] * B, blk, Tc)
+    vc, vs = _oracle_cache(y, [0] * B, blk, Tc)
+    t = lambda a: torch.from_numpy(a.copy()).to(DEV)
+    L = torch.tensor(lens0, dtype=torch.int32, device=DEV)
+    plan = N.make_plan(DEV)
+    N.nqkv_decode_plan(L, H, Tc, False, plan, hd=hd)
+    o1 = N.nqkv_decode_attention(q, t(kc), t(ks), t(vc), t(vs), L, blk, N.make_workspace(B, H, hd, Tc, DEV))
+    o2 = N.nqkv_decode_attention_planned(q, t(kc), t(ks), t(vc), t(vs), L, blk,
+                                         N.make_workspace(B, H, hd, Tc, DEV), plan,
+                                         flags=N.EARLY_START)
+    torch.cuda.synchronize()
+    assert torch.equal(o1, o2)
+    rng = np.random.default_rng(1)
+    for b in sorted(set(rng.integers(0, B, 24).tolist()) | {0, B - 1}):
+        ref = O.decode_attention(q[b:b + 1].cpu().numpy(), kc[b:b + 1], ks[b:b + 1], vc[b:b + 1],
+                                 vs[b:b + 1], [lens0[b]], blk)
+        assert np.max(np.abs(o2[b:b + 1].cpu().numpy() - ref)) <= ATOL
