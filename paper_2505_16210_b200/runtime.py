@@ -51,7 +51,11 @@ class DecodeRunner:
                        for _ in range(self.L)]
         self.ws = N.make_workspace(self.B, self.Hl, self.hd, self.Tc, self.dev)
         self.plan = N.make_plan(self.dev)
-        self.out = torch.zeros((self.L, self.B, self.Hl, self.hd), dtype=torch.float32, device=self.dev)
+        # outputs double-buffered by slot parity, so a step's device->host
+        # read can overlap the next step's kernels (bench.py e2e)
+        self.outs = torch.zeros((2, self.L, self.B, self.Hl, self.hd), dtype=torch.float32,
+                                device=self.dev)
+        self._last = 0
         steps = torch.arange(self.S, dtype=torch.int32)[:, None]
         self.pos = (lens0[None, :] + steps).to(torch.int32).to(self.dev)          # [S, B]
         self.attn_lens = (self.pos + 1).contiguous()                               # [S, B]
@@ -96,7 +100,18 @@ class DecodeRunner:
         return [a.elapsed_time(b) for a, b in times]
 
     # --------------------------------------------------------------- step --
+    @property
+    def out(self) -> torch.Tensor:
+        """Outputs [L, B, H, hd] of the most recent step (replay)."""
+        return self.outs[self._last % 2]
+
+    def out_of(self, s: int) -> torch.Tensor:
+        """Output buffer written by step slot s."""
+        return self.outs[(s % self.S) % 2]
+
     def step(self, s: int, events=None) -> None:
+        self._last = s
+        out = self.outs[s % 2]
         x = self.inputs[s]
         pos, lens = self.pos[s], self.attn_lens[s]
         cur = torch.cuda.current_stream()
@@ -111,20 +126,20 @@ class DecodeRunner:
             # layer's decode, which writes neither the plan nor this cache
             early = N.EARLY_START if (self.fused and l > 0 and _EARLY) else 0
             if self.fused and self.planned:
-                c.step_planned(x[l, 0], x[l, 1], x[l, 2], lens, self.ws, self.plan, out=self.out[l],
+                c.step_planned(x[l, 0], x[l, 1], x[l, 2], lens, self.ws, self.plan, out=out[l],
                                flags=early)
             elif self.fused:
-                c.step(x[l, 0], x[l, 1], x[l, 2], lens, self.ws, out=self.out[l])
+                c.step(x[l, 0], x[l, 1], x[l, 2], lens, self.ws, out=out[l])
             elif self.planned:
-                c.attend_planned(x[l, 2], lens, self.ws, self.plan, out=self.out[l])
+                c.attend_planned(x[l, 2], lens, self.ws, self.plan, out=out[l])
             else:
-                c.attend(x[l, 2], lens, self.ws, out=self.out[l])
+                c.attend(x[l, 2], lens, self.ws, out=out[l])
             if events is not None:
                 events[l][1].record()
             if self.world > 1:
                 self.comm.wait_stream(cur)
                 with torch.cuda.stream(self.comm):
-                    sharding.all_gather_heads(self.out[l], self.gathered[l], self.group)
+                    sharding.all_gather_heads(out[l], self.gathered[l], self.group)
         if self.world > 1:
             cur.wait_stream(self.comm)
 
@@ -148,6 +163,7 @@ class DecodeRunner:
         torch.cuda.synchronize()
 
     def replay(self, i: int) -> None:
+        self._last = i % self.S
         self.graphs[i % self.S].replay()
 
     def decode_kernel_ms(self) -> list[float]:
