@@ -400,6 +400,8 @@ def main():
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
+        # bound NCCL's SM use to the 2 SMs the decode grid leaves free (runtime.py)
+        os.environ.setdefault("NCCL_MAX_NCHANNELS", "2")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
         return run_ours(args, w, rank, world, local_rank)

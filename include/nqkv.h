@@ -125,7 +125,9 @@ size_t nqkv_decode_counter_bytes(int B, int H);
  *            16-byte aligned, ALL ZERO before the first use; every
  *            completed call leaves it zero again.  Do not share one workspace between calls
  *            that may run concurrently (calls ordered on one stream may).
- * One launch of one CTA per SM with programmatic dependent launch (PDL).  The
+ * One launch of one CTA per SM (or NQKV_DECODE_CTAS from the environment,
+ * read once, if smaller: leaves SMs free for a collective running beside it)
+ * with programmatic dependent launch (PDL).  The
  * (b, h, t) token list is cut into equal contiguous per-CTA ranges; a
  * sequence split across CTAs is merged by the last of its CTAs to arrive
  * (per-(b, h) relaxed counter; the others publish tagged partial records

@@ -72,9 +72,22 @@ int device_sms() {
   return sms > 0 ? sms : 148;
 }
 
+// One decode CTA per SM (a CTA fills an SM's registers and shared memory),
+// or fewer when NQKV_DECODE_CTAS asks for it: with a collective running on a
+// side stream (multi-GPU runtime), its kernel needs SMs of its own, because it
+// cannot share an SM with a decode CTA.  Read once per process.
 int decode_grid() {
-  const int sms = device_sms();
-  return sms > kMaxGrid ? kMaxGrid : sms;
+  static int cached = 0;
+  if (cached <= 0) {
+    const int sms = device_sms();
+    int g = sms > kMaxGrid ? kMaxGrid : sms;
+    if (const char* e = std::getenv("NQKV_DECODE_CTAS")) {
+      const int v = std::atoi(e);
+      if (v > 0 && v < g) g = v;
+    }
+    cached = g;
+  }
+  return cached;
 }
 
 long long grid_for(long long work, int threads, int per_sm) {

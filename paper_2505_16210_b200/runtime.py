@@ -33,6 +33,11 @@ class DecodeRunner:
                  gen_device=None, planned: bool = True):
         self.w = w
         self.fused = fused
+        if world > 1:
+            # the all-gather kernels on the side stream need SMs of their own (a
+            # decode CTA fills an SM): leave 2 free (read once by libnqkv)
+            sms = torch.cuda.get_device_properties(torch.device(device)).multi_processor_count
+            os.environ.setdefault("NQKV_DECODE_CTAS", str(max(1, sms - 2)))
         # one nqkv_decode_plan per step, shared by every layer's decode launch
         self.planned = planned
         self.heads = heads
