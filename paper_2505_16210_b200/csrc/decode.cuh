@@ -59,6 +59,9 @@ constexpr int kMinTokensPerCta = 512;  // below this a CTA's table build would d
 #ifndef NQKV_DEPTH
 #define NQKV_DEPTH 2             // register ring depth: stages in flight per consumer warp
 #endif
+#ifndef NQKV_PEEK
+#define NQKV_PEEK -1             // early last-arriver role for the last piece: 1 on, 0 off, -1 hd 128 only (measured)
+#endif
 #ifndef NQKV_SPLIT
 #define NQKV_SPLIT -1            // split K/V ring: 1 on, 0 off, -1 hd 64 only (measured)
 #endif
@@ -135,7 +138,12 @@ struct Smem {
   static constexpr uint32_t kLen = kPref + (kMaxBatch + 1) * 4 + 12;  // int [kMaxBatch]
   static constexpr uint32_t kOne = kLen + kMaxBatch * 4;  // u32 [kMaxBatch / 32]: fused, len == 1
   static constexpr uint32_t kWalk = kOne + kMaxBatch / 8;  // WalkState (80 B)
-  static constexpr uint32_t kBytes = kWalk + 96;   // + int4 next pieces at kWalk + 80
+  // + int4 next pieces at kWalk + 80; int "prefetched partials" flag at
+  // kWalk + 96; float [kPreRecs][HD + 2] prefetched partner records
+  static constexpr uint32_t kPreFlag = kWalk + 96;
+  static constexpr uint32_t kPre = kWalk + 112;
+  static constexpr int kPreRecs = 4;
+  static constexpr uint32_t kBytes = (kPre + kPreRecs * (HD + 2) * 4 + 15) / 16 * 16;
   static_assert(kBytes <= 227 * 1024, "decode smem over budget");
   static_assert(kMaxBatch <= 2 * NW * 32, "per-batch arrays: two entries per thread");
   static_assert((kTab % 16) == 0 && (kMbar % 8) == 0 && (kO % 16) == 0 && (kWalk % 16) == 0,
@@ -552,6 +560,71 @@ __device__ __noinline__ void build_fn(unsigned char* smem, int slot, uint4 qraw,
   }
 }
 
+__device__ __forceinline__ int ld_relaxed_s32(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Before waiting for the consumers to finish the CTA's last piece k: if it is
+// split across CTAs and every other CTA of its sequence has already arrived
+// (counter = #others), this CTA will be the last arriver -- it takes that role
+// without its own atomic, pulls the others' records into shared memory now
+// (each was, or is about to be, stored by a CTA that already arrived), clears
+// them, and flags piece k; merge_fn then needs no global round trip at the
+// end of the kernel.
+template <int HD, int NW>
+__device__ __noinline__ void peek_fn(const DecodeParams& p, unsigned char* smem, int k, Sched sc, int cta) {
+  using Sm = Smem<HD, NW>;
+  constexpr int PPL = Geo<HD>::PPL, R = Geo<HD>::R;
+  const int lane = threadIdx.x & 31;
+  const Piece pc = reinterpret_cast<const Piece*>(smem + Sm::kPc)[k % R];
+  if (pc.t0 == 0 && pc.t1 == pc.len) return;
+  const int st0 = pc.gs - pc.t0;
+  const int ca = sc.cta_of(st0), cb = sc.cta_of(st0 + pc.len - 1);
+  if (cb - ca > Sm::kPreRecs) return;
+  const long long bh = static_cast<long long>(pc.b) * p.H + pc.h;
+  int arrived = 0;
+  if (lane == 0) arrived = ld_relaxed_s32(p.cnt + bh);
+  arrived = __shfl_sync(0xffffffffu, arrived, 0);
+  if (arrived != cb - ca) return;
+  float* pre = reinterpret_cast<float*>(smem + Sm::kPre);
+  auto dim = [&](int u) { return 2 * (lane + 32 * u); };
+  for (int c = ca; c <= cb; ++c) {
+    if (c == cta) continue;
+    unsigned long long* r = p.part + (static_cast<long long>(c) * 2 + ((c == ca && sc.bnd(c) != st0) ? 1 : 0)) * (HD + 2);
+    unsigned long long wm, wl, wo[2 * PPL];
+    for (;;) {
+      wm = ld_relaxed_u64(r + HD);
+      wl = ld_relaxed_u64(r + HD + 1);
+      bool ok = (wm >> 32) && (wl >> 32);
+#pragma unroll
+      for (int u = 0; u < PPL; ++u) {
+        wo[2 * u] = ld_relaxed_u64(r + dim(u));
+        wo[2 * u + 1] = ld_relaxed_u64(r + dim(u) + 1);
+        ok = ok && (wo[2 * u] >> 32) && (wo[2 * u + 1] >> 32);
+      }
+      if (__all_sync(0xffffffffu, ok)) break;
+    }
+    float* dst = pre + (c - ca - (c > cta ? 1 : 0)) * (HD + 2);
+#pragma unroll
+    for (int u = 0; u < PPL; ++u) {
+      dst[dim(u)] = __uint_as_float(static_cast<uint32_t>(wo[2 * u]));
+      dst[dim(u) + 1] = __uint_as_float(static_cast<uint32_t>(wo[2 * u + 1]));
+      st_relaxed_u64(r + dim(u), 0ull);
+      st_relaxed_u64(r + dim(u) + 1, 0ull);
+    }
+    if (lane == 0) {
+      dst[HD] = __uint_as_float(static_cast<uint32_t>(wm));
+      dst[HD + 1] = __uint_as_float(static_cast<uint32_t>(wl));
+      st_relaxed_u64(r + HD, 0ull);
+      st_relaxed_u64(r + HD + 1, 0ull);
+    }
+  }
+  __syncwarp();
+  if (lane == 0) *reinterpret_cast<int*>(smem + Sm::kPreFlag) = k + 1;
+}
+
 // Merge piece k's NC consumer states (ring slot k % R) and, in a fused step,
 // the appended token's state: write the output, or a partial (+ the
 // last-arriver merge of the sequence's partials across CTAs).
@@ -567,6 +640,10 @@ __device__ __noinline__ void merge_fn(const DecodeParams& p, unsigned char* smem
   const float2* s_ml = reinterpret_cast<const float2*>(smem + Sm::kMl) + slot * NC;
   const float* s_o = reinterpret_cast<const float*>(smem + Sm::kO) + slot * NC * HD;
   auto dim = [&](int u) { return 2 * (lane + 32 * u); };
+#ifdef NQKV_TRACE
+  const int warp = threadIdx.x >> 5;
+  if (p.trace && lane == 0) p.trace[(blockIdx.x * NW + warp) * 16 + 12] = gtimer();   // merge entry
+#endif
   const float snew = st[HD];
   float mw[NC];
   float M = snew;
@@ -600,6 +677,9 @@ __device__ __noinline__ void merge_fn(const DecodeParams& p, unsigned char* smem
     }
   }
   const long long bh = static_cast<long long>(pc.b) * p.H + pc.h;
+#ifdef NQKV_TRACE
+  if (p.trace && lane == 0) p.trace[(blockIdx.x * NW + warp) * 16 + 14] = gtimer();   // combined
+#endif
   if (pc.t0 == 0 && pc.t1 == pc.len) {
     const float inv = 1.0f / den;
 #pragma unroll
@@ -617,9 +697,14 @@ __device__ __noinline__ void merge_fn(const DecodeParams& p, unsigned char* smem
   // the critical path (atomic, poll), no fence.
   const int st0 = pc.gs - pc.t0;                                // global index of token 0
   const int ca = sc.cta_of(st0), cb = sc.cta_of(st0 + pc.len - 1);
-  int last = 0;
-  if (lane == 0) last = atom_add_relaxed(p.cnt + bh, 1) == cb - ca;
-  last = __shfl_sync(0xffffffffu, last, 0);
+  // prefetched by peek_fn: this CTA is the last arriver, the others' records
+  // are in shared memory (already cleared in global memory)
+  const bool pre = *reinterpret_cast<const int*>(smem + Sm::kPreFlag) == k + 1;
+  int last = 1;
+  if (!pre) {
+    if (lane == 0) last = atom_add_relaxed(p.cnt + bh, 1) == cb - ca;
+    last = __shfl_sync(0xffffffffu, last, 0);
+  }
   auto rec = [&](int c, int sl) { return p.part + (static_cast<long long>(c) * 2 + sl) * (HD + 2); };
   auto tag = [](float v) {
     return static_cast<unsigned long long>(__float_as_uint(v)) | (1ull << 32);
@@ -652,6 +737,17 @@ __device__ __noinline__ void merge_fn(const DecodeParams& p, unsigned char* smem
         rm[i] = M; rl[i] = den;
 #pragma unroll
         for (int d = 0; d < 2 * PPL; ++d) ro[i][d] = acc[d];
+        continue;
+      }
+      if (pre) {
+        const float* src = reinterpret_cast<const float*>(smem + Sm::kPre) + (c - ca - (c > cta ? 1 : 0)) * (HD + 2);
+        rm[i] = src[HD];
+        rl[i] = src[HD + 1];
+#pragma unroll
+        for (int u = 0; u < PPL; ++u) {
+          ro[i][2 * u] = src[dim(u)];
+          ro[i][2 * u + 1] = src[dim(u) + 1];
+        }
         continue;
       }
       const unsigned long long* r = rec(c, (c == ca && sc.bnd(c) != st0) ? 1 : 0);
@@ -753,6 +849,7 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
   if (tid < 16) s_lv[tid] = p.lv.v[tid];
   if (tid < kNumBuckets) s_tab[tid] = p.tab.e[tid];
   if (tid == 0) {
+    *reinterpret_cast<int*>(smem + Sm::kPreFlag) = 0;
     for (int r = 0; r < R; ++r) {
       mbar_init(mb_full + 8 * r, 1);
       mbar_init(mb_done + 8 * r, NC);
@@ -1243,6 +1340,10 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
     }
     TRACE(9);
     for (int j = max(0, k + 1 - R); j <= k; ++j) {
+      // the last piece: try to take the last-arriver role early (after the
+      // previous pieces' merges, so the partners have had time to arrive)
+      if (j == k && (NQKV_PEEK > 0 || (NQKV_PEEK < 0 && HD == 128)))
+        peek_fn<HD, NW>(p, smem, k, sc, cta);
       mbar_wait(mb_done + 8 * (j % R), (j / R) & 1);
       if (j == k) TRACE(11);
       merge_fn<HD, NW>(p, smem, j, sc, cta, g0);

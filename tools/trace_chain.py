@@ -109,7 +109,7 @@ for i in range(L):
 
 # detail for one steady-state layer: per-role medians of every stamp, and the slowest CTA
 names = ["entry", "pdl_wait", "prefix", "walk", "loads issued", "V LUT", "table0", "sync", "full0",
-         "loop end", "exit", "prod: last done", "last odd step", "g0/g1", "walk-computed"]
+         "loop end", "exit", "prod: last done", "last odd step|merge in", "g0/g1", "smid|merge comb"]
 i = min(3, L - 1)
 x = t[i] - t[i, :, :, 0][~torch.isnan(t[i, :, :, 0])].min()
 for role, sl in (("consumer", slice(0, NW - 1)), ("producer", slice(NW - 1, NW))):
