@@ -569,10 +569,10 @@ __device__ __forceinline__ int ld_relaxed_s32(const int* p) {
 // Before waiting for the consumers to finish the CTA's last piece k: if it is
 // split across CTAs and every other CTA of its sequence has already arrived
 // (counter = #others), this CTA will be the last arriver -- it takes that role
-// without its own atomic, pulls the others' records into shared memory now
-// (each was, or is about to be, stored by a CTA that already arrived), clears
-// them, and flags piece k; merge_fn then needs no global round trip at the
-// end of the kernel.
+// without its own atomic.  If the others' records are already complete (one
+// read, no spinning) it pulls them into shared memory, clears them and flags
+// piece k; merge_fn then needs no global round trip at the end of the
+// kernel.  Otherwise merge_fn runs the normal protocol.
 template <int HD, int NW>
 __device__ __noinline__ void peek_fn(const DecodeParams& p, unsigned char* smem, int k, Sched sc, int cta) {
   using Sm = Smem<HD, NW>;
@@ -590,33 +590,41 @@ __device__ __noinline__ void peek_fn(const DecodeParams& p, unsigned char* smem,
   if (arrived != cb - ca) return;
   float* pre = reinterpret_cast<float*>(smem + Sm::kPre);
   auto dim = [&](int u) { return 2 * (lane + 32 * u); };
+  auto rec_of = [&](int c) {
+    return p.part + (static_cast<long long>(c) * 2 + ((c == ca && sc.bnd(c) != st0) ? 1 : 0)) * (HD + 2);
+  };
+  // one read of every record (no spinning: a record not yet complete makes
+  // the final merge take the normal path); all complete -> keep and clear
+  bool ok = true;
   for (int c = ca; c <= cb; ++c) {
     if (c == cta) continue;
-    unsigned long long* r = p.part + (static_cast<long long>(c) * 2 + ((c == ca && sc.bnd(c) != st0) ? 1 : 0)) * (HD + 2);
-    unsigned long long wm, wl, wo[2 * PPL];
-    for (;;) {
-      wm = ld_relaxed_u64(r + HD);
-      wl = ld_relaxed_u64(r + HD + 1);
-      bool ok = (wm >> 32) && (wl >> 32);
-#pragma unroll
-      for (int u = 0; u < PPL; ++u) {
-        wo[2 * u] = ld_relaxed_u64(r + dim(u));
-        wo[2 * u + 1] = ld_relaxed_u64(r + dim(u) + 1);
-        ok = ok && (wo[2 * u] >> 32) && (wo[2 * u + 1] >> 32);
-      }
-      if (__all_sync(0xffffffffu, ok)) break;
-    }
+    const unsigned long long* r = rec_of(c);
+    const unsigned long long wm = ld_relaxed_u64(r + HD), wl = ld_relaxed_u64(r + HD + 1);
+    bool good = (wm >> 32) && (wl >> 32);
     float* dst = pre + (c - ca - (c > cta ? 1 : 0)) * (HD + 2);
 #pragma unroll
     for (int u = 0; u < PPL; ++u) {
-      dst[dim(u)] = __uint_as_float(static_cast<uint32_t>(wo[2 * u]));
-      dst[dim(u) + 1] = __uint_as_float(static_cast<uint32_t>(wo[2 * u + 1]));
-      st_relaxed_u64(r + dim(u), 0ull);
-      st_relaxed_u64(r + dim(u) + 1, 0ull);
+      const unsigned long long w0 = ld_relaxed_u64(r + dim(u)), w1 = ld_relaxed_u64(r + dim(u) + 1);
+      good = good && (w0 >> 32) && (w1 >> 32);
+      dst[dim(u)] = __uint_as_float(static_cast<uint32_t>(w0));
+      dst[dim(u) + 1] = __uint_as_float(static_cast<uint32_t>(w1));
     }
     if (lane == 0) {
       dst[HD] = __uint_as_float(static_cast<uint32_t>(wm));
       dst[HD + 1] = __uint_as_float(static_cast<uint32_t>(wl));
+    }
+    ok = ok && __all_sync(0xffffffffu, good);
+  }
+  if (!ok) return;
+  for (int c = ca; c <= cb; ++c) {
+    if (c == cta) continue;
+    unsigned long long* r = rec_of(c);
+#pragma unroll
+    for (int u = 0; u < PPL; ++u) {
+      st_relaxed_u64(r + dim(u), 0ull);
+      st_relaxed_u64(r + dim(u) + 1, 0ull);
+    }
+    if (lane == 0) {
       st_relaxed_u64(r + HD, 0ull);
       st_relaxed_u64(r + HD + 1, 0ull);
     }
