@@ -505,3 +505,47 @@ def test_planned_large_batch_arrays(N):
         ref = O.decode_attention(q[b:b + 1].cpu().numpy(), kc[b:b + 1], ks[b:b + 1], vc[b:b + 1],
                                  vs[b:b + 1], [lens0[b]], blk)
         assert np.max(np.abs(o2[b:b + 1].cpu().numpy() - ref)) <= ATOL
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_geometries_planned_fused(N, seed):
+    """Random (B, H, hd, blk, lengths incl. 0, 1 and Tc): unplanned ==
+    planned (with and without early start) bit for bit, and the fused step
+    matches the oracle on sampled (b, h) rows."""
+    rng = np.random.default_rng(1000 + seed)
+    hd = int(rng.choice([64, 128]))
+    blk = int(rng.choice([32, 64] if hd == 64 else [32, 64, 128]))
+    B = int(rng.integers(1, 48))
+    H = int(rng.integers(1, 9))
+    Tc = 64 * int(rng.integers(1, 12))
+    lens0 = rng.integers(0, Tc, B)                              # existing rows (< Tc: one is appended)
+    lens0[rng.integers(0, B)] = 0
+    lens0 = [int(x) for x in lens0]
+    T = max(max(lens0), 1)
+    x = _rand_kv(B, T, H, hd, seed=seed * 7 + 1)
+    y = _rand_kv(B, T, H, hd, seed=seed * 7 + 2, outlier=False)
+    kn = _rand_kv(B, 1, H, hd, seed=seed * 7 + 3)[:, 0].to(DEV)
+    vn = _rand_kv(B, 1, H, hd, seed=seed * 7 + 4, outlier=False)[:, 0].to(DEV)
+    q = torch.randn(B, H, hd, generator=torch.Generator().manual_seed(seed * 7 + 5)).to(torch.float16).to(DEV)
+    kc, ks = _oracle_cache(x, [0] * B, blk, Tc)
+    vc, vs = _oracle_cache(y, [0] * B, blk, Tc)
+    t = lambda a: torch.from_numpy(a.copy()).to(DEV)
+    L1 = torch.tensor([n + 1 for n in lens0], dtype=torch.int32, device=DEV)
+    plan = N.make_plan(DEV)
+    N.nqkv_decode_plan(L1, H, Tc, True, plan, hd=hd)
+    caches = [[t(z) for z in (kc, ks, vc, vs)] for _ in range(3)]
+    f0 = N.nqkv_decode_step(kn, vn, q, *caches[0], L1, blk, N.make_workspace(B, H, hd, Tc, DEV))
+    f1 = N.nqkv_decode_step_planned(kn, vn, q, *caches[1], L1, blk, N.make_workspace(B, H, hd, Tc, DEV), plan)
+    f2 = N.nqkv_decode_step_planned(kn, vn, q, *caches[2], L1, blk, N.make_workspace(B, H, hd, Tc, DEV), plan,
+                                    flags=N.EARLY_START)
+    torch.cuda.synchronize()
+    assert torch.equal(f0, f1) and torch.equal(f0, f2)
+    for c in caches[1:]:
+        assert all(torch.equal(u, v) for u, v in zip(caches[0], c))
+    O.quantize_append(kn.unsqueeze(1).cpu().numpy(), lens0, blk, kc, ks)
+    O.quantize_append(vn.unsqueeze(1).cpu().numpy(), lens0, blk, vc, vs)
+    assert np.array_equal(caches[0][0].cpu().numpy(), kc) and np.array_equal(caches[0][3].cpu().numpy(), vs)
+    for b in sorted({0, B - 1} | set(rng.integers(0, B, 4).tolist())):
+        ref = O.decode_attention(q[b:b + 1].cpu().numpy(), kc[b:b + 1], ks[b:b + 1], vc[b:b + 1],
+                                 vs[b:b + 1], [lens0[b] + 1], blk)
+        assert np.max(np.abs(f0[b:b + 1].cpu().numpy() - ref)) <= ATOL
