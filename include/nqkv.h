@@ -77,6 +77,14 @@ int nqkv_levels(float levels[16]);
  * index.  Host only. */
 int nqkv_thresholds(float thresholds[15]);
 
+/* Block-scale storage: every call that takes `blk`
+ * accepts blk | NQKV_SCALE_F16, meaning the scales tensor holds fp16 instead
+ * of fp32 values.  This is lossless: a block's scale is the absmax of fp16
+ * inputs, itself an fp16 value, so codes, dequantised values and attention
+ * are identical to the fp32-scale layout; scale bytes halve (-5.6 % of the
+ * cache at blk 64).  Scales: 2-byte aligned instead of 4. */
+#define NQKV_SCALE_F16 0x100
+
 /* a1-a3. Quantize + pack + append.
  * x      device fp16, logical [B][n_new][H][hd] with element strides
  *        stride_b, stride_t, stride_h (hd contiguous); 16-byte aligned, all
@@ -86,21 +94,22 @@ int nqkv_thresholds(float thresholds[15]);
  *        codes/scales are left untouched (append-only).  Rows
  *        outside [0, Tc) are skipped.
  * codes  device uint8  [B][H][Tc][hd/2]    (16-byte aligned)
- * scales device float  [B][H][Tc][hd/blk]  (4-byte aligned)
+ * scales device float  [B][H][Tc][hd/blk]  (4-byte aligned; fp16 with
+ *        NQKV_SCALE_F16, 2-byte aligned)
  * Per block: s = max|x| (fp32, exact); code = nearest level to n = RN32(x/s),
  * ties lower; s == 0 -> code 7 (the zero level).  The kernel normalises with
  * n' = RN32(x * RN32(1/s)), which gives the identical code for every fp16
  * pair |x| <= s (exhaustive: tests/test_exactness_cpu.py). */
 int nqkv_quantize(const void* x, int64_t stride_b, int64_t stride_t, int64_t stride_h,
                   int B, int H, int hd, int n_new, int blk,
-                  const int32_t* d_pos, int Tc, uint8_t* codes, float* scales,
+                  const int32_t* d_pos, int Tc, uint8_t* codes, void* scales,
                   void* stream);
 
 /* a4 (standalone). Dequantize rows [0, n_tokens) of every (b, h)
  * (no padding).
  * out: device, [B][H][n_tokens][hd], out_dtype 0 = fp32 (RN32(s*L[code])),
  * 1 = fp16 (RN16 of that fp32 value); 16-byte aligned.  n_tokens <= Tc. */
-int nqkv_dequantize(const uint8_t* codes, const float* scales, int B, int H, int Tc, int hd,
+int nqkv_dequantize(const uint8_t* codes, const void* scales, int B, int H, int Tc, int hd,
                     int blk, int n_tokens, int out_dtype, void* out, void* stream);
 
 /* Bytes of workspace nqkv_decode_attention / nqkv_decode_step need for this
@@ -135,8 +144,8 @@ size_t nqkv_decode_counter_bytes(int B, int H);
  * given (B, H, seq_lens, GPU); a different head shard of the same data may
  * differ by fp32 reassociation only (reading R7).  B <= 1024 and
  * B*H*Tc < 2^31. */
-int nqkv_decode_attention(const void* q, const uint8_t* k_codes, const float* k_scales,
-                          const uint8_t* v_codes, const float* v_scales,
+int nqkv_decode_attention(const void* q, const uint8_t* k_codes, const void* k_scales,
+                          const uint8_t* v_codes, const void* v_scales,
                           const int32_t* d_seq_lens, int B, int H, int hd, int blk, int Tc,
                           float softmax_scale, float* out, void* workspace, size_t ws_bytes,
                           void* stream);
@@ -153,8 +162,8 @@ int nqkv_decode_attention(const void* q, const uint8_t* k_codes, const float* k_
  *               nqkv_decode_attention's on the updated cache.
  * Other arguments as nqkv_decode_attention. */
 int nqkv_decode_step(const void* k_new, const void* v_new, int64_t new_stride_b,
-                     int64_t new_stride_h, const void* q, uint8_t* k_codes, float* k_scales,
-                     uint8_t* v_codes, float* v_scales, const int32_t* d_seq_lens, int B, int H,
+                     int64_t new_stride_h, const void* q, uint8_t* k_codes, void* k_scales,
+                     uint8_t* v_codes, void* v_scales, const int32_t* d_seq_lens, int B, int H,
                      int hd, int blk, int Tc, float softmax_scale, float* out, void* workspace,
                      size_t ws_bytes, void* stream);
 
@@ -184,14 +193,14 @@ int nqkv_decode_step(const void* k_new, const void* v_new, int64_t new_stride_b,
 size_t nqkv_decode_plan_bytes(void);
 int nqkv_decode_plan(const int32_t* d_seq_lens, int B, int H, int hd, int Tc, int fused, void* plan,
                      size_t plan_bytes, void* stream);
-int nqkv_decode_attention_planned(const void* q, const uint8_t* k_codes, const float* k_scales,
-                                  const uint8_t* v_codes, const float* v_scales,
+int nqkv_decode_attention_planned(const void* q, const uint8_t* k_codes, const void* k_scales,
+                                  const uint8_t* v_codes, const void* v_scales,
                                   const int32_t* d_seq_lens, int B, int H, int hd, int blk, int Tc,
                                   float softmax_scale, float* out, void* workspace,
                                   size_t ws_bytes, const void* plan, int flags, void* stream);
 int nqkv_decode_step_planned(const void* k_new, const void* v_new, int64_t new_stride_b,
                              int64_t new_stride_h, const void* q, uint8_t* k_codes,
-                             float* k_scales, uint8_t* v_codes, float* v_scales,
+                             void* k_scales, uint8_t* v_codes, void* v_scales,
                              const int32_t* d_seq_lens, int B, int H, int hd, int blk, int Tc,
                              float softmax_scale, float* out, void* workspace, size_t ws_bytes,
                              const void* plan, int flags, void* stream);

@@ -76,9 +76,9 @@ constexpr uint32_t kSmemWindow = 0x400;  // shared address of dynamic smem offse
 struct DecodeParams {
   const __half* q;
   const uint8_t* kc;
-  const float* ks;
+  const void* ks;            // block scales, fp32 or fp16 (kernel template F16S)
   const uint8_t* vc;
-  const float* vs;
+  const void* vs;
   const int32_t* seq_lens;
   const __half* k_new;      // fused append (nullptr: attention only)
   const __half* v_new;
@@ -205,12 +205,12 @@ __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
 // 18-19 / 20-21 the K / V scale lines (only lines holding bytes of the rows,
 // so every address is inside the cache tensors).  A prefetch is a hint: it
 // never changes what a load returns, so it may run before the PDL wait.
-template <int HD, int NBLK, typename P>
+template <int HD, int NBLK, int SB, typename P>
 __device__ __forceinline__ void prefetch_rows_l2(const P& p, int lane, long long r0, long long r1) {
   const bool sc = lane >= 18;
   const bool isv = sc ? lane >= 20 : lane >= 9;
   const int li = lane - (sc ? (isv ? 20 : 18) : (isv ? 9 : 0));
-  const long long w = sc ? NBLK * 4 : HD / 2;
+  const long long w = sc ? NBLK * SB : HD / 2;
   const long long f = (r0 * w) >> 7, l = (r1 * w - 1) >> 7;
   const unsigned char* base = sc ? reinterpret_cast<const unsigned char*>(isv ? p.vs : p.ks)
                                  : (isv ? p.vc : p.kc);
@@ -226,6 +226,19 @@ __device__ __forceinline__ float ldg_nc_f32(const float* p) {
   float r;
   asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(r) : "l"(p));
   return r;
+}
+// block scale at byte offset `off` of a scale tensor: fp32, or fp16 (F16S;
+// exact -- a block absmax of fp16 inputs is an fp16 value)
+template <bool F16S>
+__device__ __forceinline__ float ld_scale(const void* base, uint32_t off) {
+  if constexpr (F16S) {
+    unsigned short h;
+    asm volatile("ld.global.nc.L1::no_allocate.b16 %0, [%1];" : "=h"(h)
+                 : "l"(reinterpret_cast<const uint8_t*>(base) + off));
+    return __half2float(__ushort_as_half(h));
+  } else {
+    return ldg_nc_f32(reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(base) + off));
+  }
 }
 
 // One CTA-contiguous run of tokens of one (b, h): tokens [t0, t1) of a
@@ -458,7 +471,7 @@ __global__ void __launch_bounds__(1024) decode_plan_kernel(const int32_t* seq_le
 // 32u (dims 2j, 2j+1).  Quantised exactly as quantize_kernel does, written to
 // the cache row `row` of (b, h); vh gets its dequantised values and the return
 // value is its score (log2 domain) from the q-table in `slot` (slot < 0: 0).
-template <int HD, int NW>
+template <int HD, int NW, bool F16S>
 __device__ __noinline__ float new_token_fn(const DecodeParams& p, unsigned char* smem, int b, int h,
                                            int row, int slot, float* vh) {
   using Sm = Smem<HD, NW>;
@@ -506,8 +519,14 @@ __device__ __noinline__ float new_token_fn(const DecodeParams& p, unsigned char*
     const_cast<uint8_t*>(p.kc)[r * (HD / 2) + j] = static_cast<uint8_t>(ck);
     const_cast<uint8_t*>(p.vc)[r * (HD / 2) + j] = static_cast<uint8_t>(cvl | (cvh << 4));
     if (((2 * j) & ((1 << p.blk_shift) - 1)) == 0) {
-      const_cast<float*>(p.ks)[r * nblk + ((2 * j) >> p.blk_shift)] = sk[u];
-      const_cast<float*>(p.vs)[r * nblk + ((2 * j) >> p.blk_shift)] = sv[u];
+      const long long si = r * nblk + ((2 * j) >> p.blk_shift);
+      if constexpr (F16S) {                   // exact: an absmax of fp16 values
+        reinterpret_cast<__half*>(const_cast<void*>(p.ks))[si] = __float2half_rn(sk[u]);
+        reinterpret_cast<__half*>(const_cast<void*>(p.vs))[si] = __float2half_rn(sv[u]);
+      } else {
+        reinterpret_cast<float*>(const_cast<void*>(p.ks))[si] = sk[u];
+        reinterpret_cast<float*>(const_cast<void*>(p.vs))[si] = sv[u];
+      }
     }
     vh[2 * u] = __fmul_rn(sv[u], s_lv[cvl]);
     vh[2 * u + 1] = __fmul_rn(sv[u], s_lv[cvh]);
@@ -815,8 +834,9 @@ __device__ __noinline__ void merge_fn(const DecodeParams& p, unsigned char* smem
   if (lane == 0) p.cnt[bh] = 0;
 }
 
-template <int HD, int BLK, int NW>
+template <int HD, int BLK, int NW, bool F16S>
 __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constant__ DecodeParams p) {
+  constexpr int SB = F16S ? 2 : 4;   // bytes per stored block scale
   using Ge = Geo<HD>;
   using Sm = Smem<HD, NW>;
   constexpr int LPT = Ge::LPT, G = Ge::G, ST = Ge::ST, R = Ge::R, PPL = Ge::PPL;
@@ -998,7 +1018,7 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
       const int b = bh / p.H, h = bh - b * p.H;
       if (!((s_one[b >> 5] >> (b & 31)) & 1u)) continue;
       float vh[2 * PPL];
-      new_token_fn<HD, NW>(p, smem, b, h, 0, -1, vh);
+      new_token_fn<HD, NW, F16S>(p, smem, b, h, 0, -1, vh);
 #pragma unroll
       for (int u = 0; u < PPL; ++u)
         *reinterpret_cast<float2*>(p.out + static_cast<long long>(bh) * HD + 2 * (lane + 32 * u)) =
@@ -1036,7 +1056,7 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
   // p_j * vs_j to the other lanes of the block.  1 scale load, 1 exp2 per lane
   // and stage instead of kTPS.
   constexpr bool RS = BLK == kLaneDims * kTPS && kTPS == 4;
-  const uint32_t soff_rs = RS ? static_cast<uint32_t>((sub & 3) * G * NBLK * 4) : 0u;
+  const uint32_t soff_rs = RS ? static_cast<uint32_t>((sub & 3) * G * NBLK * SB) : 0u;
   // Per-lane 32-bit byte offsets (codes, scales) of the load cursor: this
   // lane's bytes of the stage to load next (token tok0 + g of its (b, h));
   // slot i is at the immediate offset i*G rows.  Advanced by NC*ST rows per
@@ -1045,7 +1065,7 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
   auto set_ptrs = [&](int rb, int tok0) {
     const uint32_t r = static_cast<uint32_t>(rb + tok0 + g);
     loff_c = r * (HD / 2) + sub * 8;
-    loff_s = (r * NBLK + sidx) * 4;
+    loff_s = (r * NBLK + sidx) * SB;
   };
   using StageRegs = StageRegsT<RS>;
   auto load_stage = [&](StageRegs& Rg, int rb, int tok0, int t1) {
@@ -1071,15 +1091,15 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
         Rg.k[i] = ldg_stream_64(p.kc + loff_c + i * G * (HD / 2));
         Rg.v[i] = ldg_stream_64(p.vc + loff_c + i * G * (HD / 2));
         if constexpr (!RS) {
-          Rg.ks[i] = ldg_nc_f32(reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(p.ks) + loff_s) + i * G * NBLK);
-          Rg.vs[i] = ldg_nc_f32(reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(p.vs) + loff_s) + i * G * NBLK);
+          Rg.ks[i] = ld_scale<F16S>(p.ks, loff_s + i * G * NBLK * SB);
+          Rg.vs[i] = ld_scale<F16S>(p.vs, loff_s + i * G * NBLK * SB);
         }
       }
     }
     if constexpr (RS) {
       if (tok0 + (sub & 3) * G + g < t1) {
-        Rg.ks[0] = ldg_nc_f32(reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(p.ks) + loff_s + soff_rs));
-        Rg.vs[0] = ldg_nc_f32(reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(p.vs) + loff_s + soff_rs));
+        Rg.ks[0] = ld_scale<F16S>(p.ks, loff_s + soff_rs);
+        Rg.vs[0] = ld_scale<F16S>(p.vs, loff_s + soff_rs);
       }
     }
   };
@@ -1120,7 +1140,7 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
     if (ladv) {
       ls += NC;
       loff_c += NC * ST * (HD / 2);
-      loff_s += NC * ST * NBLK * 4;
+      loff_s += NC * ST * NBLK * SB;
     }
     ladv = true;
     if (ls >= nstages(lp)) {
@@ -1140,7 +1160,7 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
     // L2 prefetch of this warp's stage PF ahead in the same piece
     if (PF > 0 && ls + PF * NC < nstages(lp)) {
       const int t = lp.t0 + (ls + PF * NC) * ST;
-      prefetch_rows_l2<HD, NBLK>(p, lane, static_cast<long long>(lrb) + t,
+      prefetch_rows_l2<HD, NBLK, SB>(p, lane, static_cast<long long>(lrb) + t,
                                  static_cast<long long>(lrb) + min(t + ST, lp.t1));
     }
     return true;
@@ -1157,7 +1177,7 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
     if (ladv) {
       ls += NC;
       loff_c += NC * ST * (HD / 2);
-      loff_s += NC * ST * NBLK * 4;
+      loff_s += NC * ST * NBLK * SB;
     }
     ladv = true;
     if (ls >= nstages(lp)) {
@@ -1182,16 +1202,16 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
       if (tok0 + i * G + g < t1) {
         Rg.k[i] = ldg_stream_64(p.kc + loff_c + i * G * (HD / 2));
         if constexpr (!RS)
-          Rg.ks[i] = ldg_nc_f32(reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(p.ks) + loff_s) + i * G * NBLK);
+          Rg.ks[i] = ld_scale<F16S>(p.ks, loff_s + i * G * NBLK * SB);
       }
     }
     if constexpr (RS) {
       if (tok0 + (sub & 3) * G + g < t1)
-        Rg.ks[0] = ldg_nc_f32(reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(p.ks) + loff_s + soff_rs));
+        Rg.ks[0] = ld_scale<F16S>(p.ks, loff_s + soff_rs);
     }
     if (PF > 0 && ls + PF * NC < nstages(lp)) {
       const int t = lp.t0 + (ls + PF * NC) * ST;
-      prefetch_rows_l2<HD, NBLK>(p, lane, static_cast<long long>(lrb) + t,
+      prefetch_rows_l2<HD, NBLK, SB>(p, lane, static_cast<long long>(lrb) + t,
                                  static_cast<long long>(lrb) + min(t + ST, lp.t1));
     }
     return true;
@@ -1204,12 +1224,12 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
       if (tok0 + i * G + g < t1) {
         Rg.v[i] = ldg_stream_64(p.vc + voff_c[d] + i * G * (HD / 2));
         if constexpr (!RS)
-          Rg.vs[i] = ldg_nc_f32(reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(p.vs) + voff_s[d]) + i * G * NBLK);
+          Rg.vs[i] = ld_scale<F16S>(p.vs, voff_s[d] + i * G * NBLK * SB);
       }
     }
     if constexpr (RS) {
       if (tok0 + (sub & 3) * G + g < t1)
-        Rg.vs[0] = ldg_nc_f32(reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(p.vs) + voff_s[d] + soff_rs));
+        Rg.vs[0] = ld_scale<F16S>(p.vs, voff_s[d] + soff_rs);
     }
   };
 #pragma unroll
@@ -1308,7 +1328,7 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
       float* st = s_new + (k % R) * (HD + 4);
       if (fused && pc.t1 == pc.len) {
         float vh[2 * PPL];
-        const float sco = new_token_fn<HD, NW>(p, smem, pc.b, pc.h, min(pc.len, p.Tc - 1), k % R, vh);
+        const float sco = new_token_fn<HD, NW, F16S>(p, smem, pc.b, pc.h, min(pc.len, p.Tc - 1), k % R, vh);
 #pragma unroll
         for (int u = 0; u < PPL; ++u)
           *reinterpret_cast<float2*>(st + 2 * (lane + 32 * u)) = make_float2(vh[2 * u], vh[2 * u + 1]);

@@ -20,6 +20,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <type_traits>
 #include <utility>
 
 #include "../../include/nqkv.h"
@@ -44,8 +45,16 @@ int blk_shift_of(int blk) { return blk == 32 ? 5 : blk == 64 ? 6 : blk == 128 ? 
 
 int check_geometry(int hd, int blk) {
   if (hd != 64 && hd != 128) return NQKV_ERR_UNSUPPORTED;
+  if (blk & ~(0xff | NQKV_SCALE_F16)) return NQKV_ERR_UNSUPPORTED;
+  blk &= 0xff;
   if (blk_shift_of(blk) < 0 || blk > hd) return NQKV_ERR_UNSUPPORTED;
   return NQKV_OK;
+}
+// blk argument -> (block size, scales stored as fp16)
+int blk_of(int blk) { return blk & 0xff; }
+bool f16s_of(int blk) { return (blk & NQKV_SCALE_F16) != 0; }
+bool scale_aligned(const void* p, bool f16s) {
+  return (reinterpret_cast<uintptr_t>(p) & (f16s ? 1u : 3u)) == 0;
 }
 
 BucketTab make_bucket_tab() {
@@ -132,9 +141,9 @@ cudaError_t launch_pdl(void (*kern)(P), dim3 grid, dim3 block, size_t smem, cuda
   return cudaLaunchKernelEx(&cfg, kern, prm);
 }
 
-template <int HD, int BLK>
+template <int HD, int BLK, bool F16S>
 int launch_decode_blk(const DecodeParams& p, cudaStream_t st) {
-  auto kern = decode_kernel<HD, BLK, kDecodeWarps>;
+  auto kern = decode_kernel<HD, BLK, kDecodeWarps, F16S>;
   const size_t smem = Smem<HD, kDecodeWarps>::kBytes;
   static bool attr_set = false;
   static std::mutex mu;
@@ -154,12 +163,12 @@ int launch_decode_blk(const DecodeParams& p, cudaStream_t st) {
   return e == cudaSuccess ? NQKV_OK : cuda_fail(e);
 }
 
-template <int HD>
+template <int HD, bool F16S>
 int launch_decode(const DecodeParams& p, cudaStream_t st) {
   switch (p.blk_shift) {
-    case 5: return launch_decode_blk<HD, 32>(p, st);
-    case 6: return launch_decode_blk<HD, 64>(p, st);
-    default: return HD == 128 ? launch_decode_blk<HD, 128>(p, st) : NQKV_ERR_UNSUPPORTED;
+    case 5: return launch_decode_blk<HD, 32, F16S>(p, st);
+    case 6: return launch_decode_blk<HD, 64, F16S>(p, st);
+    default: return HD == 128 ? launch_decode_blk<HD, 128, F16S>(p, st) : NQKV_ERR_UNSUPPORTED;
   }
 }
 
@@ -179,8 +188,8 @@ WsLayout ws_layout(long long B, long long H, int hd) {
   return w;
 }
 
-int decode_common(const void* q, const uint8_t* k_codes, const float* k_scales,
-                  const uint8_t* v_codes, const float* v_scales, const int32_t* d_seq_lens,
+int decode_common(const void* q, const uint8_t* k_codes, const void* k_scales,
+                  const uint8_t* v_codes, const void* v_scales, const int32_t* d_seq_lens,
                   const void* k_new, const void* v_new, int64_t new_sb, int64_t new_sh, int B,
                   int H, int hd, int blk, int Tc, float softmax_scale, float* out, void* workspace,
                   size_t ws_bytes, const void* plan, int flags, cudaStream_t st) {
@@ -190,6 +199,8 @@ int decode_common(const void* q, const uint8_t* k_codes, const float* k_scales,
   if (B < 0 || H < 0 || Tc <= 0 || Tc % 64 || B > kMaxBatch) return NQKV_ERR_SHAPE;
   if (static_cast<long long>(B) * H * Tc >= (1ll << 31)) return NQKV_ERR_SHAPE;
   if (static_cast<long long>(B) * H * Tc * (hd / 2) >= (1ll << 32)) return NQKV_ERR_SHAPE;  // 32-bit offsets
+  const bool f16s = f16s_of(blk);
+  blk = blk_of(blk);
   if (!aligned16(q) || !aligned16(k_codes) || !aligned16(v_codes) || !aligned16(out) ||
       !aligned16(k_scales) || !aligned16(v_scales))
     return NQKV_ERR_ALIGN;
@@ -224,7 +235,8 @@ int decode_common(const void* q, const uint8_t* k_codes, const float* k_scales,
   if (const char* t = std::getenv("NQKV_TRACE_PTR"))
     p.trace = reinterpret_cast<unsigned long long*>(std::strtoull(t, nullptr, 0));
 #endif
-  return hd == 64 ? launch_decode<64>(p, st) : launch_decode<128>(p, st);
+  if (f16s) return hd == 64 ? launch_decode<64, true>(p, st) : launch_decode<128, true>(p, st);
+  return hd == 64 ? launch_decode<64, false>(p, st) : launch_decode<128, false>(p, st);
 }
 
 }  // namespace nqkv
@@ -268,11 +280,13 @@ int nqkv_thresholds(float thresholds[15]) {
 
 int nqkv_quantize(const void* x, int64_t stride_b, int64_t stride_t, int64_t stride_h, int B,
                   int H, int hd, int n_new, int blk, const int32_t* d_pos, int Tc,
-                  uint8_t* codes, float* scales, void* stream) {
+                  uint8_t* codes, void* scales, void* stream) {
   if (!x || !d_pos || !codes || !scales) return NQKV_ERR_NULL;
   if (int s = check_geometry(hd, blk)) return s;
+  const bool f16s = f16s_of(blk);
+  blk = blk_of(blk);
   if (B < 0 || H < 0 || n_new < 0 || Tc <= 0 || Tc % 64) return NQKV_ERR_SHAPE;
-  if (!aligned16(x) || !aligned16(codes) || (reinterpret_cast<uintptr_t>(scales) & 3u) ||
+  if (!aligned16(x) || !aligned16(codes) || !scale_aligned(scales, f16s) ||
       (stride_b % 8) || (stride_t % 8) || (stride_h % 8))
     return NQKV_ERR_ALIGN;
   if (tables_status() != 0) return NQKV_ERR_INTERNAL;
@@ -300,25 +314,29 @@ int nqkv_quantize(const void* x, int64_t stride_b, int64_t stride_t, int64_t str
   const dim3 grid(static_cast<unsigned>(grid_for((chunks + 1) / 2, 256, 8)));
   cudaError_t e;
   const size_t sm = kQuantSmem;
-  if (hd == 64) {
-    e = blk == 32 ? launch_pdl(quantize_kernel<64, 32>, grid, dim3(256), sm, st, p)
-                  : launch_pdl(quantize_kernel<64, 64>, grid, dim3(256), sm, st, p);
-  } else {
-    e = blk == 32   ? launch_pdl(quantize_kernel<128, 32>, grid, dim3(256), sm, st, p)
-        : blk == 64 ? launch_pdl(quantize_kernel<128, 64>, grid, dim3(256), sm, st, p)
-                    : launch_pdl(quantize_kernel<128, 128>, grid, dim3(256), sm, st, p);
-  }
+  auto launch = [&](auto f16s_tag) {
+    constexpr bool F = decltype(f16s_tag)::value;
+    if (hd == 64)
+      return blk == 32 ? launch_pdl(quantize_kernel<64, 32, F>, grid, dim3(256), sm, st, p)
+                       : launch_pdl(quantize_kernel<64, 64, F>, grid, dim3(256), sm, st, p);
+    return blk == 32   ? launch_pdl(quantize_kernel<128, 32, F>, grid, dim3(256), sm, st, p)
+           : blk == 64 ? launch_pdl(quantize_kernel<128, 64, F>, grid, dim3(256), sm, st, p)
+                       : launch_pdl(quantize_kernel<128, 128, F>, grid, dim3(256), sm, st, p);
+  };
+  e = f16s ? launch(std::true_type{}) : launch(std::false_type{});
   return e == cudaSuccess ? NQKV_OK : cuda_fail(e);
 }
 
-int nqkv_dequantize(const uint8_t* codes, const float* scales, int B, int H, int Tc, int hd,
+int nqkv_dequantize(const uint8_t* codes, const void* scales, int B, int H, int Tc, int hd,
                     int blk, int n_tokens, int out_dtype, void* out, void* stream) {
   if (!codes || !scales || !out) return NQKV_ERR_NULL;
   if (int s = check_geometry(hd, blk)) return s;
+  const bool f16s = f16s_of(blk);
+  blk = blk_of(blk);
   if (B < 0 || H < 0 || Tc <= 0 || Tc % 64 || n_tokens < 0 || n_tokens > Tc)
     return NQKV_ERR_SHAPE;
   if (out_dtype != 0 && out_dtype != 1) return NQKV_ERR_UNSUPPORTED;
-  if (!aligned16(codes) || !aligned16(out) || (reinterpret_cast<uintptr_t>(scales) & 3u))
+  if (!aligned16(codes) || !aligned16(out) || !scale_aligned(scales, f16s))
     return NQKV_ERR_ALIGN;
   if (tables_status() != 0) return NQKV_ERR_INTERNAL;
   const long long total = static_cast<long long>(B) * H * n_tokens * (hd / 8);
@@ -332,9 +350,11 @@ int nqkv_dequantize(const uint8_t* codes, const float* scales, int B, int H, int
   p.lv = make_levels();
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const dim3 grid(static_cast<unsigned>(grid_for(total, 256, 8)));
-  const cudaError_t e = out_dtype == 1
-                            ? launch_pdl(dequant_kernel<true>, grid, dim3(256), 0, st, p)
-                            : launch_pdl(dequant_kernel<false>, grid, dim3(256), 0, st, p);
+  const cudaError_t e =
+      out_dtype == 1 ? (f16s ? launch_pdl(dequant_kernel<true, true>, grid, dim3(256), 0, st, p)
+                             : launch_pdl(dequant_kernel<true, false>, grid, dim3(256), 0, st, p))
+                     : (f16s ? launch_pdl(dequant_kernel<false, true>, grid, dim3(256), 0, st, p)
+                             : launch_pdl(dequant_kernel<false, false>, grid, dim3(256), 0, st, p));
   return e == cudaSuccess ? NQKV_OK : cuda_fail(e);
 }
 
@@ -348,8 +368,8 @@ size_t nqkv_decode_counter_bytes(int B, int H) {
   return static_cast<size_t>(B) * H * sizeof(int);
 }
 
-int nqkv_decode_attention(const void* q, const uint8_t* k_codes, const float* k_scales,
-                          const uint8_t* v_codes, const float* v_scales,
+int nqkv_decode_attention(const void* q, const uint8_t* k_codes, const void* k_scales,
+                          const uint8_t* v_codes, const void* v_scales,
                           const int32_t* d_seq_lens, int B, int H, int hd, int blk, int Tc,
                           float softmax_scale, float* out, void* workspace, size_t ws_bytes,
                           void* stream) {
@@ -375,8 +395,8 @@ int nqkv_decode_plan(const int32_t* d_seq_lens, int B, int H, int hd, int Tc, in
   return e == cudaSuccess ? NQKV_OK : cuda_fail(e);
 }
 
-int nqkv_decode_attention_planned(const void* q, const uint8_t* k_codes, const float* k_scales,
-                                  const uint8_t* v_codes, const float* v_scales,
+int nqkv_decode_attention_planned(const void* q, const uint8_t* k_codes, const void* k_scales,
+                                  const uint8_t* v_codes, const void* v_scales,
                                   const int32_t* d_seq_lens, int B, int H, int hd, int blk, int Tc,
                                   float softmax_scale, float* out, void* workspace,
                                   size_t ws_bytes, const void* plan, int flags, void* stream) {
@@ -387,8 +407,8 @@ int nqkv_decode_attention_planned(const void* q, const uint8_t* k_codes, const f
 }
 
 int nqkv_decode_step(const void* k_new, const void* v_new, int64_t new_stride_b,
-                     int64_t new_stride_h, const void* q, uint8_t* k_codes, float* k_scales,
-                     uint8_t* v_codes, float* v_scales, const int32_t* d_seq_lens, int B, int H,
+                     int64_t new_stride_h, const void* q, uint8_t* k_codes, void* k_scales,
+                     uint8_t* v_codes, void* v_scales, const int32_t* d_seq_lens, int B, int H,
                      int hd, int blk, int Tc, float softmax_scale, float* out, void* workspace,
                      size_t ws_bytes, void* stream) {
   if (!k_new || !v_new) return NQKV_ERR_NULL;
@@ -399,7 +419,7 @@ int nqkv_decode_step(const void* k_new, const void* v_new, int64_t new_stride_b,
 
 int nqkv_decode_step_planned(const void* k_new, const void* v_new, int64_t new_stride_b,
                              int64_t new_stride_h, const void* q, uint8_t* k_codes,
-                             float* k_scales, uint8_t* v_codes, float* v_scales,
+                             void* k_scales, uint8_t* v_codes, void* v_scales,
                              const int32_t* d_seq_lens, int B, int H, int hd, int blk, int Tc,
                              float softmax_scale, float* out, void* workspace, size_t ws_bytes,
                              const void* plan, int flags, void* stream) {

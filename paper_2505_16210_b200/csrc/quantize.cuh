@@ -11,7 +11,7 @@ struct QuantParams {
   long long sb, st, sh;          // element strides
   const int32_t* pos;
   uint8_t* codes;
-  float* scales;
+  void* scales;                  // fp32, or fp16 (template F16S; exact for fp16 inputs)
   int B, n_new, H, Tc, blk_shift;
   uint32_t total;                // 16-element chunks: B * n_new * H * hd / 16
   int v256;                      // bit 0: x and strides 32-byte aligned (256-bit loads);
@@ -76,7 +76,7 @@ __device__ __forceinline__ float absmax16(const uint4 a, const uint4 b) {
 // blk = 32).  Units are strided over the warps of the grid; the next unit's
 // loads are issued before the current one is encoded (ping-pong registers).
 // When x is contiguous ([B][n_new][H][hd] packed), chunk c starts at x + 16c.
-template <int HD, int BLK>
+template <int HD, int BLK, bool F16S>
 __global__ void __launch_bounds__(256) quantize_kernel(const __grid_constant__ QuantParams p) {
   constexpr int CPT = HD / 16;                 // chunks per (token, head)
   constexpr int LOG_CPT = CPT == 4 ? 2 : 3;
@@ -123,7 +123,13 @@ __global__ void __launch_bounds__(256) quantize_kernel(const __grid_constant__ Q
     const uint32_t h = within >> LOG_CPT, cr = within & (CPT - 1);
     const long long rr = (static_cast<long long>(bb) * p.H + h) * p.Tc + pos;
     reinterpret_cast<uint2*>(p.codes + rr * (HD / 2))[cr] = word;
-    if (scale_writer) p.scales[rr * nblk + ((cr * 16) >> p.blk_shift)] = s;
+    if (scale_writer) {
+      const long long si = rr * nblk + ((cr * 16) >> p.blk_shift);
+      if constexpr (F16S)
+        reinterpret_cast<__half*>(p.scales)[si] = __float2half_rn(s);   // exact: s is an fp16 value
+      else
+        reinterpret_cast<float*>(p.scales)[si] = s;
+    }
   };
   auto encode = [&](uint32_t unit, const Buf& B) {
     const uint32_t c = unit * 64u + 2u * lane;
@@ -141,7 +147,7 @@ __global__ void __launch_bounds__(256) quantize_kernel(const __grid_constant__ Q
     const uint2 w0 = make_uint2(encode8_rep(B.v[0], r0, lane8), encode8_rep(B.v[1], r0, lane8));
     const uint2 w1 = make_uint2(encode8_rep(B.v[2], r1, lane8), encode8_rep(B.v[3], r1, lane8));
 #ifdef NQKV_EXP_QNOSTORE
-    if (w0.x == 0x12345678u && w1.y == 0x9abcdef0u && s0 == 1.5f) p.scales[0] = s0;
+    if (w0.x == 0x12345678u && w1.y == 0x9abcdef0u && s0 == 1.5f) reinterpret_cast<float*>(p.scales)[0] = s0;
     return;
 #endif
     if (!valid) return;
@@ -167,14 +173,14 @@ __global__ void __launch_bounds__(256) quantize_kernel(const __grid_constant__ Q
 // ------------------------------------------------- a4 standalone: dequant
 struct DequantParams {
   const uint8_t* codes;
-  const float* scales;
+  const void* scales;       // fp32, or fp16 (template F16S)
   void* out;
   long long total_chunks;   // B*H*n_tokens*hd/8
   int Tc, hd, n_tokens, blk_shift, chunks_per_row;
   Levels lv;
 };
 
-template <bool F16>
+template <bool F16, bool F16S>
 __global__ void __launch_bounds__(256) dequant_kernel(const DequantParams p) {
   __shared__ float s_lv[16];
   if (threadIdx.x == 0) {
@@ -192,7 +198,9 @@ __global__ void __launch_bounds__(256) dequant_kernel(const DequantParams p) {
     const int t = static_cast<int>(tok % p.n_tokens);
     const long long rowid = bh * p.Tc + t;
     const uint32_t w = reinterpret_cast<const uint32_t*>(p.codes + rowid * (p.hd / 2))[cr];
-    const float s = p.scales[rowid * (p.hd >> p.blk_shift) + ((cr * 8) >> p.blk_shift)];
+    const long long si = rowid * (p.hd >> p.blk_shift) + ((cr * 8) >> p.blk_shift);
+    const float s = F16S ? __half2float(reinterpret_cast<const __half*>(p.scales)[si])
+                         : reinterpret_cast<const float*>(p.scales)[si];
     float v[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) v[k] = __fmul_rn(s, s_lv[(w >> (4 * k)) & 15u]);

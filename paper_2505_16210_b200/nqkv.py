@@ -110,18 +110,29 @@ def nqkv_decode_counter_bytes(B: int, H: int) -> int:
     return int(_lib.nqkv_decode_counter_bytes(B, H))
 
 
+SCALE_F16 = 0x100   # NQKV_SCALE_F16: block scales stored as fp16 (lossless for fp16 inputs)
+
+
+def _blkarg(blk: int, *scales: torch.Tensor) -> int:
+    """blk, or blk | NQKV_SCALE_F16 when the scale tensors are fp16."""
+    dt = {t.dtype for t in scales}
+    assert len(dt) == 1 and dt <= {torch.float32, torch.float16}, dt
+    return blk | SCALE_F16 if torch.float16 in dt else blk
+
+
 # --------------------------------------------------------------- device ----
 def nqkv_quantize(x: torch.Tensor, pos: torch.Tensor, codes: torch.Tensor, scales: torch.Tensor,
                   blk: int, stream=None) -> None:
     """Append x (fp16 [B, n_new, H, hd], hd contiguous, any outer strides) at
     rows pos[b].. of the cache tensors codes [B,H,Tc,hd/2] u8 / scales
-    [B,H,Tc,hd/blk] f32 (PAPER.md:219-228)."""
+    [B,H,Tc,hd/blk] f32 or f16 (PAPER.md:219-228)."""
     B, n_new, H, hd = x.shape
     Tc = codes.shape[2]
     assert x.dtype == torch.float16 and x.stride(3) == 1
-    assert pos.dtype == torch.int32 and codes.dtype == torch.uint8 and scales.dtype == torch.float32
+    assert pos.dtype == torch.int32 and codes.dtype == torch.uint8
     assert codes.is_contiguous() and scales.is_contiguous() and tuple(codes.shape[:2]) == (B, H)
-    _check(_lib.nqkv_quantize(_ptr(x), x.stride(0), x.stride(1), x.stride(2), B, H, hd, n_new, blk,
+    _check(_lib.nqkv_quantize(_ptr(x), x.stride(0), x.stride(1), x.stride(2), B, H, hd, n_new,
+                              _blkarg(blk, scales),
                               _ptr(pos), Tc, _ptr(codes), _ptr(scales), _stream(stream)),
            "nqkv_quantize")
 
@@ -134,7 +145,8 @@ def nqkv_dequantize(codes: torch.Tensor, scales: torch.Tensor, blk: int, n_token
     if out is None:
         out = torch.empty((B, H, n_tokens, hd), dtype=out_dtype, device=codes.device)
     code = {torch.float32: 0, torch.float16: 1}[out.dtype]
-    _check(_lib.nqkv_dequantize(_ptr(codes), _ptr(scales), B, H, Tc, hd, blk, n_tokens, code,
+    _check(_lib.nqkv_dequantize(_ptr(codes), _ptr(scales), B, H, Tc, hd, _blkarg(blk, scales),
+                                n_tokens, code,
                                 _ptr(out), _stream(stream)), "nqkv_dequantize")
     return out
 
@@ -155,7 +167,8 @@ def nqkv_decode_attention(q: torch.Tensor, k_codes: torch.Tensor, k_scales: torc
     assert q.dtype == torch.float16 and q.is_contiguous() and out.is_contiguous()
     assert seq_lens.dtype == torch.int32
     _check(_lib.nqkv_decode_attention(_ptr(q), _ptr(k_codes), _ptr(k_scales), _ptr(v_codes),
-                                      _ptr(v_scales), _ptr(seq_lens), B, H, hd, blk, Tc,
+                                      _ptr(v_scales), _ptr(seq_lens), B, H, hd,
+                                      _blkarg(blk, k_scales, v_scales), Tc,
                                       float(softmax_scale), _ptr(out), _ptr(workspace),
                                       workspace.numel() * workspace.element_size(),
                                       _stream(stream)), "nqkv_decode_attention")
@@ -181,7 +194,8 @@ def nqkv_decode_step(k_new: torch.Tensor, v_new: torch.Tensor, q: torch.Tensor,
     assert seq_lens.dtype == torch.int32
     _check(_lib.nqkv_decode_step(_ptr(k_new), _ptr(v_new), k_new.stride(0), k_new.stride(1),
                                  _ptr(q), _ptr(k_codes), _ptr(k_scales), _ptr(v_codes),
-                                 _ptr(v_scales), _ptr(seq_lens), B, H, hd, blk, Tc,
+                                 _ptr(v_scales), _ptr(seq_lens), B, H, hd,
+                                 _blkarg(blk, k_scales, v_scales), Tc,
                                  float(softmax_scale), _ptr(out), _ptr(workspace),
                                  workspace.numel() * workspace.element_size(), _stream(stream)),
            "nqkv_decode_step")
@@ -215,7 +229,7 @@ def nqkv_decode_attention_planned(q, k_codes, k_scales, v_codes, v_scales, seq_l
     assert q.dtype == torch.float16 and q.is_contiguous() and out.is_contiguous()
     _check(_lib.nqkv_decode_attention_planned(
         _ptr(q), _ptr(k_codes), _ptr(k_scales), _ptr(v_codes), _ptr(v_scales), _ptr(seq_lens), B, H,
-        hd, blk, Tc, float(softmax_scale), _ptr(out), _ptr(workspace),
+        hd, _blkarg(blk, k_scales, v_scales), Tc, float(softmax_scale), _ptr(out), _ptr(workspace),
         workspace.numel() * workspace.element_size(), _ptr(plan), int(flags), _stream(stream)),
         "nqkv_decode_attention_planned")
     return out
@@ -234,7 +248,8 @@ def nqkv_decode_step_planned(k_new, v_new, q, k_codes, k_scales, v_codes, v_scal
     assert q.dtype == torch.float16 and q.is_contiguous() and out.is_contiguous()
     _check(_lib.nqkv_decode_step_planned(
         _ptr(k_new), _ptr(v_new), k_new.stride(0), k_new.stride(1), _ptr(q), _ptr(k_codes),
-        _ptr(k_scales), _ptr(v_codes), _ptr(v_scales), _ptr(seq_lens), B, H, hd, blk, Tc,
+        _ptr(k_scales), _ptr(v_codes), _ptr(v_scales), _ptr(seq_lens), B, H, hd,
+        _blkarg(blk, k_scales, v_scales), Tc,
         float(softmax_scale), _ptr(out), _ptr(workspace), workspace.numel() * workspace.element_size(),
         _ptr(plan), int(flags), _stream(stream)), "nqkv_decode_step_planned")
     return out
@@ -257,12 +272,15 @@ class KVCache:
     """Per-layer packed NF4 K/V cache in the library's layout:
     codes u8 [B,H,Tc,hd/2], scales f32 [B,H,Tc,hd/blk] for K and for V."""
 
-    def __init__(self, B: int, H: int, hd: int, Tc: int, blk: int = 64, device="cuda"):
-        assert Tc % 64 == 0
+    def __init__(self, B: int, H: int, hd: int, Tc: int, blk: int = 64, device="cuda",
+                 scale_dtype=torch.float32):
+        """scale_dtype torch.float16 stores block scales as fp16 (lossless for
+        fp16 inputs: NQKV_SCALE_F16)."""
+        assert Tc % 64 == 0 and scale_dtype in (torch.float32, torch.float16)
         self.B, self.H, self.hd, self.Tc, self.blk = B, H, hd, Tc, blk
         self.k_codes = torch.zeros((B, H, Tc, hd // 2), dtype=torch.uint8, device=device)
         self.v_codes = torch.zeros_like(self.k_codes)
-        self.k_scales = torch.zeros((B, H, Tc, hd // blk), dtype=torch.float32, device=device)
+        self.k_scales = torch.zeros((B, H, Tc, hd // blk), dtype=scale_dtype, device=device)
         self.v_scales = torch.zeros_like(self.k_scales)
 
     def append(self, k: torch.Tensor, v: torch.Tensor, pos: torch.Tensor, stream=None) -> None:

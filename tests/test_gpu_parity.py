@@ -549,3 +549,48 @@ def test_random_geometries_planned_fused(N, seed):
         ref = O.decode_attention(q[b:b + 1].cpu().numpy(), kc[b:b + 1], ks[b:b + 1], vc[b:b + 1],
                                  vs[b:b + 1], [lens0[b] + 1], blk)
         assert np.max(np.abs(f0[b:b + 1].cpu().numpy() - ref)) <= ATOL
+
+
+@pytest.mark.parametrize("hd,blk", [(64, 32), (64, 64), (128, 64), (128, 128)])
+def test_fp16_scales_lossless(N, hd, blk):
+    """NQKV_SCALE_F16: a block scale is the absmax of fp16
+    inputs, itself an fp16 value, so storing it as fp16 changes nothing --
+    codes, dequantised values, attention (plain, fused, planned) are bit-for-
+    bit those of the fp32-scale layout, and the scales equal the oracle's."""
+    B, H = 5, 3
+    lens0 = [0, 1, 70, 333, 511]
+    T, Tc = max(lens0), 576
+    x = _rand_kv(B, T, H, hd, seed=81)
+    y = _rand_kv(B, T, H, hd, seed=82, outlier=False)
+    kn = _rand_kv(B, 1, H, hd, seed=83)[:, 0].to(DEV)
+    vn = _rand_kv(B, 1, H, hd, seed=84, outlier=False)[:, 0].to(DEV)
+    q = torch.randn(B, H, hd, generator=torch.Generator().manual_seed(85)).to(torch.float16).to(DEV)
+    c32 = N.KVCache(B, H, hd, Tc, blk, DEV)
+    c16 = N.KVCache(B, H, hd, Tc, blk, DEV, scale_dtype=torch.float16)
+    z = torch.zeros(B, dtype=torch.int32, device=DEV)
+    for c in (c32, c16):
+        c.append(x.to(DEV), y.to(DEV), z)
+    torch.cuda.synchronize()
+    assert torch.equal(c32.k_codes, c16.k_codes) and torch.equal(c32.v_codes, c16.v_codes)
+    assert torch.equal(c32.k_scales, c16.k_scales.float()) and torch.equal(c32.v_scales, c16.v_scales.float())
+    kc, ks = _oracle_cache(x, [0] * B, blk, Tc)
+    assert np.array_equal(c16.k_scales.float().cpu().numpy(), ks)
+    assert torch.equal(N.nqkv_dequantize(c32.k_codes, c32.k_scales, blk),
+                       N.nqkv_dequantize(c16.k_codes, c16.k_scales, blk))
+    L = torch.tensor(lens0, dtype=torch.int32, device=DEV)
+    ws = lambda: N.make_workspace(B, H, hd, Tc, DEV)
+    a32, a16 = c32.attend(q, L, ws()), c16.attend(q, L, ws())
+    L1 = L + 1
+    plan = N.make_plan(DEV)
+    N.nqkv_decode_plan(L1, H, Tc, True, plan, hd=hd)
+    f32 = c32.step(kn, vn, q, L1, ws())
+    d16 = N.KVCache(B, H, hd, Tc, blk, DEV, scale_dtype=torch.float16)
+    d16.k_codes.copy_(c16.k_codes); d16.v_codes.copy_(c16.v_codes)
+    d16.k_scales.copy_(c16.k_scales); d16.v_scales.copy_(c16.v_scales)
+    f16 = c16.step(kn, vn, q, L1, ws())
+    p16 = d16.step_planned(kn, vn, q, L1, ws(), plan, flags=N.EARLY_START)
+    torch.cuda.synchronize()
+    assert torch.equal(a32, a16)
+    assert torch.equal(f32, f16) and torch.equal(f32, p16)
+    assert torch.equal(c32.k_codes, c16.k_codes) and torch.equal(c32.v_scales, c16.v_scales.float())
+    assert torch.equal(c16.k_scales, d16.k_scales) and torch.equal(c16.v_codes, d16.v_codes)

@@ -36,6 +36,7 @@ def main():
     ap.add_argument("--configs", default="c1,c2,c3,c4,c5")
     ap.add_argument("--heads5", type=int, default=12)
     ap.add_argument("--only", default="", help="attend|step|quantize: run just that once (for ncu)")
+    ap.add_argument("--scale16", action="store_true", help="fp16 block scales (NQKV_SCALE_F16)")
     args = ap.parse_args()
     dev = "cuda"
     flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)
@@ -46,7 +47,8 @@ def main():
         T = int(lens.max())
         Tc = W.capacity(T + 1)
         K, V = W.layer_kv(w, 0, heads=range(H), tokens=T, device=dev)
-        cache = N.KVCache(w.batch, H, w.head_dim, Tc, w.blk, dev)
+        cache = N.KVCache(w.batch, H, w.head_dim, Tc, w.blk, dev,
+                          scale_dtype=torch.float16 if args.scale16 else torch.float32)
         z = torch.zeros(w.batch, dtype=torch.int32, device=dev)
         if args.only == "quantize":
             N.nqkv_quantize(K, z, cache.k_codes, cache.k_scales, w.blk)
@@ -55,7 +57,8 @@ def main():
         qt = timeit(lambda: N.nqkv_quantize(K, z, cache.k_codes, cache.k_scales, w.blk), flush)
         N.nqkv_quantize(V, z, cache.v_codes, cache.v_scales, w.blk)
         elems = K.numel()
-        qbytes = elems * (2 + 0.5 + 4 / w.blk)
+        sb = 2 if args.scale16 else 4
+        qbytes = elems * (2 + 0.5 + sb / w.blk)
         k1, v1, q = W.step_inputs(w, 0, 0, heads=range(H), device=dev)
         L = (lens + 1).to(dev)
         ws = N.make_workspace(w.batch, H, w.head_dim, Tc, dev)
@@ -71,7 +74,7 @@ def main():
         at = timeit(lambda: cache.attend(q, L, ws, out=out), flush)
         st = timeit(lambda: cache.step(k1[:, 0], v1[:, 0], q, L, ws, out=out), flush)
         toks = int(L.sum())
-        dbytes = toks * H * w.head_dim * 2 * (0.5 + 4 / w.blk) + w.batch * H * w.head_dim * 6
+        dbytes = toks * H * w.head_dim * 2 * (0.5 + sb / w.blk) + w.batch * H * w.head_dim * 6
         print(f"{name}: H={H} T={T} quantize {qt*1e3:8.1f} us {qbytes/qt/1e6:7.0f} GB/s | "
               f"attend {at*1e3:8.1f} us {dbytes/at/1e6:7.0f} GB/s | step {st*1e3:8.1f} us "
               f"{dbytes/st/1e6:7.0f} GB/s | cache {dbytes/1e6:.1f} MB", flush=True)
