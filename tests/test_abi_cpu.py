@@ -134,3 +134,13 @@ def test_plan_argument_errors():
     assert f(FAKE, 4, 8, 64, 100, 0, FAKE, nb, None) == -2        # Tc not a multiple of 64
     assert f(FAKE, 4, 8, 64, 256, 0, FAKE + 4, nb, None) == -4    # misaligned plan
     assert f(FAKE, 4, 8, 64, 256, 0, FAKE, nb - 16, None) == -5   # plan buffer too small
+
+
+def test_scale_f16_flag_validation():
+    f16 = N.SCALE_F16
+    # n = 0: every check runs, nothing is launched
+    assert _q(blk=64 | f16, n=0) == 0                              # accepted
+    assert _q(blk=64 | 0x200, n=0) == -3                           # unknown flag bit
+    assert _q(blk=64 | f16, scales=FAKE + 2, n=0) == 0             # fp16 scales: 2-byte alignment suffices
+    assert _q(blk=64, scales=FAKE + 2, n=0) == -4                  # fp32 scales need 4
+    assert _q(blk=64 | f16, scales=FAKE + 1, n=0) == -4
