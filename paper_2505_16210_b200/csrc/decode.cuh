@@ -472,7 +472,15 @@ __global__ void __launch_bounds__(1024) decode_plan_kernel(const int32_t* seq_le
 // the cache row `row` of (b, h); vh gets its dequantised values and the return
 // value is its score (log2 domain) from the q-table in `slot` (slot < 0: 0).
 template <int HD, int NW, bool F16S>
-__device__ __noinline__ float new_token_fn(const DecodeParams& p, unsigned char* smem, int b, int h,
+#ifndef NQKV_NEWTOK_INLINE
+#define NQKV_NEWTOK_INLINE 1          // inlined: c3 -2.7 % (a fused step calls it once per piece)
+#endif
+#if NQKV_NEWTOK_INLINE
+__device__ __forceinline__
+#else
+__device__ __noinline__
+#endif
+float new_token_fn(const DecodeParams& p, unsigned char* smem, int b, int h,
                                            int row, int slot, float* vh) {
   using Sm = Smem<HD, NW>;
   constexpr int PPL = Geo<HD>::PPL;
@@ -593,7 +601,15 @@ __device__ __forceinline__ int ld_relaxed_s32(const int* p) {
 // piece k; merge_fn then needs no global round trip at the end of the
 // kernel.  Otherwise merge_fn runs the normal protocol.
 template <int HD, int NW>
-__device__ __noinline__ void peek_fn(const DecodeParams& p, unsigned char* smem, int k, Sched sc, int cta) {
+#ifndef NQKV_PEEK_INLINE
+#define NQKV_PEEK_INLINE 0
+#endif
+#if NQKV_PEEK_INLINE
+__device__ __forceinline__
+#else
+__device__ __noinline__
+#endif
+void peek_fn(const DecodeParams& p, unsigned char* smem, int k, Sched sc, int cta) {
   using Sm = Smem<HD, NW>;
   constexpr int PPL = Geo<HD>::PPL, R = Geo<HD>::R;
   const int lane = threadIdx.x & 31;
@@ -656,7 +672,15 @@ __device__ __noinline__ void peek_fn(const DecodeParams& p, unsigned char* smem,
 // the appended token's state: write the output, or a partial (+ the
 // last-arriver merge of the sequence's partials across CTAs).
 template <int HD, int NW>
-__device__ __noinline__ void merge_fn(const DecodeParams& p, unsigned char* smem, int k, Sched sc,
+#ifndef NQKV_MERGE_INLINE
+#define NQKV_MERGE_INLINE 1          // inlined: a call to cold code at the kernel's end costs ~1 %
+#endif
+#if NQKV_MERGE_INLINE
+__device__ __forceinline__
+#else
+__device__ __noinline__
+#endif
+void merge_fn(const DecodeParams& p, unsigned char* smem, int k, Sched sc,
                                       int cta, int g0) {
   using Sm = Smem<HD, NW>;
   constexpr int PPL = Geo<HD>::PPL, R = Geo<HD>::R, NC = NW - 1;
