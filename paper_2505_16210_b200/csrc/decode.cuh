@@ -551,7 +551,15 @@ float new_token_fn(const DecodeParams& p, unsigned char* smem, int b, int h,
 // RN(c q_{2j} L[e & 15]) + RN(c q_{2j+1} L[e >> 4]) (the same formula as the
 // cooperative table-0 build).
 template <int HD, int NW>
-__device__ __noinline__ void build_fn(unsigned char* smem, int slot, uint4 qraw, float scale_log2) {
+#ifndef NQKV_BUILD_INLINE
+#define NQKV_BUILD_INLINE 0
+#endif
+#if NQKV_BUILD_INLINE
+__device__ __forceinline__
+#else
+__device__ __noinline__
+#endif
+void build_fn(unsigned char* smem, int slot, uint4 qraw, float scale_log2) {
   using Sm = Smem<HD, NW>;
   constexpr int Q = HD / 8;
   const int lane = threadIdx.x & 31;
