@@ -310,8 +310,11 @@ int nqkv_quantize(const void* x, int64_t stride_b, int64_t stride_t, int64_t str
   p.nnew = make_fastdiv(static_cast<uint32_t>(n_new));
   p.tab = make_bucket_tab();
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  // one warp per 64-chunk unit, grid-strided: up to 8 CTAs of 8 warps per SM
-  const dim3 grid(static_cast<unsigned>(grid_for((chunks + 1) / 2, 256, 8)));
+  // one warp per 64-chunk unit, grid-strided over one wave of resident CTAs
+#ifndef NQKV_Q_CTAS_PER_SM
+#define NQKV_Q_CTAS_PER_SM 4            // = resident CTAs (64 regs x 256 threads): one wave
+#endif
+  const dim3 grid(static_cast<unsigned>(grid_for((chunks + 1) / 2, 256, NQKV_Q_CTAS_PER_SM)));
   cudaError_t e;
   const size_t sm = kQuantSmem;
   auto launch = [&](auto f16s_tag) {
