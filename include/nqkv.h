@@ -184,7 +184,9 @@ int nqkv_decode_step(const void* k_new, const void* v_new, int64_t new_stride_b,
  * launched immediately before it on the same stream -- e.g. layers 1.. of a
  * decode step whose plan was computed before layer 0.  Every kernel of this
  * library waits for its predecessor (programmatic dependent launch) before
- * it lets its successor start, so such a plan and cache are complete when
+ * it lets its successor start, so -- provided the kernels launched between
+ * the writer and this call are this library's or launched without
+ * programmatic dependent launch -- such a plan and cache are complete when
  * the call starts, and the kernel reads the plan and issues its first cache
  * loads before that wait, overlapping the predecessor's tail.  q, k_new,
  * v_new, seq_lens, out and the workspace are always accessed after the wait.
