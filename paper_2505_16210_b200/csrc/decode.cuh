@@ -62,6 +62,9 @@ constexpr int kMinTokensPerCta = 512;  // below this a CTA's table build would d
 #ifndef NQKV_PEEK
 #define NQKV_PEEK -1             // early last-arriver role for the last piece: 1 on, 0 off, -1 hd 128 only (measured)
 #endif
+#ifndef NQKV_QPF
+#define NQKV_QPF 1               // early start: L2-prefetch the first pieces' q rows before the wait
+#endif
 #ifndef NQKV_SPLIT
 #define NQKV_SPLIT -1            // split K/V ring: 1 on, 0 off, -1 hd 64 only (measured)
 #endif
@@ -1290,6 +1293,17 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
     if (tid < (p.B + 31) / 32) pa_one = __ldcg(p.plan + kPlanOne + tid);
   }
   if (pre) {
+#if NQKV_QPF
+    // L2 prefetch of the prebuilt pieces' q rows (a hint, coherent: the
+    // loads below still read after the wait; in a model the predecessor has
+    // just written q, so it is L2-resident anyway)
+    if (warp == 0 && lane < R0) {
+      const int bh = lane == 0 ? p0.b * p.H + p0.h : lane == 1 ? pbh.x : lane == 2 ? pbh.y : pbh.z;
+      asm volatile("prefetch.global.L2 [%0];" :: "l"(p.q + static_cast<long long>(bh) * HD));
+      if (HD == 128)
+        asm volatile("prefetch.global.L2 [%0];" :: "l"(p.q + static_cast<long long>(bh) * HD + 64));
+    }
+#endif
     pdl_enter();
     TRACE(1);
   }
