@@ -1085,12 +1085,14 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
   const int g = lane / LPT, sub = lane % LPT;
   constexpr int NBLK = HD / BLK;
   const int sidx = (sub * kLaneDims) / BLK;
-  // Reduce-scatter layout (BLK = 16 * kTPS, i.e. blk 64): the kTPS lanes of a
+  // Reduce-scatter layout (BLK >= 16 * kTPS, i.e. blk 64 or 128): the kTPS lanes of a
   // block each own one token slot j = sub % kTPS of the stage: they load its
   // K / V scale, finish its score, exponentiate it, and hand its weight
   // p_j * vs_j to the other lanes of the block.  1 scale load, 1 exp2 per lane
   // and stage instead of kTPS.
-  constexpr bool RS = BLK == kLaneDims * kTPS && kTPS == 4;
+  // (blk 128 at hd 128: the two 4-lane halves of the block share one scale,
+  // so the same per-half reduce-scatter applies)
+  constexpr bool RS = BLK >= kLaneDims * kTPS && kTPS == 4;
   const uint32_t soff_rs = RS ? static_cast<uint32_t>((sub & 3) * G * NBLK * SB) : 0u;
   // Per-lane 32-bit byte offsets (codes, scales) of the load cursor: this
   // lane's bytes of the stage to load next (token tok0 + g of its (b, h));

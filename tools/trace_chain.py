@@ -25,7 +25,7 @@ B, H, hd, T, L = (int(x) for x in sys.argv[1:6]) if len(sys.argv) > 5 else (8, 3
 Tc = -(-(T + 16) // 64) * 64
 caches = []
 for _ in range(L):
-    c = N.KVCache(B, H, hd, Tc, 64, "cuda")
+    c = N.KVCache(B, H, hd, Tc, int(os.environ.get("BLK", "64")), "cuda")
     c.k_codes.random_(0, 256)
     c.v_codes.random_(0, 256)
     c.k_scales.uniform_(0.5, 2)
