@@ -43,6 +43,7 @@
 // same call is bit-reproducible; a different head shard of the same data can
 // differ by fp32 reassociation (reading R7).
 #pragma once
+#include <climits>
 #include "common.cuh"
 
 namespace nqkv {
@@ -399,6 +400,16 @@ __device__ __forceinline__ int4 next_pieces(const WalkState& w, const int* len, 
   return make_int4(bh[0], bh[1], bh[2], n);
 }
 
+// CTAs for an N-token launch: ~min_tokens per CTA, at most G.  When every
+// non-empty sequence has the same streamed length and that count would give
+// between nseq and 2*nseq - 1 CTAs, use exactly nseq: each CTA then holds one
+// whole sequence and no cross-CTA merge is needed (small batches, e.g. c1).
+__device__ __forceinline__ int cta_count(int N, int G, int min_tokens, int nseq, bool uniform) {
+  int C = min(G, max(1, (N + min_tokens - 1) / min_tokens));
+  if (uniform && nseq >= 1 && nseq <= G && C >= nseq && C < 2 * nseq) C = nseq;
+  return C;
+}
+
 __global__ void __launch_bounds__(1024) decode_plan_kernel(const int32_t* seq_lens, int B, int H, int Tc,
                                                            int fused, int G, int min_tokens, int R,
                                                            int* plan) {
@@ -438,10 +449,20 @@ __global__ void __launch_bounds__(1024) decode_plan_kernel(const int32_t* seq_le
     s_pref[0] = 0;
     plan[kPlanPref] = 0;
   }
+  __shared__ int s_lmin, s_lmax;
+  if (tid == 0) {
+    s_lmin = INT_MAX;
+    s_lmax = 0;
+  }
   __syncthreads();
+  if (tid < B && len > 0) {
+    atomicMin(&s_lmin, len);
+    atomicMax(&s_lmax, len);
+  }
+  const int nb = __syncthreads_count(tid < B && len > 0);
   Sched sc;
   sc.N = s_pref[B];
-  sc.C = min(G, max(1, (sc.N + min_tokens - 1) / min_tokens));
+  sc.C = cta_count(sc.N, G, min_tokens, nb * H, nb > 0 && s_lmin == s_lmax);
   sc.q = sc.N / sc.C;
   sc.r = sc.N - sc.q * sc.C;
   if (tid == 0) {
@@ -987,7 +1008,7 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
     // Fused step: the appended row (len - 1) is not streamed; the producer
     // quantises it and folds it into the piece merge (s_len holds len').
     if (warp == 0) {
-      int carry = 0;
+      int carry = 0, lmin = INT_MAX, lmax = 0, nb = 0;
       if (lane == 0) s_pref[0] = 0;
       for (int b0 = 0; b0 < p.B; b0 += 32) {
         const int b = b0 + lane;
@@ -999,6 +1020,11 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
           const int len = fused ? max(raw - 1, 0) : raw;
           s_len[b] = len;
           n = p.H * len;
+          if (len > 0) {
+            lmin = min(lmin, len);
+            lmax = max(lmax, len);
+            ++nb;
+          }
         }
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -1008,11 +1034,23 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
         if (b < p.B) s_pref[b + 1] = carry + n;
         carry += __shfl_sync(0xffffffffu, n, 31);
       }
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        lmin = min(lmin, __shfl_xor_sync(0xffffffffu, lmin, o));
+        lmax = max(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
+        nb += __shfl_xor_sync(0xffffffffu, nb, o);
+      }
+      if (lane == 0) {
+        reinterpret_cast<int*>(smem + Sm::kPreFlag)[1] = nb;
+        reinterpret_cast<int*>(smem + Sm::kPreFlag)[2] = nb > 0 && lmin == lmax;
+      }
     }
     __syncthreads();
     sc.N = s_pref[p.B];
     if (sc.N > 0) {
-      sc.C = min(static_cast<int>(gridDim.x), max(1, (sc.N + p.min_tokens - 1) / p.min_tokens));
+      const int nb = reinterpret_cast<const int*>(smem + Sm::kPreFlag)[1];
+      sc.C = cta_count(sc.N, static_cast<int>(gridDim.x), p.min_tokens, nb * p.H,
+                       reinterpret_cast<const int*>(smem + Sm::kPreFlag)[2] != 0);
       sc.q = sc.N / sc.C;
       sc.r = sc.N - sc.q * sc.C;
       if (cta < sc.C) {
