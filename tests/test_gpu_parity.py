@@ -594,3 +594,30 @@ def test_fp16_scales_lossless(N, hd, blk):
     assert torch.equal(f32, f16) and torch.equal(f32, p16)
     assert torch.equal(c32.k_codes, c16.k_codes) and torch.equal(c32.v_scales, c16.v_scales.float())
     assert torch.equal(c16.k_scales, d16.k_scales) and torch.equal(c16.v_codes, d16.v_codes)
+
+
+@pytest.mark.parametrize("hd", [64, 128])
+def test_uniform_small_batch_one_cta_per_sequence(N, hd):
+    """Uniform lengths, few sequences: one CTA per sequence (no cross-CTA
+    merge); planned == unplanned bit for bit, matches the oracle, and the
+    workspace stays zero."""
+    blk, B, H, T = 64, 2, 5, 600
+    Tc = 640
+    x = _rand_kv(B, T, H, hd, seed=91)
+    y = _rand_kv(B, T, H, hd, seed=92, outlier=False)
+    q = torch.randn(B, H, hd, generator=torch.Generator().manual_seed(93)).to(torch.float16).to(DEV)
+    kc, ks = _oracle_cache(x, [0] * B, blk, Tc)
+    vc, vs = _oracle_cache(y, [0] * B, blk, Tc)
+    t = lambda a: torch.from_numpy(a.copy()).to(DEV)
+    L = torch.full((B,), T, dtype=torch.int32, device=DEV)
+    plan = N.make_plan(DEV)
+    N.nqkv_decode_plan(L, H, Tc, False, plan, hd=hd)
+    ws1, ws2 = N.make_workspace(B, H, hd, Tc, DEV), N.make_workspace(B, H, hd, Tc, DEV)
+    o1 = N.nqkv_decode_attention(q, t(kc), t(ks), t(vc), t(vs), L, blk, ws1)
+    o2 = N.nqkv_decode_attention_planned(q, t(kc), t(ks), t(vc), t(vs), L, blk, ws2, plan)
+    torch.cuda.synchronize()
+    assert torch.equal(o1, o2)
+    assert torch.count_nonzero(ws1) == 0 and torch.count_nonzero(ws2) == 0
+    assert int(plan[4:8].view(torch.int32)[0]) == B * H          # header: C = #sequences
+    ref = O.decode_attention(q.cpu().numpy(), kc, ks, vc, vs, [T] * B, blk)
+    assert np.max(np.abs(o1.cpu().numpy() - ref)) <= ATOL
