@@ -155,10 +155,28 @@ def unpack_nibbles(packed: np.ndarray) -> np.ndarray:
     return out
 
 
+def heads_per_block(hd: int, blk: int) -> int:
+    """blk <= hd: a block is blk channels of one head (1).  blk > hd: a block
+    is the hidden-state slice of blk / hd adjacent heads of one token -- the
+    paper's own setting, blk 256 over OPT's hidden dimension (PAPER.md:141,
+    302; reading R2b)."""
+    if blk <= hd:
+        if hd % blk:
+            raise ValueError("blk must divide hd")
+        return 1
+    if blk % hd:
+        raise ValueError("hd must divide blk")
+    return blk // hd
+
+
 def empty_cache(B: int, H: int, Tc: int, hd: int, blk: int):
-    """codes uint8 [B][H][Tc][hd/2], scales float32 [B][H][Tc][hd/blk]."""
+    """codes uint8 [B][H][Tc][hd/2]; scales float32 [B][H][Tc][hd/blk], or
+    [B][H*hd/blk][Tc][1] when a block spans blk/hd heads."""
+    hpb = heads_per_block(hd, blk)
+    if H % hpb:
+        raise ValueError("a block may not straddle the last head")
     return (np.zeros((B, H, Tc, hd // 2), np.uint8),
-            np.zeros((B, H, Tc, hd // blk), np.float32))
+            np.zeros((B, H // hpb, Tc, max(hd // blk, 1)), np.float32))
 
 
 def quantize_append(x: np.ndarray, pos, blk: int, codes: np.ndarray, scales: np.ndarray,
@@ -169,12 +187,18 @@ def quantize_append(x: np.ndarray, pos, blk: int, codes: np.ndarray, scales: np.
     Rows pos[b] .. pos[b]+n_new-1 of codes/scales are written; every other
     byte is left untouched (append-only).  A block is blk
     consecutive channels of one (token, head) -- DESIGN.md reading R2.
+    With blk > hd a block is the slice of blk/hd adjacent heads of one token's
+    hidden state (the paper's blk 256 over d): scales then
+    hold one value per (token, head group).
     """
     x = np.asarray(x)
     B, n_new, H, hd = x.shape
-    nb = hd // blk
-    blocks = x.reshape(B, n_new, H, nb, blk)
-    s, c = quantize_blocks(blocks, levels32)              # [B,n,H,nb], [B,n,H,nb,blk]
+    hpb = heads_per_block(hd, blk)
+    nb = max(hd // blk, 1)
+    # [H, hd] -> [H/hpb groups, nb blocks per group, blk]: hd is contiguous and
+    # heads are adjacent in a token's hidden state
+    blocks = x.reshape(B, n_new, H // hpb, nb, blk)
+    s, c = quantize_blocks(blocks, levels32)              # [B,n,Hs,nb], [B,n,Hs,nb,blk]
     packed = pack_nibbles(c.reshape(B, n_new, H, hd))     # [B,n,H,hd/2]
     for b in range(B):
         p0 = int(pos[b])
@@ -190,17 +214,22 @@ def dequantize(codes: np.ndarray, scales: np.ndarray, blk: int, n_tokens: int | 
     """X' = dequantize_NF4(I): v = RN32(scale * L[code])  (PAPER.md:193, 229-231;
     SPEC.md:73-81).  fp16 output is RN16 of that fp32 value.
 
-    codes [B][H][Tc][hd/2], scales [B][H][Tc][hd/blk] -> [B][H][n_tokens][hd].
+    codes [B][H][Tc][hd/2], scales [B][H][Tc][hd/blk] (blk > hd:
+    [B][H*hd/blk][Tc][1]) -> [B][H][n_tokens][hd].
     """
     if levels32 is None:
         levels32 = nf_levels_f32()
     B, H, Tc, hb = codes.shape
     hd = hb * 2
+    hpb = heads_per_block(hd, blk)
     if n_tokens is None:
         n_tokens = Tc
     c = unpack_nibbles(codes[:, :, :n_tokens, :])                 # [B,H,n,hd]
     lv = levels32[c]                                              # fp32 lookup
-    s = np.repeat(scales[:, :, :n_tokens, :], blk, axis=-1)       # [B,H,n,hd]
+    s = scales[:, :, :n_tokens, :]
+    if hpb > 1:                      # head group g -> heads g*hpb .. g*hpb+hpb-1
+        s = np.repeat(s, hpb, axis=1)
+    s = np.repeat(s, min(blk, hd), axis=-1)                       # [B,H,n,hd]
     v = (s.astype(np.float32) * lv.astype(np.float32)).astype(np.float32)
     return v.astype(out_dtype)
 

@@ -293,6 +293,82 @@ def test_fig5_geometry():
     assert codes[0, 0].shape == (1024, 12)
 
 
+def test_fig2_block256_geometry():
+    # PAPER.md:141 (Fig. 2 caption): OPT-6.7B hidden size 4096, block size 256
+    # -> 16 blocks per token (here 32 heads x 128 channels, 8 tokens)
+    rng = np.random.default_rng(16)
+    x = rng.standard_normal((1, 8, 32, 128)).astype(np.float16)
+    codes, scales = O.empty_cache(1, 32, 64, 128, 256)
+    O.quantize_append(x, [0], 256, codes, scales)
+    assert scales.shape == (1, 16, 64, 1)
+    assert np.count_nonzero(scales[0, :, :8]) == 16 * 8      # 16 blocks per token
+    # closed form: a block scale is max |x| over its 256 hidden channels
+    hid = x.reshape(1, 8, 4096).astype(np.float32)
+    for t in range(8):
+        for g in range(16):
+            assert scales[0, g, t, 0] == np.abs(hid[0, t, 256 * g:256 * (g + 1)]).max()
+
+
+@pytest.mark.parametrize("hd,blk", [(64, 128), (64, 256), (128, 256)])
+def test_head_spanning_block_reduces_to_per_head(hd, blk):
+    # a group whose other heads are zero has the absmax of the remaining head:
+    # codes and scale equal the blk = hd quantisation of that head, and the
+    # zero heads get the zero code
+    hpb = blk // hd
+    rng = np.random.default_rng(17 + blk)
+    H = 2 * hpb
+    x = np.zeros((1, 3, H, hd), np.float16)
+    live = [1, hpb + hpb - 1]                        # one head in each group
+    for h in live:
+        x[0, :, h] = (rng.standard_normal((3, hd)) * 2).astype(np.float16)
+    c, sc = O.empty_cache(1, H, 64, hd, blk)
+    O.quantize_append(x, [0], blk, c, sc)
+    for gi, h in enumerate(live):
+        sh, ch = O.quantize_blocks(x[0, :, h])
+        assert np.array_equal(sc[0, gi, :3, 0], sh)
+        assert np.array_equal(O.unpack_nibbles(c[0, h, :3]), ch)
+        for h2 in range(gi * hpb, (gi + 1) * hpb):
+            if h2 != h:
+                assert np.all(O.unpack_nibbles(c[0, h2, :3]) == O.ZERO_CODE)
+    # dequant: every head of group g uses the group's scale, RN32(s * L)
+    dq = O.dequantize(c, sc, blk, 3)
+    for h in range(H):
+        ref = (sc[0, h // hpb, :3, :] * L32[O.unpack_nibbles(c[0, h, :3])]).astype(np.float32)
+        assert np.array_equal(dq[0, h], ref)
+
+
+def test_head_spanning_grid_fixed_point():
+    # SPEC.md:70 across heads: the 16 values fp16(s * L_c) spread over the 4
+    # heads of a 256-block (hd 64) come back as codes c, scale s
+    s = 3.0
+    grid = (np.float32(s) * L32).astype(np.float16)                 # 16 values
+    x = np.zeros((1, 1, 4, 64), np.float16)
+    flat = x.reshape(256)
+    idx = np.arange(16) * 16 + 5                                     # 4 per head
+    flat[idx] = grid
+    c, sc = O.empty_cache(1, 4, 64, 64, 256)
+    O.quantize_append(flat.reshape(1, 1, 4, 64), [0], 256, c, sc)
+    assert sc[0, 0, 0, 0] == np.float32(s)
+    codes = O.unpack_nibbles(c[0, :, 0]).reshape(256)
+    assert np.array_equal(codes[idx], np.arange(16))
+    mask = np.ones(256, bool)
+    mask[idx] = False
+    assert np.all(codes[mask] == O.ZERO_CODE)
+
+
+def test_head_spanning_blocks_stream_and_reject_straddle():
+    rng = np.random.default_rng(18)
+    x = (rng.standard_normal((2, 5, 4, 128)) * 3).astype(np.float16)
+    c1, s1 = O.empty_cache(2, 4, 64, 128, 256)
+    O.quantize_append(x, [0, 7], 256, c1, s1)
+    c2, s2 = O.empty_cache(2, 4, 64, 128, 256)
+    for t in range(5):
+        O.quantize_append(x[:, t:t + 1], [t, 7 + t], 256, c2, s2)
+    assert np.array_equal(c1, c2) and np.array_equal(s1, s2)
+    with pytest.raises(ValueError):
+        O.empty_cache(1, 3, 64, 128, 256)                            # 3 heads: 1.5 blocks
+
+
 def test_pack_layout_golden_row():
     # element 2i low nibble, 2i+1 high nibble
     c = np.arange(16, dtype=np.uint8)
