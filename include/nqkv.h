@@ -30,9 +30,14 @@
  *                                          2i+1 in the high nibble
  *        scales float32 [B][H][Tc][hd/blk] absmax of each block of blk
  *                                          consecutive channels of one (token, head)
- *  - Supported geometry: hd in {64, 128}; blk in {32, 64, 128} with blk <= hd;
- *    Tc a positive multiple of 64.  Anything else -> NQKV_ERR_UNSUPPORTED /
- *    NQKV_ERR_SHAPE.
+ *    With blk > hd a block is the hidden-state slice of hpb = blk/hd adjacent
+ *    heads of one token (the paper's blk 256 over d):
+ *        scales float32 [B][H/hpb][Tc]     one scale per (token, head group);
+ *                                          head h uses group h/hpb
+ *    H must then be a multiple of hpb (a head shard must hold whole groups).
+ *  - Supported geometry: hd in {64, 128}; blk in {32, 64, 128, 256} with
+ *    blk | hd or hd | blk; Tc a positive multiple of 64.  Anything else ->
+ *    NQKV_ERR_UNSUPPORTED / NQKV_ERR_SHAPE.
  *  - Calls are thread-safe and reentrant.  The only global state is the level
  *    table, computed once on the host (std::call_once) and passed to kernels
  *    by value.
@@ -47,7 +52,7 @@
 extern "C" {
 #endif
 
-#define NQKV_ABI_VERSION 1
+#define NQKV_ABI_VERSION 2   /* 2: blk 256 / head-group scales; NQKV_SCALE_F16 moved to 0x10000 */
 
 typedef enum {
   NQKV_OK = 0,
@@ -83,7 +88,7 @@ int nqkv_thresholds(float thresholds[15]);
  * inputs, itself an fp16 value, so codes, dequantised values and attention
  * are identical to the fp32-scale layout; scale bytes halve (-5.6 % of the
  * cache at blk 64).  Scales: 2-byte aligned instead of 4. */
-#define NQKV_SCALE_F16 0x100
+#define NQKV_SCALE_F16 0x10000
 
 /* a1-a3. Quantize + pack + append.
  * x      device fp16, logical [B][n_new][H][hd] with element strides
@@ -94,8 +99,8 @@ int nqkv_thresholds(float thresholds[15]);
  *        codes/scales are left untouched (append-only).  Rows
  *        outside [0, Tc) are skipped.
  * codes  device uint8  [B][H][Tc][hd/2]    (16-byte aligned)
- * scales device float  [B][H][Tc][hd/blk]  (4-byte aligned; fp16 with
- *        NQKV_SCALE_F16, 2-byte aligned)
+ * scales device float  [B][H][Tc][hd/blk], or [B][H/hpb][Tc] for blk > hd
+ *        (4-byte aligned; fp16 with NQKV_SCALE_F16, 2-byte aligned)
  * Per block: s = max|x| (fp32, exact); code = nearest level to n = RN32(x/s),
  * ties lower; s == 0 -> code 7 (the zero level).  The kernel normalises with
  * n' = RN32(x * RN32(1/s)), which gives the identical code for every fp16

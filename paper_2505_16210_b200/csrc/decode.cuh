@@ -97,6 +97,7 @@ struct DecodeParams {
   BucketTab tab;
   const int* plan;             // optional per-step schedule (nqkv_decode_plan); nullptr: computed here
   int early;                   // NQKV_EARLY_START: plan and cache readable before the PDL wait
+  int hpb_shift;               // blk > hd: scale rows [B][H >> hpb_shift][Tc] (blk_shift = log2 hd)
   unsigned long long* trace;   // NQKV_TRACE builds: per-warp globaltimer stamps [grid][NW][16]
 };
 
@@ -209,13 +210,17 @@ __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
 // 18-19 / 20-21 the K / V scale lines (only lines holding bytes of the rows,
 // so every address is inside the cache tensors).  A prefetch is a hint: it
 // never changes what a load returns, so it may run before the PDL wait.
+// The scale rows of the same tokens start at s0 (differs from r0 when a
+// block spans several heads).
 template <int HD, int NBLK, int SB, typename P>
-__device__ __forceinline__ void prefetch_rows_l2(const P& p, int lane, long long r0, long long r1) {
+__device__ __forceinline__ void prefetch_rows_l2(const P& p, int lane, long long r0, long long r1,
+                                                 long long s0) {
   const bool sc = lane >= 18;
   const bool isv = sc ? lane >= 20 : lane >= 9;
   const int li = lane - (sc ? (isv ? 20 : 18) : (isv ? 9 : 0));
   const long long w = sc ? NBLK * SB : HD / 2;
-  const long long f = (r0 * w) >> 7, l = (r1 * w - 1) >> 7;
+  const long long a0 = sc ? s0 : r0, a1 = a0 + (r1 - r0);
+  const long long f = (a0 * w) >> 7, l = (a1 * w - 1) >> 7;
   const unsigned char* base = sc ? reinterpret_cast<const unsigned char*>(isv ? p.vs : p.ks)
                                  : (isv ? p.vc : p.kc);
   if (lane < 22 && f + li <= l) asm volatile("prefetch.global.L2 [%0];" :: "l"(base + ((f + li) << 7)));
@@ -491,11 +496,48 @@ __global__ void __launch_bounds__(1024) decode_plan_kernel(const int32_t* seq_le
 // Out of line (run once per piece by one warp): keeps the kernel's hot code
 // compact in the instruction cache.
 
+// blk > hd: this lane's max |k_new|, max |v_new| over the other (at most 3)
+// heads of head h's group; all loads issued at once (one round trip)
+template <int HD>
+__device__ __forceinline__ float2 group_absmax(const DecodeParams& p, int b, int h) {
+  constexpr int PPL = Geo<HD>::PPL;
+  const int lane = threadIdx.x & 31;
+  const int n = 1 << p.hpb_shift, h0 = h & -n;
+  uint32_t rk[3][PPL], rv[3][PPL];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const int hh = h0 + i + (h0 + i >= h ? 1 : 0);        // the group's heads other than h
+    const long long so = static_cast<long long>(b) * p.new_sb + static_cast<long long>(hh) * p.new_sh;
+#pragma unroll
+    for (int u = 0; u < PPL; ++u) {
+      rk[i][u] = rv[i][u] = 0u;
+      if (i < n - 1) {
+        rk[i][u] = __ldg(reinterpret_cast<const unsigned int*>(p.k_new + so) + lane + 32 * u);
+        rv[i][u] = __ldg(reinterpret_cast<const unsigned int*>(p.v_new + so) + lane + 32 * u);
+      }
+    }
+  }
+  float mk = 0.0f, mv = 0.0f;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+#pragma unroll
+    for (int u = 0; u < PPL; ++u) {
+      __half2 hk, hv;
+      memcpy(&hk, &rk[i][u], 4);
+      memcpy(&hv, &rv[i][u], 4);
+      const float2 fk = __half22float2(__habs2(hk)), fv = __half22float2(__habs2(hv));
+      mk = fmaxf(mk, fmaxf(fk.x, fk.y));
+      mv = fmaxf(mv, fmaxf(fv.x, fv.y));
+    }
+  }
+  return make_float2(mk, mv);
+}
+
 // The appended token of a fused step, warp-wide: lane owns pairs j = lane +
 // 32u (dims 2j, 2j+1).  Quantised exactly as quantize_kernel does, written to
 // the cache row `row` of (b, h); vh gets its dequantised values and the return
 // value is its score (log2 domain) from the q-table in `slot` (slot < 0: 0).
-template <int HD, int NW, bool F16S>
+template <int HD, int NW, bool F16S, bool GRP>
 #ifndef NQKV_NEWTOK_INLINE
 #define NQKV_NEWTOK_INLINE 1          // inlined: c3 -2.7 % (a fused step calls it once per piece)
 #endif
@@ -527,6 +569,14 @@ float new_token_fn(const DecodeParams& p, unsigned char* smem, int b, int h,
     sk[u] = fmaxf(fabsf(fk.x), fabsf(fk.y));
     sv[u] = fmaxf(fabsf(fv.x), fabsf(fv.y));
   }
+  if constexpr (GRP) {                 // blk > hd: the block is the token's slice of the
+    const float2 m = group_absmax<HD>(p, b, h);   // head group: fold in the other heads
+#pragma unroll
+    for (int u = 0; u < PPL; ++u) {
+      sk[u] = fmaxf(sk[u], m.x);
+      sv[u] = fmaxf(sv[u], m.y);
+    }
+  }
   if (bp > 32) {                       // one block spans both halves (hd 128, blk 128)
     sk[0] = sk[PPL - 1] = fmaxf(sk[0], sk[PPL - 1]);
     sv[0] = sv[PPL - 1] = fmaxf(sv[0], sv[PPL - 1]);
@@ -550,8 +600,10 @@ float new_token_fn(const DecodeParams& p, unsigned char* smem, int b, int h,
     const uint32_t cvh = nf4_code_c(__fmul_rn(xv[2 * u + 1], rv), tabc);
     const_cast<uint8_t*>(p.kc)[r * (HD / 2) + j] = static_cast<uint8_t>(ck);
     const_cast<uint8_t*>(p.vc)[r * (HD / 2) + j] = static_cast<uint8_t>(cvl | (cvh << 4));
-    if (((2 * j) & ((1 << p.blk_shift) - 1)) == 0) {
-      const long long si = r * nblk + ((2 * j) >> p.blk_shift);
+    // scale writer: first lane of each block (blk > hd: of the group's first head)
+    if (((2 * j) & ((1 << p.blk_shift) - 1)) == 0 && (!GRP || (h & ((1 << p.hpb_shift) - 1)) == 0)) {
+      const long long si = GRP ? (bh >> p.hpb_shift) * p.Tc + row
+                                       : r * nblk + ((2 * j) >> p.blk_shift);
       if constexpr (F16S) {                   // exact: an absmax of fp16 values
         reinterpret_cast<__half*>(const_cast<void*>(p.ks))[si] = __float2half_rn(sk[u]);
         reinterpret_cast<__half*>(const_cast<void*>(p.vs))[si] = __float2half_rn(sv[u]);
@@ -890,7 +942,8 @@ void merge_fn(const DecodeParams& p, unsigned char* smem, int k, Sched sc,
   if (lane == 0) p.cnt[bh] = 0;
 }
 
-template <int HD, int BLK, int NW, bool F16S>
+// GRP: blk > hd (a block spans 2^hpb_shift heads; instantiated with BLK = HD)
+template <int HD, int BLK, int NW, bool F16S, bool GRP>
 __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constant__ DecodeParams p) {
   constexpr int SB = F16S ? 2 : 4;   // bytes per stored block scale
   using Ge = Geo<HD>;
@@ -1091,7 +1144,7 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
       const int b = bh / p.H, h = bh - b * p.H;
       if (!((s_one[b >> 5] >> (b & 31)) & 1u)) continue;
       float vh[2 * PPL];
-      new_token_fn<HD, NW, F16S>(p, smem, b, h, 0, -1, vh);
+      new_token_fn<HD, NW, F16S, GRP>(p, smem, b, h, 0, -1, vh);
 #pragma unroll
       for (int u = 0; u < PPL; ++u)
         *reinterpret_cast<float2*>(p.out + static_cast<long long>(bh) * HD + 2 * (lane + 32 * u)) =
@@ -1112,6 +1165,11 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
   };
   auto nstages = [&](const Piece& pc) { return (pc.t1 - pc.t0 + ST - 1) / ST; };
   auto rowbase = [&](const Piece& pc) { return (pc.b * p.H + pc.h) * p.Tc; };
+  // scale row base: the head group's row when a block spans heads (blk > hd)
+  auto srowbase = [&](const Piece& pc) {
+    if constexpr (GRP) return ((pc.b * p.H + pc.h) >> p.hpb_shift) * p.Tc;
+    else return rowbase(pc);
+  };
   auto load_quad = [&](const Piece& pc, int qd) -> uint4 {
     const long long bh = static_cast<long long>(pc.b) * p.H + pc.h;
     return __ldg(reinterpret_cast<const uint4*>(p.q + bh * HD) + qd);
@@ -1137,10 +1195,11 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
   // slot i is at the immediate offset i*G rows.  Advanced by NC*ST rows per
   // stage.  (The host guarantees each codes tensor is < 4 GB.)
   uint32_t loff_c = 0, loff_s = 0;
-  auto set_ptrs = [&](int rb, int tok0) {
+  auto set_ptrs = [&](int rb, int srb, int tok0) {
     const uint32_t r = static_cast<uint32_t>(rb + tok0 + g);
     loff_c = r * (HD / 2) + sub * 8;
-    loff_s = (r * NBLK + sidx) * SB;
+    const uint32_t rs = GRP ? static_cast<uint32_t>(srb + tok0 + g) : r;
+    loff_s = (rs * NBLK + sidx) * SB;
   };
   using StageRegs = StageRegsT<RS>;
   auto load_stage = [&](StageRegs& Rg, int rb, int tok0, int t1) {
@@ -1192,7 +1251,7 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
   int ls = warp, lpi = 0, lro = 0;
   bool lvalid = warp < NC, ladv = false;
   int lrb = rowbase(p0);
-  set_ptrs(lrb, p0.t0 + warp * ST);
+  set_ptrs(lrb, srowbase(p0), p0.t0 + warp * ST);
   // register ring: buffer d holds the stage at (tok0 mtok[d], piece end mt1[d],
   // piece index mpi[d]); refilled with the cursor's next stage once consumed
   constexpr int D = NQKV_DEPTH;
@@ -1226,7 +1285,7 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
         ++lpi;
       } while (ls >= nstages(lp));
       lrb = rowbase(lp);
-      set_ptrs(lrb, lp.t0 + ls * ST);
+      set_ptrs(lrb, srowbase(lp), lp.t0 + ls * ST);
     }
     mtok[d] = lp.t0 + ls * ST;
     mt1[d] = lp.t1;
@@ -1236,7 +1295,9 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
     if (PF > 0 && ls + PF * NC < nstages(lp)) {
       const int t = lp.t0 + (ls + PF * NC) * ST;
       prefetch_rows_l2<HD, NBLK, SB>(p, lane, static_cast<long long>(lrb) + t,
-                                 static_cast<long long>(lrb) + min(t + ST, lp.t1));
+                                 static_cast<long long>(lrb) + min(t + ST, lp.t1),
+                                 GRP ? static_cast<long long>((loff_s / SB - sidx) / NBLK) - g + PF * NC * ST
+                                     : static_cast<long long>(lrb) + t);
     }
     return true;
   };
@@ -1263,7 +1324,7 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
         ++lpi;
       } while (ls >= nstages(lp));
       lrb = rowbase(lp);
-      set_ptrs(lrb, lp.t0 + ls * ST);
+      set_ptrs(lrb, srowbase(lp), lp.t0 + ls * ST);
     }
     const int tok0 = lp.t0 + ls * ST, t1 = lp.t1;
     mtok[d] = tok0;
@@ -1287,7 +1348,9 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
     if (PF > 0 && ls + PF * NC < nstages(lp)) {
       const int t = lp.t0 + (ls + PF * NC) * ST;
       prefetch_rows_l2<HD, NBLK, SB>(p, lane, static_cast<long long>(lrb) + t,
-                                 static_cast<long long>(lrb) + min(t + ST, lp.t1));
+                                 static_cast<long long>(lrb) + min(t + ST, lp.t1),
+                                 GRP ? static_cast<long long>((loff_s / SB - sidx) / NBLK) - g + PF * NC * ST
+                                     : static_cast<long long>(lrb) + t);
     }
     return true;
   };
@@ -1414,7 +1477,7 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
       float* st = s_new + (k % R) * (HD + 4);
       if (fused && pc.t1 == pc.len) {
         float vh[2 * PPL];
-        const float sco = new_token_fn<HD, NW, F16S>(p, smem, pc.b, pc.h, min(pc.len, p.Tc - 1), k % R, vh);
+        const float sco = new_token_fn<HD, NW, F16S, GRP>(p, smem, pc.b, pc.h, min(pc.len, p.Tc - 1), k % R, vh);
 #pragma unroll
         for (int u = 0; u < PPL; ++u)
           *reinterpret_cast<float2*>(st + 2 * (lane + 32 * u)) = make_float2(vh[2 * u], vh[2 * u + 1]);

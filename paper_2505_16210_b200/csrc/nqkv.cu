@@ -41,17 +41,22 @@ int cuda_fail(cudaError_t e) {
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
-int blk_shift_of(int blk) { return blk == 32 ? 5 : blk == 64 ? 6 : blk == 128 ? 7 : -1; }
+int blk_shift_of(int blk) {
+  return blk == 32 ? 5 : blk == 64 ? 6 : blk == 128 ? 7 : blk == 256 ? 8 : -1;
+}
 
 int check_geometry(int hd, int blk) {
   if (hd != 64 && hd != 128) return NQKV_ERR_UNSUPPORTED;
-  if (blk & ~(0xff | NQKV_SCALE_F16)) return NQKV_ERR_UNSUPPORTED;
-  blk &= 0xff;
-  if (blk_shift_of(blk) < 0 || blk > hd) return NQKV_ERR_UNSUPPORTED;
+  if (blk & ~(0x1ff | NQKV_SCALE_F16)) return NQKV_ERR_UNSUPPORTED;
+  blk &= 0x1ff;
+  if (blk_shift_of(blk) < 0) return NQKV_ERR_UNSUPPORTED;   // powers of 2: blk | hd or hd | blk
   return NQKV_OK;
 }
 // blk argument -> (block size, scales stored as fp16)
-int blk_of(int blk) { return blk & 0xff; }
+int blk_of(int blk) { return blk & 0x1ff; }
+// blk > hd: a block spans 2^hpb_shift adjacent heads (one scale per head group)
+int hpb_shift_of(int hd, int blk) { return blk > hd ? blk_shift_of(blk) - blk_shift_of(hd) : 0; }
+bool heads_fit(int H, int hd, int blk) { return H % (1 << hpb_shift_of(hd, blk_of(blk))) == 0; }
 bool f16s_of(int blk) { return (blk & NQKV_SCALE_F16) != 0; }
 bool scale_aligned(const void* p, bool f16s) {
   return (reinterpret_cast<uintptr_t>(p) & (f16s ? 1u : 3u)) == 0;
@@ -141,9 +146,9 @@ cudaError_t launch_pdl(void (*kern)(P), dim3 grid, dim3 block, size_t smem, cuda
   return cudaLaunchKernelEx(&cfg, kern, prm);
 }
 
-template <int HD, int BLK, bool F16S>
+template <int HD, int BLK, bool F16S, bool GRP = false>
 int launch_decode_blk(const DecodeParams& p, cudaStream_t st) {
-  auto kern = decode_kernel<HD, BLK, kDecodeWarps, F16S>;
+  auto kern = decode_kernel<HD, BLK, kDecodeWarps, F16S, GRP>;
   const size_t smem = Smem<HD, kDecodeWarps>::kBytes;
   static bool attr_set = false;
   static std::mutex mu;
@@ -165,6 +170,7 @@ int launch_decode_blk(const DecodeParams& p, cudaStream_t st) {
 
 template <int HD, bool F16S>
 int launch_decode(const DecodeParams& p, cudaStream_t st) {
+  if (p.hpb_shift) return launch_decode_blk<HD, HD, F16S, true>(p, st);   // blk > hd
   switch (p.blk_shift) {
     case 5: return launch_decode_blk<HD, 32, F16S>(p, st);
     case 6: return launch_decode_blk<HD, 64, F16S>(p, st);
@@ -197,6 +203,7 @@ int decode_common(const void* q, const uint8_t* k_codes, const void* k_scales,
     return NQKV_ERR_NULL;
   if (int s = check_geometry(hd, blk)) return s;
   if (B < 0 || H < 0 || Tc <= 0 || Tc % 64 || B > kMaxBatch) return NQKV_ERR_SHAPE;
+  if (!heads_fit(H, hd, blk)) return NQKV_ERR_SHAPE;
   if (static_cast<long long>(B) * H * Tc >= (1ll << 31)) return NQKV_ERR_SHAPE;
   if (static_cast<long long>(B) * H * Tc * (hd / 2) >= (1ll << 32)) return NQKV_ERR_SHAPE;  // 32-bit offsets
   const bool f16s = f16s_of(blk);
@@ -223,7 +230,10 @@ int decode_common(const void* q, const uint8_t* k_codes, const void* k_scales,
   p.cnt = reinterpret_cast<int*>(ws + w.cnt);
   p.part = reinterpret_cast<unsigned long long*>(ws + w.part);
   p.B = B; p.H = H; p.Tc = Tc;
-  p.blk_shift = blk_shift_of(blk);
+  // blk > hd: attention sees one scale per (token, head) row, as at blk = hd,
+  // read from the head group's scale row
+  p.blk_shift = blk_shift_of(blk > hd ? hd : blk);
+  p.hpb_shift = hpb_shift_of(hd, blk);
   p.min_tokens = kMinTokensPerCta;
   p.scale_log2 = softmax_scale * 1.4426950408889634f;
   p.lv = make_levels();
@@ -286,6 +296,7 @@ int nqkv_quantize(const void* x, int64_t stride_b, int64_t stride_t, int64_t str
   const bool f16s = f16s_of(blk);
   blk = blk_of(blk);
   if (B < 0 || H < 0 || n_new < 0 || Tc <= 0 || Tc % 64) return NQKV_ERR_SHAPE;
+  if (!heads_fit(H, hd, blk)) return NQKV_ERR_SHAPE;
   if (!aligned16(x) || !aligned16(codes) || !scale_aligned(scales, f16s) ||
       (stride_b % 8) || (stride_t % 8) || (stride_h % 8))
     return NQKV_ERR_ALIGN;
@@ -300,6 +311,7 @@ int nqkv_quantize(const void* x, int64_t stride_b, int64_t stride_t, int64_t str
   p.pos = d_pos; p.codes = codes; p.scales = scales;
   p.B = B; p.n_new = n_new; p.H = H; p.Tc = Tc;
   p.blk_shift = blk_shift_of(blk);
+  p.hpb_shift = hpb_shift_of(hd, blk);
   p.total = static_cast<uint32_t>(chunks);
   p.v256 = ((reinterpret_cast<uintptr_t>(x) & 31u) == 0 && stride_b % 16 == 0 && stride_t % 16 == 0 &&
             stride_h % 16 == 0) ? 1 : 0;
@@ -320,11 +332,14 @@ int nqkv_quantize(const void* x, int64_t stride_b, int64_t stride_t, int64_t str
   auto launch = [&](auto f16s_tag) {
     constexpr bool F = decltype(f16s_tag)::value;
     if (hd == 64)
-      return blk == 32 ? launch_pdl(quantize_kernel<64, 32, F>, grid, dim3(256), sm, st, p)
-                       : launch_pdl(quantize_kernel<64, 64, F>, grid, dim3(256), sm, st, p);
-    return blk == 32   ? launch_pdl(quantize_kernel<128, 32, F>, grid, dim3(256), sm, st, p)
-           : blk == 64 ? launch_pdl(quantize_kernel<128, 64, F>, grid, dim3(256), sm, st, p)
-                       : launch_pdl(quantize_kernel<128, 128, F>, grid, dim3(256), sm, st, p);
+      return blk == 32    ? launch_pdl(quantize_kernel<64, 32, F>, grid, dim3(256), sm, st, p)
+             : blk == 64  ? launch_pdl(quantize_kernel<64, 64, F>, grid, dim3(256), sm, st, p)
+             : blk == 128 ? launch_pdl(quantize_kernel<64, 128, F>, grid, dim3(256), sm, st, p)
+                          : launch_pdl(quantize_kernel<64, 256, F>, grid, dim3(256), sm, st, p);
+    return blk == 32    ? launch_pdl(quantize_kernel<128, 32, F>, grid, dim3(256), sm, st, p)
+           : blk == 64  ? launch_pdl(quantize_kernel<128, 64, F>, grid, dim3(256), sm, st, p)
+           : blk == 128 ? launch_pdl(quantize_kernel<128, 128, F>, grid, dim3(256), sm, st, p)
+                        : launch_pdl(quantize_kernel<128, 256, F>, grid, dim3(256), sm, st, p);
   };
   e = f16s ? launch(std::true_type{}) : launch(std::false_type{});
   return e == cudaSuccess ? NQKV_OK : cuda_fail(e);
@@ -338,6 +353,7 @@ int nqkv_dequantize(const uint8_t* codes, const void* scales, int B, int H, int 
   blk = blk_of(blk);
   if (B < 0 || H < 0 || Tc <= 0 || Tc % 64 || n_tokens < 0 || n_tokens > Tc)
     return NQKV_ERR_SHAPE;
+  if (!heads_fit(H, hd, blk)) return NQKV_ERR_SHAPE;
   if (out_dtype != 0 && out_dtype != 1) return NQKV_ERR_UNSUPPORTED;
   if (!aligned16(codes) || !aligned16(out) || !scale_aligned(scales, f16s))
     return NQKV_ERR_ALIGN;
@@ -348,7 +364,8 @@ int nqkv_dequantize(const uint8_t* codes, const void* scales, int B, int H, int 
   p.codes = codes; p.scales = scales; p.out = out;
   p.total_chunks = total;
   p.Tc = Tc; p.hd = hd; p.n_tokens = n_tokens;
-  p.blk_shift = blk_shift_of(blk);
+  p.blk_shift = blk_shift_of(blk > hd ? hd : blk);
+  p.hpb_shift = hpb_shift_of(hd, blk);
   p.chunks_per_row = hd / 8;
   p.lv = make_levels();
   cudaStream_t st = static_cast<cudaStream_t>(stream);

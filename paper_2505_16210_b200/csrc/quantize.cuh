@@ -13,6 +13,7 @@ struct QuantParams {
   uint8_t* codes;
   void* scales;                  // fp32, or fp16 (template F16S; exact for fp16 inputs)
   int B, n_new, H, Tc, blk_shift;
+  int hpb_shift;                 // blk > hd: a block spans 2^hpb_shift heads
   uint32_t total;                // 16-element chunks: B * n_new * H * hd / 16
   int v256;                      // bit 0: x and strides 32-byte aligned (256-bit loads);
                                  // bit 1: x contiguous [B][n_new][H][hd]
@@ -124,7 +125,9 @@ __global__ void __launch_bounds__(256) quantize_kernel(const __grid_constant__ Q
     const long long rr = (static_cast<long long>(bb) * p.H + h) * p.Tc + pos;
     reinterpret_cast<uint2*>(p.codes + rr * (HD / 2))[cr] = word;
     if (scale_writer) {
-      const long long si = rr * nblk + ((cr * 16) >> p.blk_shift);
+      // blk > hd: one scale per (token, head group): [B][H >> hpb_shift][Tc]
+      const long long si = BLK > HD ? ((static_cast<long long>(bb) * p.H + h) >> p.hpb_shift) * p.Tc + pos
+                                    : rr * nblk + ((cr * 16) >> p.blk_shift);
       if constexpr (F16S)
         reinterpret_cast<__half*>(p.scales)[si] = __float2half_rn(s);   // exact: s is an fp16 value
       else
@@ -177,6 +180,7 @@ struct DequantParams {
   void* out;
   long long total_chunks;   // B*H*n_tokens*hd/8
   int Tc, hd, n_tokens, blk_shift, chunks_per_row;
+  int hpb_shift;            // blk > hd: scales [B][H >> hpb_shift][Tc] (blk_shift = log2 hd)
   Levels lv;
 };
 
@@ -198,7 +202,8 @@ __global__ void __launch_bounds__(256) dequant_kernel(const DequantParams p) {
     const int t = static_cast<int>(tok % p.n_tokens);
     const long long rowid = bh * p.Tc + t;
     const uint32_t w = reinterpret_cast<const uint32_t*>(p.codes + rowid * (p.hd / 2))[cr];
-    const long long si = rowid * (p.hd >> p.blk_shift) + ((cr * 8) >> p.blk_shift);
+    const long long si = p.hpb_shift ? (bh >> p.hpb_shift) * p.Tc + t
+                                     : rowid * (p.hd >> p.blk_shift) + ((cr * 8) >> p.blk_shift);
     const float s = F16S ? __half2float(reinterpret_cast<const __half*>(p.scales)[si])
                          : reinterpret_cast<const float*>(p.scales)[si];
     float v[8];

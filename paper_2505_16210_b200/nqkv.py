@@ -55,7 +55,7 @@ for _name, (_res, _args) in _SIGS.items():
     _f.argtypes = _args
 
 EXPORTED = tuple(_SIGS)
-ABI_VERSION = 1
+ABI_VERSION = 2
 if _lib.nqkv_abi_version() != ABI_VERSION:
     raise ImportError("libnqkv.so ABI version mismatch; rebuild")
 
@@ -110,7 +110,7 @@ def nqkv_decode_counter_bytes(B: int, H: int) -> int:
     return int(_lib.nqkv_decode_counter_bytes(B, H))
 
 
-SCALE_F16 = 0x100   # NQKV_SCALE_F16: block scales stored as fp16 (lossless for fp16 inputs)
+SCALE_F16 = 0x10000   # NQKV_SCALE_F16: block scales stored as fp16 (lossless for fp16 inputs)
 
 
 def _blkarg(blk: int, *scales: torch.Tensor) -> int:
@@ -268,9 +268,19 @@ def make_workspace(B: int, H: int, hd: int, Tc: int, device="cuda") -> torch.Ten
     return torch.zeros(nqkv_decode_workspace_bytes(B, H, hd, Tc), dtype=torch.uint8, device=device)
 
 
+def scales_shape(B: int, H: int, Tc: int, hd: int, blk: int) -> tuple:
+    """[B, H, Tc, hd/blk]; blk > hd (a block spans blk/hd adjacent heads, the
+    paper's blk 256): [B, H*hd/blk, Tc, 1]."""
+    if blk <= hd:
+        return (B, H, Tc, hd // blk)
+    hpb = blk // hd
+    assert H % hpb == 0, "a head shard must hold whole head groups"
+    return (B, H // hpb, Tc, 1)
+
+
 class KVCache:
     """Per-layer packed NF4 K/V cache in the library's layout:
-    codes u8 [B,H,Tc,hd/2], scales f32 [B,H,Tc,hd/blk] for K and for V."""
+    codes u8 [B,H,Tc,hd/2], scales f32 (or f16) scales_shape(...) for K and V."""
 
     def __init__(self, B: int, H: int, hd: int, Tc: int, blk: int = 64, device="cuda",
                  scale_dtype=torch.float32):
@@ -280,7 +290,7 @@ class KVCache:
         self.B, self.H, self.hd, self.Tc, self.blk = B, H, hd, Tc, blk
         self.k_codes = torch.zeros((B, H, Tc, hd // 2), dtype=torch.uint8, device=device)
         self.v_codes = torch.zeros_like(self.k_codes)
-        self.k_scales = torch.zeros((B, H, Tc, hd // blk), dtype=scale_dtype, device=device)
+        self.k_scales = torch.zeros(scales_shape(B, H, Tc, hd, blk), dtype=scale_dtype, device=device)
         self.v_scales = torch.zeros_like(self.k_scales)
 
     def append(self, k: torch.Tensor, v: torch.Tensor, pos: torch.Tensor, stream=None) -> None:

@@ -27,7 +27,7 @@ def test_exports_every_declared_symbol():
     lib = ctypes.CDLL(N._LIB_PATH)
     for name in declared:
         assert hasattr(lib, name)
-    assert lib.nqkv_abi_version() == 1
+    assert lib.nqkv_abi_version() == 2
 
 
 def test_host_levels_and_thresholds_match_oracle_bits():
@@ -51,7 +51,10 @@ def _q(**kw):
 
 def test_quantize_argument_errors():
     assert _q(x=None) == -1 and _q(pos=None) == -1 and _q(codes=None) == -1
-    assert _q(hd=96) == -3 and _q(blk=16) == -3 and _q(blk=128, hd=64) == -3
+    assert _q(hd=96) == -3 and _q(blk=16) == -3 and _q(blk=512) == -3
+    # blk > hd: a block spans blk/hd heads; H must hold whole head groups
+    assert _q(blk=128, hd=64, n=0) == 0 and _q(blk=256, hd=64, n=0) == 0
+    assert _q(blk=256, hd=64, H=6, n=0) == -2 and _q(blk=256, hd=128, H=7, n=0) == -2
     assert _q(Tc=500) == -2 and _q(B=-1) == -2
     assert _q(x=FAKE + 2) == -4 and _q(sh=60) == -4 and _q(codes=FAKE + 8) == -4
     assert _q(B=0) == 0 and _q(n=0) == 0          # nothing to do, nothing launched
@@ -72,6 +75,7 @@ def test_decode_argument_errors():
     assert _d(q=None) == -1 and _d(lens=None) == -1 and _d(ws=None) == -1
     assert _d(hd=256) == -3 and _d(blk=8) == -3
     assert _d(Tc=100) == -2
+    assert _d(blk=256, H=3) == -2                     # 1.5 head groups of 2 heads
     assert _d(q=FAKE + 4) == -4 and _d(out=FAKE + 8) == -4 and _d(ks=FAKE + 2) == -4
     assert _d(ws_bytes=16) == -5
     assert _d(B=0) == 0

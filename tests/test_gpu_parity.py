@@ -41,6 +41,11 @@ def _rand_kv(B, T, H, hd, seed, outlier=True):
     return x
 
 
+def _hpb(hd, blk):
+    """heads per block: blk > hd spans blk/hd adjacent heads (paper's blk 256)"""
+    return blk // hd if blk > hd else 1
+
+
 def _oracle_cache(x, pos, blk, Tc, codes=None, scales=None):
     B, n, H, hd = x.shape
     if codes is None:
@@ -68,17 +73,20 @@ def test_encode_normalized_matches_oracle(N):
 
 
 # ----------------------------------------------------------------- quantize
-@pytest.mark.parametrize("hd,blk", [(64, 32), (64, 64), (128, 32), (128, 64), (128, 128)])
+@pytest.mark.parametrize("hd,blk", [(64, 32), (64, 64), (128, 32), (128, 64), (128, 128),
+                                    (64, 128), (64, 256), (128, 256)])
 def test_quantize_bit_exact(N, hd, blk):
-    B, T, H = 3, 200, 5
+    B, T = 3, 200
+    H = 5 if blk <= hd else 3 * _hpb(hd, blk)
     Tc = 256
     x = _rand_kv(B, T, H, hd, seed=hd + blk)
+    sshape = N.scales_shape(B, H, Tc, hd, blk)
     codes = torch.full((B, H, Tc, hd // 2), 0xAB, dtype=torch.uint8, device=DEV)
-    scales = torch.full((B, H, Tc, hd // blk), -7.0, dtype=torch.float32, device=DEV)
+    scales = torch.full(sshape, -7.0, dtype=torch.float32, device=DEV)
     pos = torch.tensor([0, 17, 56], dtype=torch.int32)
     N.nqkv_quantize(x.to(DEV), pos.to(DEV), codes, scales, blk)
     oc = np.full((B, H, Tc, hd // 2), 0xAB, np.uint8)
-    os_ = np.full((B, H, Tc, hd // blk), -7.0, np.float32)
+    os_ = np.full(sshape, -7.0, np.float32)
     _oracle_cache(x, pos.tolist(), blk, Tc, oc, os_)
     assert np.array_equal(codes.cpu().numpy(), oc)            # incl. untouched bytes
     assert np.array_equal(scales.cpu().numpy(), os_)
@@ -98,6 +106,21 @@ def test_quantize_strided_input_and_zero_blocks(N):
     c = codes.cpu().numpy()
     assert np.array_equal(c, oc) and np.array_equal(scales.cpu().numpy(), os_)
     assert np.all(c[:, 2, 3, :32] == 0x77) and np.all(scales.cpu().numpy()[:, 2, 3, 0] == 0)
+
+
+@pytest.mark.parametrize("hd", [64, 128])
+def test_quantize_strided_head_groups(N, hd):
+    # blk 256 over a strided view (heads not adjacent in memory): the block is
+    # still the token's slice of 256/hd logical heads
+    B, T, H, blk, Tc = 2, 37, 8, 256, 64
+    big = _rand_kv(B, T, H + 2, hd + 32, seed=7 + hd)
+    x = big[:, :, 1:H + 1, 16:16 + hd]
+    codes = torch.zeros((B, H, Tc, hd // 2), dtype=torch.uint8, device=DEV)
+    scales = torch.zeros(N.scales_shape(B, H, Tc, hd, blk), dtype=torch.float32, device=DEV)
+    xd = big.to(DEV)[:, :, 1:H + 1, 16:16 + hd]
+    N.nqkv_quantize(xd, torch.tensor([0, 20], dtype=torch.int32, device=DEV), codes, scales, blk)
+    oc, os_ = _oracle_cache(x.contiguous(), [0, 20], blk, Tc)
+    assert np.array_equal(codes.cpu().numpy(), oc) and np.array_equal(scales.cpu().numpy(), os_)
 
 
 def test_quantize_streaming_equivalence(N):
@@ -184,9 +207,10 @@ def test_fp16_pair_sweep_exhaustive(N):
 
 
 # --------------------------------------------------------------- dequantize
-@pytest.mark.parametrize("hd,blk", [(64, 64), (128, 32), (128, 128)])
+@pytest.mark.parametrize("hd,blk", [(64, 64), (128, 32), (128, 128), (64, 256), (128, 256)])
 def test_dequantize_bit_exact(N, hd, blk):
-    B, T, H, Tc = 2, 130, 3, 192
+    B, T, Tc = 2, 130, 192
+    H = 3 if blk <= hd else 2 * _hpb(hd, blk)
     x = _rand_kv(B, T, H, hd, seed=3)
     oc, os_ = _oracle_cache(x, [0, 0], blk, Tc)
     c, s = torch.from_numpy(oc).to(DEV), torch.from_numpy(os_).to(DEV)
@@ -214,10 +238,12 @@ def _attn_case(N, B, H, hd, blk, lens, Tc, seed, outlier=True, dev_ws=None):
     return out.cpu().numpy(), ref, (q, kc, ks, vc, vs)
 
 
-@pytest.mark.parametrize("hd,blk", [(64, 32), (64, 64), (128, 32), (128, 64), (128, 128)])
+@pytest.mark.parametrize("hd,blk", [(64, 32), (64, 64), (128, 32), (128, 64), (128, 128),
+                                    (64, 128), (64, 256), (128, 256)])
 def test_attention_ragged_lengths(N, hd, blk):
     lens = [0, 1, 63, 64, 65, 127, 128, 129, 300, 511, 512]
-    out, ref, _ = _attn_case(N, len(lens), 3, hd, blk, lens, 512, seed=hd * 7 + blk)
+    H = 3 if blk <= hd else 2 * _hpb(hd, blk)
+    out, ref, _ = _attn_case(N, len(lens), H, hd, blk, lens, 512, seed=hd * 7 + blk)
     err = np.max(np.abs(out.astype(np.float64) - ref))
     assert err <= ATOL, err
     assert np.all(out[0] == 0)                                # empty sequence
@@ -332,13 +358,14 @@ def test_full_size_layer_sampled(N, cfg):
 
 
 # ------------------------------------------------- fused append + attention
-@pytest.mark.parametrize("hd,blk", [(64, 64), (64, 32), (128, 64), (128, 128)])
+@pytest.mark.parametrize("hd,blk", [(64, 64), (64, 32), (128, 64), (128, 128), (64, 256), (128, 256)])
 def test_decode_step_fused_matches_separate_calls(N, hd, blk):
     """nqkv_decode_step == nqkv_quantize(n_new=1) + nqkv_decode_attention:
     identical cache bytes, output within 2e-3 of the oracle, and equal to the
     unfused attention on the updated cache up to fp32 reassociation (the fused
     kernel folds the appended token into the merge; reading R7)."""
-    B, H, Tc = 5, 3, 512
+    B, Tc = 5, 512
+    H = 3 if blk <= hd else 2 * _hpb(hd, blk)
     lens0 = [0, 1, 127, 128, 300]           # cached tokens before the step
     T = max(lens0)
     x = _rand_kv(B, max(T, 1), H, hd, seed=41)
@@ -401,12 +428,13 @@ def test_decode_runner_graph_matches_oracle(N):
 
 
 # ------------------------------------------------------ per-step plan API
-@pytest.mark.parametrize("hd,blk", [(64, 64), (128, 64), (128, 32)])
+@pytest.mark.parametrize("hd,blk", [(64, 64), (128, 64), (128, 32), (128, 256)])
 def test_planned_calls_match_unplanned_bit_exact(N, hd, blk):
     """nqkv_decode_plan + *_planned calls give bit-identical results to the
     unplanned calls (same schedule), for plain and fused steps, with empty,
     single-token and ragged sequences."""
-    B, H, Tc = 6, 5, 1024
+    B, Tc = 6, 1024
+    H = 5 if blk <= hd else 3 * _hpb(hd, blk)
     lens0 = [0, 1, 63, 300, 777, 1000]
     T = max(lens0)
     x = _rand_kv(B, T, H, hd, seed=51)
@@ -507,7 +535,7 @@ def test_planned_large_batch_arrays(N):
         assert np.max(np.abs(o2[b:b + 1].cpu().numpy() - ref)) <= ATOL
 
 
-@pytest.mark.parametrize("seed", range(6))
+@pytest.mark.parametrize("seed", range(10))
 def test_random_geometries_planned_fused(N, seed):
     """Random (B, H, hd, blk, lengths incl. 0, 1 and Tc): unplanned ==
     planned (with and without early start) bit for bit, and the fused step
@@ -517,6 +545,9 @@ def test_random_geometries_planned_fused(N, seed):
     blk = int(rng.choice([32, 64] if hd == 64 else [32, 64, 128]))
     B = int(rng.integers(1, 48))
     H = int(rng.integers(1, 9))
+    if seed >= 6:                       # head-spanning blocks (blk > hd)
+        blk = int(rng.choice([128, 256] if hd == 64 else [256]))
+        H = _hpb(hd, blk) * int(rng.integers(1, 4))
     Tc = 64 * int(rng.integers(1, 12))
     lens0 = rng.integers(0, Tc, B)                              # existing rows (< Tc: one is appended)
     lens0[rng.integers(0, B)] = 0
@@ -551,13 +582,14 @@ def test_random_geometries_planned_fused(N, seed):
         assert np.max(np.abs(f0[b:b + 1].cpu().numpy() - ref)) <= ATOL
 
 
-@pytest.mark.parametrize("hd,blk", [(64, 32), (64, 64), (128, 64), (128, 128)])
+@pytest.mark.parametrize("hd,blk", [(64, 32), (64, 64), (128, 64), (128, 128), (64, 256), (128, 256)])
 def test_fp16_scales_lossless(N, hd, blk):
     """NQKV_SCALE_F16: a block scale is the absmax of fp16
     inputs, itself an fp16 value, so storing it as fp16 changes nothing --
     codes, dequantised values, attention (plain, fused, planned) are bit-for-
     bit those of the fp32-scale layout, and the scales equal the oracle's."""
-    B, H = 5, 3
+    B = 5
+    H = 3 if blk <= hd else 2 * _hpb(hd, blk)
     lens0 = [0, 1, 70, 333, 511]
     T, Tc = max(lens0), 576
     x = _rand_kv(B, T, H, hd, seed=81)
