@@ -201,7 +201,7 @@ def run_ours(args, w, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     group = dist.group.WORLD if world > 1 else None
-    heads = sharding.weak_head_range(rank, w.heads)
+    heads = sharding.weak_head_range(rank, w.heads, max(w.blk // w.head_dim, 1))
     runner = DecodeRunner(w, heads, dev, group=group, world=world)
     peak, peak_src = load_peaks()
 

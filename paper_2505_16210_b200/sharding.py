@@ -13,16 +13,23 @@ import torch
 import torch.distributed as dist
 
 
-def head_range(rank: int, world: int, heads: int) -> range:
-    """Strong scaling: split a fixed head count evenly (heads % world == 0)."""
+def head_range(rank: int, world: int, heads: int, group: int = 1) -> range:
+    """Strong scaling: split a fixed head count evenly (heads % world == 0).
+    group = heads per quantisation block (blk / hd when blk > hd, the paper's
+    blk 256): a shard must hold whole head groups, or a block would straddle
+    two ranks."""
     if heads % world:
         raise ValueError(f"{heads} heads do not shard evenly over {world} ranks")
     per = heads // world
+    if per % group:
+        raise ValueError(f"a {per}-head shard splits {group}-head quantisation blocks")
     return range(rank * per, (rank + 1) * per)
 
 
-def weak_head_range(rank: int, heads_per_rank: int) -> range:
+def weak_head_range(rank: int, heads_per_rank: int, group: int = 1) -> range:
     """Weak scaling: every rank owns a fixed shard; the job has world x shard heads."""
+    if heads_per_rank % group:
+        raise ValueError(f"a {heads_per_rank}-head shard splits {group}-head quantisation blocks")
     return range(rank * heads_per_rank, (rank + 1) * heads_per_rank)
 
 

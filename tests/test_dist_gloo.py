@@ -70,6 +70,12 @@ def test_head_sharded_all_gather_matches_unsharded(tmp_path, mode):
 
 def test_head_range_validation():
     assert list(sharding.head_range(1, 4, 40)) == list(range(10, 20))
+    # blk 256 at hd 128 groups heads in pairs: a 10-head shard is fine, 5 is not
+    assert list(sharding.head_range(1, 4, 40, group=2)) == list(range(10, 20))
+    with pytest.raises(ValueError):
+        sharding.head_range(0, 8, 40, group=2)
+    with pytest.raises(ValueError):
+        sharding.weak_head_range(0, 5, group=4)
     with pytest.raises(ValueError):
         sharding.head_range(0, 3, 40)
     g = torch.arange(2 * 3 * 4 * 5, dtype=torch.float32).reshape(2, 3, 4, 5)
