@@ -2,6 +2,7 @@
 on one layer of each BASELINE config (synthetic, L2 flushed before every
 launch).  Prints achieved algorithmic GB/s.  Development tool, not the bench."""
 import argparse
+import dataclasses
 import os
 import sys
 
@@ -37,11 +38,14 @@ def main():
     ap.add_argument("--heads5", type=int, default=12)
     ap.add_argument("--only", default="", help="attend|step|quantize: run just that once (for ncu)")
     ap.add_argument("--scale16", action="store_true", help="fp16 block scales (NQKV_SCALE_F16)")
+    ap.add_argument("--blk", type=int, default=0, help="override the config's block size (e.g. 256)")
     args = ap.parse_args()
     dev = "cuda"
     flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)
     for name in args.configs.split(","):
         w = W.CONFIGS[name]
+        if args.blk:
+            w = dataclasses.replace(w, blk=args.blk)
         H = args.heads5 if name == "c5" else w.heads
         lens = W.seq_lens(w)
         T = int(lens.max())
