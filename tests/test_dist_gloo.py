@@ -3,6 +3,7 @@
 generator, computes their decode attention (oracle stands in for the CUDA
 kernel, which needs a GPU), and the per-head outputs are all-gathered and
 assembled -- the result must equal the unsharded computation exactly."""
+import dataclasses
 import os
 import socket
 
@@ -17,6 +18,8 @@ from paper_2505_16210_b200 import sharding
 from synth import workloads as W
 
 WORK = W.Workload("dist", 1, 2, 8, 64, 96, 64, 1, None, "2of64")
+# the paper's blk 256 (reading R2b): 4-head groups at hd 64, one group per rank
+WORK256 = dataclasses.replace(WORK, blk=256)
 
 
 def _free_port():
@@ -27,15 +30,15 @@ def _free_port():
     return p
 
 
-def _heads_output(heads):
-    K, V = W.layer_kv(WORK, 0, heads=heads)
-    _, _, q = W.step_inputs(WORK, 0, 0, heads=heads)
+def _heads_output(heads, w=WORK):
+    K, V = W.layer_kv(w, 0, heads=heads)
+    _, _, q = W.step_inputs(w, 0, 0, heads=heads)
     B, T, H, hd = K.shape
-    kc, ks = O.empty_cache(B, H, 128, hd, WORK.blk)
-    vc, vs = O.empty_cache(B, H, 128, hd, WORK.blk)
-    O.quantize_append(K.numpy(), [0] * B, WORK.blk, kc, ks)
-    O.quantize_append(V.numpy(), [0] * B, WORK.blk, vc, vs)
-    return O.decode_attention(q.numpy(), kc, ks, vc, vs, [T] * B, WORK.blk).astype(np.float32)
+    kc, ks = O.empty_cache(B, H, 128, hd, w.blk)
+    vc, vs = O.empty_cache(B, H, 128, hd, w.blk)
+    O.quantize_append(K.numpy(), [0] * B, w.blk, kc, ks)
+    O.quantize_append(V.numpy(), [0] * B, w.blk, vc, vs)
+    return O.decode_attention(q.numpy(), kc, ks, vc, vs, [T] * B, w.blk).astype(np.float32)
 
 
 def _worker(rank, world, port, mode, out_path):
@@ -43,11 +46,13 @@ def _worker(rank, world, port, mode, out_path):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        if mode == "strong":
-            heads = sharding.head_range(rank, world, WORK.heads)
+        w = WORK256 if mode == "strong256" else WORK
+        group = max(w.blk // w.head_dim, 1)
+        if mode in ("strong", "strong256"):
+            heads = sharding.head_range(rank, world, w.heads, group)
         else:
-            heads = sharding.weak_head_range(rank, WORK.heads // world)
-        local = torch.from_numpy(_heads_output(heads))
+            heads = sharding.weak_head_range(rank, w.heads // world, group)
+        local = torch.from_numpy(_heads_output(heads, w))
         gathered = sharding.gather_buffer(local, world)
         sharding.all_gather_heads(local, gathered)
         full = sharding.assemble(gathered, world)
@@ -57,13 +62,14 @@ def _worker(rank, world, port, mode, out_path):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode", ["strong", "weak"])
+@pytest.mark.parametrize("mode", ["strong", "weak", "strong256"])
 def test_head_sharded_all_gather_matches_unsharded(tmp_path, mode):
     world = 2
     out = str(tmp_path / "full.pt")
     mp.spawn(_worker, args=(world, _free_port(), mode, out), nprocs=world, join=True)
     full = torch.load(out).numpy()
-    ref = _heads_output(range(WORK.heads))
+    w = WORK256 if mode == "strong256" else WORK
+    ref = _heads_output(range(w.heads), w)
     assert full.shape == ref.shape
     assert np.array_equal(full, ref)
 

@@ -309,6 +309,27 @@ def test_attention_invariances_bit_exact(N):
         assert np.array_equal(out1, again.cpu().numpy())
 
 
+@pytest.mark.parametrize("hd", [64, 128])
+def test_head_group_shard_matches_unsharded(N, hd):
+    # blk 256 (R2b): a head shard holding whole head groups sees its groups'
+    # scale rows; its output equals the unsharded run's heads (fp32
+    # reassociation only, reading R7) and both match the oracle
+    blk, B = 256, 3
+    hpb = blk // hd
+    H = 3 * hpb
+    lens = [900, 1, 333]
+    out1, ref, (q, kc, ks, vc, vs) = _attn_case(N, B, H, hd, blk, lens, 1024, seed=61 + hd)
+    assert np.max(np.abs(out1 - ref)) <= ATOL
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+    h0, h1 = hpb, 3 * hpb                                     # groups 1 and 2
+    g0, g1 = 1, 3
+    out2 = N.nqkv_decode_attention(q[:, h0:h1].contiguous().to(DEV), t(kc[:, h0:h1]), t(ks[:, g0:g1]),
+                                   t(vc[:, h0:h1]), t(vs[:, g0:g1]),
+                                   torch.tensor(lens, dtype=torch.int32, device=DEV), blk,
+                                   N.make_workspace(B, h1 - h0, hd, 1024, DEV))
+    assert np.max(np.abs(out1[:, h0:h1] - out2.cpu().numpy())) <= 1e-6
+
+
 def test_attention_max_capacity_long(N):
     # c4-like long row (8192 tokens, 128 splits) on a few heads
     B, H, hd, blk, Tc = 1, 2, 128, 64, 8192
