@@ -327,7 +327,8 @@ def test_head_group_shard_matches_unsharded(N, hd):
                                    t(vc[:, h0:h1]), t(vs[:, g0:g1]),
                                    torch.tensor(lens, dtype=torch.int32, device=DEV), blk,
                                    N.make_workspace(B, h1 - h0, hd, 1024, DEV))
-    assert np.max(np.abs(out1[:, h0:h1] - out2.cpu().numpy())) <= 1e-6
+    # different CTA splits sum in a different order: a few fp32 ulps of |out|
+    assert np.allclose(out1[:, h0:h1], out2.cpu().numpy(), rtol=1e-5, atol=1e-6)
 
 
 def test_attention_max_capacity_long(N):
