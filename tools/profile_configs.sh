@@ -8,7 +8,7 @@ O=gpurun_out
 mkdir -p $O
 for c in c3 c4 c5; do
   for k in attend quantize; do
-    CMD="python tools/bench_kernels.py --configs $c --only $k"
+    CMD="python tools/bench_kernels.py --configs $c --only $k ${BLK:+--blk $BLK}"
     kern=$([ $k = attend ] && echo decode_kernel || echo quantize_kernel)
     skip=$([ $k = attend ] && echo 1 || echo 0)
     timeout 300 $CMD > $O/${R}_${c}_${k}_plain.log 2>&1 && \
