@@ -212,6 +212,34 @@ int nqkv_decode_step_planned(const void* k_new, const void* v_new, int64_t new_s
                              float softmax_scale, float* out, void* workspace, size_t ws_bytes,
                              const void* plan, int flags, void* stream);
 
+/* a8 fused into the step: nqkv_decode_step_planned
+ * whose output rows go straight to the all-gathered output of every rank, so
+ * no separate collective runs.  Rank `rank` of G owns heads
+ * [rank*H, (rank+1)*H) of an H_total = G*H head layer (heads
+ * are independent); every output row (b, h) is stored to
+ * d_peer_out[r][(b*H_total + rank*H + h)*hd ..] for r = 0..G-1.
+ * d_peer_out   device array [G] of device pointers: each rank's gathered
+ *              output float [B][H_total][hd] (peer pointers over NVLink P2P /
+ *              symmetric memory; the caller maps them).
+ * d_peer_flags device array [G] of device pointers: each rank's uint32[G]
+ *              flag array.  After all of this launch's output stores
+ *              (system-scope fence), the launch release-stores `epoch`
+ *              (!= 0) into d_peer_flags[r][rank] for every r.  A consumer on
+ *              rank r may read its gathered buffer once flags[0..G-1] all
+ *              equal the epoch (acquire, system scope).  Flags are
+ *              caller-owned; epochs must differ between uses of a buffer.
+ * The workspace's completion counter is zero between calls (reset by the
+ * launch).  G in [1, 64], 0 <= rank < G, H_total == G*H, else NQKV_ERR_SHAPE;
+ * NULL pointers -> NQKV_ERR_NULL.  Other arguments as nqkv_decode_step_planned.
+ * Results are bit-identical to nqkv_decode_step_planned on the same shard. */
+int nqkv_decode_step_gather(const void* k_new, const void* v_new, int64_t new_stride_b,
+                            int64_t new_stride_h, const void* q, uint8_t* k_codes, void* k_scales,
+                            uint8_t* v_codes, void* v_scales, const int32_t* d_seq_lens, int B,
+                            int H, int hd, int blk, int Tc, float softmax_scale,
+                            float* const* d_peer_out, unsigned* const* d_peer_flags, int G, int rank,
+                            int H_total, unsigned epoch, void* workspace, size_t ws_bytes,
+                            const void* plan, int flags, void* stream);
+
 /* Test hook: the kernels' code function on fp32 inputs already normalised
  * to [-1, 1] (values outside are clamped).  d_n device float[count],
  * d_codes device uint8[count]. */

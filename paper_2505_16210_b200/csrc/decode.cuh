@@ -99,7 +99,48 @@ struct DecodeParams {
   int early;                   // NQKV_EARLY_START: plan and cache readable before the PDL wait
   int hpb_shift;               // blk > hd: scale rows [B][H >> hpb_shift][Tc] (blk_shift = log2 hd)
   unsigned long long* trace;   // NQKV_TRACE builds: per-warp globaltimer stamps [grid][NW][16]
+  // fused all-gather epilogue (kernel template GATHER):
+  // every output row goes straight to all gather_g ranks' buffers
+  // [B][h_total][hd] (peer pointers over NVLink P2P), at head offset
+  // gather_rank * H; the last CTA then release-stores `epoch` into slot
+  // gather_rank of every rank's flag array
+  float* const* peer_out;
+  unsigned* const* peer_flags;
+  unsigned* gctr;              // CTA completion counter (zero between launches)
+  int gather_g, gather_rank, h_total;
+  unsigned epoch;
 };
+
+// one output float2 of row (b, h), dims d, d+1: local, or to every rank's
+// gathered buffer (GATHER)
+template <bool GATHER, int HD>
+__device__ __forceinline__ void store_out2(const DecodeParams& p, long long bh, int b, int h, int d,
+                                           float2 v) {
+  if constexpr (GATHER) {
+    const long long row = static_cast<long long>(b) * p.h_total + p.gather_rank * p.H + h;
+    for (int r = 0; r < p.gather_g; ++r)
+      *reinterpret_cast<float2*>(p.peer_out[r] + row * HD + d) = v;
+  } else {
+    (void)b; (void)h;
+    *reinterpret_cast<float2*>(p.out + bh * HD + d) = v;
+  }
+}
+
+// GATHER: this CTA's output stores are complete.  System-scope fence, then
+// count; the last CTA of the launch resets the counter and publishes the
+// epoch to every rank (release, system scope).
+__device__ __forceinline__ void gather_cta_done(const DecodeParams& p) {
+  __threadfence_system();
+  const unsigned old = atomicAdd(p.gctr, 1u);
+  if (old == gridDim.x - 1) {
+    *p.gctr = 0u;
+    __threadfence_system();
+    for (int r = 0; r < p.gather_g; ++r) {
+      unsigned* f = p.peer_flags[r] + p.gather_rank;
+      asm volatile("st.release.sys.global.u32 [%0], %1;" :: "l"(f), "r"(p.epoch) : "memory");
+    }
+  }
+}
 
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -755,7 +796,7 @@ void peek_fn(const DecodeParams& p, unsigned char* smem, int k, Sched sc, int ct
 // Merge piece k's NC consumer states (ring slot k % R) and, in a fused step,
 // the appended token's state: write the output, or a partial (+ the
 // last-arriver merge of the sequence's partials across CTAs).
-template <int HD, int NW>
+template <int HD, int NW, bool GATHER>
 #ifndef NQKV_MERGE_INLINE
 #define NQKV_MERGE_INLINE 1          // inlined: a call to cold code at the kernel's end costs ~1 %
 #endif
@@ -819,7 +860,7 @@ void merge_fn(const DecodeParams& p, unsigned char* smem, int k, Sched sc,
     const float inv = 1.0f / den;
 #pragma unroll
     for (int u = 0; u < PPL; ++u)
-      *reinterpret_cast<float2*>(p.out + bh * HD + dim(u)) = make_float2(acc[2 * u] * inv, acc[2 * u + 1] * inv);
+      store_out2<GATHER, HD>(p, bh, pc.b, pc.h, dim(u), make_float2(acc[2 * u] * inv, acc[2 * u + 1] * inv));
     return;
   }
   // Partial piece.  Record slot 0 = this CTA's first piece (starts at g0),
@@ -938,12 +979,12 @@ void merge_fn(const DecodeParams& p, unsigned char* smem, int k, Sched sc,
   const float inv = 1.0f / dsum;
 #pragma unroll
   for (int u = 0; u < PPL; ++u)
-    *reinterpret_cast<float2*>(p.out + bh * HD + dim(u)) = make_float2(o[2 * u] * inv, o[2 * u + 1] * inv);
+    store_out2<GATHER, HD>(p, bh, pc.b, pc.h, dim(u), make_float2(o[2 * u] * inv, o[2 * u + 1] * inv));
   if (lane == 0) p.cnt[bh] = 0;
 }
 
 // GRP: blk > hd (a block spans 2^hpb_shift heads; instantiated with BLK = HD)
-template <int HD, int BLK, int NW, bool F16S, bool GRP>
+template <int HD, int BLK, int NW, bool F16S, bool GRP, bool GATHER>
 __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constant__ DecodeParams p) {
   constexpr int SB = F16S ? 2 : 4;   // bytes per stored block scale
   using Ge = Geo<HD>;
@@ -1137,7 +1178,15 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
   auto empties = [&](int wid, int nwarps) {
     for (int i = wid * 32 + lane; i < p.B * p.H * HD; i += nwarps * 32) {
       const int b = i / (p.H * HD);
-      if (s_len[b] == 0 && !((s_one[b >> 5] >> (b & 31)) & 1u)) p.out[i] = 0.0f;
+      if (s_len[b] == 0 && !((s_one[b >> 5] >> (b & 31)) & 1u)) {
+        if constexpr (GATHER) {
+          const int bh = i / HD, h = bh - b * p.H;
+          const long long row = static_cast<long long>(b) * p.h_total + p.gather_rank * p.H + h;
+          for (int r = 0; r < p.gather_g; ++r) p.peer_out[r][row * HD + (i - bh * HD)] = 0.0f;
+        } else {
+          p.out[i] = 0.0f;
+        }
+      }
     }
     if (!fused) return;
     for (int bh = wid; bh < p.B * p.H; bh += nwarps) {
@@ -1147,13 +1196,17 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
       new_token_fn<HD, NW, F16S, GRP>(p, smem, b, h, 0, -1, vh);
 #pragma unroll
       for (int u = 0; u < PPL; ++u)
-        *reinterpret_cast<float2*>(p.out + static_cast<long long>(bh) * HD + 2 * (lane + 32 * u)) =
-            make_float2(vh[2 * u], vh[2 * u + 1]);
+        store_out2<GATHER, HD>(p, static_cast<long long>(bh), b, h, 2 * (lane + 32 * u),
+                               make_float2(vh[2 * u], vh[2 * u + 1]));
     }
   };
   if (sc.N == 0 || cta >= sc.C) {
     if (pre) pdl_enter();                     // empties read k_new / write out
     if (sc.N == 0) empties(blockIdx.x * NW + warp, gridDim.x * NW);
+    if constexpr (GATHER) {
+      __syncthreads();
+      if (tid == 0) gather_cta_done(p);
+    }
     return;
   }
   TRACE(13);
@@ -1506,7 +1559,7 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
       if (more) qn = load_quad(nx, lane % Q);
       if (k >= R) {
         mbar_wait(mb_done + 8 * ((k - R) % R), ((k - R) / R) & 1);
-        merge_fn<HD, NW>(p, smem, k - R, sc, cta, g0);
+        merge_fn<HD, NW, GATHER>(p, smem, k - R, sc, cta, g0);
       }
       if (k >= R0) build_fn<HD, NW>(smem, k % R, qc, p.scale_log2);
       __syncwarp();
@@ -1523,7 +1576,11 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
         peek_fn<HD, NW>(p, smem, k, sc, cta);
       mbar_wait(mb_done + 8 * (j % R), (j / R) & 1);
       if (j == k) TRACE(11);
-      merge_fn<HD, NW>(p, smem, j, sc, cta, g0);
+      merge_fn<HD, NW, GATHER>(p, smem, j, sc, cta, g0);
+    }
+    if constexpr (GATHER) {    // every output of this CTA was stored by this warp
+      __syncwarp();
+      if (lane == 0) gather_cta_done(p);
     }
     TRACE(10);
     return;

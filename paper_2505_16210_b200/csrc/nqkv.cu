@@ -146,9 +146,9 @@ cudaError_t launch_pdl(void (*kern)(P), dim3 grid, dim3 block, size_t smem, cuda
   return cudaLaunchKernelEx(&cfg, kern, prm);
 }
 
-template <int HD, int BLK, bool F16S, bool GRP = false>
+template <int HD, int BLK, bool F16S, bool GRP, bool GATHER>
 int launch_decode_blk(const DecodeParams& p, cudaStream_t st) {
-  auto kern = decode_kernel<HD, BLK, kDecodeWarps, F16S, GRP>;
+  auto kern = decode_kernel<HD, BLK, kDecodeWarps, F16S, GRP, GATHER>;
   const size_t smem = Smem<HD, kDecodeWarps>::kBytes;
   static bool attr_set = false;
   static std::mutex mu;
@@ -168,14 +168,19 @@ int launch_decode_blk(const DecodeParams& p, cudaStream_t st) {
   return e == cudaSuccess ? NQKV_OK : cuda_fail(e);
 }
 
+template <int HD, bool F16S, bool GATHER>
+int launch_decode_g(const DecodeParams& p, cudaStream_t st) {
+  if (p.hpb_shift) return launch_decode_blk<HD, HD, F16S, true, GATHER>(p, st);   // blk > hd
+  switch (p.blk_shift) {
+    case 5: return launch_decode_blk<HD, 32, F16S, false, GATHER>(p, st);
+    case 6: return launch_decode_blk<HD, 64, F16S, false, GATHER>(p, st);
+    default: return HD == 128 ? launch_decode_blk<HD, 128, F16S, false, GATHER>(p, st) : NQKV_ERR_UNSUPPORTED;
+  }
+}
+
 template <int HD, bool F16S>
 int launch_decode(const DecodeParams& p, cudaStream_t st) {
-  if (p.hpb_shift) return launch_decode_blk<HD, HD, F16S, true>(p, st);   // blk > hd
-  switch (p.blk_shift) {
-    case 5: return launch_decode_blk<HD, 32, F16S>(p, st);
-    case 6: return launch_decode_blk<HD, 64, F16S>(p, st);
-    default: return HD == 128 ? launch_decode_blk<HD, 128, F16S>(p, st) : NQKV_ERR_UNSUPPORTED;
-  }
+  return p.peer_out ? launch_decode_g<HD, F16S, true>(p, st) : launch_decode_g<HD, F16S, false>(p, st);
 }
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
@@ -183,23 +188,33 @@ size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 // workspace: [B*H] int arrival counters (zero between launches) | partials
 // [kMaxGrid][2][hd + 2] fp32
 struct WsLayout {
-  size_t cnt, part, total;
+  size_t cnt, part, gctr, total;
 };
 
 WsLayout ws_layout(long long B, long long H, int hd) {
   WsLayout w;
   w.cnt = 0;
   w.part = align_up(static_cast<size_t>(B * H) * sizeof(int), 256);
-  w.total = align_up(w.part + static_cast<size_t>(kMaxGrid) * 2 * (hd + 2) * sizeof(unsigned long long), 256);
+  w.gctr = align_up(w.part + static_cast<size_t>(kMaxGrid) * 2 * (hd + 2) * sizeof(unsigned long long), 256);
+  w.total = w.gctr + 256;       // [0]: gather CTA-completion counter (zero between calls)
   return w;
 }
+
+// fused all-gather epilogue arguments (nqkv_decode_step_gather)
+struct GatherArgs {
+  float* const* peer_out;
+  unsigned* const* peer_flags;
+  int G, rank, H_total;
+  unsigned epoch;
+};
 
 int decode_common(const void* q, const uint8_t* k_codes, const void* k_scales,
                   const uint8_t* v_codes, const void* v_scales, const int32_t* d_seq_lens,
                   const void* k_new, const void* v_new, int64_t new_sb, int64_t new_sh, int B,
                   int H, int hd, int blk, int Tc, float softmax_scale, float* out, void* workspace,
-                  size_t ws_bytes, const void* plan, int flags, cudaStream_t st) {
-  if (!q || !k_codes || !k_scales || !v_codes || !v_scales || !d_seq_lens || !out)
+                  size_t ws_bytes, const void* plan, int flags, cudaStream_t st,
+                  const GatherArgs* ga = nullptr) {
+  if (!q || !k_codes || !k_scales || !v_codes || !v_scales || !d_seq_lens || (!out && !ga))
     return NQKV_ERR_NULL;
   if (int s = check_geometry(hd, blk)) return s;
   if (B < 0 || H < 0 || Tc <= 0 || Tc % 64 || B > kMaxBatch) return NQKV_ERR_SHAPE;
@@ -208,7 +223,7 @@ int decode_common(const void* q, const uint8_t* k_codes, const void* k_scales,
   if (static_cast<long long>(B) * H * Tc * (hd / 2) >= (1ll << 32)) return NQKV_ERR_SHAPE;  // 32-bit offsets
   const bool f16s = f16s_of(blk);
   blk = blk_of(blk);
-  if (!aligned16(q) || !aligned16(k_codes) || !aligned16(v_codes) || !aligned16(out) ||
+  if (!aligned16(q) || !aligned16(k_codes) || !aligned16(v_codes) || (out && !aligned16(out)) ||
       !aligned16(k_scales) || !aligned16(v_scales))
     return NQKV_ERR_ALIGN;
   if (k_new && (!aligned16(k_new) || !aligned16(v_new) || (new_sb % 8) || (new_sh % 8)))
@@ -241,6 +256,13 @@ int decode_common(const void* q, const uint8_t* k_codes, const void* k_scales,
   p.plan = static_cast<const int*>(plan);
   p.early = plan && (flags & NQKV_EARLY_START) ? 1 : 0;
   p.trace = nullptr;
+  p.peer_out = ga ? ga->peer_out : nullptr;
+  p.peer_flags = ga ? ga->peer_flags : nullptr;
+  p.gctr = reinterpret_cast<unsigned*>(ws + w.gctr);
+  p.gather_g = ga ? ga->G : 1;
+  p.gather_rank = ga ? ga->rank : 0;
+  p.h_total = ga ? ga->H_total : H;
+  p.epoch = ga ? ga->epoch : 0u;
 #ifdef NQKV_TRACE
   if (const char* t = std::getenv("NQKV_TRACE_PTR"))
     p.trace = reinterpret_cast<unsigned long long*>(std::strtoull(t, nullptr, 0));
@@ -447,6 +469,22 @@ int nqkv_decode_step_planned(const void* k_new, const void* v_new, int64_t new_s
   return decode_common(q, k_codes, k_scales, v_codes, v_scales, d_seq_lens, k_new, v_new,
                        new_stride_b, new_stride_h, B, H, hd, blk, Tc, softmax_scale, out,
                        workspace, ws_bytes, plan, flags, static_cast<cudaStream_t>(stream));
+}
+
+int nqkv_decode_step_gather(const void* k_new, const void* v_new, int64_t new_stride_b,
+                            int64_t new_stride_h, const void* q, uint8_t* k_codes, void* k_scales,
+                            uint8_t* v_codes, void* v_scales, const int32_t* d_seq_lens, int B,
+                            int H, int hd, int blk, int Tc, float softmax_scale,
+                            float* const* d_peer_out, unsigned* const* d_peer_flags, int G, int rank,
+                            int H_total, unsigned epoch, void* workspace, size_t ws_bytes,
+                            const void* plan, int flags, void* stream) {
+  if (!k_new || !v_new || !plan || !d_peer_out || !d_peer_flags) return NQKV_ERR_NULL;
+  if (G < 1 || G > 64 || rank < 0 || rank >= G || epoch == 0u) return NQKV_ERR_SHAPE;
+  if (H_total != static_cast<long long>(G) * H) return NQKV_ERR_SHAPE;
+  GatherArgs ga{d_peer_out, d_peer_flags, G, rank, H_total, epoch};
+  return decode_common(q, k_codes, k_scales, v_codes, v_scales, d_seq_lens, k_new, v_new,
+                       new_stride_b, new_stride_h, B, H, hd, blk, Tc, softmax_scale, nullptr,
+                       workspace, ws_bytes, plan, flags, static_cast<cudaStream_t>(stream), &ga);
 }
 
 int nqkv_encode_normalized(const float* d_n, int64_t count, uint8_t* d_codes, void* stream) {

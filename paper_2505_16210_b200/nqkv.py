@@ -48,6 +48,9 @@ _SIGS = {
     "nqkv_decode_step_planned": (_i32, [_vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _i32,
                                         _i32, _i32, _i32, _i32, ctypes.c_float, _vp, _vp, _sz,
                                         _vp, _i32, _vp]),
+    "nqkv_decode_step_gather": (_i32, [_vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _i32,
+                                       _i32, _i32, _i32, _i32, ctypes.c_float, _vp, _vp, _i32,
+                                       _i32, _i32, ctypes.c_uint, _vp, _sz, _vp, _i32, _vp]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -253,6 +256,32 @@ def nqkv_decode_step_planned(k_new, v_new, q, k_codes, k_scales, v_codes, v_scal
         float(softmax_scale), _ptr(out), _ptr(workspace), workspace.numel() * workspace.element_size(),
         _ptr(plan), int(flags), _stream(stream)), "nqkv_decode_step_planned")
     return out
+
+
+def nqkv_decode_step_gather(k_new, v_new, q, k_codes, k_scales, v_codes, v_scales, seq_lens, blk,
+                            workspace, plan, peer_out_ptrs: torch.Tensor, peer_flag_ptrs: torch.Tensor,
+                            G: int, rank: int, epoch: int, softmax_scale=None, stream=None, flags=0):
+    """nqkv_decode_step_planned with the all-gather fused into the epilogue:
+    output rows go to every rank's [B, G*H, hd] buffer (peer_out_ptrs: int64
+    device tensor [G] of their addresses), then epoch is release-stored into
+    flags[rank] of every rank (peer_flag_ptrs: int64 device tensor [G] of
+    uint32[G] flag arrays)."""
+    B, H, hd = q.shape
+    Tc = k_codes.shape[2]
+    if softmax_scale is None:
+        softmax_scale = 1.0 / math.sqrt(hd)
+    assert k_new.shape == (B, H, hd) and v_new.shape == (B, H, hd)
+    assert k_new.stride() == v_new.stride() and k_new.stride(2) == 1
+    assert q.dtype == torch.float16 and q.is_contiguous()
+    assert peer_out_ptrs.dtype == torch.int64 and peer_flag_ptrs.dtype == torch.int64
+    assert peer_out_ptrs.numel() == G and peer_flag_ptrs.numel() == G
+    _check(_lib.nqkv_decode_step_gather(
+        _ptr(k_new), _ptr(v_new), k_new.stride(0), k_new.stride(1), _ptr(q), _ptr(k_codes),
+        _ptr(k_scales), _ptr(v_codes), _ptr(v_scales), _ptr(seq_lens), B, H, hd,
+        _blkarg(blk, k_scales, v_scales), Tc, float(softmax_scale), _ptr(peer_out_ptrs),
+        _ptr(peer_flag_ptrs), int(G), int(rank), int(G * H), int(epoch), _ptr(workspace),
+        workspace.numel() * workspace.element_size(), _ptr(plan), int(flags), _stream(stream)),
+        "nqkv_decode_step_gather")
 
 
 def nqkv_encode_normalized(n: torch.Tensor, stream=None) -> torch.Tensor:

@@ -148,3 +148,22 @@ def test_scale_f16_flag_validation():
     assert _q(blk=64 | f16, scales=FAKE + 2, n=0) == 0             # fp16 scales: 2-byte alignment suffices
     assert _q(blk=64, scales=FAKE + 2, n=0) == -4                  # fp32 scales need 4
     assert _q(blk=64 | f16, scales=FAKE + 1, n=0) == -4
+
+
+def test_decode_gather_argument_errors():
+    f = N._lib.nqkv_decode_step_gather
+    ws = N.nqkv_decode_workspace_bytes(2, 4, 128, 256)
+    base = [FAKE, FAKE, 4 * 128, 128, FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, 2, 4, 128, 64, 256, 0.088,
+            FAKE, FAKE, 2, 0, 8, 1, FAKE, ws, FAKE, 0, None]
+    a = list(base); a[16] = None                     # peer output array
+    assert f(*a) == -1
+    a = list(base); a[24] = None                     # plan
+    assert f(*a) == -1
+    a = list(base); a[19] = 2                        # rank >= G
+    assert f(*a) == -2
+    a = list(base); a[20] = 12                       # H_total != G * H
+    assert f(*a) == -2
+    a = list(base); a[21] = 0                        # epoch 0 is reserved
+    assert f(*a) == -2
+    a = list(base); a[12] = 96
+    assert f(*a) == -3

@@ -675,3 +675,55 @@ def test_uniform_small_batch_one_cta_per_sequence(N, hd):
     assert int(plan[4:8].view(torch.int32)[0]) == B * H          # header: C = #sequences
     ref = O.decode_attention(q.cpu().numpy(), kc, ks, vc, vs, [T] * B, blk)
     assert np.max(np.abs(o1.cpu().numpy() - ref)) <= ATOL
+
+
+@pytest.mark.parametrize("hd,blk,G", [(64, 64, 2), (128, 64, 3), (128, 256, 2)])
+def test_fused_gather_simulated_ranks(N, hd, blk, G):
+    """nqkv_decode_step_gather (all-gather fused into the epilogue, SURVEY
+    8(f) row 3) with G ranks simulated on one GPU: the peers' buffers are
+    local, and each rank's launch completes before the next starts (no launch
+    waits on another).  Every rank's buffer must hold every shard's rows,
+    bit-identical to nqkv_decode_step_planned on that shard; each flag holds
+    the epoch; the caches equal the unfused step's; the workspace is zero."""
+    hpb = _hpb(hd, blk)
+    B, Hl, Tc = 4, 2 * hpb, 1024
+    Ht = G * Hl
+    lens0 = [0, 1, 300, 700]
+    x = _rand_kv(B, max(lens0), Ht, hd, seed=71)
+    y = _rand_kv(B, max(lens0), Ht, hd, seed=72, outlier=False)
+    kn = _rand_kv(B, 1, Ht, hd, seed=73)[:, 0].to(DEV)
+    vn = _rand_kv(B, 1, Ht, hd, seed=74, outlier=False)[:, 0].to(DEV)
+    q = torch.randn(B, Ht, hd, generator=torch.Generator().manual_seed(75)).to(torch.float16).to(DEV)
+    kc, ks = _oracle_cache(x, [0] * B, blk, Tc)
+    vc, vs = _oracle_cache(y, [0] * B, blk, Tc)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+    L1 = torch.tensor([n + 1 for n in lens0], dtype=torch.int32, device=DEV)
+    bufs = [torch.full((B, Ht, hd), float("nan"), device=DEV) for _ in range(G)]
+    flags = [torch.zeros(G, dtype=torch.int32, device=DEV) for _ in range(G)]
+    out_ptrs = torch.tensor([b.data_ptr() for b in bufs], dtype=torch.int64, device=DEV)
+    flag_ptrs = torch.tensor([f.data_ptr() for f in flags], dtype=torch.int64, device=DEV)
+    plan = N.make_plan(DEV)
+    N.nqkv_decode_plan(L1, Hl, Tc, True, plan, hd=hd)
+    refs = []
+    for r in range(G):
+        hs, gs = slice(r * Hl, (r + 1) * Hl), slice(r * Hl // hpb, (r + 1) * Hl // hpb)
+        shard = lambda c, s_: [t(c[:, hs]), t(s_[:, gs])]
+        a = shard(kc, ks) + shard(vc, vs)
+        b = shard(kc, ks) + shard(vc, vs)
+        ws = N.make_workspace(B, Hl, hd, Tc, DEV)
+        N.nqkv_decode_step_gather(kn[:, hs], vn[:, hs], q[:, hs].contiguous(), a[0], a[1], a[2], a[3], L1,
+                                  blk, ws, plan, out_ptrs, flag_ptrs, G, r, epoch=7)
+        o = N.nqkv_decode_step_planned(kn[:, hs], vn[:, hs], q[:, hs].contiguous(), b[0], b[1], b[2], b[3],
+                                       L1, blk, N.make_workspace(B, Hl, hd, Tc, DEV), plan)
+        torch.cuda.synchronize()
+        assert all(torch.equal(u, v) for u, v in zip(a, b))
+        assert torch.count_nonzero(ws) == 0
+        refs.append(o)
+    full = torch.cat(refs, dim=1)
+    for r in range(G):
+        assert torch.equal(bufs[r], full)
+        assert flags[r].tolist() == [7] * G
+    O.quantize_append(kn.unsqueeze(1).cpu().numpy(), lens0, blk, kc, ks)
+    O.quantize_append(vn.unsqueeze(1).cpu().numpy(), lens0, blk, vc, vs)
+    ref = O.decode_attention(q.cpu().numpy(), kc, ks, vc, vs, [n + 1 for n in lens0], blk)
+    assert np.max(np.abs(bufs[0].cpu().numpy() - ref)) <= ATOL
