@@ -224,7 +224,8 @@ int nqkv_decode_step_planned(const void* k_new, const void* v_new, int64_t new_s
  * d_peer_flags device array [G] of device pointers: each rank's uint32[G]
  *              flag array.  After all of this launch's output stores
  *              (system-scope fence), the launch release-stores `epoch`
- *              (!= 0) into d_peer_flags[r][rank] for every r.  A consumer on
+ *              (!= 0; or *d_epoch when d_epoch is not NULL) into
+ *              d_peer_flags[r][rank] for every r.  A consumer on
  *              rank r may read its gathered buffer once flags[0..G-1] all
  *              equal the epoch (acquire, system scope).  Flags are
  *              caller-owned; epochs must differ between uses of a buffer.
@@ -237,8 +238,19 @@ int nqkv_decode_step_gather(const void* k_new, const void* v_new, int64_t new_st
                             uint8_t* v_codes, void* v_scales, const int32_t* d_seq_lens, int B,
                             int H, int hd, int blk, int Tc, float softmax_scale,
                             float* const* d_peer_out, unsigned* const* d_peer_flags, int G, int rank,
-                            int H_total, unsigned epoch, void* workspace, size_t ws_bytes,
-                            const void* plan, int flags, void* stream);
+                            int H_total, unsigned epoch, const unsigned* d_epoch, void* workspace,
+                            size_t ws_bytes, const void* plan, int flags, void* stream);
+
+/* Helpers for the fused gather under CUDA-graph replay, where a launch's
+ * `epoch` argument is frozen: pass d_epoch (device uint32, read at the end
+ * of the launch instead of `epoch`) and bump it once per step.
+ * nqkv_gather_epoch_bump: *d_epoch += 1 (stream-ordered).
+ * nqkv_gather_wait: stream-ordered wait until d_flags[0..n) (this rank's
+ *   flag arrays, device) all equal *d_epoch, with system-scope acquire loads;
+ *   kernels after it on the stream may read the gathered buffers.  It spins
+ *   on the device: every rank must issue its gather launches for the epoch. */
+int nqkv_gather_epoch_bump(unsigned* d_epoch, void* stream);
+int nqkv_gather_wait(const unsigned* d_flags, int n, const unsigned* d_epoch, void* stream);
 
 /* Test hook: the kernels' code function on fp32 inputs already normalised
  * to [-1, 1] (values outside are clamped).  d_n device float[count],

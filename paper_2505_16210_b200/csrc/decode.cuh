@@ -109,6 +109,7 @@ struct DecodeParams {
   unsigned* gctr;              // CTA completion counter (zero between launches)
   int gather_g, gather_rank, h_total;
   unsigned epoch;
+  const unsigned* epoch_ptr;   // non-null: the epoch is read here (graph replays bump it)
 };
 
 // one output float2 of row (b, h), dims d, d+1: local, or to every rank's
@@ -135,9 +136,10 @@ __device__ __forceinline__ void gather_cta_done(const DecodeParams& p) {
   if (old == gridDim.x - 1) {
     *p.gctr = 0u;
     __threadfence_system();
+    const unsigned e = p.epoch_ptr ? *p.epoch_ptr : p.epoch;
     for (int r = 0; r < p.gather_g; ++r) {
       unsigned* f = p.peer_flags[r] + p.gather_rank;
-      asm volatile("st.release.sys.global.u32 [%0], %1;" :: "l"(f), "r"(p.epoch) : "memory");
+      asm volatile("st.release.sys.global.u32 [%0], %1;" :: "l"(f), "r"(e) : "memory");
     }
   }
 }
@@ -1845,6 +1847,26 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
 #ifdef NQKV_TRACE
   if (p.trace && lane == 0) p.trace[(blockIdx.x * NW + warp) * 16 + 15] = waited + 1;
 #endif
+}
+
+// ----------------------------------------------- fused all-gather helpers
+// epoch += 1 (one thread; stream-ordered before the step's gather launches)
+__global__ void gather_epoch_bump_kernel(unsigned* epoch) {
+  pdl_enter();
+  *epoch += 1u;
+}
+// wait until flags[0..n) all equal *epoch (acquire, system scope): the
+// gathered buffer this rank reads is then complete
+__global__ void gather_wait_kernel(const unsigned* flags, int n, const unsigned* epoch) {
+  pdl_enter();
+  const unsigned e = *epoch;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + i) : "memory");
+    } while (v != e);
+  }
+  __syncthreads();
 }
 
 }  // namespace nqkv

@@ -206,6 +206,7 @@ struct GatherArgs {
   unsigned* const* peer_flags;
   int G, rank, H_total;
   unsigned epoch;
+  const unsigned* epoch_ptr;
 };
 
 int decode_common(const void* q, const uint8_t* k_codes, const void* k_scales,
@@ -263,6 +264,7 @@ int decode_common(const void* q, const uint8_t* k_codes, const void* k_scales,
   p.gather_rank = ga ? ga->rank : 0;
   p.h_total = ga ? ga->H_total : H;
   p.epoch = ga ? ga->epoch : 0u;
+  p.epoch_ptr = ga ? ga->epoch_ptr : nullptr;
 #ifdef NQKV_TRACE
   if (const char* t = std::getenv("NQKV_TRACE_PTR"))
     p.trace = reinterpret_cast<unsigned long long*>(std::strtoull(t, nullptr, 0));
@@ -476,15 +478,31 @@ int nqkv_decode_step_gather(const void* k_new, const void* v_new, int64_t new_st
                             uint8_t* v_codes, void* v_scales, const int32_t* d_seq_lens, int B,
                             int H, int hd, int blk, int Tc, float softmax_scale,
                             float* const* d_peer_out, unsigned* const* d_peer_flags, int G, int rank,
-                            int H_total, unsigned epoch, void* workspace, size_t ws_bytes,
-                            const void* plan, int flags, void* stream) {
+                            int H_total, unsigned epoch, const unsigned* d_epoch, void* workspace,
+                            size_t ws_bytes, const void* plan, int flags, void* stream) {
   if (!k_new || !v_new || !plan || !d_peer_out || !d_peer_flags) return NQKV_ERR_NULL;
-  if (G < 1 || G > 64 || rank < 0 || rank >= G || epoch == 0u) return NQKV_ERR_SHAPE;
+  if (G < 1 || G > 64 || rank < 0 || rank >= G || (epoch == 0u && !d_epoch)) return NQKV_ERR_SHAPE;
   if (H_total != static_cast<long long>(G) * H) return NQKV_ERR_SHAPE;
-  GatherArgs ga{d_peer_out, d_peer_flags, G, rank, H_total, epoch};
+  GatherArgs ga{d_peer_out, d_peer_flags, G, rank, H_total, epoch, d_epoch};
   return decode_common(q, k_codes, k_scales, v_codes, v_scales, d_seq_lens, k_new, v_new,
                        new_stride_b, new_stride_h, B, H, hd, blk, Tc, softmax_scale, nullptr,
                        workspace, ws_bytes, plan, flags, static_cast<cudaStream_t>(stream), &ga);
+}
+
+int nqkv_gather_epoch_bump(unsigned* d_epoch, void* stream) {
+  if (!d_epoch) return NQKV_ERR_NULL;
+  const cudaError_t e = launch_pdl_n(gather_epoch_bump_kernel, dim3(1), dim3(1), 0,
+                                   static_cast<cudaStream_t>(stream), d_epoch);
+  return e == cudaSuccess ? NQKV_OK : cuda_fail(e);
+}
+
+int nqkv_gather_wait(const unsigned* d_flags, int n, const unsigned* d_epoch, void* stream) {
+  if (!d_flags || !d_epoch) return NQKV_ERR_NULL;
+  if (n < 0) return NQKV_ERR_SHAPE;
+  if (n == 0) return NQKV_OK;
+  const cudaError_t e = launch_pdl_n(gather_wait_kernel, dim3(1), dim3(256), 0,
+                                   static_cast<cudaStream_t>(stream), d_flags, n, d_epoch);
+  return e == cudaSuccess ? NQKV_OK : cuda_fail(e);
 }
 
 int nqkv_encode_normalized(const float* d_n, int64_t count, uint8_t* d_codes, void* stream) {

@@ -50,7 +50,9 @@ _SIGS = {
                                         _vp, _i32, _vp]),
     "nqkv_decode_step_gather": (_i32, [_vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _i32,
                                        _i32, _i32, _i32, _i32, ctypes.c_float, _vp, _vp, _i32,
-                                       _i32, _i32, ctypes.c_uint, _vp, _sz, _vp, _i32, _vp]),
+                                       _i32, _i32, ctypes.c_uint, _vp, _vp, _sz, _vp, _i32, _vp]),
+    "nqkv_gather_epoch_bump": (_i32, [_vp, _vp]),
+    "nqkv_gather_wait": (_i32, [_vp, _i32, _vp, _vp]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -260,12 +262,14 @@ def nqkv_decode_step_planned(k_new, v_new, q, k_codes, k_scales, v_codes, v_scal
 
 def nqkv_decode_step_gather(k_new, v_new, q, k_codes, k_scales, v_codes, v_scales, seq_lens, blk,
                             workspace, plan, peer_out_ptrs: torch.Tensor, peer_flag_ptrs: torch.Tensor,
-                            G: int, rank: int, epoch: int, softmax_scale=None, stream=None, flags=0):
+                            G: int, rank: int, epoch: int = 0, epoch_ptr: torch.Tensor | None = None,
+                            softmax_scale=None, stream=None, flags=0):
     """nqkv_decode_step_planned with the all-gather fused into the epilogue:
     output rows go to every rank's [B, G*H, hd] buffer (peer_out_ptrs: int64
     device tensor [G] of their addresses), then epoch is release-stored into
     flags[rank] of every rank (peer_flag_ptrs: int64 device tensor [G] of
-    uint32[G] flag arrays)."""
+    uint32[G] flag arrays).  epoch_ptr (int32 device scalar, read at the end
+    of the launch) replaces epoch under CUDA-graph replay."""
     B, H, hd = q.shape
     Tc = k_codes.shape[2]
     if softmax_scale is None:
@@ -279,9 +283,21 @@ def nqkv_decode_step_gather(k_new, v_new, q, k_codes, k_scales, v_codes, v_scale
         _ptr(k_new), _ptr(v_new), k_new.stride(0), k_new.stride(1), _ptr(q), _ptr(k_codes),
         _ptr(k_scales), _ptr(v_codes), _ptr(v_scales), _ptr(seq_lens), B, H, hd,
         _blkarg(blk, k_scales, v_scales), Tc, float(softmax_scale), _ptr(peer_out_ptrs),
-        _ptr(peer_flag_ptrs), int(G), int(rank), int(G * H), int(epoch), _ptr(workspace),
+        _ptr(peer_flag_ptrs), int(G), int(rank), int(G * H), int(epoch), _ptr(epoch_ptr), _ptr(workspace),
         workspace.numel() * workspace.element_size(), _ptr(plan), int(flags), _stream(stream)),
         "nqkv_decode_step_gather")
+
+
+def nqkv_gather_epoch_bump(epoch_ptr: torch.Tensor, stream=None) -> None:
+    _check(_lib.nqkv_gather_epoch_bump(_ptr(epoch_ptr), _stream(stream)), "nqkv_gather_epoch_bump")
+
+
+def nqkv_gather_wait(flags: torch.Tensor, epoch_ptr: torch.Tensor, stream=None) -> None:
+    """Stream-ordered wait until every entry of flags (this rank's int32 flag
+    arrays) equals *epoch_ptr (system-scope acquire)."""
+    assert flags.dtype == torch.int32 and flags.is_contiguous()
+    _check(_lib.nqkv_gather_wait(_ptr(flags), flags.numel(), _ptr(epoch_ptr), _stream(stream)),
+           "nqkv_gather_wait")
 
 
 def nqkv_encode_normalized(n: torch.Tensor, stream=None) -> torch.Tensor:

@@ -30,9 +30,14 @@ _EARLY = os.environ.get("NQKV_EARLY_START", "1") != "0"   # A/B switch for measu
 class DecodeRunner:
     def __init__(self, w: W.Workload, heads: range, device, group=None, world: int = 1,
                  step_slots: int | None = None, layers: int | None = None, fused: bool = True,
-                 gen_device=None, planned: bool = True):
+                 gen_device=None, planned: bool = True, fused_gather: bool | None = None):
         self.w = w
         self.fused = fused
+        if fused_gather is None:
+            fused_gather = os.environ.get("NQKV_FUSED_GATHER", "0") == "1"
+        # the all-gather fused into the decode epilogue (nqkv_decode_step_gather)
+        # over symmetric-memory buffers instead of NCCL on a side stream
+        self.fused_gather = fused_gather and fused and planned
         if world > 1:
             # the all-gather kernels on the side stream need SMs of their own (a
             # decode CTA fills an SM): leave 2 free (read once by libnqkv)
@@ -73,12 +78,40 @@ class DecodeRunner:
                 self.inputs[s, l, 1] = v[:, 0]
                 self.inputs[s, l, 2] = q
         self.gathered = None
-        if world > 1:
+        if self.fused_gather:
+            self._setup_fused_gather(group, world)
+        elif world > 1:
             self.gathered = torch.empty((self.L, world * self.B, self.Hl, self.hd),
                                         dtype=torch.float32, device=self.dev)
             self.comm = torch.cuda.Stream(device=self.dev)
         self.graphs: list[torch.cuda.CUDAGraph] = []
         self.events: list[list[tuple[torch.cuda.Event, torch.cuda.Event]]] = []
+
+    def _setup_fused_gather(self, group, world):
+        """Gathered outputs [L, B, world*Hl, hd] and per-layer flag arrays
+        [L, world] in symmetric memory; every rank's kernels store into every
+        rank's buffer through the peer pointers (sharding: rank r owns heads
+        [r*Hl, (r+1)*Hl))."""
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+        grp = group if group is not None else dist.group.WORLD
+        G, L, B, Hl, hd = world, self.L, self.B, self.Hl, self.hd
+        self.g_rank = dist.get_rank(grp)
+        self.g_world = G
+        self.g_out = symm_mem.empty(L * B * G * Hl * hd, dtype=torch.float32, device=self.dev)
+        self.g_flags = symm_mem.empty(L * G, dtype=torch.int32, device=self.dev)
+        self.g_flags.zero_()
+        h_out = symm_mem.rendezvous(self.g_out, grp)
+        h_flg = symm_mem.rendezvous(self.g_flags, grp)
+        per = B * G * Hl * hd * 4
+        self.g_out_ptrs = torch.tensor([[h_out.buffer_ptrs[r] + l * per for r in range(G)] for l in range(L)],
+                                       dtype=torch.int64, device=self.dev)
+        self.g_flag_ptrs = torch.tensor([[h_flg.buffer_ptrs[r] + l * G * 4 for r in range(G)]
+                                         for l in range(L)], dtype=torch.int64, device=self.dev)
+        self.epoch = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        self.gathered = self.g_out.view(L, B, G * Hl, hd)
+        torch.cuda.synchronize()
+        dist.barrier(grp)
 
     # ------------------------------------------------------------ prefill --
     def prefill(self, flush: torch.Tensor | None = None) -> list[float]:
@@ -120,6 +153,9 @@ class DecodeRunner:
         x = self.inputs[s]
         pos, lens = self.pos[s], self.attn_lens[s]
         cur = torch.cuda.current_stream()
+        if self.fused_gather:
+            self._step_fused_gather(x, lens)
+            return
         if self.planned:
             N.nqkv_decode_plan(lens, self.Hl, self.Tc, self.fused, self.plan, hd=self.hd)
         for l, c in enumerate(self.caches):
@@ -147,6 +183,18 @@ class DecodeRunner:
                     sharding.all_gather_heads(out[l], self.gathered[l], self.group)
         if self.world > 1:
             cur.wait_stream(self.comm)
+
+    def _step_fused_gather(self, x, lens) -> None:
+        N.nqkv_gather_epoch_bump(self.epoch)
+        N.nqkv_decode_plan(lens, self.Hl, self.Tc, True, self.plan, hd=self.hd)
+        for l, c in enumerate(self.caches):
+            early = N.EARLY_START if (l > 0 and _EARLY) else 0
+            N.nqkv_decode_step_gather(x[l, 0], x[l, 1], x[l, 2], c.k_codes, c.k_scales, c.v_codes,
+                                      c.v_scales, lens, self.blk, self.ws, self.plan,
+                                      self.g_out_ptrs[l], self.g_flag_ptrs[l], self.g_world,
+                                      self.g_rank, epoch_ptr=self.epoch, flags=early)
+        # every rank's rows of every layer have landed in this rank's buffer
+        N.nqkv_gather_wait(self.g_flags, self.epoch)
 
     def capture(self, timing_slots=(0,)) -> None:
         """One CUDA graph per step slot (pointers differ per slot).  Slots in

@@ -154,16 +154,20 @@ def test_decode_gather_argument_errors():
     f = N._lib.nqkv_decode_step_gather
     ws = N.nqkv_decode_workspace_bytes(2, 4, 128, 256)
     base = [FAKE, FAKE, 4 * 128, 128, FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, 2, 4, 128, 64, 256, 0.088,
-            FAKE, FAKE, 2, 0, 8, 1, FAKE, ws, FAKE, 0, None]
+            FAKE, FAKE, 2, 0, 8, 1, None, FAKE, ws, FAKE, 0, None]
     a = list(base); a[16] = None                     # peer output array
     assert f(*a) == -1
-    a = list(base); a[24] = None                     # plan
+    a = list(base); a[25] = None                     # plan
     assert f(*a) == -1
     a = list(base); a[19] = 2                        # rank >= G
     assert f(*a) == -2
     a = list(base); a[20] = 12                       # H_total != G * H
     assert f(*a) == -2
-    a = list(base); a[21] = 0                        # epoch 0 is reserved
+    a = list(base); a[21] = 0                        # epoch 0 is reserved (without d_epoch)
     assert f(*a) == -2
+    assert N._lib.nqkv_gather_epoch_bump(None, None) == -1
+    assert N._lib.nqkv_gather_wait(None, 4, FAKE, None) == -1
+    assert N._lib.nqkv_gather_wait(FAKE, -1, FAKE, None) == -2
+    assert N._lib.nqkv_gather_wait(FAKE, 0, FAKE, None) == 0
     a = list(base); a[12] = 96
     assert f(*a) == -3

@@ -727,3 +727,42 @@ def test_fused_gather_simulated_ranks(N, hd, blk, G):
     O.quantize_append(vn.unsqueeze(1).cpu().numpy(), lens0, blk, vc, vs)
     ref = O.decode_attention(q.cpu().numpy(), kc, ks, vc, vs, [n + 1 for n in lens0], blk)
     assert np.max(np.abs(bufs[0].cpu().numpy() - ref)) <= ATOL
+
+
+def test_runtime_fused_gather_single_rank(N):
+    """DecodeRunner with the all-gather fused into the epilogue over
+    symmetric memory (one rank: the plumbing -- peer pointers, device epoch
+    bumped per step and graph replay, flag wait): the gathered outputs equal
+    the plain fused runtime's, eagerly and under CUDA-graph replay."""
+    import socket
+    import torch.distributed as dist
+    from paper_2505_16210_b200.runtime import DecodeRunner
+    s_ = socket.socket()
+    s_.bind(("127.0.0.1", 0))
+    port = s_.getsockname()[1]
+    s_.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device(DEV, 0))
+    try:
+        w = W.CONFIGS["c1"]
+        a = DecodeRunner(w, range(w.heads), DEV, group=dist.group.WORLD, world=1, step_slots=2, layers=2,
+                         fused_gather=True)
+        b = DecodeRunner(w, range(w.heads), DEV, step_slots=2, layers=2, fused_gather=False)
+        a.prefill()
+        b.prefill()
+        for s in range(2):
+            a.step(s)
+            b.step(s)
+            torch.cuda.synchronize()
+            assert torch.equal(a.gathered, b.out_of(s))
+            assert a.g_flags.tolist() == [s + 1] * 2
+        a.capture()
+        b.capture()
+        for s in (0, 1):
+            a.replay(s)
+            b.replay(s)
+        torch.cuda.synchronize()
+        assert torch.equal(a.gathered, b.out_of(1))
+        assert a.g_flags.tolist() == [int(a.epoch.item())] * 2 and int(a.epoch.item()) == 4
+    finally:
+        dist.destroy_process_group()
