@@ -130,12 +130,22 @@ __device__ __forceinline__ void store_out2(const DecodeParams& p, long long bh, 
 // GATHER: this CTA's output stores are complete.  System-scope fence, then
 // count; the last CTA of the launch resets the counter and publishes the
 // epoch to every rank (release, system scope).
-__device__ __forceinline__ void gather_cta_done(const DecodeParams& p) {
+#ifndef NQKV_GFENCE
+#define NQKV_GFENCE 1           // 0: none (timing only), 1: fence.sc.sys, 2: fence.acq_rel.sys
+#endif
+__device__ __forceinline__ void gather_fence() {
+#if NQKV_GFENCE == 1
   __threadfence_system();
+#elif NQKV_GFENCE == 2
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void gather_cta_done(const DecodeParams& p) {
+  gather_fence();
   const unsigned old = atomicAdd(p.gctr, 1u);
   if (old == gridDim.x - 1) {
     *p.gctr = 0u;
-    __threadfence_system();
+    gather_fence();
     const unsigned e = p.epoch_ptr ? *p.epoch_ptr : p.epoch;
     for (int r = 0; r < p.gather_g; ++r) {
       unsigned* f = p.peer_flags[r] + p.gather_rank;
