@@ -174,7 +174,9 @@ int launch_decode_g(const DecodeParams& p, cudaStream_t st) {
   switch (p.blk_shift) {
     case 5: return launch_decode_blk<HD, 32, F16S, false, GATHER>(p, st);
     case 6: return launch_decode_blk<HD, 64, F16S, false, GATHER>(p, st);
-    default: return HD == 128 ? launch_decode_blk<HD, 128, F16S, false, GATHER>(p, st) : NQKV_ERR_UNSUPPORTED;
+    default:
+      if constexpr (HD == 128) return launch_decode_blk<HD, 128, F16S, false, GATHER>(p, st);
+      else return NQKV_ERR_UNSUPPORTED;    // blk 128 at hd 64 is a head-group block (GRP)
   }
 }
 
