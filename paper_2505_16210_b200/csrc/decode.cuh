@@ -131,21 +131,25 @@ __device__ __forceinline__ void store_out2(const DecodeParams& p, long long bh, 
 // count; the last CTA of the launch resets the counter and publishes the
 // epoch to every rank (release, system scope).
 #ifndef NQKV_GFENCE
-#define NQKV_GFENCE 1           // 0: none (timing only), 1: fence.sc.sys, 2: fence.acq_rel.sys
-#endif
-__device__ __forceinline__ void gather_fence() {
+#define NQKV_GFENCE 1           // 0: none (timing only), 1: fence.sc.sys, 2: fence.acq_rel.sys,
+#endif                          // 3: gpu-scope per CTA, system scope by the last CTA only
+__device__ __forceinline__ void gather_fence(bool last) {
 #if NQKV_GFENCE == 1
   __threadfence_system();
 #elif NQKV_GFENCE == 2
   asm volatile("fence.acq_rel.sys;" ::: "memory");
+#elif NQKV_GFENCE == 3
+  if (last) __threadfence_system();
+  else __threadfence();
 #endif
+  (void)last;
 }
 __device__ __forceinline__ void gather_cta_done(const DecodeParams& p) {
-  gather_fence();
+  gather_fence(false);
   const unsigned old = atomicAdd(p.gctr, 1u);
   if (old == gridDim.x - 1) {
     *p.gctr = 0u;
-    gather_fence();
+    gather_fence(true);
     const unsigned e = p.epoch_ptr ? *p.epoch_ptr : p.epoch;
     for (int r = 0; r < p.gather_g; ++r) {
       unsigned* f = p.peer_flags[r] + p.gather_rank;
