@@ -12,6 +12,11 @@
  *   nqkv_decode_attention  t_O = Softmax(t_Q X_K'^T/sqrt(d)) X_V'  with the
  *                          dequantisation fused in registers
  *
+ * plus the decode step with the append fused in (nqkv_decode_step), planned
+ * variants of both (nqkv_decode_plan, *_planned) and the step with the
+ * head-sharded all-gather fused into its epilogue (nqkv_decode_step_gather,
+ * nqkv_gather_epoch_bump, nqkv_gather_wait).
+ *
  * Conventions (all entry points)
  *  - The caller owns every buffer.  The library never allocates, frees or
  *    synchronises; device work is enqueued on `stream` (a cudaStream_t passed
