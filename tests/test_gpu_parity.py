@@ -501,13 +501,13 @@ def test_planned_calls_match_unplanned_bit_exact(N, hd, blk):
 
 
 @pytest.mark.parametrize("hd", [64, 128])
-def test_planned_many_pieces_deferred_order(N, hd):
+@pytest.mark.parametrize("blk", [64, 256])
+def test_planned_many_pieces_deferred_order(N, hd, blk):
     """CTAs holding more pieces than prebuilt q-table slots process a split
     first piece last (WalkState "defer"): planned == unplanned bit for bit,
-    and both match the oracle."""
-    blk = 64
+    and both match the oracle (also with head-group blocks, blk 256)."""
     lens0 = [(37 * i) % 190 + 3 for i in range(40)]
-    B, H, T = len(lens0), 6, max(lens0)
+    B, H, T = len(lens0), 6 if blk <= hd else 4, max(lens0)
     Tc = -(-T // 64) * 64
     x = _rand_kv(B, T, H, hd, seed=61)
     y = _rand_kv(B, T, H, hd, seed=62, outlier=False)
