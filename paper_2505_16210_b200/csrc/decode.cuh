@@ -133,6 +133,14 @@ __device__ __forceinline__ void store_out2(const DecodeParams& p, long long bh, 
 #ifndef NQKV_GFENCE
 #define NQKV_GFENCE 1           // 0: none (timing only), 1: fence.sc.sys, 2: fence.acq_rel.sys,
 #endif                          // 3: gpu-scope per CTA, system scope by the last CTA only
+#if NQKV_GFENCE == 0 && !defined(NQKV_TIMING_ONLY)
+#error "NQKV_GFENCE=0 builds a racy gather (no fences): timing experiments only, define NQKV_TIMING_ONLY"
+#endif
+#if NQKV_GFENCE == 3 && !defined(NQKV_GFENCE3_UNVERIFIED)
+// gpu-scope fences per CTA rely on fence cumulativity to carry other CTAs' NVLink peer
+// stores; only serialized simulated ranks on one GPU have run it
+#error "NQKV_GFENCE=3 is unverified across GPUs: define NQKV_GFENCE3_UNVERIFIED to build it"
+#endif
 __device__ __forceinline__ void gather_fence(bool last) {
 #if NQKV_GFENCE == 1
   __threadfence_system();
@@ -1869,8 +1877,10 @@ __global__ void gather_epoch_bump_kernel(unsigned* epoch) {
   pdl_enter();
   *epoch += 1u;
 }
-// wait until flags[0..n) all equal *epoch (acquire, system scope): the
-// gathered buffer this rank reads is then complete
+// wait until flags[0..n) all reached *epoch (acquire, system scope): the
+// gathered buffer this rank reads is then complete.  Wrap-safe: a flag that
+// a faster peer has already advanced past the epoch also satisfies the wait
+// (epochs compare as a 32-bit serial number).
 __global__ void gather_wait_kernel(const unsigned* flags, int n, const unsigned* epoch) {
   pdl_enter();
   const unsigned e = *epoch;
@@ -1878,9 +1888,20 @@ __global__ void gather_wait_kernel(const unsigned* flags, int n, const unsigned*
     unsigned v;
     do {
       asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + i) : "memory");
-    } while (v != e);
+    } while (static_cast<int>(v - e) < 0);
   }
   __syncthreads();
+}
+// a rank with nothing to compute (B == 0 or H == 0) still publishes its epoch
+// to every rank, so no peer waits for it forever
+__global__ void gather_publish_kernel(unsigned* const* peer_flags, int G, int rank, unsigned epoch,
+                                      const unsigned* epoch_ptr) {
+  pdl_enter();
+  const unsigned e = epoch_ptr ? *epoch_ptr : epoch;
+  for (int r = threadIdx.x; r < G; r += blockDim.x) {
+    unsigned* f = peer_flags[r] + rank;
+    asm volatile("st.release.sys.global.u32 [%0], %1;" :: "l"(f), "r"(e) : "memory");
+  }
 }
 
 }  // namespace nqkv

@@ -231,7 +231,12 @@ int decode_common(const void* q, const uint8_t* k_codes, const void* k_scales,
     return NQKV_ERR_ALIGN;
   if (k_new && (!aligned16(k_new) || !aligned16(v_new) || (new_sb % 8) || (new_sh % 8)))
     return NQKV_ERR_ALIGN;
-  if (B == 0 || H == 0) return NQKV_OK;
+  if (B == 0 || H == 0) {
+    if (!ga) return NQKV_OK;
+    const cudaError_t e = launch_pdl_n(gather_publish_kernel, dim3(1), dim3(64), 0, st, ga->peer_flags,
+                                       ga->G, ga->rank, ga->epoch, ga->epoch_ptr);
+    return e == cudaSuccess ? NQKV_OK : cuda_fail(e);
+  }
   const WsLayout w = ws_layout(B, H, hd);
   if (!workspace) return NQKV_ERR_NULL;
   if (!aligned16(workspace)) return NQKV_ERR_ALIGN;

@@ -30,7 +30,8 @@ _EARLY = os.environ.get("NQKV_EARLY_START", "1") != "0"   # A/B switch for measu
 class DecodeRunner:
     def __init__(self, w: W.Workload, heads: range, device, group=None, world: int = 1,
                  step_slots: int | None = None, layers: int | None = None, fused: bool = True,
-                 gen_device=None, planned: bool = True, fused_gather: bool | None = None):
+                 gen_device=None, planned: bool = True, fused_gather: bool | None = None,
+                 nccl_gather: bool | None = None):
         self.w = w
         self.fused = fused
         if fused_gather is None:
@@ -78,9 +79,12 @@ class DecodeRunner:
                 self.inputs[s, l, 1] = v[:, 0]
                 self.inputs[s, l, 2] = q
         self.gathered = None
+        # NCCL all-gather of each layer's outputs on a side stream: always at
+        # world > 1; selectable at world 1 (tests run it under graph capture)
+        self.nccl_gather = (world > 1 if nccl_gather is None else nccl_gather) and not self.fused_gather
         if self.fused_gather:
             self._setup_fused_gather(group, world)
-        elif world > 1:
+        elif self.nccl_gather:
             self.gathered = torch.empty((self.L, world * self.B, self.Hl, self.hd),
                                         dtype=torch.float32, device=self.dev)
             self.comm = torch.cuda.Stream(device=self.dev)
@@ -88,30 +92,44 @@ class DecodeRunner:
         self.events: list[list[tuple[torch.cuda.Event, torch.cuda.Event]]] = []
 
     def _setup_fused_gather(self, group, world):
-        """Gathered outputs [L, B, world*Hl, hd] and per-layer flag arrays
-        [L, world] in symmetric memory; every rank's kernels store into every
-        rank's buffer through the peer pointers (sharding: rank r owns heads
-        [r*Hl, (r+1)*Hl))."""
+        """Gathered outputs [2, L, B, world*Hl, hd] and per-layer flag arrays
+        [2, L, world] in symmetric memory, double-buffered by step parity;
+        every rank's kernels store into every rank's buffer through the peer
+        pointers (sharding: rank r owns heads [r*Hl, (r+1)*Hl)).
+
+        Read contract: a consumer of step n's gathered buffer (parity n % 2)
+        must be stream-ordered before this rank's step n + 1 gather launches
+        (which publish epoch n + 1).  A peer can then overwrite parity n % 2
+        (its step n + 2) only after waiting for epoch n + 1 from every rank,
+        i.e. after those reads.  Graph slots alternate parity, so the number
+        of captured step graphs is even (doubled when step_slots is odd)."""
         import torch.distributed as dist
         import torch.distributed._symmetric_memory as symm_mem
         grp = group if group is not None else dist.group.WORLD
         G, L, B, Hl, hd = world, self.L, self.B, self.Hl, self.hd
         self.g_rank = dist.get_rank(grp)
         self.g_world = G
-        self.g_out = symm_mem.empty(L * B * G * Hl * hd, dtype=torch.float32, device=self.dev)
-        self.g_flags = symm_mem.empty(L * G, dtype=torch.int32, device=self.dev)
+        per = B * G * Hl * hd
+        self.g_out = symm_mem.empty(2 * L * per, dtype=torch.float32, device=self.dev)
+        self.g_flags = symm_mem.empty(2 * L * G, dtype=torch.int32, device=self.dev)
         self.g_flags.zero_()
         h_out = symm_mem.rendezvous(self.g_out, grp)
         h_flg = symm_mem.rendezvous(self.g_flags, grp)
-        per = B * G * Hl * hd * 4
-        self.g_out_ptrs = torch.tensor([[h_out.buffer_ptrs[r] + l * per for r in range(G)] for l in range(L)],
-                                       dtype=torch.int64, device=self.dev)
-        self.g_flag_ptrs = torch.tensor([[h_flg.buffer_ptrs[r] + l * G * 4 for r in range(G)]
-                                         for l in range(L)], dtype=torch.int64, device=self.dev)
+        self.g_out_ptrs = torch.tensor(
+            [[[h_out.buffer_ptrs[r] + ((p * L + l) * per) * 4 for r in range(G)] for l in range(L)]
+             for p in range(2)], dtype=torch.int64, device=self.dev)
+        self.g_flag_ptrs = torch.tensor(
+            [[[h_flg.buffer_ptrs[r] + ((p * L + l) * G) * 4 for r in range(G)] for l in range(L)]
+             for p in range(2)], dtype=torch.int64, device=self.dev)
         self.epoch = torch.zeros(1, dtype=torch.int32, device=self.dev)
-        self.gathered = self.g_out.view(L, B, G * Hl, hd)
+        self.gathered = self.g_out.view(2, L, B, G * Hl, hd)
         torch.cuda.synchronize()
         dist.barrier(grp)
+
+    def _graph_slots(self) -> int:
+        """Captured step graphs: one per step slot; the fused gather alternates
+        buffer parity, so it needs an even count."""
+        return self.S * 2 if (self.fused_gather and self.S % 2) else self.S
 
     # ------------------------------------------------------------ prefill --
     def prefill(self, flush: torch.Tensor | None = None) -> list[float]:
@@ -140,21 +158,25 @@ class DecodeRunner:
     # --------------------------------------------------------------- step --
     @property
     def out(self) -> torch.Tensor:
-        """Outputs [L, B, H, hd] of the most recent step (replay)."""
-        return self.outs[self._last % 2]
+        """Outputs [L, B, H, hd] of the most recent step (replay); the
+        gathered [L, B, world*H, hd] outputs with the fused gather."""
+        return self.out_of(self._last)
 
     def out_of(self, s: int) -> torch.Tensor:
-        """Output buffer written by step slot s."""
+        """Output buffer written by step (graph) slot s."""
+        if self.fused_gather:
+            return self.gathered[s % 2]
         return self.outs[(s % self.S) % 2]
 
     def step(self, s: int, events=None) -> None:
+        """One decode step with the inputs of step slot s % S (graph slot s)."""
         self._last = s
         out = self.outs[s % 2]
-        x = self.inputs[s]
-        pos, lens = self.pos[s], self.attn_lens[s]
+        x = self.inputs[s % self.S]
+        pos, lens = self.pos[s % self.S], self.attn_lens[s % self.S]
         cur = torch.cuda.current_stream()
         if self.fused_gather:
-            self._step_fused_gather(x, lens)
+            self._step_fused_gather(x, lens, s % 2, events)
             return
         if self.planned:
             N.nqkv_decode_plan(lens, self.Hl, self.Tc, self.fused, self.plan, hd=self.hd)
@@ -177,24 +199,29 @@ class DecodeRunner:
                 c.attend(x[l, 2], lens, self.ws, out=out[l])
             if events is not None:
                 events[l][1].record()
-            if self.world > 1:
+            if self.nccl_gather:
                 self.comm.wait_stream(cur)
                 with torch.cuda.stream(self.comm):
                     sharding.all_gather_heads(out[l], self.gathered[l], self.group)
-        if self.world > 1:
+        if self.nccl_gather:
             cur.wait_stream(self.comm)
 
-    def _step_fused_gather(self, x, lens) -> None:
+    def _step_fused_gather(self, x, lens, parity, events=None) -> None:
         N.nqkv_gather_epoch_bump(self.epoch)
         N.nqkv_decode_plan(lens, self.Hl, self.Tc, True, self.plan, hd=self.hd)
         for l, c in enumerate(self.caches):
+            if events is not None:
+                events[l][0].record()
             early = N.EARLY_START if (l > 0 and _EARLY) else 0
             N.nqkv_decode_step_gather(x[l, 0], x[l, 1], x[l, 2], c.k_codes, c.k_scales, c.v_codes,
                                       c.v_scales, lens, self.blk, self.ws, self.plan,
-                                      self.g_out_ptrs[l], self.g_flag_ptrs[l], self.g_world,
-                                      self.g_rank, epoch_ptr=self.epoch, flags=early)
+                                      self.g_out_ptrs[parity, l], self.g_flag_ptrs[parity, l],
+                                      self.g_world, self.g_rank, epoch_ptr=self.epoch, flags=early)
+            if events is not None:
+                events[l][1].record()
         # every rank's rows of every layer have landed in this rank's buffer
-        N.nqkv_gather_wait(self.g_flags, self.epoch)
+        L, G = self.L, self.g_world
+        N.nqkv_gather_wait(self.g_flags[parity * L * G:(parity + 1) * L * G], self.epoch)
 
     def capture(self, timing_slots=(0,)) -> None:
         """One CUDA graph per step slot (pointers differ per slot).  Slots in
@@ -203,7 +230,7 @@ class DecodeRunner:
         carry them)."""
         torch.cuda.synchronize()
         self.graphs, self.events = [], []
-        for s in range(self.S):
+        for s in range(self._graph_slots()):
             ev = None
             if s in timing_slots:
                 ev = [(torch.cuda.Event(enable_timing=True, external=True),
@@ -216,8 +243,9 @@ class DecodeRunner:
         torch.cuda.synchronize()
 
     def replay(self, i: int) -> None:
-        self._last = i % self.S
-        self.graphs[i % self.S].replay()
+        n = len(self.graphs)
+        self._last = i % n
+        self.graphs[i % n].replay()
 
     def decode_kernel_ms(self) -> list[float]:
         """Durations of the decode-attention launches of the most recent replay

@@ -220,6 +220,27 @@ def test_dequantize_bit_exact(N, hd, blk):
         assert got.dtype == want.dtype and np.array_equal(got.view(np.uint8), want.view(np.uint8))
 
 
+def test_dequantize_fp16_every_scale_code_pair(N):
+    """All 31,743 positive finite fp16 scales x 16 codes (507,888 pairs, plus
+    s = 0) through nqkv_dequantize with fp16 output: RN16(RN32(s * L[c])),
+    bit for bit (57 of these pairs differ from RN16(s * L))."""
+    s = np.arange(1, 0x7C00, dtype=np.uint16).view(np.float16).astype(np.float32)
+    s = np.concatenate([s, np.zeros(1, np.float32)])
+    Tc = -(-s.size // 64) * 64
+    scales = np.zeros((1, 1, Tc, 2), np.float32)            # hd 64, blk 32: two blocks per row
+    scales[0, 0, :s.size, 0] = s
+    scales[0, 0, :s.size, 1] = s
+    codes = np.arange(64, dtype=np.uint8) % 16              # every code in both blocks
+    packed = O.pack_nibbles(np.broadcast_to(codes, (1, 1, Tc, 64)).copy())
+    got = N.nqkv_dequantize(torch.from_numpy(packed).to(DEV), torch.from_numpy(scales).to(DEV), 32,
+                            s.size, out_dtype=torch.float16).cpu().numpy()
+    want = O.dequantize(packed, scales, 32, s.size, out_dtype=np.float16)
+    assert np.array_equal(got.view(np.uint16), want.view(np.uint16))
+    # the double-rounding cases are really in the sweep
+    exact16 = (s[:, None].astype(np.float64) * O.nf_levels_f32()[None, :].astype(np.float64)).astype(np.float16)
+    assert np.count_nonzero(want[0, 0, :, :16].view(np.uint16) != exact16.view(np.uint16)) > 0
+
+
 # ---------------------------------------------------------------- attention
 def _attn_case(N, B, H, hd, blk, lens, Tc, seed, outlier=True, dev_ws=None):
     T = max(max(lens), 1)
@@ -447,6 +468,60 @@ def test_decode_runner_graph_matches_oracle(N):
         ref = O.decode_attention(q.numpy(), kc, ks, vc, vs, [n + 3 for n in lens], w.blk)
         assert np.max(np.abs(run.out[l].cpu().numpy() - ref)) <= ATOL
     assert all(t > 0 for t in run.decode_kernel_ms())
+
+
+@pytest.mark.parametrize("cfg", ["c2", "c5"])
+def test_bench_path_full_size(N, cfg):
+    """The exact path bench.py times -- DecodeRunner with the per-step plan,
+    fused append + attention, NQKV_EARLY_START on layers 1.. and CUDA-graph
+    replay -- at the config's full per-launch size (c5: the 12-head shard,
+    B 64, 4096 tokens), inputs generated on the GPU as in the bench.  Every
+    cache byte of the checked (layer, b, h) slabs and their outputs against
+    the oracle; all step slots replayed in order."""
+    from paper_2505_16210_b200.runtime import DecodeRunner
+    w = W.CONFIGS[cfg]
+    layers = 3 if cfg == "c5" else w.layers
+    heads = range(12) if cfg == "c5" else range(w.heads)
+    free = torch.cuda.mem_get_info()[0]
+    T = int(W.seq_lens(w).max())
+    per_layer = 2 * w.batch * len(heads) * W.capacity(T + w.decode_steps) * (w.head_dim // 2 + 4 * w.head_dim // w.blk)
+    if layers * per_layer + 3 * w.batch * T * len(heads) * w.head_dim * 2 > 0.8 * free:
+        pytest.skip("not enough device memory")
+    run = DecodeRunner(w, heads, DEV, layers=layers)
+    run.prefill()
+    run.step(0)                         # eager warm-up (slot 0)
+    run.capture(timing_slots=())
+    for s in range(run.S):              # graph replays of every slot, in order
+        run.replay(s)
+    torch.cuda.synchronize()
+    assert torch.count_nonzero(run.ws) == 0
+    lens = W.seq_lens(w).tolist()
+    S = run.S
+    rng = np.random.default_rng(7)
+    H = len(heads)
+    picks = {(0, 0, 0), (layers - 1, w.batch - 1, H - 1)}
+    picks |= {(int(rng.integers(layers)), int(rng.integers(w.batch)), int(rng.integers(H))) for _ in range(6)}
+    for l, b, h in sorted(picks):
+        n = lens[b]
+        K, V = W.layer_kv(w, l, heads=range(heads[h], heads[h] + 1), tokens=T, device=DEV)
+        kx, vx = [K[b:b + 1, :n].cpu()], [V[b:b + 1, :n].cpu()]
+        for s in range(S):
+            k1, v1, q = W.step_inputs(w, l, s, heads=range(heads[h], heads[h] + 1), device=DEV)
+            kx.append(k1[b:b + 1].cpu())
+            vx.append(v1[b:b + 1].cpu())
+        kc, ks = _oracle_cache(torch.cat(kx, 1), [0], w.blk, run.Tc)
+        vc, vs = _oracle_cache(torch.cat(vx, 1), [0], w.blk, run.Tc)
+        c = run.caches[l]
+        m = n + S
+        assert np.array_equal(c.k_codes[b, h, :m].cpu().numpy(), kc[0, 0, :m])
+        assert np.array_equal(c.v_codes[b, h, :m].cpu().numpy(), vc[0, 0, :m])
+        assert np.array_equal(c.k_scales[b, h, :m].cpu().numpy(), ks[0, 0, :m])
+        assert np.array_equal(c.v_scales[b, h, :m].cpu().numpy(), vs[0, 0, :m])
+        ref = O.decode_attention(q[b:b + 1].cpu().numpy(), kc, ks, vc, vs, [m], w.blk)
+        got = run.out_of(S - 1)[l, b, h].cpu().numpy()
+        assert np.max(np.abs(got - ref[0, 0])) <= ATOL
+    del run
+    torch.cuda.empty_cache()
 
 
 # ------------------------------------------------------ per-step plan API
@@ -754,15 +829,63 @@ def test_runtime_fused_gather_single_rank(N):
             a.step(s)
             b.step(s)
             torch.cuda.synchronize()
-            assert torch.equal(a.gathered, b.out_of(s))
-            assert a.g_flags.tolist() == [s + 1] * 2
-        a.capture()
+            assert torch.equal(a.out_of(s), b.out_of(s))
+            assert a.out is a.out_of(s) or torch.equal(a.out, a.out_of(s))
+        assert a.g_flags.tolist() == [1, 1, 2, 2]          # [parity][layer][rank]: epochs 1, 2
+        ev = [[(torch.cuda.Event(enable_timing=True, external=True),
+                torch.cuda.Event(enable_timing=True, external=True)) for _ in range(2)]]
+        a.capture(timing_slots=(0,))
         b.capture()
         for s in (0, 1):
             a.replay(s)
             b.replay(s)
         torch.cuda.synchronize()
-        assert torch.equal(a.gathered, b.out_of(1))
-        assert a.g_flags.tolist() == [int(a.epoch.item())] * 2 and int(a.epoch.item()) == 4
+        assert torch.equal(a.out_of(1), b.out_of(1)) and torch.equal(a.out_of(0), b.out_of(0))
+        assert a.g_flags.tolist() == [3, 3, 4, 4] and int(a.epoch.item()) == 4
+        assert all(t > 0 for t in a.decode_kernel_ms())   # events recorded around the gather launches
+        del ev
+        # odd step-slot count: graphs are doubled so buffer parity alternates
+        c = DecodeRunner(w, range(w.heads), DEV, group=dist.group.WORLD, world=1, step_slots=1, layers=2,
+                         fused_gather=True)
+        c.prefill()
+        c.capture(timing_slots=())
+        assert len(c.graphs) == 2
+        for i in range(3):
+            c.replay(i)
+        torch.cuda.synchronize()
+        assert c.g_flags.tolist() == [3, 3, 2, 2]
+    finally:
+        dist.destroy_process_group()
+
+
+def test_runtime_nccl_side_stream_gather_world1(N):
+    """The runtime's NCCL all-gather of per-head outputs on a side stream
+    (the multi-GPU exchange step), forced on at world size 1
+    and run eagerly and under CUDA-graph capture/replay: the gathered buffer
+    equals the rank's own outputs bit for bit."""
+    import socket
+    import torch.distributed as dist
+    from paper_2505_16210_b200.runtime import DecodeRunner
+    s_ = socket.socket()
+    s_.bind(("127.0.0.1", 0))
+    port = s_.getsockname()[1]
+    s_.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device(DEV, 0))
+    try:
+        w = W.CONFIGS["c1"]
+        r = DecodeRunner(w, range(w.heads), DEV, group=dist.group.WORLD, world=1, step_slots=2, layers=3,
+                         nccl_gather=True)
+        assert r.nccl_gather
+        r.prefill()
+        r.step(0)
+        torch.cuda.synchronize()
+        assert torch.equal(r.gathered, r.out_of(0))
+        r.capture(timing_slots=())
+        r.gathered.zero_()
+        r.replay(1)
+        torch.cuda.synchronize()
+        assert torch.equal(r.gathered, r.out_of(1))
+        assert r.launches_per_step() == 3 + 1
     finally:
         dist.destroy_process_group()

@@ -529,3 +529,55 @@ def test_paper_memory_arithmetic():
     assert round(kv / 2 ** 40, 1) == 2.3 or round(kv / 1e12, 1) == 2.5
     assert round(kv / 2 ** 40, 2) == 2.25
     assert round(kv / (175e9 * 2)) == 7
+
+
+# ------------------------------------------------- softmax temperature pin --
+def _grid_rows(codes: np.ndarray) -> np.ndarray:
+    """fp16 rows whose block absmax is exactly 1.0 (code 15 present) and whose
+    elements are fp16(L[c]): the grid fixed point maps them back to codes c,
+    so the dequantised row is exactly L32[c] (scale 1.0)."""
+    return L32[codes].astype(np.float16)
+
+
+@pytest.mark.parametrize("hd", [64, 128])
+def test_softmax_temperature_two_token_closed_form(hd):
+    """Two cached tokens with grid-exact keys: p1/p0 = exp(q.(k1 - k0)/sqrt(hd))
+    (PAPER.md:233 writes Softmax(t_Q X_K'^T); the 1/sqrt(d) factor is DESIGN.md
+    reading R6).  The expected output is evaluated at 50 digits
+    from exact rationals, independently of the oracle's arithmetic.  The same
+    closed form with no temperature, 1/hd, or base 2 misses the oracle by far,
+    so a plausible temperature mistake in the oracle fails here."""
+    rng = np.random.default_rng(2025 + hd)
+    kc = rng.integers(0, 16, size=(2, hd))
+    vc = rng.integers(0, 16, size=(2, hd))
+    kc[:, 0] = 15                      # absmax 1.0 in every block (blk = hd)
+    vc[:, 0] = 15
+    # q with a moderate q.(k1 - k0): keep the ratio away from 0 and infinity
+    for _ in range(100):
+        q = (rng.standard_normal(hd) * 0.35).astype(np.float16)
+        d = sum(Fraction(float(a)) * (Fraction(float(L32[c1])) - Fraction(float(L32[c0])))
+                for a, c0, c1 in zip(q, kc[0], kc[1]))
+        if 2.0 < abs(float(d)) < 12.0:
+            break
+    kx = _grid_rows(kc).reshape(1, 2, 1, hd)
+    vx = _grid_rows(vc).reshape(1, 2, 1, hd)
+    kcache, ks = _cache_from(kx, hd)
+    vcache, vs = _cache_from(vx, hd)
+    assert np.all(ks[0, 0, :2] == 1.0) and np.all(vs[0, 0, :2] == 1.0)
+    kd = O.dequantize(kcache, ks, hd, 2)[0, 0]
+    assert np.array_equal(kd, L32[kc])                     # keys exactly on the grid
+    out = O.decode_attention(q.reshape(1, 1, hd), kcache, ks, vcache, vs, [2], hd)[0, 0]
+
+    mpmath.mp.dps = 50
+    v0 = [mpmath.mpf(float(L32[c])) for c in vc[0]]
+    v1 = [mpmath.mpf(float(L32[c])) for c in vc[1]]
+    dm = mpmath.mpf(d.numerator) / d.denominator
+
+    def expect(ratio):
+        return np.array([float((a + ratio * b) / (1 + ratio)) for a, b in zip(v0, v1)])
+
+    right = expect(mpmath.exp(dm / mpmath.sqrt(hd)))
+    assert np.max(np.abs(out - right)) < 1e-12
+    # mutation sensitivity: the wrong temperatures are far from the oracle
+    for wrong in (mpmath.exp(dm), mpmath.exp(dm / hd), mpmath.power(2, dm / mpmath.sqrt(hd))):
+        assert np.max(np.abs(out - expect(wrong))) > 1e-3

@@ -1,0 +1,571 @@
+// Development experiment (not part of the library): steady-state streaming
+// designs for the hd-128 decode consumer loop.  Every CTA streams one long
+// contiguous run of (K codes, V codes, K scales, V scales) rows and does the
+// decode kernel's full per-token work (q-table K scores, online softmax, V
+// pair-LUT accumulation), so the numbers bound what a decode kernel built on
+// each loader can reach.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo -o /tmp/sx tools/stream_exp.cu
+//   /tmp/sx
+// Loaders:
+//   LDG : consumers load their stages straight into a D-deep register ring
+//         (the round-1 kernel's scheme); optional cp.async.bulk.prefetch.L2
+//         of the stages PF ahead by a loader warp.
+//   TMA : a loader warp streams stages with cp.async.bulk into an NS-slot
+//         shared ring (mbarrier complete_tx); a consumer copies its stage to
+//         registers (LDS), releases the slot, then computes.
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("%s:%d %s\n", __FILE__, __LINE__, cudaGetErrorString(e)); exit(1); } } while (0)
+
+constexpr int HD = 128, ROWB = HD / 2;       // code bytes per token row
+constexpr int ST = 16;                       // tokens per stage
+constexpr int STAGE_BYTES = 2 * ST * ROWB + 2 * ST * 8;   // K, V codes + K, V scales (fp32, 2 blocks)
+constexpr uint32_t kWin = 0x400;
+
+__device__ __forceinline__ uint2 ld64(const void* p) {
+  uint2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ float ld32(const void* p) {
+  float r;
+  asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(r) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t s) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(s));
+  return d;
+}
+__device__ __forceinline__ uint64_t pack2(float x, float y) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(x), "f"(y));
+  return r;
+}
+__device__ __forceinline__ float2 unpack2(uint64_t v) {
+  float2 r;
+  asm("mov.b64 {%0,%1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// K q-table at window + 64 KB, V LUT at window + 0
+template <uint32_t KB>
+__device__ __forceinline__ uint64_t lds_k2t(uint32_t o1, uint32_t o2) {
+  uint64_t v;
+  asm volatile("{.reg .b32 a, b;\n ld.shared.b32 a, [%1+%3];\n ld.shared.b32 b, [%2+%3];\n mov.b64 %0, {a, b};}"
+               : "=l"(v) : "r"(o1), "r"(o2), "n"(KB + 0x400));
+  return v;
+}
+template <uint32_t KB>
+__device__ __forceinline__ float lds_kt(uint32_t off) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(v) : "r"(off), "n"(KB + 0x400));
+  return v;
+}
+__device__ __forceinline__ uint64_t lds_v(uint32_t off) {
+  uint64_t v;
+  asm volatile("ld.shared.b64 %0, [%1+0x400];" : "=l"(v) : "r"(off));
+  return v;
+}
+// 16-bit V LUT: entry = (lo16, hi16) fixed point u = (L + 1) * 2^15 (clamped),
+// value = (256 + u * 2^-15) - 257
+__device__ __forceinline__ uint32_t lds_v16(uint32_t off) {
+  uint32_t v;
+  asm volatile("ld.shared.b32 %0, [%1+0x400];" : "=r"(v) : "r"(off));
+  return v;
+}
+__device__ __forceinline__ void mbar_init(uint32_t a, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(a), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t a) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(a) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint32_t a, uint32_t tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(a), "r"(tx) : "memory");
+}
+__device__ unsigned long long* g_dbg;
+__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t ph) {
+  uint32_t ok = 0;
+  for (long long it = 0; !ok; ++it) {
+    asm volatile(
+        "{\n.reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n}\n" : "=r"(ok) : "r"(a), "r"(ph) : "memory");
+    if (it > (1ll << 24)) {
+      if (atomicAdd(g_dbg, 1ull) == 0) { g_dbg[1] = blockIdx.x; g_dbg[2] = threadIdx.x; g_dbg[3] = a; g_dbg[4] = ph; }
+      __threadfence_system();
+      __trap();
+    }
+  }
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               :: "r"(dst), "l"(src), "r"(bytes), "r"(mbar) : "memory");
+}
+__device__ __forceinline__ void cp16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void bulk_pf(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(src), "r"(bytes) : "memory");
+}
+
+struct Args {
+  const uint8_t* kc;
+  const uint8_t* vc;
+  const float* ks;
+  const float* vs;
+  const __half* q;
+  long long rows_per_cta;
+  float* out;
+  float lv[16];
+};
+
+struct StageRegs {
+  uint2 k[4], v[4];
+  float ks, vs;
+};
+
+// MODE 0: LDG register ring (D deep); MODE 1: TMA smem ring (NS slots)
+// COMPUTE 0: loads only.  V16: 16-bit fixed-point V LUT.
+template <int MODE, int NW, int D, int NS, int PF, int COMPUTE, bool V16, int OPT = 0>
+__global__ void __launch_bounds__(NW * 32, 1) stream_kernel(const __grid_constant__ Args a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int NC = NW - 1;           // last warp: loader (TMA / L2 prefetch) or idle
+  constexpr uint32_t kK = V16 ? 0x8000 : 0x10000, kRing = kK + 0x10000;
+  auto lds_k = [](uint32_t off) { return lds_kt<kK>(off); };
+  auto lds_k2 = [](uint32_t o1, uint32_t o2) { return lds_k2t<kK>(o1, o2); };
+  constexpr int NSL = NS * NC;        // slots: NS per consumer warp
+  constexpr uint32_t kMbar = kRing + (MODE >= 1 ? NSL : 0) * STAGE_BYTES;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (static_cast<uint32_t>(__cvta_generic_to_shared(smem)) != kWin) __trap();
+  // V LUT (32 lane copies)
+  for (int i = tid; i < 256 * 32; i += NW * 32) {
+    const int e = i >> 5, l = i & 31;
+    const float lo = a.lv[e & 15], hi = a.lv[e >> 4];
+    if (V16) {
+      const uint32_t ul = static_cast<uint32_t>(__float2int_rn((lo + 1.0f) * 32768.0f));
+      const uint32_t uh = static_cast<uint32_t>(__float2int_rn((hi + 1.0f) * 32768.0f));
+      reinterpret_cast<uint32_t*>(smem)[e * 32 + l] = (ul > 65535u ? 65535u : ul) | ((uh > 65535u ? 65535u : uh) << 16);
+    } else {
+      reinterpret_cast<float2*>(smem)[e * 32 + l] = make_float2(lo, hi);
+    }
+  }
+  // q-table (one per CTA: the CTA streams one sequence)
+  const long long bh = blockIdx.x;
+  for (int i = tid; i < 256 * 64; i += NW * 32) {
+    const int e = i >> 6, j = i & 63;
+    const float2 qf = __half22float2(reinterpret_cast<const __half2*>(a.q + bh * HD)[j]);
+    const float c = 0.12752f;   // log2(e) / sqrt(128)
+    reinterpret_cast<float*>(smem + kK)[e * 64 + j] = __fadd_rn(__fmul_rn(qf.x * c, a.lv[e & 15]), __fmul_rn(qf.y * c, a.lv[e >> 4]));
+  }
+  const uint32_t mb_full = kWin + kMbar, mb_empty = kWin + kMbar + 8 * NSL;
+  uint32_t* s_prog = reinterpret_cast<uint32_t*>(smem + kMbar + 16 * NSL);
+  if (tid == 0) {
+    for (int s = 0; s < NSL; ++s) {
+      mbar_init(mb_full + 8 * s, 1);
+      mbar_init(mb_empty + 8 * s, 1);
+    }
+    *s_prog = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const long long r0 = blockIdx.x * a.rows_per_cta;
+  const int nst = static_cast<int>(a.rows_per_cta / ST);
+
+  if (warp == NC) {
+    if (lane != 0) return;
+    if (MODE == 1) {
+      for (int k = 0; k < nst; ++k) {
+        const int w = k % NC, j = k / NC;
+        const int s = w * NS + j % NS;
+        if (j >= NS) mbar_wait(mb_empty + 8 * s, ((j / NS) - 1) & 1);
+        const uint32_t dst = kWin + kRing + s * STAGE_BYTES;
+        const long long r = r0 + static_cast<long long>(k) * ST;
+        mbar_expect(mb_full + 8 * s, STAGE_BYTES);
+        bulk_g2s(dst, a.kc + r * ROWB, ST * ROWB, mb_full + 8 * s);
+        bulk_g2s(dst + ST * ROWB, a.vc + r * ROWB, ST * ROWB, mb_full + 8 * s);
+        bulk_g2s(dst + 2 * ST * ROWB, a.ks + r * 2, ST * 8, mb_full + 8 * s);
+        bulk_g2s(dst + 2 * ST * ROWB + ST * 8, a.vs + r * 2, ST * 8, mb_full + 8 * s);
+        if (PF > 0 && k + PF < nst) {
+          const long long rp = r0 + static_cast<long long>(k + PF) * ST;
+          bulk_pf(a.kc + rp * ROWB, ST * ROWB);
+          bulk_pf(a.vc + rp * ROWB, ST * ROWB);
+          bulk_pf(a.ks + rp * 2, ST * 8);
+          bulk_pf(a.vs + rp * 2, ST * 8);
+        }
+      }
+    } else if (PF > 0) {
+      // L2 prefetch PF stages ahead of the consumers' progress
+      int k = 0;
+      while (k < nst) {
+        const uint32_t done = *reinterpret_cast<volatile uint32_t*>(s_prog);
+        if (k < static_cast<int>(done) + PF) {
+          const long long rp = r0 + static_cast<long long>(k) * ST;
+          const int n = min(8, nst - k);     // 8 stages per instruction group
+          bulk_pf(a.kc + rp * ROWB, n * ST * ROWB);
+          bulk_pf(a.vc + rp * ROWB, n * ST * ROWB);
+          bulk_pf(a.ks + rp * 2, n * ST * 8);
+          bulk_pf(a.vs + rp * 2, n * ST * 8);
+          k += n;
+        } else {
+          __nanosleep(200);
+        }
+      }
+    }
+    return;
+  }
+
+  const int g = lane >> 3, sub = lane & 7;
+  const int rho = (g + 4 * (sub >> 2)) & 7;
+  uint32_t rotA = 0, rotB = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    rotA |= static_cast<uint32_t>((i + rho) & 7) << (4 * i);
+    rotB |= static_cast<uint32_t>((i + 4 + rho) & 7) << (4 * i);
+  }
+  uint32_t jsel[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) jsel[k] = static_cast<uint32_t>(sub * 8 + ((k + rho) & 7)) * 4u;
+  const uint32_t vsel = static_cast<uint32_t>(lane) * (V16 ? 4u : 8u);
+  uint64_t o2[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) o2[j] = 0;
+  uint32_t c65536, magic;
+  asm volatile("mov.u32 %0, 65536;" : "=r"(c65536));
+  asm volatile("mov.u32 %0, 0x43800000;" : "=r"(magic));
+  float m = -INFINITY, l = 0.0f;
+  uint32_t sink = 0;
+
+  // per-lane cursors (advanced by NC stages per consumed stage); slot i at
+  // immediate offset i*4 rows
+  const uint8_t* kp = a.kc + (r0 + warp * ST + g) * ROWB + sub * 8;
+  const uint8_t* vp = a.vc + (r0 + warp * ST + g) * ROWB + sub * 8;
+  const float* ksp = a.ks + (r0 + warp * ST + (sub & 3) * 4 + g) * 2 + (sub >> 2);
+  const float* vsp = a.vs + (r0 + warp * ST + (sub & 3) * 4 + g) * 2 + (sub >> 2);
+  auto load_ldg = [&](StageRegs& R, int k) {
+    if (OPT & 2) {
+      const uint32_t h = static_cast<uint32_t>(k) * 2654435761u + lane;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        R.k[i] = make_uint2(h * (i + 3), h ^ (0x9e3779b9u * i));
+        R.v[i] = make_uint2(h + 0x1234567u * i, h * 5u + i);
+      }
+      R.ks = 0.75f; R.vs = 1.25f;
+      return;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      R.k[i] = ld64(kp + i * 4 * ROWB);
+      R.v[i] = ld64(vp + i * 4 * ROWB);
+    }
+    R.ks = ld32(ksp);
+    R.vs = ld32(vsp);
+    kp += NC * ST * ROWB;
+    vp += NC * ST * ROWB;
+    ksp += NC * ST * 2;
+    vsp += NC * ST * 2;
+  };
+  auto load_smem = [&](StageRegs& R, int s) {
+    const unsigned char* b = smem + kRing + s * STAGE_BYTES;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      R.k[i] = *reinterpret_cast<const uint2*>(b + (i * 4 + g) * ROWB + sub * 8);
+      R.v[i] = *reinterpret_cast<const uint2*>(b + ST * ROWB + (i * 4 + g) * ROWB + sub * 8);
+    }
+    R.ks = *reinterpret_cast<const float*>(b + 2 * ST * ROWB + (((sub & 3) * 4 + g) * 2 + (sub >> 2)) * 4);
+    R.vs = *reinterpret_cast<const float*>(b + 2 * ST * ROWB + ST * 8 + (((sub & 3) * 4 + g) * 2 + (sub >> 2)) * 4);
+  };
+  auto consume = [&](const StageRegs& R) {
+    if (!COMPUTE) {
+      uint32_t x = __float_as_uint(R.ks) ^ __float_as_uint(R.vs);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) x ^= R.k[i].x ^ R.k[i].y ^ R.v[i].x ^ R.v[i].y;
+      sink ^= x;
+      return;
+    }
+    float s[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (COMPUTE == 3) { s[i] = __uint_as_float((R.k[i].x & 0x007fffffu) | 0x3f000000u); continue; }
+      const uint32_t q0 = prmt(R.k[i].x, R.k[i].y, rotA), q1 = prmt(R.k[i].x, R.k[i].y, rotB);
+      uint64_t x = lds_k2(prmt(q0, jsel[0], 0x7604), prmt(q0, jsel[1], 0x7614));
+      x = fadd2(x, lds_k2(prmt(q0, jsel[2], 0x7624), prmt(q0, jsel[3], 0x7634)));
+      const uint64_t y = lds_k2(prmt(q1, jsel[4], 0x7604), prmt(q1, jsel[5], 0x7614));
+      x = fadd2(x, fadd2(y, lds_k2(prmt(q1, jsel[6], 0x7624), prmt(q1, jsel[7], 0x7634))));
+      const float2 f = unpack2(x);
+      s[i] = f.x + f.y;
+    }
+    const bool b1 = (lane >> 1) & 1, b0 = lane & 1;
+    const float x0 = __shfl_xor_sync(0xffffffffu, b1 ? s[0] : s[2], 2);
+    const float x1 = __shfl_xor_sync(0xffffffffu, b1 ? s[1] : s[3], 2);
+    const float k0 = (b1 ? s[2] : s[0]) + x0, k1 = (b1 ? s[3] : s[1]) + x1;
+    float sj = (b0 ? k1 : k0) + __shfl_xor_sync(0xffffffffu, b0 ? k0 : k1, 1);
+    sj *= R.ks;
+    sj += __shfl_xor_sync(0xffffffffu, sj, 4);
+    float mt = fmaxf(sj, __shfl_xor_sync(0xffffffffu, sj, 1));
+    mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, 2));
+    bool up = mt > m;
+    if (OPT & 1) {                 // lazy: rescale only when a score exceeds the running max by 8
+      up = __any_sync(0xffffffffu, sj > m + 8.0f);
+      if (up) {
+        float mm = mt;
+#pragma unroll
+        for (int o = 4; o < 32; o <<= 1) mm = fmaxf(mm, __shfl_xor_sync(0xffffffffu, mm, o));
+        mt = mm;
+        up = true;
+      }
+    }
+    if ((OPT & 1) ? up : __any_sync(0xffffffffu, up)) {
+      const float corr = up ? ex2(m - mt) : 1.0f;
+      m = up ? mt : m;
+      l *= corr;
+      const uint64_t c2 = pack2(corr, corr);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o2[j] = fmul2(o2[j], c2);
+    }
+    const float pr = ex2(sj - m);
+    l += pr;
+    const float w = pr * R.vs;
+    float wv[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) wv[i] = __shfl_sync(0xffffffffu, w, (lane & ~3) | i);
+    if (V16) {
+      const float W = wv[0] + wv[1] + wv[2] + wv[3];
+      const uint64_t mW = pack2(-256.0f * W, -256.0f * W);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o2[j] = fadd2(o2[j], mW);
+    }
+    if (COMPUTE == 2) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) o2[i] = fadd2(o2[i], pack2(wv[i], __uint_as_float(R.v[i].x ^ R.v[i].y)));
+      return;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint64_t w2 = pack2(wv[i], wv[i]);
+      if (V16) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t ex = lds_v16(prmt(R.v[i].x, vsel, 0x7604 | (k << 4)));
+          const uint32_t ey = lds_v16(prmt(R.v[i].y, vsel, 0x7604 | (k << 4)));
+          uint64_t fx, fy;
+          asm("{.reg .b32 a, b;\n mad.hi.u32 a, %1, %2, %3;\n prmt.b32 b, %1, %3, 0x7610;\n mov.b64 %0, {a, b};}"
+              : "=l"(fx) : "r"(ex), "r"(c65536), "r"(magic));
+          asm("{.reg .b32 a, b;\n mad.hi.u32 a, %1, %2, %3;\n prmt.b32 b, %1, %3, 0x7610;\n mov.b64 %0, {a, b};}"
+              : "=l"(fy) : "r"(ey), "r"(c65536), "r"(magic));
+          o2[k] = ffma2(fx, w2, o2[k]);
+          o2[4 + k] = ffma2(fy, w2, o2[4 + k]);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          o2[k] = ffma2(lds_v(prmt(R.v[i].x, vsel, 0x7604 | (k << 4))), w2, o2[k]);
+          o2[4 + k] = ffma2(lds_v(prmt(R.v[i].y, vsel, 0x7604 | (k << 4))), w2, o2[4 + k]);
+        }
+      }
+    }
+  };
+
+  if (MODE == 0) {
+    StageRegs RG[D];
+    int kk[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      kk[d] = warp + d * NC;
+      if (kk[d] < nst) load_ldg(RG[d], kk[d]);
+    }
+    int k = warp;
+    while (k < nst) {
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        if (kk[d] >= nst) break;
+        StageRegs cur = RG[d];
+        const int kn = kk[d] + D * NC;
+        kk[d] = kn;
+        if (kn < nst) load_ldg(RG[d], kn);
+        consume(cur);
+        if (PF > 0 && lane == 0) atomicAdd(s_prog, 1u);
+        k += NC;
+      }
+    }
+  } else if (MODE == 1) {
+    for (int k = warp; k < nst; k += NC) {
+      const int j = k / NC;
+      const int s = warp * NS + j % NS;
+      mbar_wait(mb_full + 8 * s, (j / NS) & 1);
+      StageRegs R;
+      load_smem(R, s);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(mb_empty + 8 * s);
+      consume(R);
+    }
+  } else if (MODE == 2) {
+    // per-warp cp.async ring: own stages k_j = warp + j*NC, slot j % NS
+    const int nj = (nst - warp + NC - 1) / NC;
+    auto issue = [&](int j) {
+      if (j < nj) {
+        const long long r = r0 + static_cast<long long>(warp + j * NC) * ST;
+        const uint32_t dst = kWin + kRing + (warp * NS + j % NS) * STAGE_BYTES;
+        const uint8_t* kb = a.kc + r * ROWB;
+        const uint8_t* vb = a.vc + r * ROWB;
+        cp16(dst + lane * 16, kb + lane * 16);
+        cp16(dst + 512 + lane * 16, kb + 512 + lane * 16);
+        cp16(dst + 1024 + lane * 16, vb + lane * 16);
+        cp16(dst + 1536 + lane * 16, vb + 512 + lane * 16);
+        if (lane < 8) cp16(dst + 2048 + lane * 16, reinterpret_cast<const uint8_t*>(a.ks) + r * 8 + lane * 16);
+        else if (lane < 16) cp16(dst + 2176 + (lane - 8) * 16, reinterpret_cast<const uint8_t*>(a.vs) + r * 8 + (lane - 8) * 16);
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    for (int j = 0; j < NS - 1; ++j) issue(j);
+    for (int j = 0; j < nj; ++j) {
+      __syncwarp();                       // slot (j - 1) % NS fully read
+      issue(j + NS - 1);
+      asm volatile("cp.async.wait_group %0;" :: "n"(NS - 1) : "memory");
+      __syncwarp();
+      StageRegs R;
+      load_smem(R, warp * NS + j % NS);
+      consume(R);
+    }
+  } else {
+    // per-warp bulk-TMA ring issued by lane 0
+    const int nj = (nst - warp + NC - 1) / NC;
+    auto issue = [&](int j) {
+      if (lane == 0 && j < nj) {
+        const long long r = r0 + static_cast<long long>(warp + j * NC) * ST;
+        const int sl = warp * NS + j % NS;
+        const uint32_t dst = kWin + kRing + sl * STAGE_BYTES;
+        mbar_expect(mb_full + 8 * sl, STAGE_BYTES);
+        bulk_g2s(dst, a.kc + r * ROWB, ST * ROWB, mb_full + 8 * sl);
+        bulk_g2s(dst + ST * ROWB, a.vc + r * ROWB, ST * ROWB, mb_full + 8 * sl);
+        bulk_g2s(dst + 2 * ST * ROWB, a.ks + r * 2, ST * 8, mb_full + 8 * sl);
+        bulk_g2s(dst + 2 * ST * ROWB + ST * 8, a.vs + r * 2, ST * 8, mb_full + 8 * sl);
+      }
+    };
+    for (int j = 0; j < NS; ++j) issue(j);
+    for (int j = 0; j < nj; ++j) {
+      const int sl = warp * NS + j % NS;
+      mbar_wait(mb_full + 8 * sl, (j / NS) & 1);
+      StageRegs R;
+      load_smem(R, sl);
+      __syncwarp();
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(j + NS);
+      consume(R);
+    }
+  }
+  float acc = l + m + __uint_as_float(sink & 0x3fffffff);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float2 f = unpack2(o2[j]);
+    acc += f.x + f.y;
+  }
+  a.out[(blockIdx.x * NW + warp) * 32 + lane] = acc;
+}
+
+static int g_skip = 0, g_idx = 0;
+static unsigned long long* g_hdbg;
+template <int MODE, int NW, int D, int NS, int PF, int COMPUTE, bool V16, int OPT = 0>
+void run(const char* name, Args a, int grid, double bytes, int reps = 20) {
+  if (g_idx++ < g_skip) return;
+  auto k = stream_kernel<MODE, NW, D, NS, PF, COMPUTE, V16, OPT>;
+  const int smem = (V16 ? 0x18000 : 0x20000) + (MODE >= 1 ? NS * (NW - 1) : 0) * STAGE_BYTES + 16 * NS * (NW - 1) + 16;
+  CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  printf("%-44s ...", name);
+  k<<<grid, NW * 32, smem>>>(a);
+  CK(cudaGetLastError());
+  {
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+      unsigned long long* d = g_hdbg;
+      printf("FAIL %s: dbg %llu blk %llu tid %llu mbar %llx ph %llu\n", cudaGetErrorString(e), d[0], d[1], d[2], d[3], d[4]);
+      exit(1);
+    }
+  }
+  CK(cudaEventRecord(e0));
+  for (int i = 0; i < reps; ++i) k<<<grid, NW * 32, smem>>>(a);
+  CK(cudaEventRecord(e1));
+  CK(cudaEventSynchronize(e1));
+  float ms;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  const double us = 1e3 * ms / reps;
+  printf(" %8.1f us  %7.0f GB/s\n", us, bytes / (us * 1e-6) / 1e9);
+}
+
+int main(int argc, char** argv) {
+  setvbuf(stdout, nullptr, _IONBF, 0);
+  int dev = 0;
+  cudaDeviceProp pr;
+  CK(cudaGetDeviceProperties(&pr, dev));
+  const int grid = pr.multiProcessorCount;
+  const long long rpc = argc > 1 ? atoll(argv[1]) : 16384;   // rows per CTA
+  g_skip = argc > 2 ? atoi(argv[2]) : 0;
+  CK(cudaHostAlloc(&g_hdbg, 64, cudaHostAllocMapped));
+  {
+    unsigned long long* dp;
+    CK(cudaHostGetDevicePointer(&dp, g_hdbg, 0));
+    CK(cudaMemcpyToSymbol(g_dbg, &dp, sizeof(dp)));
+  }
+  const long long rows = rpc * grid;
+  uint8_t *kc, *vc;
+  float *ks, *vs, *out;
+  __half* q;
+  CK(cudaMalloc(&kc, rows * ROWB));
+  CK(cudaMalloc(&vc, rows * ROWB));
+  CK(cudaMalloc(&ks, rows * 8));
+  CK(cudaMalloc(&vs, rows * 8));
+  CK(cudaMalloc(&q, grid * HD * 2));
+  CK(cudaMalloc(&out, grid * 32 * 32 * 4));
+  std::vector<uint8_t> h(rows * ROWB);
+  for (size_t i = 0; i < h.size(); ++i) h[i] = static_cast<uint8_t>((i * 2654435761u) >> 13);
+  CK(cudaMemcpy(kc, h.data(), h.size(), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(vc, h.data(), h.size(), cudaMemcpyHostToDevice));
+  std::vector<float> hs(rows * 2);
+  for (size_t i = 0; i < hs.size(); ++i) hs[i] = 0.5f + (i % 7) * 0.25f;
+  CK(cudaMemcpy(ks, hs.data(), hs.size() * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(vs, hs.data(), hs.size() * 4, cudaMemcpyHostToDevice));
+  std::vector<__half> hq(grid * HD);
+  for (size_t i = 0; i < hq.size(); ++i) hq[i] = __float2half(((i * 37) % 11) * 0.1f - 0.5f);
+  CK(cudaMemcpy(q, hq.data(), hq.size() * 2, cudaMemcpyHostToDevice));
+  Args a{kc, vc, ks, vs, q, rpc, out, {}};
+  const float L[16] = {-1.0f, -0.6961928f, -0.52507293f, -0.39491743f, -0.28444132f, -0.1847734f, -0.09104998f, 0.0f,
+                       0.079580314f, 0.16093014f, 0.24611226f, 0.33791512f, 0.44070974f, 0.5626169f, 0.72295666f, 1.0f};
+  for (int i = 0; i < 16; ++i) a.lv[i] = L[i];
+  const double bytes = static_cast<double>(rows) * (2 * ROWB + 16);
+  printf("grid %d, %lld rows/CTA, %.1f MB\n", grid, rpc, bytes / 1e6);
+  run<0, 16, 2, 1, 0, 1, false>("LDG D2 compute fp32 V", a, grid, bytes);
+  run<0, 16, 2, 1, 0, 1, false, 2>("compute only fp32 V (no loads)", a, grid, bytes);
+  run<0, 16, 2, 1, 0, 1, true, 2>("compute only V16c (no loads)", a, grid, bytes);
+  run<0, 16, 2, 1, 0, 1, true>("LDG D2 compute V16c", a, grid, bytes);
+  run<2, 16, 1, 3, 0, 1, true>("cp.async DW3 V16c", a, grid, bytes);
+  run<3, 16, 1, 3, 0, 1, true>("bulk/warp DW3 V16c", a, grid, bytes);
+  return 0;
+}
