@@ -1,23 +1,31 @@
 #!/usr/bin/env python
 """NQKV decode benchmark (BASELINE.json metric: decode-attn KV tokens/s over
-the 4-bit cache; HBM GB/s vs peak).
+the 4-bit cache; HBM GB/s vs peak at 1/2/4/8 GPU).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload c2]
+                    [--workload c5] [--scaling weak|strong] [--no-configs]
 
 A step = one decode step of the whole hot path over every layer of the
-workload: 1-token NF4 quantize-append of K and V (nqkv_quantize) and fused
-dequant decode attention (nqkv_decode_attention), per layer, in layer order.
-Default workload: configs[1] (c2, OPT-1.3B-shaped: 24 layers, B=8, 32 heads,
-head_dim 64, 2048 prompt tokens, 16 decode-step slots replayed cyclically).
-Inputs are synthetic (synth/workloads.py) and resident in HBM; one step
-touches 24 layers x ~38 MB = ~0.9 GB of packed cache, more than the 126 MB L2.
+workload: per layer, the 1-token NF4 quantize-append of K and V fused with the
+dequant-in-registers decode attention (nqkv_decode_step_planned), captured as
+one CUDA graph per step.  Inputs are synthetic (synth/workloads.py) and
+resident in HBM.
 
-N > 1 (torchrun): weak scaling over heads -- every rank owns a 32-head shard
-of a 32*N-head model and the per-layer outputs are all-gathered over NCCL.
+Default workload: BASELINE.json configs[4] (c5, OPT-175B-shaped: 96 layers,
+B = 64, head_dim 128, 4096 cached tokens, blk 64) as the 8-GPU weak shard of
+12 heads per GPU (43.5 GB of 4-bit cache per GPU), the configuration
+BASELINE.json times at 1/2/4/8 GPUs.  --scaling strong splits the fixed
+96 heads over the GPUs instead (at 1 GPU the layer count is cut to what fits).
+
+At N = 1 the same JSON line also carries a "configs" block: c2, c3 (blk
+32/64/128), c4 and c5 with all 96 heads on one GPU, each with its decode and
+quantize rooflines (--no-configs skips it).
+
+N > 1 (torchrun): every rank owns its head shard; the per-layer outputs are
+all-gathered over NCCL on a side stream.
 
 --impl reference: the CPU oracle (oracle/) on rank 0, timed on a bounded
-sample of the same workload (one layer, a few heads); other ranks exit 0.
+sample of the same workload; other ranks exit 0.
 """
 from __future__ import annotations
 
@@ -104,28 +112,49 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------ cpu baseline --
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def host_cores() -> dict:
+    return {"os_cpu_count": os.cpu_count(), "affinity": len(os.sched_getaffinity(0)),
+            "cpu_model": cpu_model(), "blas_threads": blas_threads()}
+
+
 class OracleSample:
     """The CPU oracle on a bounded sample of the workload: one layer's decode
     step (1-token append of K and V + attention over the dequantised cache)
-    for `heads` heads of all B sequences.  Prefill is untimed, as on the GPU."""
+    for `heads` heads of the first `batch` sequences.  Prefill is untimed, as
+    on the GPU.  `scale` converts the sample's KV tokens to the full step's
+    (all heads of the shard, all sequences, all layers are the same work)."""
 
-    def __init__(self, w, heads: int):
+    def __init__(self, w, heads: int, batch: int | None = None, shard_heads: int | None = None):
         from oracle import nqkv_oracle as O
         from synth import workloads as W
         self.O, self.w, self.h = O, w, heads
+        self.b = w.batch if batch is None else min(batch, w.batch)
+        self.shard = w.heads if shard_heads is None else shard_heads
         hr = range(heads)
-        self.lens = W.seq_lens(w).tolist()
-        T = max(self.lens)
+        lens = W.seq_lens(w)
+        T = int(lens.max())
+        self.lens = lens[:self.b].tolist()
         Tc = W.capacity(T + 1)
         K, V = W.layer_kv(w, 0, heads=hr, tokens=T)
         k1, v1, q = W.step_inputs(w, 0, 0, heads=hr)
-        self.kc, self.ks = O.empty_cache(w.batch, heads, Tc, w.head_dim, w.blk)
-        self.vc, self.vs = O.empty_cache(w.batch, heads, Tc, w.head_dim, w.blk)
-        O.quantize_append(K.numpy(), [0] * w.batch, w.blk, self.kc, self.ks)
-        O.quantize_append(V.numpy(), [0] * w.batch, w.blk, self.vc, self.vs)
-        self.k1, self.v1, self.q = k1.numpy(), v1.numpy(), q.numpy()
-        # KV tokens of the full-H model represented by one sampled step
-        self.tokens = sum(n + 1 for n in self.lens) * heads / w.heads
+        b = self.b
+        self.kc, self.ks = O.empty_cache(b, heads, Tc, w.head_dim, w.blk)
+        self.vc, self.vs = O.empty_cache(b, heads, Tc, w.head_dim, w.blk)
+        O.quantize_append(K[:b].numpy(), [0] * b, w.blk, self.kc, self.ks)
+        O.quantize_append(V[:b].numpy(), [0] * b, w.blk, self.vc, self.vs)
+        self.k1, self.v1, self.q = k1[:b].numpy(), v1[:b].numpy(), q[:b].numpy()
+        # KV tokens (a token = all heads of the shard) represented by one sampled step
+        self.tokens = sum(n + 1 for n in self.lens) * heads / self.shard
 
     def step(self):
         O, w = self.O, self.w
@@ -136,9 +165,10 @@ class OracleSample:
 
     def describe(self, reps):
         w = self.w
-        return (f"1 of {w.layers} layers, {self.h} of {w.heads} heads, all {w.batch} sequences "
-                f"({max(self.lens)} tokens), 1-token append + attention, {reps} reps; "
-                f"value scaled to {w.heads}-head KV tokens")
+        return (f"{w.name}: 1 of {w.layers} layers, {self.h} of the {self.shard}-head shard, "
+                f"{self.b} of {w.batch} sequences ({max(self.lens)} tokens), 1-token append + "
+                f"attention, {reps} reps; value scaled to KV tokens of the full shard (a token = "
+                f"all {self.shard} heads); extrapolated linearly in heads and sequences")
 
 
 def blas_threads():
@@ -149,8 +179,15 @@ def blas_threads():
         return 1
 
 
-def cpu_baseline(w, seconds=10.0, heads=2):
-    smp = OracleSample(w, heads)
+def sample_for(w, shard_heads):
+    """Bounded oracle sample (~10-30 s of CPU work per timed loop)."""
+    per_seq = (int(w.seq_len) + 1) * w.head_dim
+    batch = max(1, min(w.batch, (1 << 22) // per_seq))      # ~4 M cached elements per head
+    return OracleSample(w, 1, batch=batch, shard_heads=shard_heads)
+
+
+def cpu_baseline(w, shard_heads, seconds=10.0):
+    smp = sample_for(w, shard_heads)
     smp.step()
     times = []
     t_end = time.perf_counter() + seconds
@@ -159,53 +196,81 @@ def cpu_baseline(w, seconds=10.0, heads=2):
         smp.step()
         times.append(time.perf_counter() - t0)
     per = statistics.median(times)
-    return {"value": smp.tokens / per, "unit": UNIT, "cores": blas_threads(), "kind": "oracle",
-            "sample": smp.describe(len(times)) + f"; host cores available {len(os.sched_getaffinity(0))}"}
+    hc = host_cores()
+    return {"value": smp.tokens / per, "unit": UNIT, "cores": hc["blas_threads"], "kind": "oracle",
+            "sample": smp.describe(len(times)), "host": hc}
 
 
 def run_reference(args, w, rank, world):
     """Base-contract reference arm = the oracle, timed as it stands."""
     if rank != 0:
         return 0
-    smp = OracleSample(w, 1)
+    shard = shard_heads(w, args.scaling, world)
+    smp = sample_for(w, shard)
     for _ in range(args.warmup):
         smp.step()
     t0 = time.perf_counter()
     for _ in range(args.steps):
         smp.step()
     el = time.perf_counter() - t0
-    val = smp.tokens * args.steps / el
+    val = smp.tokens * args.steps / el          # KV tokens of the sampled layer-steps / time
+    hc = host_cores()
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT,
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": w.name, "oracle": "numpy float64 oracle/nqkv_oracle.py",
-                       "step": smp.describe(args.steps)},
-            "cpu_baseline": {"value": val, "unit": UNIT, "cores": blas_threads(), "kind": "oracle",
-                             "sample": smp.describe(args.steps)},
+            "config": {"workload": workload_name(w, shard, world, args.scaling),
+                       "oracle": "numpy float64 oracle/nqkv_oracle.py", "step": smp.describe(args.steps)},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": hc["blas_threads"], "kind": "oracle",
+                             "sample": smp.describe(args.steps), "host": hc},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 
 
 # -------------------------------------------------------------------- ours --
-def run_ours(args, w, rank, world, local_rank):
+WEAK_SHARD = {"c1": 12, "c2": 32, "c3": 32, "c4": 5, "c5": 12}    # heads per GPU (c4/c5: the 8-GPU shard)
+
+
+def shard_heads(w, scaling, world):
+    key = w.name.split("-")[0]
+    if scaling == "strong":
+        return w.heads // world
+    return WEAK_SHARD.get(key, w.heads)
+
+
+def workload_name(w, shard, world, scaling):
+    return (f"{w.name} (BASELINE configs[{int(w.name[1]) - 1}]): {w.layers} layers, B={w.batch}, "
+            f"{shard} heads/GPU x {world} GPU ({scaling}), head_dim {w.head_dim}, "
+            f"{'lengths U[%d, %d]' % (w.ragged_min, w.seq_len) if w.ragged_min else '%d cached tokens' % w.seq_len}"
+            f" + 1 appended per step, NF4 blk {w.blk}, fp32 scales")
+
+
+def layers_that_fit(w, heads, dev, reserve=0.80):
+    """Largest layer count whose cache fits in `reserve` of free memory
+    (BASELINE.json c5: "scaling the layer count to fit a single GPU")."""
+    import torch
+    from synth import workloads as W
+    T = int(W.seq_lens(w).max())
+    Tc = W.capacity(T + w.decode_steps)
+    per = 2 * w.batch * heads * Tc * (w.head_dim // 2 + 4 * w.head_dim // w.blk)
+    gen = 3 * w.batch * T * heads * w.head_dim * 2          # prefill generation buffers
+    free = torch.cuda.mem_get_info(dev)[0]
+    return max(1, min(w.layers, int((reserve * free - gen) // per)))
+
+
+def measure(args, w, heads, dev, world, group, layers=None, steps=None, warmup=None, e2e=False,
+            isolated=True):
+    """Prefill (bulk quantize, L2 flushed per launch), capture the step
+    graphs, time `steps` replays on the device.  Returns a result dict (and the
+    runner when e2e is requested)."""
     import torch
     import torch.distributed as dist
-
-    import __graft_entry__
-    __graft_entry__.build()
-    from paper_2505_16210_b200 import sharding
     from paper_2505_16210_b200.runtime import DecodeRunner
 
-    dev = torch.device("cuda", local_rank)
-    torch.cuda.set_device(dev)
-    group = dist.group.WORLD if world > 1 else None
-    heads = sharding.weak_head_range(rank, w.heads, max(w.blk // w.head_dim, 1))
-    runner = DecodeRunner(w, heads, dev, group=group, world=world)
-    peak, peak_src = load_peaks()
-
-    # prefill (bulk quantize) with L2 flushed before each launch: quantize roofline
+    steps = args.steps if steps is None else steps
+    warmup = args.warmup if warmup is None else warmup
+    runner = DecodeRunner(w, heads, dev, group=group, world=world, layers=layers)
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     flush = torch.empty(max(2 * l2, 256 << 20) // 4, dtype=torch.float32, device=dev)
     q_ms = runner.prefill(flush=flush)
@@ -215,20 +280,16 @@ def run_ours(args, w, rank, world, local_rank):
     q_gbs = [q_bytes / (t * 1e-3) / 1e9 for t in q_ms]
     del flush
     torch.cuda.synchronize()
-
-    # warm-up (eager, initialises kernel attributes) then capture graphs
     runner.step(0)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    runner.capture(timing_slots=(0,))
-    for i in range(args.warmup):
+    runner.capture(timing_slots=(0,) if isolated else ())
+    for i in range(warmup):
         runner.replay(i)
     torch.cuda.synchronize()
-
-    # ---------------------------------------------------------- timed region
     sampler = ClockSampler(torch.cuda.current_device() if "CUDA_VISIBLE_DEVICES" in os.environ
-                           else local_rank)
+                           else dev.index or 0)
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     if world > 1:
@@ -236,15 +297,15 @@ def run_ours(args, w, rank, world, local_rank):
     torch.cuda.synchronize()
     with sampler:
         e0.record()
-        for i in range(args.steps):
-            runner.replay(args.warmup + i)
+        for i in range(steps):
+            runner.replay(warmup + i)
         e1.record()
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     ms = e0.elapsed_time(e1)
-    dec_ms = runner.decode_kernel_ms()          # slot 0's last replay (inside the region)
-    tokens = sum(runner.tokens_per_step(args.warmup + i) for i in range(args.steps))
+    dec_ms = runner.decode_kernel_ms() if isolated else []
+    tokens = sum(runner.tokens_per_step(warmup + i) for i in range(steps))
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -252,43 +313,67 @@ def run_ours(args, w, rank, world, local_rank):
         tok = torch.tensor([tokens], dtype=torch.float64, device=dev)
         dist.all_reduce(tok, op=dist.ReduceOp.SUM)
         tokens = float(tok.item())
-    value = tokens / (ms * 1e-3)
+    L = runner.L
+    bytes_per_launch = runner.decode_bytes(0)
+    chained_ms = (ms / steps) / L
+    res = {"value": tokens / (ms * 1e-3), "ms_per_step": ms / steps, "layers": L,
+           "heads": runner.Hl, "bytes_per_launch": bytes_per_launch, "chained_launch_us": chained_ms * 1e3,
+           "decode_gbs": bytes_per_launch / (chained_ms * 1e-3) / 1e9,
+           "isolated_launch_us": statistics.mean(dec_ms) * 1e3 if dec_ms else None,
+           "quantize_gbs": statistics.median(q_gbs), "quantize_bytes_per_launch": q_bytes,
+           "quantize_launches": len(q_ms), "clocks": sampler.summary(),
+           "gpu_launches": runner.launches_per_step() * steps, "steps": steps}
+    if e2e:
+        return res, runner
+    del runner
+    torch.cuda.empty_cache()
+    return res, None
 
-    # ------------------------------------------------------------- e2e (host)
+
+def e2e_measure(args, runner, world, dev):
+    """Same metric through the public API with host buffers: every step's new
+    k/v/q go host->device (pinned) and every layer's output device->host,
+    inside the timed region (pipelined on a copy stream)."""
+    import torch
+    import torch.distributed as dist
     host_in = torch.empty(runner.inputs.shape, dtype=runner.inputs.dtype, pin_memory=True)
     host_in.copy_(runner.inputs.cpu())
     host_out = torch.empty(runner.out.shape, dtype=runner.out.dtype, pin_memory=True)
     h2d = host_in[0].numel() * host_in.element_size()
     d2h = host_out.numel() * host_out.element_size()
-    # Pipelined: step i+1's inputs go host->device on a copy stream while step
-    # i computes, and step i's outputs come back device->host on it right after
-    # step i (outputs are double-buffered by slot parity, so step i+1 never
-    # waits for that read).  Every step still moves its own inputs in and its
-    # own outputs out inside the timed region.
     main = torch.cuda.current_stream()
     cs = torch.cuda.Stream()
-    h2d_ev = [torch.cuda.Event() for _ in range(runner.S)]
+    n_slots = len(runner.graphs)
+    # H2D lands in one of two device staging buffers on the copy stream (the
+    # next step's inputs while this step computes); the step then takes them
+    # with one device-to-device copy into its input slot (stream-ordered)
+    stage = torch.empty((2,) + tuple(runner.inputs.shape[1:]), dtype=runner.inputs.dtype,
+                        device=runner.inputs.device)
+    h2d_ev = [torch.cuda.Event() for _ in range(2)]
+    used_ev = [torch.cuda.Event() for _ in range(2)]
     d2h_ev = [torch.cuda.Event() for _ in range(2)]
     comp_ev = torch.cuda.Event()
 
     def e2e_run(first, n):
         with torch.cuda.stream(cs):
-            s0 = first % runner.S
-            runner.inputs[s0].copy_(host_in[s0], non_blocking=True)
-            h2d_ev[s0].record(cs)
+            stage[first % 2].copy_(host_in[first % runner.S], non_blocking=True)
+            h2d_ev[first % 2].record(cs)
         for i in range(first, first + n):
-            s, s1 = i % runner.S, (i + 1) % runner.S
-            main.wait_event(h2d_ev[s])
-            main.wait_event(d2h_ev[s % 2])       # this slot's output buffer was read back
-            runner.replay(s)
+            p, s = i % 2, i % runner.S
+            main.wait_event(h2d_ev[p])
+            main.wait_event(d2h_ev[p])           # this parity's output buffer was read back
+            runner.inputs[s].copy_(stage[p])
+            used_ev[p].record(main)
+            runner.replay(i % n_slots)
             comp_ev.record(main)
             with torch.cuda.stream(cs):
                 if i + 1 < first + n:
-                    runner.inputs[s1].copy_(host_in[s1], non_blocking=True)
-                    h2d_ev[s1].record(cs)
+                    cs.wait_event(used_ev[1 - p])    # staging buffer free again
+                    stage[1 - p].copy_(host_in[(i + 1) % runner.S], non_blocking=True)
+                    h2d_ev[1 - p].record(cs)
                 cs.wait_event(comp_ev)
-                host_out.copy_(runner.out_of(s), non_blocking=True)
-                d2h_ev[s % 2].record(cs)
+                host_out.copy_(runner.out_of(i % n_slots), non_blocking=True)
+                d2h_ev[p].record(cs)
         main.wait_stream(cs)
 
     e2e_run(0, min(args.warmup, 4))
@@ -306,73 +391,144 @@ def run_ours(args, w, rank, world, local_rank):
         t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
-    e2e_value = tokens / (e2e_ms * 1e-3)
+    tokens = sum(runner.tokens_per_step(args.warmup + i) for i in range(args.steps))
+    if world > 1:
+        tok = torch.tensor([tokens], dtype=torch.float64, device=dev)
+        dist.all_reduce(tok, op=dist.ReduceOp.SUM)
+        tokens = float(tok.item())
+    return {"value": tokens / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h,
+            "how": "pinned H2D of every layer's new k/v/q into a device staging buffer, a D2D copy "
+                   "into the step's input slot, graph replay, D2H of every layer's output; the next "
+                   "step's H2D and this step's D2H run on a copy stream beside the step's kernels "
+                   "(staging and outputs double-buffered)"}
 
+
+def load_traffic(name):
+    """DRAM bytes per decode launch from the committed ncu capture of the same
+    launch configuration (profiles/traffic.json; in-process DRAM counters are
+    not available to this process)."""
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        d = json.load(open(tp)).get(name, {})
+        return d.get("decode_dram_bytes_per_launch"), d.get("quantize_dram_bytes_per_launch"), d.get("source")
+    except Exception:
+        return None, None, None
+
+
+def extra_configs(args, dev, peak):
+    """Per-config rooflines at N = 1 (BASELINE configs[1..4]); fewer steps,
+    the sweep variants with fewer layers (per-launch numbers do not depend on
+    the layer count once a step reads more than L2)."""
+    import dataclasses
+    from synth import workloads as W
+    out = {}
+    plan = [("c2", W.CONFIGS["c2"], 32, None), ("c3", W.CONFIGS["c3"], 32, None),
+            ("c3-blk32", dataclasses.replace(W.CONFIGS["c3"], blk=32), 32, 8),
+            ("c3-blk128", dataclasses.replace(W.CONFIGS["c3"], blk=128), 32, 8),
+            ("c4", W.CONFIGS["c4"], 40, None), ("c5-96heads", W.CONFIGS["c5"], 96, -1)]
+    for key, w, heads, layers in plan:
+        if layers == -1:
+            layers = layers_that_fit(w, heads, dev)
+        try:
+            r, _ = measure(args, w, range(heads), dev, 1, None, layers=layers, steps=10, warmup=3,
+                           isolated=False)
+        except Exception as e:  # noqa: BLE001 -- report, keep the headline
+            out[key] = {"error": str(e)[:200]}
+            continue
+        out[key] = {"workload": workload_name(w, heads, 1, "strong" if key.startswith("c5") else "weak"),
+                    "layers_timed": r["layers"], "value": r["value"], "unit": UNIT,
+                    "ms_per_step": r["ms_per_step"],
+                    "decode_roofline": {"achieved": r["decode_gbs"], "peak": peak, "unit": "GB/s",
+                                        "frac": r["decode_gbs"] / peak,
+                                        "bytes_per_launch": r["bytes_per_launch"],
+                                        "mean_launch_us": r["chained_launch_us"]},
+                    "quantize_roofline": {"achieved": r["quantize_gbs"], "peak": peak, "unit": "GB/s",
+                                          "frac": r["quantize_gbs"] / peak,
+                                          "bytes_per_launch": r["quantize_bytes_per_launch"]},
+                    "clocks": r["clocks"]}
+    return out
+
+
+def run_ours(args, w, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import __graft_entry__
+    __graft_entry__.build()
+    from paper_2505_16210_b200 import sharding
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    group = dist.group.WORLD if world > 1 else None
+    shard = shard_heads(w, args.scaling, world)
+    grp = max(w.blk // w.head_dim, 1)
+    if args.scaling == "strong":
+        heads = sharding.head_range(rank, world, w.heads, grp)
+        layers = layers_that_fit(w, shard, dev)
+        if world > 1:
+            t = torch.tensor([layers], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MIN)
+            layers = int(t.item())
+    else:
+        heads = sharding.weak_head_range(rank, shard, grp)
+        layers = None
+    peak, peak_src = load_peaks()
+    r, runner = measure(args, w, heads, dev, world, group, layers=layers, e2e=True)
+    e2e = e2e_measure(args, runner, world, dev)
+    L = runner.L
+    del runner
+    torch.cuda.empty_cache()
     if rank != 0:
         return 0
-    # roofline for the dominant kernel (decode attention): algorithmic bytes
-    # per launch / average launch duration.  The launches of a step are
-    # PDL-chained (each one's prologue overlaps its predecessor's tail), so the
-    # average duration is the device-timed step time over the decode launches
-    # of a step -- conservative: the per-step plan kernel is charged to them.
-    # The isolated duration (CUDA events around each launch, which break the
-    # chaining) is reported beside it.
-    bytes_per_launch = runner.decode_bytes(0)
-    dec_mean_ms = statistics.mean(dec_ms) if dec_ms else float("nan")
-    chained_ms = (ms / args.steps) / w.layers
-    achieved = bytes_per_launch / (chained_ms * 1e-3) / 1e9
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tp):
-        try:
-            traffic = json.load(open(tp)).get(w.name, {}).get("decode_dram_bytes_per_launch")
-        except Exception:
-            traffic = None
+    traffic, q_traffic, t_src = load_traffic(w.name)
     cpu = None
+    configs = None
     if world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(w)
-    clocks = sampler.summary()
+        cpu = cpu_baseline(w, shard)
+    if world == 1 and not args.no_configs:
+        configs = extra_configs(args, dev, peak)
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True,
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {
-            "workload": f"{w.name}: {w.layers} layers, B={w.batch}, {w.heads} heads/GPU x "
-                        f"{world} GPU, head_dim {w.head_dim}, prompt {T} + {runner.S} decode-step "
-                        f"slots replayed cyclically, NF4 blk {w.blk}, fp32 scales",
+            "workload": workload_name(w, shard, world, args.scaling) +
+                        (f"; {L} of {w.layers} layers (fit one GPU)" if L != w.layers else ""),
             "storage": "nf4 codes (u4) + fp32 block scales; fp32 arithmetic",
-            "l2": f"inputs larger than L2: one step reads {w.layers} layers x "
-                  f"{runner.caches[0].nbytes() / 1e6:.1f} MB of packed cache (L2 "
-                  f"{l2 / 1e6:.0f} MB)",
-            "execution": "per-step CUDA graph; one fused nqkv_decode_step launch per layer (append + attend, PDL-chained)",
-            "parallelism": f"head-sharded x{world} (weak)" + (", NCCL all-gather of outputs"
-                                                              if world > 1 else ""),
+            "l2": f"inputs larger than L2: one step reads {L} layers x "
+                  f"{r['bytes_per_launch'] / 1e6:.1f} MB of packed cache (L2 "
+                  f"{torch.cuda.get_device_properties(dev).L2_cache_size / 1e6:.0f} MB)",
+            "execution": "per-step CUDA graph; per-step plan kernel + one fused nqkv_decode_step "
+                         "launch per layer (append + attend, PDL-chained)",
+            "parallelism": f"head-sharded x{world} ({args.scaling})" +
+                           (", NCCL all-gather of outputs on a side stream" if world > 1 else ""),
         },
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "decode_kernel (nqkv_decode_attention)",
-                     "bytes_per_launch": bytes_per_launch, "mean_launch_us": chained_ms * 1e3,
-                     "launches_timed": args.steps * w.layers, "peak_source": peak_src,
+        "roofline": {"bound": "hbm", "achieved": r["decode_gbs"], "peak": peak, "unit": "GB/s",
+                     "frac": r["decode_gbs"] / peak, "traffic": traffic,
+                     "traffic_source": t_src or "none",
+                     "kernel": "decode_kernel (nqkv_decode_step_planned)",
+                     "bytes_per_launch": r["bytes_per_launch"], "mean_launch_us": r["chained_launch_us"],
+                     "launches_timed": args.steps * L, "peak_source": peak_src,
                      "timing": "device-timed step (CUDA events around the timed region) / decode "
                                "launches per step; launches PDL-chained inside the step graph; the "
                                "per-step plan kernel is charged to them",
-                     "isolated_launch_us": dec_mean_ms * 1e3,
+                     "isolated_launch_us": r["isolated_launch_us"],
                      "isolated_timing": "CUDA events around every layer's launch in step slot "
-                                        "0's graph (its last replay inside the timed region; "
-                                        "the events break the PDL chaining)"},
-        "quantize_roofline": {"bound": "hbm", "achieved": statistics.median(q_gbs), "peak": peak,
-                              "unit": "GB/s", "frac": statistics.median(q_gbs) / peak,
+                                        "0's graph (last replay inside the timed region; the "
+                                        "events break the PDL chaining)"},
+        "quantize_roofline": {"bound": "hbm", "achieved": r["quantize_gbs"], "peak": peak,
+                              "unit": "GB/s", "frac": r["quantize_gbs"] / peak, "traffic": q_traffic,
                               "kernel": "quantize_kernel (nqkv_quantize, bulk prefill, L2 flushed)",
-                              "bytes_per_launch": q_bytes, "launches": len(q_ms)},
+                              "bytes_per_launch": r["quantize_bytes_per_launch"],
+                              "launches": r["quantize_launches"]},
         "cpu_baseline": cpu,
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h,
-                "how": "pinned H2D of every layer's new k/v/q, graph replay, D2H of every "
-                       "layer's output; the next step's H2D and this step's D2H run on a "
-                       "copy stream beside the step's kernels (outputs double-buffered)"},
-        "gpu_launches": runner.launches_per_step() * args.steps,
-        "clocks": clocks,
+        "e2e": e2e,
+        "gpu_launches": r["gpu_launches"],
+        "clocks": r["clocks"],
     }
+    if configs is not None:
+        line["configs"] = configs
     print(json.dumps(line), flush=True)
     return 0
 
@@ -380,11 +536,13 @@ def run_ours(args, w, rank, world, local_rank):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=1000)
-    ap.add_argument("--warmup", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c2")
+    ap.add_argument("--workload", default="c5")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-configs", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
