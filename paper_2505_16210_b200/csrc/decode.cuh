@@ -70,7 +70,7 @@ constexpr int kMinTokensPerCta = 512;  // below this a CTA's table build would d
 #define NQKV_SPLIT -1            // split K/V ring: 1 on, 0 off, -1 hd 64 only (measured)
 #endif
 #ifndef NQKV_PF
-#define NQKV_PF -1               // L2 prefetch distance in a warp's own stages (-1: per head_dim default)
+#define NQKV_PF 0                // bulk L2 prefetch distance in a warp's own stages (0: off; measured: no gain)
 #endif
 constexpr int kDecodeWarps = NQKV_DECODE_WARPS;
 constexpr int kLaneDims = 16;          // head dims owned by one lane
@@ -233,6 +233,18 @@ __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
       ".reg .pred p;\n"
       "WAIT_%=:\n"
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" :: "r"(mbar), "r"(phase) : "memory");
+}
+// the same with a suspend-time hint: a waiter that is expected to wait long
+// (the producer, for a whole piece) sleeps instead of re-polling, leaving the
+// issue slots of its scheduler to the consumer warps
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t mbar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n"
       "@!p bra WAIT_%=;\n"
       "}\n" :: "r"(mbar), "r"(phase) : "memory");
 }
@@ -1267,198 +1279,127 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
   // so the same per-half reduce-scatter applies)
   constexpr bool RS = BLK >= kLaneDims * kTPS && kTPS == 4;
   const uint32_t soff_rs = RS ? static_cast<uint32_t>((sub & 3) * G * NBLK * SB) : 0u;
-  // Per-lane 32-bit byte offsets (codes, scales) of the load cursor: this
-  // lane's bytes of the stage to load next (token tok0 + g of its (b, h));
-  // slot i is at the immediate offset i*G rows.  Advanced by NC*ST rows per
-  // stage.  (The host guarantees each codes tensor is < 4 GB.)
-  uint32_t loff_c = 0, loff_s = 0;
-  auto set_ptrs = [&](int rb, int srb, int tok0) {
-    const uint32_t r = static_cast<uint32_t>(rb + tok0 + g);
-    loff_c = r * (HD / 2) + sub * 8;
-    const uint32_t rs = GRP ? static_cast<uint32_t>(srb + tok0 + g) : r;
-    loff_s = (rs * NBLK + sidx) * SB;
-  };
+  // ---- load cursor: this lane's bytes of the next stage this warp loads.
+  // Stage ls of piece lp (ST tokens from lp.t0 + ls * ST) belongs to
+  // consumer (ls + lro) mod NC, where lro (the warp of the piece's first
+  // stage) continues the previous piece's round robin: over a CTA's whole
+  // range the warps' stage counts differ by at most one.  Fast path (the next
+  // stage is in the same piece): pointer increments only; the piece walk runs
+  // at piece boundaries.  (The host guarantees each codes tensor is < 4 GB,
+  // so row offsets fit 32 bits.)
   using StageRegs = StageRegsT<RS>;
-  auto load_stage = [&](StageRegs& Rg, int rb, int tok0, int t1) {
+  Piece lp = p0;
+  int ls = warp, lpi = 0, lro = 0, lns = nstages(p0), ltok = 0;
+  bool lvalid = warp < NC;
+  const uint8_t* kcp = p.kc;
+  const uint8_t* vcp = p.vc;
+  const uint8_t* ksp = static_cast<const uint8_t*>(p.ks);
+  const uint8_t* vsp = static_cast<const uint8_t*>(p.vs);
+  constexpr int KSTEP = NC * ST * (HD / 2), SSTEP = NC * ST * NBLK * SB;
+  auto set_cursor = [&]() {
+    ltok = lp.t0 + ls * ST;
+    const uint32_t r = static_cast<uint32_t>(rowbase(lp) + ltok + g);
+    const uint32_t rs = GRP ? static_cast<uint32_t>(srowbase(lp) + ltok + g) : r;
+    kcp = p.kc + (r * (HD / 2) + sub * 8);
+    vcp = p.vc + (r * (HD / 2) + sub * 8);
+    const uint32_t so = (rs * NBLK + sidx) * SB + soff_rs;
+    ksp = static_cast<const uint8_t*>(p.ks) + so;
+    vsp = static_cast<const uint8_t*>(p.vs) + so;
+  };
+  // cursor at this warp's first stage at or after (lp, ls): walks pieces
+  auto seek = [&]() -> bool {
+    while (ls >= lns) {
+      lro = (lro + lns) % NC;
+      if (!walk_next(lp, lpi)) { lvalid = false; return false; }
+      ++lpi;
+      lns = nstages(lp);
+      ls = warp >= lro ? warp - lro : warp + NC - lro;
+    }
+    set_cursor();
+    return true;
+  };
+  // bulk L2 prefetch (a hint: may run before the PDL wait) of this warp's
+  // stage NQKV_PF ahead in the same piece, issued by lane 0 (whose cursor is
+  // the stage's first row, byte 0)
+  auto prefetch_ahead = [&]() {
+    if (NQKV_PF > 0 && lane == 0 && ls + NQKV_PF * NC < lns) {
+      prefetch_l2(kcp + NQKV_PF * KSTEP, ST * (HD / 2));
+      prefetch_l2(vcp + NQKV_PF * KSTEP, ST * (HD / 2));
+      prefetch_l2(ksp + NQKV_PF * SSTEP, ST * NBLK * SB);
+      prefetch_l2(vsp + NQKV_PF * SSTEP, ST * NBLK * SB);
+    }
+  };
+  // this warp's next stage
+  auto advance = [&]() -> bool {
+    if (!lvalid) return false;
+    ls += NC;
+    if (ls < lns) {
+      ltok += NC * ST;
+      kcp += KSTEP;
+      vcp += KSTEP;
+      ksp += SSTEP;
+      vsp += SSTEP;
+      return true;
+    }
+    return seek();
+  };
+  // loads of the cursor's stage; rows >= t1 are not loaded (a partial stage
+  // -- only a piece's last -- keeps earlier finite data in those slots, and
+  // consume masks them)
+  auto load_stage = [&](StageRegs& Rg, int& tok0, int& t1, int& pi, int dep) {
+    tok0 = ltok;
+    t1 = lp.t1;
+    pi = lpi;
 #ifdef NQKV_EXP_NOLOAD
 #pragma unroll
     for (int i = 0; i < kTPS; ++i) {
       Rg.k[i] = make_uint2(0x12345678u * (i + 1) + tok0, 0x9abcdef0u + lane);
       Rg.v[i] = make_uint2(0x31415926u * (i + 3) + tok0, 0x27182818u + lane);
     }
-#pragma unroll
-    for (int i = 0; i < (RS ? 1 : kTPS); ++i) {
-      Rg.ks[i] = 1.0f;
-      Rg.vs[i] = 0.5f;
-    }
     return;
 #endif
-    (void)rb;
-    // rows >= t1 are not loaded: the slot keeps earlier (finite) data and is
-    // masked in consume
+    // The loads are predicated on rows < t1, and the predicate carries `dep`
+    // (always 0, but computed from the previous stage's first code word):
+    // ptxas puts every global load of this loop on one scoreboard, so the
+    // next stage's loads must not issue before the wait for the current
+    // stage's data -- otherwise that wait would also wait for them.
+    const int row0 = ltok + g + dep;
 #pragma unroll
     for (int i = 0; i < kTPS; ++i) {
-      if (tok0 + i * G + g < t1) {
-        Rg.k[i] = ldg_stream_64(p.kc + loff_c + i * G * (HD / 2));
-        Rg.v[i] = ldg_stream_64(p.vc + loff_c + i * G * (HD / 2));
+      if (row0 + i * G < t1) {
+        Rg.k[i] = ldg_stream_64(kcp + i * G * (HD / 2));
+        Rg.v[i] = ldg_stream_64(vcp + i * G * (HD / 2));
         if constexpr (!RS) {
-          Rg.ks[i] = ld_scale<F16S>(p.ks, loff_s + i * G * NBLK * SB);
-          Rg.vs[i] = ld_scale<F16S>(p.vs, loff_s + i * G * NBLK * SB);
+          Rg.ks[i] = ld_scale<F16S>(ksp, i * G * NBLK * SB);
+          Rg.vs[i] = ld_scale<F16S>(vsp, i * G * NBLK * SB);
         }
       }
     }
     if constexpr (RS) {
-      if (tok0 + (sub & 3) * G + g < t1) {
-        Rg.ks[0] = ld_scale<F16S>(p.ks, loff_s + soff_rs);
-        Rg.vs[0] = ld_scale<F16S>(p.vs, loff_s + soff_rs);
+      if (row0 + (sub & 3) * G < t1) {
+        Rg.ks[0] = ld_scale<F16S>(ksp, 0);
+        Rg.vs[0] = ld_scale<F16S>(vsp, 0);
       }
     }
   };
-  // Load cursor (piece lp, stage ls, piece index lpi): D - 1 stages ahead of
-  // consumption, across piece boundaries.  It advances lazily (at the next
-  // fill), so a warp whose first stage lies in piece 0 issues that load before
-  // any piece walking -- in plan mode before the per-batch arrays are in
-  // shared memory.
-  Piece lp = p0;
-  // Stage ls of piece lp belongs to warp (ls + lro) mod NC, where lro (the
-  // warp of the piece's first stage) continues the previous piece's round
-  // robin: over a CTA's whole range the warps' stage counts differ by at most
-  // one (a per-piece restart at warp 0 would give the low warps one extra
-  // stage per piece).
-  int ls = warp, lpi = 0, lro = 0;
-  bool lvalid = warp < NC, ladv = false;
-  int lrb = rowbase(p0);
-  set_ptrs(lrb, srowbase(p0), p0.t0 + warp * ST);
-  // register ring: buffer d holds the stage at (tok0 mtok[d], piece end mt1[d],
-  // piece index mpi[d]); refilled with the cursor's next stage once consumed
-  constexpr int D = NQKV_DEPTH;
-  // L2 prefetch distance (own stages): +11% steady state at hd 128, none at
-  // hd 64 (tools/run_var.sh)
-  constexpr int PF = NQKV_PF >= 0 ? NQKV_PF : (HD == 128 ? 2 : 0);
-  StageRegs RG[D];
+  // two-stage register ring, unrolled as buffers A and B
+  StageRegs RA, RB;
 #pragma unroll
-  for (int d = 0; d < D; ++d) {
-#pragma unroll
-    for (int i = 0; i < kTPS; ++i) {
-      RG[d].k[i] = RG[d].v[i] = make_uint2(0, 0);
-      RG[d].ks[i] = RG[d].vs[i] = 0.0f;
-    }
+  for (int i = 0; i < kTPS; ++i) {
+    RA.k[i] = RA.v[i] = RB.k[i] = RB.v[i] = make_uint2(0, 0);
+    RA.ks[RS ? 0 : i] = RA.vs[RS ? 0 : i] = RB.ks[RS ? 0 : i] = RB.vs[RS ? 0 : i] = 0.0f;
   }
-  int mtok[D], mt1[D], mpi[D];
-  bool has[D];
-  auto fill = [&](int d) -> bool {
-    if (!lvalid) return false;
-    if (ladv) {
-      ls += NC;
-      loff_c += NC * ST * (HD / 2);
-      loff_s += NC * ST * NBLK * SB;
-    }
-    ladv = true;
-    if (ls >= nstages(lp)) {
-      do {
-        lro = (lro + nstages(lp)) % NC;
-        if (!walk_next(lp, lpi)) { lvalid = false; return false; }
-        ls = warp >= lro ? warp - lro : warp + NC - lro;
-        ++lpi;
-      } while (ls >= nstages(lp));
-      lrb = rowbase(lp);
-      set_ptrs(lrb, srowbase(lp), lp.t0 + ls * ST);
-    }
-    mtok[d] = lp.t0 + ls * ST;
-    mt1[d] = lp.t1;
-    mpi[d] = lpi;
-    load_stage(RG[d], lrb, mtok[d], mt1[d]);
-    // L2 prefetch of this warp's stage PF ahead in the same piece
-    if (PF > 0 && ls + PF * NC < nstages(lp)) {
-      const int t = lp.t0 + (ls + PF * NC) * ST;
-      prefetch_rows_l2<HD, NBLK, SB>(p, lane, static_cast<long long>(lrb) + t,
-                                 static_cast<long long>(lrb) + min(t + ST, lp.t1),
-                                 GRP ? static_cast<long long>((loff_s / SB - sidx) / NBLK) - g + PF * NC * ST
-                                     : static_cast<long long>(lrb) + t);
-    }
-    return true;
-  };
-  constexpr bool SPL = NQKV_SPLIT > 0 || (NQKV_SPLIT < 0 && HD == 64);
-  // Split ring (D = 2, SPL): a stage's K half is consumed before its V half, so
-  // K slot d is refilled with stage k + 2 right after stage k's scores and V
-  // slot d with stage k + 1... one step later: K loads get ~1.5 steps and V
-  // loads ~1.5 steps to land instead of one, with the same registers.
-  static_assert(!SPL || D == 2, "split ring needs D = 2");
-  uint32_t voff_c[D], voff_s[D];
-  auto fill_k = [&](int d) -> bool {
-    if (!lvalid) return false;
-    if (ladv) {
-      ls += NC;
-      loff_c += NC * ST * (HD / 2);
-      loff_s += NC * ST * NBLK * SB;
-    }
-    ladv = true;
-    if (ls >= nstages(lp)) {
-      do {
-        lro = (lro + nstages(lp)) % NC;
-        if (!walk_next(lp, lpi)) { lvalid = false; return false; }
-        ls = warp >= lro ? warp - lro : warp + NC - lro;
-        ++lpi;
-      } while (ls >= nstages(lp));
-      lrb = rowbase(lp);
-      set_ptrs(lrb, srowbase(lp), lp.t0 + ls * ST);
-    }
-    const int tok0 = lp.t0 + ls * ST, t1 = lp.t1;
-    mtok[d] = tok0;
-    mt1[d] = t1;
-    mpi[d] = lpi;
-    voff_c[d] = loff_c;
-    voff_s[d] = loff_s;
-    StageRegs& Rg = RG[d];
-#pragma unroll
-    for (int i = 0; i < kTPS; ++i) {
-      if (tok0 + i * G + g < t1) {
-        Rg.k[i] = ldg_stream_64(p.kc + loff_c + i * G * (HD / 2));
-        if constexpr (!RS)
-          Rg.ks[i] = ld_scale<F16S>(p.ks, loff_s + i * G * NBLK * SB);
-      }
-    }
-    if constexpr (RS) {
-      if (tok0 + (sub & 3) * G + g < t1)
-        Rg.ks[0] = ld_scale<F16S>(p.ks, loff_s + soff_rs);
-    }
-    if (PF > 0 && ls + PF * NC < nstages(lp)) {
-      const int t = lp.t0 + (ls + PF * NC) * ST;
-      prefetch_rows_l2<HD, NBLK, SB>(p, lane, static_cast<long long>(lrb) + t,
-                                 static_cast<long long>(lrb) + min(t + ST, lp.t1),
-                                 GRP ? static_cast<long long>((loff_s / SB - sidx) / NBLK) - g + PF * NC * ST
-                                     : static_cast<long long>(lrb) + t);
-    }
-    return true;
-  };
-  auto fill_v = [&](int d) {
-    const int tok0 = mtok[d], t1 = mt1[d];
-    StageRegs& Rg = RG[d];
-#pragma unroll
-    for (int i = 0; i < kTPS; ++i) {
-      if (tok0 + i * G + g < t1) {
-        Rg.v[i] = ldg_stream_64(p.vc + voff_c[d] + i * G * (HD / 2));
-        if constexpr (!RS)
-          Rg.vs[i] = ld_scale<F16S>(p.vs, voff_s[d] + i * G * NBLK * SB);
-      }
-    }
-    if constexpr (RS) {
-      if (tok0 + (sub & 3) * G + g < t1)
-        Rg.vs[0] = ld_scale<F16S>(p.vs, voff_s[d] + soff_rs);
+  int ta = 0, t1a = 0, pia = 0, tb = 0, t1b = 0, pib = 0;
+  bool ha = false, hb = false;
+  auto fill_first = [&]() {
+    if (lvalid && seek()) {
+      load_stage(RA, ta, t1a, pia, 0);
+      ha = true;
     }
   };
-#pragma unroll
-  for (int d = 0; d < D; ++d) has[d] = false;
   // first stage now if it needs no walking (and the arrays are present)
   const bool early = !p.plan || warp < nstages(p0);
-  if (early) {
-    if constexpr (SPL) {
-      has[0] = fill_k(0);
-      if (has[0]) fill_v(0);
-    } else {
-      has[0] = fill(0);
-    }
-  }
+  if (early) fill_first();
   // per-batch arrays (plan mode): loaded now, stored to shared memory after
   // the table build, so their latency overlaps the q loads' instead of
   // stalling the builders (they are first read after the barrier below)
@@ -1535,17 +1476,7 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
   TRACE(6);
   __syncthreads();
   TRACE(7);
-  if constexpr (SPL) {
-    if (!early) {
-      has[0] = fill_k(0);
-      if (has[0]) fill_v(0);
-    }
-    has[1] = has[0] && fill_k(1);
-  } else {
-    if (!early) has[0] = fill(0);
-#pragma unroll
-    for (int d = 1; d < D - 1; ++d) has[d] = fill(d);
-  }
+  if (!early) fill_first();
 
   if (warp == NC) {
     // ================================================================ producer
@@ -1582,7 +1513,7 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
       more = walk_next(nx, k);
       if (more) qn = load_quad(nx, lane % Q);
       if (k >= R) {
-        mbar_wait(mb_done + 8 * ((k - R) % R), ((k - R) / R) & 1);
+        mbar_wait_sleep(mb_done + 8 * ((k - R) % R), ((k - R) / R) & 1);
         merge_fn<HD, NW, GATHER>(p, smem, k - R, sc, cta, g0);
       }
       if (k >= R0) build_fn<HD, NW>(smem, k % R, qc, p.scale_log2);
@@ -1598,7 +1529,7 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
       // previous pieces' merges, so the partners have had time to arrive)
       if (j == k && (NQKV_PEEK > 0 || (NQKV_PEEK < 0 && HD == 128)))
         peek_fn<HD, NW>(p, smem, k, sc, cta);
-      mbar_wait(mb_done + 8 * (j % R), (j / R) & 1);
+      mbar_wait_sleep(mb_done + 8 * (j % R), (j / R) & 1);
       if (j == k) TRACE(11);
       merge_fn<HD, NW, GATHER>(p, smem, j, sc, cta, g0);
     }
@@ -1816,38 +1747,39 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
   };
   open_piece();
   TRACE(8);
-  // buffer d-1 (consumed in the previous step) is refilled BEFORE buffer d is
-  // consumed, so D stages are in flight while one is being computed
-  bool running = has[0];
-  while (running) {
-#pragma unroll
-    for (int d = 0; d < D; ++d) {
-      if constexpr (SPL) {
-        // slot d: K and V of stage k; slot 1 - d: K of stage k + 1
-        if (!has[d]) { running = false; break; }
-        if (has[1 - d]) fill_v((d + 1) % D);
-        while (cpi < mpi[d]) {
-          end_piece(cpi);
-          ++cpi;
-          open_piece();
-        }
-        float wv[kTPS];
-        consume_s(RG[d], mtok[d], mt1[d], wv);
-        has[d] = fill_k(d);                    // K of stage k + 2
-        consume_v(RG[d], wv);
-      } else {
-        const int pd = (d + D - 1) % D;
-        has[pd] = fill(pd);
-        if (!has[d]) { running = false; break; }
-        while (cpi < mpi[d]) {
-          end_piece(cpi);
-          ++cpi;
-          open_piece();
-        }
-        float wv[kTPS];
-        consume_s(RG[d], mtok[d], mt1[d], wv);
-        consume_v(RG[d], wv);
-      }
+  // Buffers A and B alternate: once a stage's data has arrived (the first
+  // use of its first word waits for it), the next stage's loads are issued
+  // into the other buffer and stay in flight while this stage is computed.
+  uint32_t zero;
+  asm volatile("mov.u32 %0, 0;" : "=r"(zero));
+  auto close_to = [&](int pi) {
+    while (cpi < pi) {
+      end_piece(cpi);
+      ++cpi;
+      open_piece();
+    }
+  };
+  while (ha) {
+    {
+      const int dep = static_cast<int>(RA.k[0].x & zero);
+      hb = advance();
+      load_stage(RB, tb, t1b, pib, dep);     // no next stage: re-reads the last one (unused)
+      prefetch_ahead();
+      close_to(pia);
+      float wv[kTPS];
+      consume_s(RA, ta, t1a, wv);
+      consume_v(RA, wv);
+    }
+    if (!hb) break;
+    {
+      const int dep = static_cast<int>(RB.k[0].x & zero);
+      ha = advance();
+      load_stage(RA, ta, t1a, pia, dep);
+      prefetch_ahead();
+      close_to(pib);
+      float wv[kTPS];
+      consume_s(RB, tb, t1b, wv);
+      consume_v(RB, wv);
     }
     TRACE(12);
   }
