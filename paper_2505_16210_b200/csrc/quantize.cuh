@@ -30,7 +30,10 @@ struct QuantParams {
 // byte 0 = lane*8, byte 1 = idx + 4, bytes 2-3 = 0.
 constexpr int kRepEntryBytes = 256;
 constexpr size_t kQuantSmem = static_cast<size_t>(kNumBuckets) * kRepEntryBytes;
-constexpr float kBucketMagic = 12582932.0f;   // 1.5*2^23 + 16 + 4
+constexpr float kBucketMagic = 12582932.0f;   // 1.5*2^23 + 16 + 4 (bits 0x4B400014)
+#ifndef NQKV_Q_PAIRS
+#define NQKV_Q_PAIRS 1             // fp32x2 pair arithmetic in the quantize kernel
+#endif
 
 __device__ __forceinline__ uint32_t nf4_code_rep(float n, uint32_t lane8) {
   const float y = __fmaf_rn(n, 16.0f, kBucketMagic);
@@ -50,6 +53,35 @@ __device__ __forceinline__ uint32_t encode8_rep(const uint4 raw, float r, uint32
     const float2 xf = __half22float2(hv[k]);
     const uint32_t lo = nf4_code_rep(__fmul_rn(xf.x, r), lane8);
     const uint32_t hi = nf4_code_rep(__fmul_rn(xf.y, r), lane8);
+    b[k] = hi * 16u + lo;
+  }
+  return __byte_perm(__byte_perm(b[0], b[1], 0x0040), __byte_perm(b[2], b[3], 0x0040), 0x5410);
+}
+
+// Codes of 8 fp16 values, element pairs in fp32x2 arithmetic: n = RN32(x * r)
+// and y = RN32(16 n + magic) are the same per-element roundings as
+// nf4_code_rep's (fma.rn.f32x2 / mul.rn.f32x2 round each lane exactly like
+// the scalar forms), so the codes are identical; the pair conversion, one
+// FMUL2 and one FFMA2 per two elements, and a set-and-subtract compare save
+// ~3 instructions per element.
+__device__ __forceinline__ uint32_t encode8_rep2(const uint4 raw, uint64_t r2, uint32_t lane8) {
+  const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
+  uint32_t b[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    uint64_t x2;
+    asm("{.reg .f16 a, b;\n .reg .f32 fa, fb;\n mov.b32 {a, b}, %1;\n cvt.f32.f16 fa, a;\n"
+        " cvt.f32.f16 fb, b;\n mov.b64 %0, {fa, fb};}" : "=l"(x2) : "r"(w[k]));
+    uint64_t n2, y2;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(n2) : "l"(x2), "l"(r2));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(y2)
+        : "l"(n2), "l"(0x4180000041800000ull), "l"(0x4B4000144B400014ull));   // 16, kBucketMagic
+    const float2 n = unpack2(n2), y = unpack2(y2);
+    const float2 e0 = unpack2(lds64(__byte_perm(__float_as_uint(y.x), lane8, 0x5504)));
+    const float2 e1 = unpack2(lds64(__byte_perm(__float_as_uint(y.y), lane8, 0x5504)));
+    // lo + (n > thr): the sign bit of thr - n (thr = +inf -> never; equal -> +0)
+    const uint32_t lo = __float_as_uint(e0.y) + (__float_as_uint(__fsub_rn(e0.x, n.x)) >> 31);
+    const uint32_t hi = __float_as_uint(e1.y) + (__float_as_uint(__fsub_rn(e1.x, n.y)) >> 31);
     b[k] = hi * 16u + lo;
   }
   return __byte_perm(__byte_perm(b[0], b[1], 0x0040), __byte_perm(b[2], b[3], 0x0040), 0x5410);
@@ -78,7 +110,7 @@ __device__ __forceinline__ float absmax16(const uint4 a, const uint4 b) {
 // loads are issued before the current one is encoded (ping-pong registers).
 // When x is contiguous ([B][n_new][H][hd] packed), chunk c starts at x + 16c.
 template <int HD, int BLK, bool F16S>
-__global__ void __launch_bounds__(256) quantize_kernel(const __grid_constant__ QuantParams p) {
+__global__ void __launch_bounds__(256, 4) quantize_kernel(const __grid_constant__ QuantParams p) {
   constexpr int CPT = HD / 16;                 // chunks per (token, head)
   constexpr int LOG_CPT = CPT == 4 ? 2 : 3;
   constexpr int GL = BLK >= 32 ? BLK / 32 : 1; // lanes per block (>= 1)
@@ -100,8 +132,8 @@ __global__ void __launch_bounds__(256) quantize_kernel(const __grid_constant__ Q
     return p.x + b * p.sb + t * p.st + (within >> LOG_CPT) * p.sh + (within & (CPT - 1)) * 16;
   };
   struct Buf { uint4 v[4]; };
-  auto load = [&](uint32_t unit, Buf& B) {
-    const uint32_t c = unit * 64u + 2u * lane;
+  auto load = [&](uint32_t unit, Buf& B, uint32_t dep) {
+    const uint32_t c = unit * 64u + 2u * lane + dep;
     if (c < p.total) {
       const __half* s0 = src_of(c);
       const __half* s1 = contig ? s0 + 16 : src_of(c + 1);
@@ -116,14 +148,17 @@ __global__ void __launch_bounds__(256) quantize_kernel(const __grid_constant__ Q
       }
     }
   };
-  auto store_chunk = [&](uint32_t c, uint2 word, float s, bool scale_writer) {
+  // chunks c and c + 1 of a lane (c even; CPT even) lie in the same (b, t, h)
+  // row: one 16-byte store of both code words, and the block scale (both
+  // chunks share a block: blk >= 32) by the block's first lane
+  auto store_pair = [&](uint32_t c, uint4 words, float s, bool scale_writer) {
     const uint32_t row = fdiv(c, p.cpr), within = c - row * p.cpr.d;
     const uint32_t bb = fdiv(row, p.nnew), t = row - bb * p.nnew.d;
     const int pos = __ldg(p.pos + bb) + static_cast<int>(t);
     if (pos < 0 || pos >= p.Tc) return;
     const uint32_t h = within >> LOG_CPT, cr = within & (CPT - 1);
     const long long rr = (static_cast<long long>(bb) * p.H + h) * p.Tc + pos;
-    reinterpret_cast<uint2*>(p.codes + rr * (HD / 2))[cr] = word;
+    *reinterpret_cast<uint4*>(p.codes + rr * (HD / 2) + cr * 8) = words;
     if (scale_writer) {
       // blk > hd: one scale per (token, head group): [B][H >> hpb_shift][Tc]
       const long long si = BLK > HD ? ((static_cast<long long>(bb) * p.H + h) >> p.hpb_shift) * p.Tc + pos
@@ -147,27 +182,39 @@ __global__ void __launch_bounds__(256) quantize_kernel(const __grid_constant__ Q
     }
     if (BLK > 16) s1 = s0;
     const float r0 = block_rcp(s0), r1 = BLK > 16 ? r0 : block_rcp(s1);
+#if NQKV_Q_PAIRS
+    const uint64_t r0p = pack2(r0, r0), r1p = pack2(r1, r1);
+    const uint2 w0 = make_uint2(encode8_rep2(B.v[0], r0p, lane8), encode8_rep2(B.v[1], r0p, lane8));
+    const uint2 w1 = make_uint2(encode8_rep2(B.v[2], r1p, lane8), encode8_rep2(B.v[3], r1p, lane8));
+#else
     const uint2 w0 = make_uint2(encode8_rep(B.v[0], r0, lane8), encode8_rep(B.v[1], r0, lane8));
     const uint2 w1 = make_uint2(encode8_rep(B.v[2], r1, lane8), encode8_rep(B.v[3], r1, lane8));
+#endif
 #ifdef NQKV_EXP_QNOSTORE
     if (w0.x == 0x12345678u && w1.y == 0x9abcdef0u && s0 == 1.5f) reinterpret_cast<float*>(p.scales)[0] = s0;
     return;
 #endif
     if (!valid) return;
-    // scale writer: the first lane of each block (blk 32: every lane's first chunk)
+    // scale writer: the first lane of each block (blk 32: every lane)
     const bool first = ((2 * lane * 16) & ((1 << p.blk_shift) - 1)) == 0;
-    store_chunk(c, w0, s0, first);
-    store_chunk(c + 1, w1, s1, false);
+    static_assert(BLK > 16, "both chunks of a lane share one block");
+    store_pair(c, make_uint4(w0.x, w0.y, w1.x, w1.y), s0, first);
   };
+  // Two units in flight per warp.  ptxas puts every global load on one
+  // scoreboard, so a unit's loads are issued only after the previous unit's
+  // data has arrived (`dep`, always 0, is computed from its first word):
+  // otherwise the wait for a unit would also wait for the loads just issued.
+  uint32_t zero;
+  asm volatile("mov.u32 %0, 0;" : "=r"(zero));
   uint32_t u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  Buf A, Bb;
-  load(u, A);
+  Buf A{}, Bb{};
+  load(u, A, 0u);
   while (u * 64u < p.total) {
-    load(u + nw, Bb);
+    load(u + nw, Bb, A.v[0].x & zero);
     encode(u, A);
     u += nw;
     if (u * 64u >= p.total) break;
-    load(u + nw, A);
+    load(u + nw, A, Bb.v[0].x & zero);
     encode(u, Bb);
     u += nw;
   }
