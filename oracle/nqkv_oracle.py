@@ -267,6 +267,39 @@ def decode_attention(q: np.ndarray, k_codes, k_scales, v_codes, v_scales, seq_le
     return out
 
 
+def prefill_attention(q: np.ndarray, k_codes, k_scales, v_codes, v_scales, seq_lens, blk: int,
+                      softmax_scale: float | None = None, levels32=None) -> np.ndarray:
+    """Causal attention of the prompt's own queries over the DEQUANTISED
+    prompt cache (PAPER.md:213-221 prefill phase: I_K = quantize_NF4(X_K), the
+    cache holds indices; causal multi-head scaled dot-product
+    attention over the dequantised K, V, so prefill and decode see the same
+    quantised world).  The 1/sqrt(hd) factor is reading R6.
+
+    q: float16 [B][T][H][hd] (token-major, as the projections produce it);
+    row i of sequence b attends to cached tokens j <= i, j < seq_lens[b].
+    Returns float64 [B][T][H][hd]; rows i >= seq_lens[b] are 0.
+    """
+    B, T, H, hd = q.shape
+    if softmax_scale is None:
+        softmax_scale = 1.0 / math.sqrt(hd)
+    out = np.zeros((B, T, H, hd), np.float64)
+    for b in range(B):
+        L = min(int(seq_lens[b]), T)
+        if L == 0:
+            continue
+        K = dequantize(k_codes[b:b + 1], k_scales[b:b + 1], blk, L, np.float32, levels32)[0]
+        V = dequantize(v_codes[b:b + 1], v_scales[b:b + 1], blk, L, np.float32, levels32)[0]
+        for h in range(H):
+            Q = q[b, :L, h].astype(np.float64)                        # [L, hd]
+            S = (Q @ K[h].astype(np.float64).T) * float(softmax_scale)  # [L, L]
+            S[np.triu_indices(L, 1)] = -np.inf                         # causal: j <= i
+            S = S - S.max(axis=1, keepdims=True)
+            P = np.exp(S)
+            P = P / P.sum(axis=1, keepdims=True)
+            out[b, :L, h] = P @ V[h].astype(np.float64)
+    return out
+
+
 def attention_weights(q_h: np.ndarray, K_h: np.ndarray, softmax_scale: float) -> np.ndarray:
     """Softmax row for one head (diagnostic)."""
     s = (K_h.astype(np.float64) @ q_h.astype(np.float64)) * softmax_scale

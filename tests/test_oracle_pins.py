@@ -581,3 +581,91 @@ def test_softmax_temperature_two_token_closed_form(hd):
     # mutation sensitivity: the wrong temperatures are far from the oracle
     for wrong in (mpmath.exp(dm), mpmath.exp(dm / hd), mpmath.power(2, dm / mpmath.sqrt(hd))):
         assert np.max(np.abs(out - expect(wrong))) > 1e-3
+
+
+# ------------------------------------------------------ prefill attention --
+def test_prefill_single_token_returns_value():
+    # l = 1 -> the output row is the dequantised value row
+    rng = np.random.default_rng(21)
+    k = rng.standard_normal((2, 1, 3, 64)).astype(np.float16)
+    v = rng.standard_normal((2, 1, 3, 64)).astype(np.float16)
+    q = rng.standard_normal((2, 1, 3, 64)).astype(np.float16)
+    kc, ks = _cache_from(k, 64)
+    vc, vs = _cache_from(v, 64)
+    out = O.prefill_attention(q, kc, ks, vc, vs, [1, 1], 64)
+    assert np.array_equal(out[:, 0], O.dequantize(vc, vs, 64, 1)[:, :, 0, :].astype(np.float64))
+
+
+def test_prefill_identical_keys_causal_mean():
+    # identical keys -> uniform weights over j <= i -> the running mean of V
+    rng = np.random.default_rng(22)
+    k = np.repeat(rng.standard_normal((1, 1, 2, 64)).astype(np.float16), 9, axis=1)
+    v = rng.standard_normal((1, 9, 2, 64)).astype(np.float16)
+    q = rng.standard_normal((1, 9, 2, 64)).astype(np.float16)
+    kc, ks = _cache_from(k, 32)
+    vc, vs = _cache_from(v, 32)
+    out = O.prefill_attention(q, kc, ks, vc, vs, [9], 32)
+    vd = O.dequantize(vc, vs, 32, 9)[0].astype(np.float64)            # [H, 9, hd]
+    run = np.cumsum(vd, axis=1) / np.arange(1, 10)[None, :, None]
+    assert np.max(np.abs(out[0].transpose(1, 0, 2) - run)) < 1e-12
+
+
+def test_prefill_causality_and_padding_rows():
+    # row i does not depend on tokens > i; rows >= seq_len are zero
+    rng = np.random.default_rng(23)
+    k = rng.standard_normal((1, 12, 2, 64)).astype(np.float16)
+    v = rng.standard_normal((1, 12, 2, 64)).astype(np.float16)
+    q = rng.standard_normal((1, 12, 2, 64)).astype(np.float16)
+    a = O.prefill_attention(q, *_cache_from(k, 64), *_cache_from(v, 64), [12], 64)
+    k2, v2 = k.copy(), v.copy()
+    k2[:, 7:] = rng.standard_normal(k2[:, 7:].shape).astype(np.float16)
+    v2[:, 7:] = rng.standard_normal(v2[:, 7:].shape).astype(np.float16)
+    b = O.prefill_attention(q, *_cache_from(k2, 64), *_cache_from(v2, 64), [12], 64)
+    assert np.array_equal(a[:, :7], b[:, :7]) and not np.array_equal(a[:, 7:], b[:, 7:])
+    c = O.prefill_attention(q, *_cache_from(k, 64), *_cache_from(v, 64), [5], 64)
+    assert np.all(c[:, 5:] == 0) and np.max(np.abs(c[:, :5] - a[:, :5])) < 1e-12
+
+
+@pytest.mark.parametrize("hd", [64, 128])
+def test_prefill_two_token_row_closed_form(hd):
+    """Row 1 of a 2-token prompt with grid-exact keys: p1/p0 = exp(q1.(k1 - k0)
+    / sqrt(hd)), evaluated at 50 digits from exact rationals (as the decode
+    temperature pin); row 0 is v0."""
+    rng = np.random.default_rng(3030 + hd)
+    kc_ = rng.integers(0, 16, size=(2, hd))
+    vc_ = rng.integers(0, 16, size=(2, hd))
+    kc_[:, 0] = 15
+    vc_[:, 0] = 15
+    for _ in range(100):
+        q1 = (rng.standard_normal(hd) * 0.35).astype(np.float16)
+        d = sum(Fraction(float(a)) * (Fraction(float(L32[c1])) - Fraction(float(L32[c0])))
+                for a, c0, c1 in zip(q1, kc_[0], kc_[1]))
+        if 2.0 < abs(float(d)) < 12.0:
+            break
+    q = np.stack([rng.standard_normal(hd).astype(np.float16), q1]).reshape(1, 2, 1, hd)
+    kx = _grid_rows(kc_).reshape(1, 2, 1, hd)
+    vx = _grid_rows(vc_).reshape(1, 2, 1, hd)
+    out = O.prefill_attention(q, *_cache_from(kx, hd), *_cache_from(vx, hd), [2], hd)[0, :, 0]
+    mpmath.mp.dps = 50
+    r = mpmath.exp((mpmath.mpf(d.numerator) / d.denominator) / mpmath.sqrt(hd))
+    want1 = np.array([float((mpmath.mpf(float(L32[a])) + r * mpmath.mpf(float(L32[b]))) / (1 + r))
+                      for a, b in zip(vc_[0], vc_[1])])
+    assert np.array_equal(out[0], L32[vc_[0]].astype(np.float64))
+    assert np.max(np.abs(out[1] - want1)) < 1e-12
+
+
+def test_prefill_rows_equal_decode_steps():
+    # row i of prefill == the (separately pinned) decode attention of q_i over i + 1 tokens
+    rng = np.random.default_rng(24)
+    k = rng.standard_normal((2, 10, 3, 128)).astype(np.float16) * 3
+    v = rng.standard_normal((2, 10, 3, 128)).astype(np.float16)
+    q = rng.standard_normal((2, 10, 3, 128)).astype(np.float16)
+    kc, ks = _cache_from(k, 64)
+    vc, vs = _cache_from(v, 64)
+    out = O.prefill_attention(q, kc, ks, vc, vs, [10, 6], 64)
+    for i in range(10):
+        lens = [min(i + 1, 10), min(i + 1, 6)]
+        dec = O.decode_attention(q[:, i], kc, ks, vc, vs, lens, 64)
+        for b, L in enumerate([10, 6]):
+            if i < L:
+                assert np.max(np.abs(out[b, i] - dec[b])) < 1e-12
