@@ -57,7 +57,8 @@
 extern "C" {
 #endif
 
-#define NQKV_ABI_VERSION 2   /* 2: blk 256 / head-group scales; NQKV_SCALE_F16 moved to 0x10000 */
+#define NQKV_ABI_VERSION 3   /* 2: blk 256 / head-group scales; NQKV_SCALE_F16 moved to 0x10000;
+                                3: nqkv_prefill_attention, nqkv_build_id */
 
 typedef enum {
   NQKV_OK = 0,
@@ -71,6 +72,9 @@ typedef enum {
 } nqkv_status;
 
 int nqkv_abi_version(void);
+/* Hash of the sources the library was built from (build.py passes it in):
+ * lets a caller detect a stale build.  Host only. */
+const char* nqkv_build_id(void);
 const char* nqkv_status_string(int status);
 const char* nqkv_last_error(void);
 
@@ -257,7 +261,28 @@ int nqkv_decode_step_gather(const void* k_new, const void* v_new, int64_t new_st
 int nqkv_gather_epoch_bump(unsigned* d_epoch, void* stream);
 int nqkv_gather_wait(const unsigned* d_flags, int n, const unsigned* d_epoch, void* stream);
 
-/* Test hook: the kernels' code function on fp32 inputs already normalised
+/* NEXT f4: prefill attention over the 4-bit cache.
+ * PAPER.md:213-221 (prefill phase: the prompt's K/V are quantised into the
+ * cache, I_K = quantize_NF4(X_K)); SPEC.md:236-244 (causal multi-head scaled
+ * dot-product attention of the prompt over the DEQUANTISED K, V).  For query
+ * row i of sequence b and head h:
+ *   out[b][i][h] = sum_{j <= i, j < seq_lens[b]} softmax_j(softmax_scale * q_i . k^_j) v^_j
+ * with k^, v^ = RN32(s * L[code]) dequantised in shared memory (never
+ * written to memory).  Runs on the tensor cores (fp16 hi/lo split of k^, v^
+ * and the probabilities: ~22-bit operands, fp32 accumulation).
+ * q          device fp16 [B][T][H][hd] (token-major, contiguous), 16-byte aligned
+ * k_codes,…  the cache tensors (rows 0 .. seq_lens[b]-1 hold the prompt)
+ * d_seq_lens device int32[B], prompt lengths (clamped to [0, T])
+ * T          query rows per sequence, T <= Tc
+ * out        device fp32 [B][T][H][hd], 16-byte aligned; rows i >= seq_lens[b]
+ *            are written as 0.
+ * No workspace; B, H < 65536. */
+int nqkv_prefill_attention(const void* q, const uint8_t* k_codes, const void* k_scales,
+                           const uint8_t* v_codes, const void* v_scales, const int32_t* d_seq_lens,
+                           int B, int H, int hd, int blk, int Tc, int T, float softmax_scale,
+                           float* out, void* stream);
+
+/* Test hook: the kernels' code function on fp32 inputs already normalised/* Test hook: the kernels' code function on fp32 inputs already normalised
  * to [-1, 1] (values outside are clamped).  d_n device float[count],
  * d_codes device uint8[count]. */
 int nqkv_encode_normalized(const float* d_n, int64_t count, uint8_t* d_codes, void* stream);

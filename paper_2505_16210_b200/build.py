@@ -28,18 +28,46 @@ def nvcc() -> str:
     return "nvcc"
 
 
+def source_id() -> str:
+    """sha256 (16 hex digits) of every source the library is built from."""
+    import hashlib
+    h = hashlib.sha256()
+    for d in DEPS:
+        h.update(os.path.basename(d).encode())
+        with open(d, "rb") as f:
+            h.update(f.read())
+    return h.hexdigest()[:16]
+
+
+def built_id(lib: str = LIB) -> str | None:
+    """The build id embedded in a built library, read from the file (loading it
+    here would pin the old image in this process: dlopen caches by path)."""
+    try:
+        with open(lib, "rb") as f:
+            data = f.read()
+    except OSError:
+        return None
+    i = data.find(b"NQKV_BUILD_ID=")
+    if i < 0:
+        return None
+    j = data.find(b"\0", i)
+    return data[i + 14:j].decode(errors="replace")
+
+
 def needs_build() -> bool:
+    """Rebuild when the library is missing or was built from other sources
+    (embedded build id != hash of the current sources)."""
     if not os.path.exists(LIB):
         return True
-    t = os.path.getmtime(LIB)
-    return any(os.path.getmtime(d) > t for d in DEPS)
+    return built_id() != source_id()
 
 
 def build_library(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return LIB
     tmp = LIB + ".tmp"
-    cmd = [nvcc()] + NVCC_FLAGS + ["-I", os.path.join(ROOT, "include"), "-o", tmp] + SOURCES
+    cmd = [nvcc()] + NVCC_FLAGS + ["-I", os.path.join(ROOT, "include"), "-o", tmp,
+                                   f'-DNQKV_BUILD_ID="{source_id()}"'] + SOURCES
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + r.stdout + r.stderr)

@@ -28,6 +28,7 @@
 #include "decode.cuh"
 #include "nqkv_internal.h"
 #include "quantize.cuh"
+#include "prefill.cuh"
 
 namespace nqkv {
 
@@ -289,6 +290,13 @@ extern "C" {
 
 int nqkv_abi_version(void) { return NQKV_ABI_VERSION; }
 
+#ifndef NQKV_BUILD_ID
+#define NQKV_BUILD_ID "unknown"
+#endif
+// "NQKV_BUILD_ID=<id>" is also found by build.py in the file itself (no dlopen)
+__attribute__((used)) static const char kBuildIdTag[] = "NQKV_BUILD_ID=" NQKV_BUILD_ID;
+const char* nqkv_build_id(void) { return kBuildIdTag + 14; }
+
 const char* nqkv_status_string(int status) {
   switch (status) {
     case NQKV_OK: return "ok";
@@ -509,6 +517,53 @@ int nqkv_gather_wait(const unsigned* d_flags, int n, const unsigned* d_epoch, vo
   if (n == 0) return NQKV_OK;
   const cudaError_t e = launch_pdl_n(gather_wait_kernel, dim3(1), dim3(256), 0,
                                    static_cast<cudaStream_t>(stream), d_flags, n, d_epoch);
+  return e == cudaSuccess ? NQKV_OK : cuda_fail(e);
+}
+
+int nqkv_prefill_attention(const void* q, const uint8_t* k_codes, const void* k_scales,
+                           const uint8_t* v_codes, const void* v_scales, const int32_t* d_seq_lens,
+                           int B, int H, int hd, int blk, int Tc, int T, float softmax_scale,
+                           float* out, void* stream) {
+  if (!q || !k_codes || !k_scales || !v_codes || !v_scales || !d_seq_lens || !out) return NQKV_ERR_NULL;
+  if (int s = check_geometry(hd, blk)) return s;
+  const bool f16s = f16s_of(blk);
+  blk = blk_of(blk);
+  if (B < 0 || H < 0 || T < 0 || Tc <= 0 || Tc % 64 || T > Tc) return NQKV_ERR_SHAPE;
+  if (!heads_fit(H, hd, blk)) return NQKV_ERR_SHAPE;
+  if (static_cast<long long>(B) * H * Tc >= (1ll << 31) || B > 65535 || H > 65535) return NQKV_ERR_SHAPE;
+  if (!aligned16(q) || !aligned16(k_codes) || !aligned16(v_codes) || !aligned16(out) ||
+      !scale_aligned(k_scales, f16s) || !scale_aligned(v_scales, f16s))
+    return NQKV_ERR_ALIGN;
+  if (tables_status() != 0) return NQKV_ERR_INTERNAL;
+  if (B == 0 || H == 0 || T == 0) return NQKV_OK;
+  PrefillParams p;
+  p.q = static_cast<const __half*>(q);
+  p.kc = k_codes; p.ks = k_scales; p.vc = v_codes; p.vs = v_scales;
+  p.seq_lens = d_seq_lens; p.out = out;
+  p.B = B; p.H = H; p.T = T; p.Tc = Tc;
+  p.blk_shift = blk_shift_of(blk > hd ? hd : blk);
+  p.hpb_shift = hpb_shift_of(hd, blk);
+  p.scale_log2 = softmax_scale * 1.4426950408889634f;
+  p.lv = make_levels();
+  const dim3 grid(static_cast<unsigned>((T + kPfQ - 1) / kPfQ), static_cast<unsigned>(H), static_cast<unsigned>(B));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool grp = blk > hd;
+  auto go = [&](auto kern, size_t sm) {
+    static_assert(true, "");
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+    if (e != cudaSuccess) return e;
+    return launch_pdl(kern, grid, dim3(128), sm, st, p);
+  };
+  cudaError_t e;
+  if (hd == 64) {
+    constexpr size_t sm = prefill_smem_bytes<64>();
+    e = f16s ? (grp ? go(prefill_kernel<64, true, true>, sm) : go(prefill_kernel<64, true, false>, sm))
+             : (grp ? go(prefill_kernel<64, false, true>, sm) : go(prefill_kernel<64, false, false>, sm));
+  } else {
+    constexpr size_t sm = prefill_smem_bytes<128>();
+    e = f16s ? (grp ? go(prefill_kernel<128, true, true>, sm) : go(prefill_kernel<128, true, false>, sm))
+             : (grp ? go(prefill_kernel<128, false, true>, sm) : go(prefill_kernel<128, false, false>, sm));
+  }
   return e == cudaSuccess ? NQKV_OK : cuda_fail(e);
 }
 

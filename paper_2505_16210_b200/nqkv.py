@@ -53,6 +53,9 @@ _SIGS = {
                                        _i32, _i32, ctypes.c_uint, _vp, _vp, _sz, _vp, _i32, _vp]),
     "nqkv_gather_epoch_bump": (_i32, [_vp, _vp]),
     "nqkv_gather_wait": (_i32, [_vp, _i32, _vp, _vp]),
+    "nqkv_prefill_attention": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32,
+                                      _i32, ctypes.c_float, _vp, _vp]),
+    "nqkv_build_id": (ctypes.c_char_p, []),
 }
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -60,7 +63,7 @@ for _name, (_res, _args) in _SIGS.items():
     _f.argtypes = _args
 
 EXPORTED = tuple(_SIGS)
-ABI_VERSION = 2
+ABI_VERSION = 3
 if _lib.nqkv_abi_version() != ABI_VERSION:
     raise ImportError("libnqkv.so ABI version mismatch; rebuild")
 
@@ -204,6 +207,29 @@ def nqkv_decode_step(k_new: torch.Tensor, v_new: torch.Tensor, q: torch.Tensor,
                                  float(softmax_scale), _ptr(out), _ptr(workspace),
                                  workspace.numel() * workspace.element_size(), _stream(stream)),
            "nqkv_decode_step")
+    return out
+
+
+def nqkv_prefill_attention(q: torch.Tensor, k_codes: torch.Tensor, k_scales: torch.Tensor,
+                           v_codes: torch.Tensor, v_scales: torch.Tensor, seq_lens: torch.Tensor,
+                           blk: int, softmax_scale: float | None = None,
+                           out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Causal prefill attention of the prompt over the dequantised cache
+    (PAPER.md:213-221): q fp16 [B, T, H, hd] -> out fp32
+    [B, T, H, hd]; rows >= seq_lens[b] are zero."""
+    B, T, H, hd = q.shape
+    Tc = k_codes.shape[2]
+    if softmax_scale is None:
+        softmax_scale = 1.0 / math.sqrt(hd)
+    if out is None:
+        out = torch.empty((B, T, H, hd), dtype=torch.float32, device=q.device)
+    assert q.dtype == torch.float16 and q.is_contiguous() and out.is_contiguous()
+    assert seq_lens.dtype == torch.int32
+    _check(_lib.nqkv_prefill_attention(_ptr(q), _ptr(k_codes), _ptr(k_scales), _ptr(v_codes),
+                                       _ptr(v_scales), _ptr(seq_lens), B, H, hd,
+                                       _blkarg(blk, k_scales, v_scales), Tc, T,
+                                       float(softmax_scale), _ptr(out), _stream(stream)),
+           "nqkv_prefill_attention")
     return out
 
 

@@ -27,7 +27,7 @@ def test_exports_every_declared_symbol():
     lib = ctypes.CDLL(N._LIB_PATH)
     for name in declared:
         assert hasattr(lib, name)
-    assert lib.nqkv_abi_version() == 2
+    assert lib.nqkv_abi_version() == 3
 
 
 def test_host_levels_and_thresholds_match_oracle_bits():
@@ -171,3 +171,13 @@ def test_decode_gather_argument_errors():
     assert N._lib.nqkv_gather_wait(FAKE, 0, FAKE, None) == 0
     a = list(base); a[12] = 96
     assert f(*a) == -3
+
+
+def test_build_id_matches_sources():
+    """The library embeds the hash of the sources it was built from; build()
+    rebuilds on a mismatch, so a stale library is never reused."""
+    from paper_2505_16210_b200 import build as bld
+    from paper_2505_16210_b200 import nqkv as N
+    assert bld.built_id() == bld.source_id()
+    assert N._lib.nqkv_build_id().decode() == bld.source_id()
+    assert not bld.needs_build()

@@ -889,3 +889,74 @@ def test_runtime_nccl_side_stream_gather_world1(N):
         assert r.launches_per_step() == 3 + 1
     finally:
         dist.destroy_process_group()
+
+
+# ---------------------------------------------- prefill attention (8(f) row 4)
+def _prefill_case(N, B, T, H, hd, blk, lens, Tc, seed, f16s=False):
+    k = _rand_kv(B, T, H, hd, seed)
+    v = _rand_kv(B, T, H, hd, seed + 1, False)
+    q = torch.randn(B, T, H, hd, generator=torch.Generator().manual_seed(seed + 2)).to(torch.float16)
+    kc, ks = _oracle_cache(k, [0] * B, blk, Tc)
+    vc, vs = _oracle_cache(v, [0] * B, blk, Tc)
+    ref = O.prefill_attention(q.numpy(), kc, ks, vc, vs, lens, blk)
+    t = lambda a: torch.from_numpy(a).to(DEV)
+    sk, sv = t(ks), t(vs)
+    if f16s:
+        sk, sv = sk.half(), sv.half()
+    out = N.nqkv_prefill_attention(q.to(DEV), t(kc), sk, t(vc), sv,
+                                   torch.tensor(lens, dtype=torch.int32, device=DEV), blk)
+    torch.cuda.synchronize()
+    return out.cpu().numpy(), ref
+
+
+@pytest.mark.parametrize("hd,blk", [(64, 64), (64, 32), (128, 64), (128, 32), (128, 128), (64, 256), (128, 256)])
+def test_prefill_attention_matches_oracle(N, hd, blk):
+    """Causal prefill attention over the dequantised cache (PAPER.md:213-221,
+    SPEC.md:236-244) within 2e-3 of the float64 oracle: ragged prompt lengths
+    spanning several 64-query / 64-key tiles and a ragged tail, an empty and a
+    one-token prompt, K outlier channels."""
+    H = 2 if blk <= hd else 2 * _hpb(hd, blk)
+    lens = [0, 1, 63, 64, 65, 200]
+    out, ref = _prefill_case(N, len(lens), 200, H, hd, blk, lens, 256, seed=hd + blk)
+    err = np.max(np.abs(out.astype(np.float64) - ref))
+    assert err <= ATOL, err
+    assert np.all(out[0] == 0) and np.all(out[2, 63:] == 0)          # rows >= len are zero
+
+
+def test_prefill_attention_fp16_scales_and_long(N):
+    out, ref = _prefill_case(N, 2, 700, 3, 128, 64, [700, 513], 704, seed=77, f16s=True)
+    assert np.max(np.abs(out.astype(np.float64) - ref)) <= ATOL
+
+
+@pytest.mark.parametrize("cfg", ["c3", "c4"])
+def test_prefill_attention_config_prompt_sampled(N, cfg):
+    """The config's prompt length (c3: U[1024, 2048], c4: 8192) on the GPU for
+    a few heads; the oracle checks sampled query rows of sampled sequences
+    (each row equals the oracle's decode attention of q_i over i + 1 tokens,
+    which is cheap to evaluate one row at a time)."""
+    w = W.CONFIGS[cfg]
+    H = 2
+    lens = W.seq_lens(w)
+    B = min(w.batch, 3)
+    lens = lens[:B]
+    T = int(lens.max())
+    Tc = W.capacity(T)
+    K, V = W.layer_kv(w, 0, heads=range(H), tokens=T, device=DEV)
+    K, V = K[:B].contiguous(), V[:B].contiguous()
+    q = torch.randn(B, T, H, w.head_dim, generator=torch.Generator(device=DEV).manual_seed(5), device=DEV).half()
+    cache = N.KVCache(B, H, w.head_dim, Tc, w.blk, DEV)
+    cache.append(K, V, torch.zeros(B, dtype=torch.int32, device=DEV))
+    L = lens.to(DEV)
+    out = N.nqkv_prefill_attention(q, cache.k_codes, cache.k_scales, cache.v_codes, cache.v_scales, L, w.blk)
+    torch.cuda.synchronize()
+    kc, ks = cache.k_codes.cpu().numpy(), cache.k_scales.cpu().numpy()
+    vc, vs = cache.v_codes.cpu().numpy(), cache.v_scales.cpu().numpy()
+    qn = q.cpu().numpy()
+    on = out.cpu().numpy()
+    rng = np.random.default_rng(1)
+    for b in range(B):
+        n = int(lens[b])
+        for i in sorted({0, 63, 64, n - 1} | {int(rng.integers(n)) for _ in range(4)}):
+            ref = O.decode_attention(qn[b:b + 1, i], kc[b:b + 1], ks[b:b + 1], vc[b:b + 1], vs[b:b + 1], [i + 1], w.blk)
+            assert np.max(np.abs(on[b, i] - ref[0])) <= ATOL, (b, i)
+        assert np.all(on[b, n:] == 0)
