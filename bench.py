@@ -411,7 +411,10 @@ def load_traffic(name):
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         d = json.load(open(tp)).get(name, {})
-        return d.get("decode_dram_bytes_per_launch"), d.get("quantize_dram_bytes_per_launch"), d.get("source")
+        src = d.get("source")
+        if src and d.get("quantize_source"):
+            src = f"ncu --set full of this launch configuration: decode {src}, quantize {d['quantize_source']}"
+        return d.get("decode_dram_bytes_per_launch"), d.get("quantize_dram_bytes_per_launch"), src
     except Exception:
         return None, None, None
 

@@ -6,7 +6,7 @@ set -u
 R=${1:-r1}
 O=gpurun_out
 mkdir -p $O
-CMD="python bench.py --steps 4 --warmup 3 --no-cpu-baseline"
+CMD="python bench.py --steps 4 --warmup 3 --no-cpu-baseline --no-configs"
 $CMD > $O/${R}_bench_small_plain.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"decode_kernel|quantize_kernel" --csv --log-file $O/${R}_launches.csv $CMD > $O/${R}_launches_run.log 2>&1
 $CMD > $O/${R}_bench_small_plain2.log 2>&1 && \
