@@ -284,7 +284,10 @@ def measure(args, w, heads, dev, world, group, layers=None, steps=None, warmup=N
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    runner.capture(timing_slots=(0,) if isolated else ())
+    # the timed graphs carry no event nodes (events around a launch break the
+    # PDL chaining between layers; with one step slot, as at c5, an
+    # instrumented slot would be every step)
+    runner.capture(timing_slots=())
     for i in range(warmup):
         runner.replay(i)
     torch.cuda.synchronize()
@@ -304,7 +307,17 @@ def measure(args, w, heads, dev, world, group, layers=None, steps=None, warmup=N
     if world > 1:
         dist.barrier()
     ms = e0.elapsed_time(e1)
-    dec_ms = runner.decode_kernel_ms() if isolated else []
+    dec_ms = []
+    if isolated:
+        # isolated launch durations: one replay of an instrumented capture of
+        # slot 0, after the timed region
+        if world > 1:
+            dist.barrier()
+        runner.capture(timing_slots=(0,))
+        runner.replay(0)
+        torch.cuda.synchronize()
+        dec_ms = runner.decode_kernel_ms()
+        runner.capture(timing_slots=())
     tokens = sum(runner.tokens_per_step(warmup + i) for i in range(steps))
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
@@ -517,9 +530,10 @@ def run_ours(args, w, rank, world, local_rank):
                                "launches per step; launches PDL-chained inside the step graph; the "
                                "per-step plan kernel is charged to them",
                      "isolated_launch_us": r["isolated_launch_us"],
-                     "isolated_timing": "CUDA events around every layer's launch in step slot "
-                                        "0's graph (last replay inside the timed region; the "
-                                        "events break the PDL chaining)"},
+                     "isolated_timing": "CUDA events around every layer's launch in one replay "
+                                        "of an instrumented capture of step slot 0, after the "
+                                        "timed region (the events break the PDL chaining; the "
+                                        "timed graphs carry none)"},
         "quantize_roofline": {"bound": "hbm", "achieved": r["quantize_gbs"], "peak": peak,
                               "unit": "GB/s", "frac": r["quantize_gbs"] / peak, "traffic": q_traffic,
                               "kernel": "quantize_kernel (nqkv_quantize, bulk prefill, L2 flushed)",
