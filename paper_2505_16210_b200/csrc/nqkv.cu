@@ -552,7 +552,7 @@ int nqkv_prefill_attention(const void* q, const uint8_t* k_codes, const void* k_
     static_assert(true, "");
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
     if (e != cudaSuccess) return e;
-    return launch_pdl(kern, grid, dim3(128), sm, st, p);
+    return launch_pdl(kern, grid, dim3(kPfW * 32), sm, st, p);
   };
   cudaError_t e;
   if (hd == 64) {

@@ -36,7 +36,8 @@ struct PrefillParams {
   Levels lv;
 };
 
-constexpr int kPfQ = 64;     // queries per CTA (4 warps x 16 rows)
+constexpr int kPfW = 8;      // warps per CTA
+constexpr int kPfQ = 16 * kPfW;   // queries per CTA (16 rows per warp): each dequantised tile serves them all
 constexpr int kPfK = 64;     // keys per tile
 
 __device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
@@ -57,21 +58,27 @@ __device__ __forceinline__ void split2(float x, float y, uint32_t& hi, uint32_t&
 
 template <int HD>
 constexpr size_t prefill_smem_bytes() {
-  return (2 * static_cast<size_t>(kPfK) * (HD + 8) + 2 * static_cast<size_t>(HD) * (kPfK + 8)) * 2 + 64;
+  return 4 * static_cast<size_t>(kPfK) * (HD + 8) * 2 + 64;
+}
+// B fragments (k = 16 keys, n = 8 dims) of P.V from V stored [key][dim]
+__device__ __forceinline__ void ldsm_x2_trans(uint32_t addr, uint32_t& b0, uint32_t& b1) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0, %1}, [%2];"
+               : "=r"(b0), "=r"(b1) : "r"(addr));
 }
 
 template <int HD, bool F16S, bool GRP>
-__global__ void __launch_bounds__(128) prefill_kernel(const __grid_constant__ PrefillParams p) {
+__global__ void __launch_bounds__(kPfW * 32) prefill_kernel(const __grid_constant__ PrefillParams p) {
   constexpr int KS = HD + 8;          // K tile row stride (halves): conflict-free B-fragment loads
-  constexpr int VS = kPfK + 8;        // V^T tile row stride (halves)
+  constexpr int VS = HD + 8;          // V tile row stride (halves): conflict-free ldmatrix rows
+  constexpr int NT = kPfW * 32;
   constexpr int NKT = kPfK / 8;       // n-tiles of S per warp
   constexpr int NDT = HD / 8;         // n-tiles of O per warp
   extern __shared__ __align__(16) unsigned char pf_smem[];
   __half* sKh = reinterpret_cast<__half*>(pf_smem);
   __half* sKl = sKh + kPfK * KS;
   __half* sVh = sKl + kPfK * KS;
-  __half* sVl = sVh + HD * VS;
-  float* s_lv = reinterpret_cast<float*>(sVl + HD * VS);
+  __half* sVl = sVh + kPfK * VS;
+  float* s_lv = reinterpret_cast<float*>(sVl + kPfK * VS);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int qt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
@@ -82,7 +89,7 @@ __global__ void __launch_bounds__(128) prefill_kernel(const __grid_constant__ Pr
   const long long rstride = static_cast<long long>(p.H) * HD;      // elements between tokens
   float* outb = p.out + (static_cast<long long>(b) * p.T) * rstride + static_cast<long long>(h) * HD;
   if (q0 >= len) {                    // rows beyond the prompt: zeros
-    for (int i = tid; i < kPfQ * HD; i += 128) {
+    for (int i = tid; i < kPfQ * HD; i += NT) {
       const int r = q0 + i / HD;
       if (r < p.T) outb[r * rstride + (i % HD)] = 0.0f;
     }
@@ -112,7 +119,7 @@ __global__ void __launch_bounds__(128) prefill_kernel(const __grid_constant__ Pr
   for (int k0 = 0; k0 < last_key; k0 += kPfK) {
     __syncthreads();                  // previous tile fully consumed
     // ---- dequantise the K and V tiles: thread -> (token, 16 dims) x 2 passes
-    for (int it = tid; it < kPfK * (HD / 16); it += 128) {
+    for (int it = tid; it < kPfK * (HD / 16); it += NT) {
       const int tk = it / (HD / 16), c = it % (HD / 16);     // token in tile, 16-dim chunk
       const int tok = k0 + tk;
       float kv[16], vv[16];
@@ -147,13 +154,13 @@ __global__ void __launch_bounds__(128) prefill_kernel(const __grid_constant__ Pr
       *reinterpret_cast<uint4*>(sKh + tk * KS + c * 16 + 8) = make_uint4(khi[4], khi[5], khi[6], khi[7]);
       *reinterpret_cast<uint4*>(sKl + tk * KS + c * 16) = make_uint4(klo[0], klo[1], klo[2], klo[3]);
       *reinterpret_cast<uint4*>(sKl + tk * KS + c * 16 + 8) = make_uint4(klo[4], klo[5], klo[6], klo[7]);
+      uint32_t vhi[8], vlo[8];
 #pragma unroll
-      for (int e = 0; e < 16; ++e) {         // V transposed: [dim][token]
-        const __half vh = __float2half_rn(vv[e]);
-        const __half vl = __float2half_rn(vv[e] - __half2float(vh));
-        sVh[(c * 16 + e) * VS + tk] = vh;
-        sVl[(c * 16 + e) * VS + tk] = vl;
-      }
+      for (int e = 0; e < 8; ++e) split2(vv[2 * e], vv[2 * e + 1], vhi[e], vlo[e]);
+      *reinterpret_cast<uint4*>(sVh + tk * VS + c * 16) = make_uint4(vhi[0], vhi[1], vhi[2], vhi[3]);
+      *reinterpret_cast<uint4*>(sVh + tk * VS + c * 16 + 8) = make_uint4(vhi[4], vhi[5], vhi[6], vhi[7]);
+      *reinterpret_cast<uint4*>(sVl + tk * VS + c * 16) = make_uint4(vlo[0], vlo[1], vlo[2], vlo[3]);
+      *reinterpret_cast<uint4*>(sVl + tk * VS + c * 16 + 8) = make_uint4(vlo[4], vlo[5], vlo[6], vlo[7]);
     }
     (void)NBLK_MAX;
     __syncthreads();
@@ -221,12 +228,15 @@ __global__ void __launch_bounds__(128) prefill_kernel(const __grid_constant__ Pr
       split2(sacc[2 * kk][2], sacc[2 * kk][3], ph[1], pl[1]);
       split2(sacc[2 * kk + 1][0], sacc[2 * kk + 1][1], ph[2], pl[2]);
       split2(sacc[2 * kk + 1][2], sacc[2 * kk + 1][3], ph[3], pl[3]);
+      // ldmatrix.trans row addresses: lanes 0-15 -> keys kk*16 + (lane & 15)
+      const uint32_t vrow = static_cast<uint32_t>(((kk * 16 + (lane & 15)) * VS) * 2);
+      const uint32_t vh_base = static_cast<uint32_t>(__cvta_generic_to_shared(sVh)) + vrow;
+      const uint32_t vl_base = static_cast<uint32_t>(__cvta_generic_to_shared(sVl)) + vrow;
 #pragma unroll
       for (int j = 0; j < NDT; ++j) {
-        const __half* vr = sVh + (j * 8 + g) * VS + kk * 16 + 2 * t;
-        const __half* vl = sVl + (j * 8 + g) * VS + kk * 16 + 2 * t;
-        const uint32_t vh0 = *reinterpret_cast<const uint32_t*>(vr), vh1 = *reinterpret_cast<const uint32_t*>(vr + 8);
-        const uint32_t vl0 = *reinterpret_cast<const uint32_t*>(vl), vl1 = *reinterpret_cast<const uint32_t*>(vl + 8);
+        uint32_t vh0, vh1, vl0, vl1;
+        ldsm_x2_trans(vh_base + j * 16, vh0, vh1);
+        ldsm_x2_trans(vl_base + j * 16, vl0, vl1);
         mma16816(o[j], ph, vh0, vh1);
         mma16816(o[j], pl, vh0, vh1);
         mma16816(o[j], ph, vl0, vl1);
