@@ -29,6 +29,7 @@
 #include "nqkv_internal.h"
 #include "quantize.cuh"
 #include "prefill.cuh"
+#include "prefill_tc.cuh"
 
 namespace nqkv {
 
@@ -545,16 +546,17 @@ int nqkv_prefill_attention(const void* q, const uint8_t* k_codes, const void* k_
   p.hpb_shift = hpb_shift_of(hd, blk);
   p.scale_log2 = softmax_scale * 1.4426950408889634f;
   p.lv = make_levels();
-  const dim3 grid(static_cast<unsigned>((T + kPfQ - 1) / kPfQ), static_cast<unsigned>(H), static_cast<unsigned>(B));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool grp = blk > hd;
+  cudaError_t e;
+#if NQKV_PREFILL_MMA_SYNC
+  // legacy tensor-core path (mma.sync m16n8k16), kept for comparison builds
+  const dim3 grid(static_cast<unsigned>((T + kPfQ - 1) / kPfQ), static_cast<unsigned>(H), static_cast<unsigned>(B));
   auto go = [&](auto kern, size_t sm) {
-    static_assert(true, "");
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
-    if (e != cudaSuccess) return e;
+    cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+    if (e2 != cudaSuccess) return e2;
     return launch_pdl(kern, grid, dim3(kPfW * 32), sm, st, p);
   };
-  cudaError_t e;
   if (hd == 64) {
     constexpr size_t sm = prefill_smem_bytes<64>();
     e = f16s ? (grp ? go(prefill_kernel<64, true, true>, sm) : go(prefill_kernel<64, true, false>, sm))
@@ -564,6 +566,24 @@ int nqkv_prefill_attention(const void* q, const uint8_t* k_codes, const void* k_
     e = f16s ? (grp ? go(prefill_kernel<128, true, true>, sm) : go(prefill_kernel<128, true, false>, sm))
              : (grp ? go(prefill_kernel<128, false, true>, sm) : go(prefill_kernel<128, false, false>, sm));
   }
+#else
+  // tcgen05 / TMEM path: 256 queries per CTA
+  const dim3 grid(static_cast<unsigned>((T + kTcQ - 1) / kTcQ), static_cast<unsigned>(H), static_cast<unsigned>(B));
+  auto go = [&](auto kern, size_t sm) {
+    cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+    if (e2 != cudaSuccess) return e2;
+    return launch_pdl(kern, grid, dim3(kTcThreads), sm, st, p);
+  };
+  if (hd == 64) {
+    constexpr size_t sm = prefill_tc_smem_bytes<64>();
+    e = f16s ? (grp ? go(prefill_tc_kernel<64, true, true>, sm) : go(prefill_tc_kernel<64, true, false>, sm))
+             : (grp ? go(prefill_tc_kernel<64, false, true>, sm) : go(prefill_tc_kernel<64, false, false>, sm));
+  } else {
+    constexpr size_t sm = prefill_tc_smem_bytes<128>();
+    e = f16s ? (grp ? go(prefill_tc_kernel<128, true, true>, sm) : go(prefill_tc_kernel<128, true, false>, sm))
+             : (grp ? go(prefill_tc_kernel<128, false, true>, sm) : go(prefill_tc_kernel<128, false, false>, sm));
+  }
+#endif
   return e == cudaSuccess ? NQKV_OK : cuda_fail(e);
 }
 
