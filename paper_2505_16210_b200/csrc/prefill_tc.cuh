@@ -30,8 +30,8 @@ constexpr int kTcThreads = 256;
 
 template <int HD>
 constexpr size_t prefill_tc_smem_bytes() {
-  // Q (256 x HD) + K hi/lo + V hi/lo (64 x HD each) + P hi/lo (2 x 128 x 64 each) + slack
-  return static_cast<size_t>(kTcQ) * HD * 2 + 4 * static_cast<size_t>(kTcK) * HD * 2 +
+  // Q (256 x HD) + K hi/lo + 2 x V hi/lo (64 x HD each) + P hi/lo (2 x 128 x 64 each) + slack
+  return static_cast<size_t>(kTcQ) * HD * 2 + 6 * static_cast<size_t>(kTcK) * HD * 2 +
          2 * 2 * 128 * kTcK * 2 + 1024;
 }
 
@@ -92,12 +92,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) prefill_tc_kernel(const __grid_
   extern __shared__ __align__(1024) unsigned char tc_smem[];
   const uint32_t sbase = (static_cast<uint32_t>(__cvta_generic_to_shared(tc_smem)) + 1023u) & ~1023u;
   unsigned char* gbase = tc_smem + (sbase - static_cast<uint32_t>(__cvta_generic_to_shared(tc_smem)));
+  // layout: Q | K hi | K lo | V hi (x2) | V lo (x2) | P hi (2 sets) | P lo (2 sets)
   const uint32_t sQ = sbase, sKh = sQ + kQBytes, sKl = sKh + kTileBytes, sVh = sKl + kTileBytes,
-                 sVl = sVh + kTileBytes, sPh = sVl + kTileBytes, sPl = sPh + 2 * kPBytes;
+                 sVl = sVh + 2 * kTileBytes, sPh = sVl + 2 * kTileBytes, sPl = sPh + 2 * kPBytes;
   unsigned char* gQ = gbase;
   unsigned char* gK[2] = {gbase + kQBytes, gbase + kQBytes + kTileBytes};
-  unsigned char* gV[2] = {gbase + kQBytes + 2 * kTileBytes, gbase + kQBytes + 3 * kTileBytes};
-  unsigned char* gP[2] = {gbase + kQBytes + 4 * kTileBytes, gbase + kQBytes + 4 * kTileBytes + 2 * kPBytes};
+  unsigned char* gV[2] = {gbase + kQBytes + 2 * kTileBytes, gbase + kQBytes + 4 * kTileBytes};   // hi, lo (+ buffer)
+  unsigned char* gP[2] = {gbase + kQBytes + 6 * kTileBytes, gbase + kQBytes + 6 * kTileBytes + 2 * kPBytes};
   __shared__ float s_lv[16];
   __shared__ uint32_t s_tmem;
   __shared__ __align__(8) uint64_t s_mbar[2];      // S ready, O ready
@@ -158,20 +159,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) prefill_tc_kernel(const __grid_
   float m_ref = -INFINITY, lsum = 0.0f;
   constexpr uint32_t idS = umma_idesc_f16(128, kTcK, false);
   constexpr uint32_t idO = umma_idesc_f16(128, HD, true);
-  int tile = 0;
-  for (int k0 = 0; k0 < last_key; k0 += kTcK, ++tile) {
-    // ---- 1. dequantise K and V: item = (tensor, 8-key group, 8-dim group)
+  // dequantise the K tile and V tile `buf` for keys [k0, k0 + 64):
+  // item = (tensor, 8-key group, 8-dim group)
+  auto dequant = [&](int k0, int buf) {
     for (int it = tid; it < 2 * (kTcK / 8) * DG; it += kTcThreads) {
       const int isv = it >= (kTcK / 8) * DG;
       const int rem = it - isv * (kTcK / 8) * DG;
       const int kg = rem / DG, dg = rem % DG;
       const uint8_t* codes = isv ? p.vc : p.kc;
       const void* scales = isv ? p.vs : p.ks;
-      uint4 hi[2], lo[2];
-      uint32_t* hw = reinterpret_cast<uint32_t*>(hi);
-      uint32_t* lw = reinterpret_cast<uint32_t*>(lo);
-      unsigned char* dst_h = (isv ? gV[0] : gK[0]) + (kg * DG + dg) * 128;
-      unsigned char* dst_l = (isv ? gV[1] : gK[1]) + (kg * DG + dg) * 128;
+      unsigned char* dst_h = (isv ? gV[0] + buf * kTileBytes : gK[0]) + (kg * DG + dg) * 128;
+      unsigned char* dst_l = (isv ? gV[1] + buf * kTileBytes : gK[1]) + (kg * DG + dg) * 128;
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const int tok = k0 + kg * 8 + j;
@@ -194,12 +192,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) prefill_tc_kernel(const __grid_
         *reinterpret_cast<uint4*>(dst_h + j * 16) = vh;
         *reinterpret_cast<uint4*>(dst_l + j * 16) = vl;
       }
-      (void)hw; (void)lw;
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     tc_fence_before();
     __syncthreads();
-    // ---- 2. S_s = Q_s K^T (hi, lo)
+  };
+  auto issue_s = [&]() {       // S_s = Q_s K_hi^T + Q_s K_lo^T
     if (tid == 0) {
       tc_fence_after();
 #pragma unroll
@@ -213,9 +211,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) prefill_tc_kernel(const __grid_
       }
       umma_commit(mb_s);
     }
+  };
+  // Pipeline per tile t: softmax(t) -> issue P.V(t) -> dequantise tile t + 1
+  // (K single-buffered: S(t) is complete; V double-buffered: P.V(t) reads
+  // V(t) meanwhile) -> issue S(t + 1).  P and the O rescale wait for P.V(t-1).
+  const int ntiles = (last_key + kTcK - 1) / kTcK;
+  dequant(0, 0);
+  issue_s();
+  for (int tile = 0; tile < ntiles; ++tile) {
+    const int k0 = tile * kTcK;
     mbar_wait_tc(mb_s, tile & 1);
     tc_fence_after();
-    // ---- 3. softmax of this thread's row (64 keys)
     float sv[kTcK];
     {
       uint32_t v[32];
@@ -229,11 +235,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) prefill_tc_kernel(const __grid_
       for (int c = 0; c < 32; ++c) sv[32 + c] = __uint_as_float(v[c]);
     }
     float mx = -INFINITY;
+    if (k0 + kTcK <= q0 + 1 && k0 + kTcK <= len) {       // interior tile: every key valid for every row
 #pragma unroll
-    for (int c = 0; c < kTcK; ++c) {
-      const int key = k0 + c;
-      sv[c] = (key <= row && key < len) ? sv[c] * p.scale_log2 : -INFINITY;
-      mx = fmaxf(mx, sv[c]);
+      for (int c = 0; c < kTcK; ++c) {
+        sv[c] *= p.scale_log2;
+        mx = fmaxf(mx, sv[c]);
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < kTcK; ++c) {
+        const int key = k0 + c;
+        sv[c] = (key <= row && key < len) ? sv[c] * p.scale_log2 : -INFINITY;
+        mx = fmaxf(mx, sv[c]);
+      }
     }
     // lazy reference max: rescale only when the max grows by more than 2^8
     const bool grow = mx > m_ref + 8.0f;
@@ -243,8 +257,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) prefill_tc_kernel(const __grid_
       m_ref = mx;
       lsum *= corr;
     }
+    if (tile > 0) {
+      mbar_wait_tc(mb_o, (tile - 1) & 1);       // P.V(t - 1) done: O stable, P free
+      tc_fence_after();
+    }
     if (tile > 0 && __any_sync(0xffffffffu, grow && corr != 1.0f)) {
-      // rescale this warp's rows of O in TMEM (the previous P.V has completed)
 #pragma unroll
       for (int c = 0; c < HD; c += 32) {
         uint32_t v[32];
@@ -276,17 +293,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) prefill_tc_kernel(const __grid_
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     tc_fence_before();
     __syncthreads();
-    // ---- 4. O_s += P_hi V_hi + P_lo V_hi + P_hi V_lo
+    // O_s += P_hi V_hi + P_lo V_hi + P_hi V_lo  (V buffer tile & 1)
     if (tid == 0) {
       tc_fence_after();
+      const uint32_t vb = (tile & 1) * kTileBytes;
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
 #pragma unroll
         for (int kk = 0; kk < kTcK / 16; ++kk) {
           const uint64_t ah = umma_sdesc(sPh + s * kPBytes + kk * 256, 128, (kTcK / 8) * 128);
           const uint64_t al = umma_sdesc(sPl + s * kPBytes + kk * 256, 128, (kTcK / 8) * 128);
-          const uint64_t bh = umma_sdesc(sVh + kk * 2 * DG * 128, DG * 128, 128);
-          const uint64_t bl = umma_sdesc(sVl + kk * 2 * DG * 128, DG * 128, 128);
+          const uint64_t bh = umma_sdesc(sVh + vb + kk * 2 * DG * 128, DG * 128, 128);
+          const uint64_t bl = umma_sdesc(sVl + vb + kk * 2 * DG * 128, DG * 128, 128);
           const uint32_t d = tmem + 2 * kTcK + s * HD;
           umma_f16(d, ah, bh, idO, (tile > 0 || kk > 0) ? 1u : 0u);
           umma_f16(d, al, bh, idO, 1u);
@@ -295,9 +313,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) prefill_tc_kernel(const __grid_
       }
       umma_commit(mb_o);
     }
-    mbar_wait_tc(mb_o, tile & 1);
-    tc_fence_after();
+    if (tile + 1 < ntiles) {
+      dequant(k0 + kTcK, (tile + 1) & 1);        // overlaps P.V(t)
+      issue_s();
+    }
   }
+  mbar_wait_tc(mb_o, (ntiles - 1) & 1);
+  tc_fence_after();
   // ---- epilogue: O / l for rows < len (0 beyond)
   const float inv = lsum > 0.0f ? 1.0f / lsum : 0.0f;
 #pragma unroll
