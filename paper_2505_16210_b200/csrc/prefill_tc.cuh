@@ -132,15 +132,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) prefill_tc_kernel(const __grid_
   }
   // ---- Q (fp16, exact) into the K-major A layout: core (row group, dim group)
   const __half* qb = p.q + (static_cast<long long>(b) * p.T) * rstride + static_cast<long long>(h) * HD;
-  for (int it = tid; it < (kTcQ / 8) * DG; it += kTcThreads) {
-    const int rg = it / DG, dg = it % DG;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int row = q0 + rg * 8 + j;
-      uint4 v = make_uint4(0, 0, 0, 0);
-      if (row < len) v = *reinterpret_cast<const uint4*>(qb + row * rstride + dg * 8);
-      *reinterpret_cast<uint4*>(gQ + (rg * DG + dg) * 128 + j * 16) = v;
-    }
+  for (int it = tid; it < kTcQ * DG; it += kTcThreads) {     // (row group, dim group, row): row fastest
+    const int j = it & 7, dg = (it >> 3) % DG, rg = (it >> 3) / DG;
+    const int row = q0 + rg * 8 + j;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (row < len) v = *reinterpret_cast<const uint4*>(qb + row * rstride + dg * 8);
+    *reinterpret_cast<uint4*>(gQ + (rg * DG + dg) * 128 + j * 16) = v;
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   tc_fence_before();
@@ -159,39 +156,46 @@ __global__ void __launch_bounds__(kTcThreads, 1) prefill_tc_kernel(const __grid_
   float m_ref = -INFINITY, lsum = 0.0f;
   constexpr uint32_t idS = umma_idesc_f16(128, kTcK, false);
   constexpr uint32_t idO = umma_idesc_f16(128, HD, true);
-  // dequantise the K tile and V tile `buf` for keys [k0, k0 + 64):
-  // item = (tensor, 8-key group, 8-dim group)
+  // dequantise the K tile and V tile `buf` for keys [k0, k0 + 64).  Item =
+  // one key row of one 8-dim group (16 B hi + 16 B lo); the row index within
+  // the core matrix varies fastest across lanes, so a warp stores 4 whole core
+  // matrices (512 contiguous bytes: no bank conflicts); each thread's items
+  // load first, then convert.
+  constexpr int kItems = 2 * kTcK * DG;               // (tensor, key, dim group)
+  constexpr int kPer = kItems / kTcThreads;            // 8 (hd 128) / 4 (hd 64)
   auto dequant = [&](int k0, int buf) {
-    for (int it = tid; it < 2 * (kTcK / 8) * DG; it += kTcThreads) {
-      const int isv = it >= (kTcK / 8) * DG;
-      const int rem = it - isv * (kTcK / 8) * DG;
-      const int kg = rem / DG, dg = rem % DG;
-      const uint8_t* codes = isv ? p.vc : p.kc;
-      const void* scales = isv ? p.vs : p.ks;
-      unsigned char* dst_h = (isv ? gV[0] + buf * kTileBytes : gK[0]) + (kg * DG + dg) * 128;
-      unsigned char* dst_l = (isv ? gV[1] + buf * kTileBytes : gK[1]) + (kg * DG + dg) * 128;
+    uint32_t w[kPer];
+    float sc[kPer];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int tok = k0 + kg * 8 + j;
-        uint4 vh = make_uint4(0, 0, 0, 0), vl = make_uint4(0, 0, 0, 0);
-        if (tok < len) {
-          const uint32_t w = *reinterpret_cast<const uint32_t*>(codes + (row_base + tok) * (HD / 2) + dg * 4);
-          const long long si = GRP ? srow_base + tok : (row_base + tok) * nblk + ((dg * 8) >> p.blk_shift);
-          const float s = F16S ? __half2float(reinterpret_cast<const __half*>(scales)[si])
-                               : reinterpret_cast<const float*>(scales)[si];
-          uint32_t hh[4], ll[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float x0 = __fmul_rn(s, s_lv[(w >> (8 * e)) & 15u]);        // RN32(s * L[code])
-            const float x1 = __fmul_rn(s, s_lv[(w >> (8 * e + 4)) & 15u]);
-            split2(x0, x1, hh[e], ll[e]);
-          }
-          vh = make_uint4(hh[0], hh[1], hh[2], hh[3]);
-          vl = make_uint4(ll[0], ll[1], ll[2], ll[3]);
-        }
-        *reinterpret_cast<uint4*>(dst_h + j * 16) = vh;
-        *reinterpret_cast<uint4*>(dst_l + j * 16) = vl;
+    for (int u = 0; u < kPer; ++u) {
+      const int it = tid + u * kTcThreads;
+      const int j = it & 7, dg = (it >> 3) % DG, kg = (it >> 3) / DG % (kTcK / 8), isv = it >= kItems / 2;
+      const int tok = k0 + kg * 8 + j;
+      w[u] = 0u;
+      sc[u] = 0.0f;
+      if (tok < len) {
+        const uint8_t* codes = isv ? p.vc : p.kc;
+        const void* scales = isv ? p.vs : p.ks;
+        w[u] = *reinterpret_cast<const uint32_t*>(codes + (row_base + tok) * (HD / 2) + dg * 4);
+        const long long si = GRP ? srow_base + tok : (row_base + tok) * nblk + ((dg * 8) >> p.blk_shift);
+        sc[u] = F16S ? __half2float(reinterpret_cast<const __half*>(scales)[si])
+                     : reinterpret_cast<const float*>(scales)[si];
       }
+    }
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int it = tid + u * kTcThreads;
+      const int j = it & 7, dg = (it >> 3) % DG, kg = (it >> 3) / DG % (kTcK / 8), isv = it >= kItems / 2;
+      uint32_t hh[4], ll[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float x0 = __fmul_rn(sc[u], s_lv[(w[u] >> (8 * e)) & 15u]);        // RN32(s * L[code])
+        const float x1 = __fmul_rn(sc[u], s_lv[(w[u] >> (8 * e + 4)) & 15u]);
+        split2(x0, x1, hh[e], ll[e]);
+      }
+      const uint32_t off = (kg * DG + dg) * 128 + j * 16;
+      *reinterpret_cast<uint4*>((isv ? gV[0] + buf * kTileBytes : gK[0]) + off) = make_uint4(hh[0], hh[1], hh[2], hh[3]);
+      *reinterpret_cast<uint4*>((isv ? gV[1] + buf * kTileBytes : gK[1]) + off) = make_uint4(ll[0], ll[1], ll[2], ll[3]);
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     tc_fence_before();
