@@ -804,6 +804,70 @@ def test_fused_gather_simulated_ranks(N, hd, blk, G):
     assert np.max(np.abs(bufs[0].cpu().numpy() - ref)) <= ATOL
 
 
+@pytest.mark.parametrize("hd,blk,G", [(64, 64, 2), (128, 64, 4)])
+def test_fused_gather_ranks_in_flight(N, hd, blk, G):
+    """The fused gather with G simulated ranks launched on G streams with no
+    host synchronisation between them, two back-to-back epochs each into
+    parity-double-buffered outputs and flags (the runtime's protocol): the
+    ranks' kernels overlap (a later rank starts as earlier CTAs retire),
+    their peer stores, fences, completion counters and flag releases
+    interleave.  No kernel waits on another (the profiling recipe forbids
+    that pattern on one GPU): the flags are checked after a device sync.
+    Every buffer holds every shard's rows bit for bit; flags hold the epoch."""
+    B, Hl, Tc = 4, 2, 1024
+    Ht = G * Hl
+    lens0 = [5, 1, 300, 700]
+    x = _rand_kv(B, max(lens0), Ht, hd, seed=81)
+    y = _rand_kv(B, max(lens0), Ht, hd, seed=82, outlier=False)
+    kc, ks = _oracle_cache(x, [0] * B, blk, Tc)
+    vc, vs = _oracle_cache(y, [0] * B, blk, Tc)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+    L1 = torch.tensor([n + 1 for n in lens0], dtype=torch.int32, device=DEV)
+    plan = N.make_plan(DEV)
+    N.nqkv_decode_plan(L1, Hl, Tc, True, plan, hd=hd)
+    bufs = [[torch.full((B, Ht, hd), float("nan"), device=DEV) for _ in range(G)] for _ in range(2)]
+    flags = [[torch.zeros(G, dtype=torch.int32, device=DEV) for _ in range(G)] for _ in range(2)]
+    optr = [torch.tensor([b.data_ptr() for b in bufs[par]], dtype=torch.int64, device=DEV) for par in range(2)]
+    fptr = [torch.tensor([f.data_ptr() for f in flags[par]], dtype=torch.int64, device=DEV) for par in range(2)]
+    caches, wss, steps = [], [], {}
+    for r in range(G):
+        hs = slice(r * Hl, (r + 1) * Hl)
+        caches.append([t(kc[:, hs]), t(ks[:, hs]), t(vc[:, hs]), t(vs[:, hs])])
+        wss.append(N.make_workspace(B, Hl, hd, Tc, DEV))
+    ref_caches = [[c.clone() for c in cc] for cc in caches]
+    for e in (8, 9):
+        kn = _rand_kv(B, 1, Ht, hd, seed=83 + e)[:, 0].to(DEV)
+        vn = _rand_kv(B, 1, Ht, hd, seed=85 + e, outlier=False)[:, 0].to(DEV)
+        q = torch.randn(B, Ht, hd, generator=torch.Generator().manual_seed(87 + e)).to(torch.float16).to(DEV)
+        steps[e] = (kn, vn, q)
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream() for _ in range(G)]
+    for e in (8, 9):                              # launch everything, no host sync
+        kn, vn, q = steps[e]
+        for r in range(G):
+            hs = slice(r * Hl, (r + 1) * Hl)
+            with torch.cuda.stream(streams[r]):
+                c = caches[r]
+                N.nqkv_decode_step_gather(kn[:, hs], vn[:, hs], q[:, hs].contiguous(), c[0], c[1], c[2], c[3],
+                                          L1, blk, wss[r], plan, optr[e & 1], fptr[e & 1], G, r, epoch=e)
+    torch.cuda.synchronize()
+    for e in (8, 9):                              # the same steps, one rank at a time, unfused gather
+        kn, vn, q = steps[e]
+        outs = []
+        for r in range(G):
+            hs = slice(r * Hl, (r + 1) * Hl)
+            c = ref_caches[r]
+            outs.append(N.nqkv_decode_step_planned(kn[:, hs], vn[:, hs], q[:, hs].contiguous(), c[0], c[1], c[2],
+                                                   c[3], L1, blk, N.make_workspace(B, Hl, hd, Tc, DEV), plan))
+        full = torch.cat(outs, dim=1)
+        for r in range(G):
+            assert torch.equal(bufs[e & 1][r], full), (e, r)
+            assert flags[e & 1][r].tolist() == [e] * G
+    for r in range(G):
+        assert all(torch.equal(a, b) for a, b in zip(caches[r], ref_caches[r]))
+        assert torch.count_nonzero(wss[r]) == 0
+
+
 def test_runtime_fused_gather_single_rank(N):
     """DecodeRunner with the all-gather fused into the epilogue over
     symmetric memory (one rank: the plumbing -- peer pointers, device epoch
