@@ -213,7 +213,8 @@ struct Smem {
   static constexpr uint32_t kPreFlag = kWalk + 96;
   static constexpr uint32_t kPre = kWalk + 112;
   static constexpr int kPreRecs = 4;
-  static constexpr uint32_t kBytes = (kPre + kPreRecs * (HD + 2) * 4 + 15) / 16 * 16;
+  static constexpr uint32_t kCur = (kPre + kPreRecs * (HD + 2) * 4 + 15) / 16 * 16;   // per-warp cursor (48 B)
+  static constexpr uint32_t kBytes = kCur + NW * 48;
   static_assert(kBytes <= 227 * 1024, "decode smem over budget");
   static_assert(kMaxBatch <= 2 * NW * 32, "per-batch arrays: two entries per thread");
   static_assert((kTab % 16) == 0 && (kMbar % 8) == 0 && (kO % 16) == 0 && (kWalk % 16) == 0,
@@ -1288,26 +1289,43 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
   // at piece boundaries.  (The host guarantees each codes tensor is < 4 GB,
   // so row offsets fit 32 bits.)
   using StageRegs = StageRegsT<RS>;
-  Piece lp = p0;
-  int ls = warp, lpi = 0, lro = 0, lns = nstages(p0), ltok = 0;
-  bool lvalid = warp < NC;
+  // Registers hold only the fast path: this lane's K-code pointer (V codes at
+  // a fixed distance), its scale byte offset, the rows left in the piece from
+  // its slot-0 row, the warp's stages left in the piece, and the piece index.
+  // The walk state (piece, first/last stage, round-robin origin) lives in a
+  // per-warp shared-memory slot, read only at piece boundaries.
+  struct WCur {
+    Piece lp;
+    int ls_last, lro, lns, pad[3];
+  };
+  static_assert(sizeof(WCur) == 48, "cursor slot");
+  WCur* s_cur = reinterpret_cast<WCur*>(smem + Sm::kCur) + warp;
   const uint8_t* kcp = p.kc;
-  const uint8_t* vcp = p.vc;
-  const uint8_t* ksp = static_cast<const uint8_t*>(p.ks);
-  const uint8_t* vsp = static_cast<const uint8_t*>(p.vs);
+  const long long vdelta = p.vc - p.kc;
+  uint32_t soff = 0;
+  int nvl = 0, left = 0, lpi = 0;
+  bool lvalid = warp < NC;
   constexpr int KSTEP = NC * ST * (HD / 2), SSTEP = NC * ST * NBLK * SB;
-  auto set_cursor = [&]() {
-    ltok = lp.t0 + ls * ST;
+  auto set_cursor = [&](const Piece& lp, int ls, int lro, int lns) {
+    const int ltok = lp.t0 + ls * ST;
     const uint32_t r = static_cast<uint32_t>(rowbase(lp) + ltok + g);
     const uint32_t rs = GRP ? static_cast<uint32_t>(srowbase(lp) + ltok + g) : r;
     kcp = p.kc + (r * (HD / 2) + sub * 8);
-    vcp = p.vc + (r * (HD / 2) + sub * 8);
-    const uint32_t so = (rs * NBLK + sidx) * SB + soff_rs;
-    ksp = static_cast<const uint8_t*>(p.ks) + so;
-    vsp = static_cast<const uint8_t*>(p.vs) + so;
+    soff = (rs * NBLK + sidx) * SB + soff_rs;
+    nvl = lp.t1 - ltok - g;                 // slot i of this lane holds a row iff i*G < nvl
+    left = (lns - 1 - ls) / NC;             // this warp's further stages in the piece
+    if (lane == 0) {
+      WCur c;
+      c.lp = lp;
+      c.ls_last = ls + NC * left;
+      c.lro = lro;
+      c.lns = lns;
+      *s_cur = c;
+    }
+    __syncwarp();
   };
   // cursor at this warp's first stage at or after (lp, ls): walks pieces
-  auto seek = [&]() -> bool {
+  auto seek = [&](Piece lp, int ls, int lro, int lns) -> bool {
     while (ls >= lns) {
       lro = (lro + lns) % NC;
       if (!walk_next(lp, lpi)) { lvalid = false; return false; }
@@ -1315,46 +1333,33 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
       lns = nstages(lp);
       ls = warp >= lro ? warp - lro : warp + NC - lro;
     }
-    set_cursor();
+    set_cursor(lp, ls, lro, lns);
     return true;
-  };
-  // bulk L2 prefetch (a hint: may run before the PDL wait) of this warp's
-  // stage NQKV_PF ahead in the same piece, issued by lane 0 (whose cursor is
-  // the stage's first row, byte 0)
-  auto prefetch_ahead = [&]() {
-    if (NQKV_PF > 0 && lane == 0 && ls + NQKV_PF * NC < lns) {
-      prefetch_l2(kcp + NQKV_PF * KSTEP, ST * (HD / 2));
-      prefetch_l2(vcp + NQKV_PF * KSTEP, ST * (HD / 2));
-      prefetch_l2(ksp + NQKV_PF * SSTEP, ST * NBLK * SB);
-      prefetch_l2(vsp + NQKV_PF * SSTEP, ST * NBLK * SB);
-    }
   };
   // this warp's next stage
   auto advance = [&]() -> bool {
     if (!lvalid) return false;
-    ls += NC;
-    if (ls < lns) {
-      ltok += NC * ST;
+    if (left > 0) {
+      --left;
       kcp += KSTEP;
-      vcp += KSTEP;
-      ksp += SSTEP;
-      vsp += SSTEP;
+      soff += SSTEP;
+      nvl -= NC * ST;
       return true;
     }
-    return seek();
+    const WCur c = *s_cur;
+    return seek(c.lp, c.ls_last + NC, c.lro, c.lns);
   };
   // loads of the cursor's stage; rows >= t1 are not loaded (a partial stage
   // -- only a piece's last -- keeps earlier finite data in those slots, and
   // consume masks them)
-  auto load_stage = [&](StageRegs& Rg, int& tok0, int& t1, int& pi, int dep) {
-    tok0 = ltok;
-    t1 = lp.t1;
+  auto load_stage = [&](StageRegs& Rg, int& nv, int& pi, int dep) {
+    nv = nvl;
     pi = lpi;
 #ifdef NQKV_EXP_NOLOAD
 #pragma unroll
     for (int i = 0; i < kTPS; ++i) {
-      Rg.k[i] = make_uint2(0x12345678u * (i + 1) + tok0, 0x9abcdef0u + lane);
-      Rg.v[i] = make_uint2(0x31415926u * (i + 3) + tok0, 0x27182818u + lane);
+      Rg.k[i] = make_uint2(0x12345678u * (i + 1) + nv, 0x9abcdef0u + lane);
+      Rg.v[i] = make_uint2(0x31415926u * (i + 3) + nv, 0x27182818u + lane);
     }
     return;
 #endif
@@ -1363,10 +1368,12 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
     // ptxas puts every global load of this loop on one scoreboard, so the
     // next stage's loads must not issue before the wait for the current
     // stage's data -- otherwise that wait would also wait for them.
-    const int row0 = ltok + g + dep;
+    const uint8_t* vcp = kcp + vdelta;
+    const uint8_t* ksp = static_cast<const uint8_t*>(p.ks) + soff;
+    const uint8_t* vsp = static_cast<const uint8_t*>(p.vs) + soff;
 #pragma unroll
     for (int i = 0; i < kTPS; ++i) {
-      if (row0 + i * G < t1) {
+      if (i * G + dep < nvl) {
         Rg.k[i] = ldg_stream_64(kcp + i * G * (HD / 2));
         Rg.v[i] = ldg_stream_64(vcp + i * G * (HD / 2));
         if constexpr (!RS) {
@@ -1376,7 +1383,7 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
       }
     }
     if constexpr (RS) {
-      if (row0 + (sub & 3) * G < t1) {
+      if ((sub & 3) * G + dep < nvl) {
         Rg.ks[0] = ld_scale<F16S>(ksp, 0);
         Rg.vs[0] = ld_scale<F16S>(vsp, 0);
       }
@@ -1389,11 +1396,11 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
     RA.k[i] = RA.v[i] = RB.k[i] = RB.v[i] = make_uint2(0, 0);
     RA.ks[RS ? 0 : i] = RA.vs[RS ? 0 : i] = RB.ks[RS ? 0 : i] = RB.vs[RS ? 0 : i] = 0.0f;
   }
-  int ta = 0, t1a = 0, pia = 0, tb = 0, t1b = 0, pib = 0;
+  int nva = 0, pia = 0, nvb = 0, pib = 0;
   bool ha = false, hb = false;
   auto fill_first = [&]() {
-    if (lvalid && seek()) {
-      load_stage(RA, ta, t1a, pia, 0);
+    if (lvalid && seek(p0, warp, 0, nstages(p0))) {
+      load_stage(RA, nva, pia, 0);
       ha = true;
     }
   };
@@ -1570,7 +1577,7 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
   };
 
   // scores, online-softmax update and the V weights of one stage ...
-  auto consume_s = [&](const StageRegs& Rg, int tok0, int t1, float (&wv)[kTPS]) {
+  auto consume_s = [&](const StageRegs& Rg, int nv, float (&wv)[kTPS]) {
     any = true;
 #ifdef NQKV_EXP_NOCOMPUTE
     {
@@ -1612,8 +1619,8 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
       float sj = (b0 ? k1 : k0) + __shfl_xor_sync(0xffffffffu, b0 ? k0 : k1, 1);
       sj *= Rg.ks[0];
       if (LPT == 8) sj += __shfl_xor_sync(0xffffffffu, sj, 4);
-      if (tok0 + ST > t1)             // warp-uniform: only a piece's last stage is partial
-        sj = (tok0 + (sub & 3) * G + g < t1) ? sj : -INFINITY;
+      if (nv + g < ST)                // warp-uniform: only a piece's last stage is partial
+        sj = ((sub & 3) * G < nv) ? sj : -INFINITY;
       // running max per token row group g (its 4 / 8 lanes share the V
       // weights, so they must share the max): 2 shuffle rounds, not 4-5;
       // groups are brought to a common max once per piece in end_piece
@@ -1642,9 +1649,9 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
 #pragma unroll
         for (int i = 0; i < kTPS; ++i) s[i] += __shfl_xor_sync(0xffffffffu, s[i], o);
       }
-      if (tok0 + ST > t1) {           // warp-uniform: only a piece's last stage is partial
+      if (nv + g < ST) {              // warp-uniform: only a piece's last stage is partial
 #pragma unroll
-        for (int i = 0; i < kTPS; ++i) s[i] = (tok0 + i * G + g < t1) ? s[i] : -INFINITY;
+        for (int i = 0; i < kTPS; ++i) s[i] = (i * G < nv) ? s[i] : -INFINITY;
       }
       float mt = s[0];
 #pragma unroll
@@ -1763,22 +1770,20 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
     {
       const int dep = static_cast<int>(RA.k[0].x & zero);
       hb = advance();
-      load_stage(RB, tb, t1b, pib, dep);     // no next stage: re-reads the last one (unused)
-      prefetch_ahead();
+      load_stage(RB, nvb, pib, dep);         // no next stage: re-reads the last one (unused)
       close_to(pia);
       float wv[kTPS];
-      consume_s(RA, ta, t1a, wv);
+      consume_s(RA, nva, wv);
       consume_v(RA, wv);
     }
     if (!hb) break;
     {
       const int dep = static_cast<int>(RB.k[0].x & zero);
       ha = advance();
-      load_stage(RA, ta, t1a, pia, dep);
-      prefetch_ahead();
+      load_stage(RA, nva, pia, dep);
       close_to(pib);
       float wv[kTPS];
-      consume_s(RB, tb, t1b, wv);
+      consume_s(RB, nvb, wv);
       consume_v(RB, wv);
     }
     TRACE(12);
