@@ -4,21 +4,22 @@
 // softmax(q . k^ / sqrt(hd)) . v^ with k^, v^ = RN32(s * L[code]) split into
 // fp16 hi + lo parts, P split the same way, fp32 accumulation.
 //
-// CTA = 8 warps, 256 queries of one (b, h) in two sets of 128 (one tcgen05
-// M = 128 accumulator each).  Per 64-key tile:
-//   1. all threads dequantise the K and V tiles into shared memory (fp16 hi
-//      and lo, no-swizzle canonical core-matrix layout: 8 keys x 8 dims per
-//      128-byte core matrix, rows = keys) -- K serves as the K-major B operand
-//      of S = Q K^T, V as the MN-major B operand of O += P V;
-//   2. one thread issues S_s = Q_s K_hi^T + Q_s K_lo^T (S in TMEM, 64 columns
-//      per set) and commits to an mbarrier;
-//   3. every thread owns one query row = one TMEM lane (tcgen05.ld 32x32b):
-//      causal mask, online softmax with a lazy reference max (O is rescaled
-//      in TMEM only when the row max grows by more than 2^8), P = exp2(s - m)
-//      split into hi / lo fp16 and written to shared memory (K-major A);
-//   4. one thread issues O_s += P_hi V_hi + P_lo V_hi + P_hi V_lo (O in TMEM,
-//      hd columns per set).
-// The output rows are read from TMEM, normalised and stored (fp32).
+// CTA = 256 queries of one (b, h) in two sets of 128 rows (one tcgen05
+// M = 128 accumulator each), warp-specialised (FlashAttention-4 style):
+//   - 4 dequantisation warps fill a 2-stage ring of K and V tiles (64 keys)
+//     in shared memory: fp16 hi and lo, no-swizzle canonical core-matrix
+//     layout (8 keys x 8 dims per 128-byte core matrix).  K serves as the
+//     K-major B operand of S = Q K^T, V as the MN-major B operand of P V;
+//   - one thread issues the MMAs: S_s(t+1) = Q_s K_hi^T + Q_s K_lo^T into a
+//     double-buffered TMEM S region per set while the softmax of tile t runs,
+//     then O_s += P_hi V_hi + P_lo V_hi + P_hi V_lo with P read from TMEM;
+//   - 8 softmax warps, one query row per thread (= TMEM lane, tcgen05.ld
+//     32x32b): causal mask, online softmax with a lazy reference max (O is
+//     rescaled in TMEM only when the row max grows by more than 2^8),
+//     P = exp2(s - m) split into hi / lo fp16 and written over the row's S
+//     columns (tcgen05.st), the A operand of P V.
+// Hand-offs are mbarriers (K/V full/empty, S full, P full, O done).  The
+// output rows are read from TMEM, normalised and stored (fp32).
 #pragma once
 #include "prefill.cuh"
 
@@ -26,13 +27,14 @@ namespace nqkv {
 
 constexpr int kTcQ = 256;        // queries per CTA (2 x M = 128)
 constexpr int kTcK = 64;         // keys per tile
-constexpr int kTcThreads = 256;
+constexpr int kTcSoftW = 8;      // softmax warps (4 per row set)
+constexpr int kTcDqW = 4;        // dequantisation warps
+constexpr int kTcThreads = (kTcSoftW + kTcDqW + 1) * 32;   // + the MMA warp
 
 template <int HD>
 constexpr size_t prefill_tc_smem_bytes() {
-  // Q (256 x HD) + K hi/lo + 2 x V hi/lo (64 x HD each) + P hi/lo (2 x 128 x 64 each) + slack
-  return static_cast<size_t>(kTcQ) * HD * 2 + 6 * static_cast<size_t>(kTcK) * HD * 2 +
-         2 * 2 * 128 * kTcK * 2 + 1024;
+  // Q (256 x HD) + 2 stages x (K hi/lo + V hi/lo) (64 x HD each) + alignment slack
+  return static_cast<size_t>(kTcQ) * HD * 2 + 8 * static_cast<size_t>(kTcK) * HD * 2 + 1024;
 }
 
 __device__ __forceinline__ uint64_t umma_sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -50,6 +52,14 @@ __device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t a, uint64_t b
       "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n"
       :: "r"(tmem_d), "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+// A operand in TMEM (row m at lane m, two fp16 per 32-bit column, even element low)
+__device__ __forceinline__ void umma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc,
+                                            uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n"
+      :: "r"(tmem_d), "r"(tmem_a), "l"(b), "r"(idesc), "r"(acc));
 }
 __device__ __forceinline__ void umma_commit(uint32_t mbar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" :: "r"(mbar) : "memory");
@@ -76,6 +86,13 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32
         "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
       : "memory");
 }
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+      :: "r"(taddr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+        "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void mbar_wait_tc(uint32_t mbar, uint32_t phase) {
@@ -83,29 +100,51 @@ __device__ __forceinline__ void mbar_wait_tc(uint32_t mbar, uint32_t phase) {
       "{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra W_%=;\n}\n"
       :: "r"(mbar), "r"(phase) : "memory");
 }
+// (hi, lo) fp16 split of an fp32 pair: hi = RN16(x), lo = RN16(x - hi), with
+// x - hi (exact in fp32) from the mixed-precision FMA hi * -1 + x
+__device__ __forceinline__ void split2_tc(uint64_t xy, uint32_t& hi, uint32_t& lo) {
+  asm("{\n.reg .b16 h0, h1, m1;\n.reg .f32 x, y, r0, r1;\n"
+      "mov.b64 {x, y}, %2;\n"
+      "cvt.rn.f16x2.f32 %0, y, x;\n"
+      "mov.b32 {h0, h1}, %0;\n"
+      "mov.b16 m1, 0xBC00;\n"
+      "fma.rn.f32.f16 r0, h0, m1, x;\n"
+      "fma.rn.f32.f16 r1, h1, m1, y;\n"
+      "cvt.rn.f16x2.f32 %1, r1, r0;\n}"
+      : "=r"(hi), "=r"(lo) : "l"(xy));
+}
+__device__ __forceinline__ uint64_t fadd2_tc(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ void mbar_arrive_tc(uint32_t mbar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(mbar) : "memory");
+}
 
 template <int HD, bool F16S, bool GRP>
 __global__ void __launch_bounds__(kTcThreads, 1) prefill_tc_kernel(const __grid_constant__ PrefillParams p) {
   constexpr int DG = HD / 8;                       // 8-dim groups
-  constexpr uint32_t kQBytes = kTcQ * HD * 2, kTileBytes = kTcK * HD * 2, kPBytes = 128 * kTcK * 2;
-  constexpr uint32_t kCols = HD == 128 ? 512 : 256;  // S: 2 x 64, O: 2 x HD (power of two)
+  constexpr uint32_t kQBytes = kTcQ * HD * 2, kTileBytes = kTcK * HD * 2;
+  constexpr uint32_t kCols = 512;
+  constexpr uint32_t kSP = 2 * HD;                 // TMEM: O_s at s * HD; S/P (set s, buffer j) at kSP + (2s + j) * 64
+  static_assert(kSP + 4 * kTcK <= kCols, "TMEM columns");
   extern __shared__ __align__(1024) unsigned char tc_smem[];
   const uint32_t sbase = (static_cast<uint32_t>(__cvta_generic_to_shared(tc_smem)) + 1023u) & ~1023u;
   unsigned char* gbase = tc_smem + (sbase - static_cast<uint32_t>(__cvta_generic_to_shared(tc_smem)));
-  // layout: Q | K hi | K lo | V hi (x2) | V lo (x2) | P hi (2 sets) | P lo (2 sets)
-  const uint32_t sQ = sbase, sKh = sQ + kQBytes, sKl = sKh + kTileBytes, sVh = sKl + kTileBytes,
-                 sVl = sVh + 2 * kTileBytes, sPh = sVl + 2 * kTileBytes, sPl = sPh + 2 * kPBytes;
+  // layout: Q | K stage 0 (hi, lo) | K stage 1 | V stage 0 (hi, lo) | V stage 1
+  const uint32_t sQ = sbase, sK = sQ + kQBytes, sV = sK + 4 * kTileBytes;
   unsigned char* gQ = gbase;
-  unsigned char* gK[2] = {gbase + kQBytes, gbase + kQBytes + kTileBytes};
-  unsigned char* gV[2] = {gbase + kQBytes + 2 * kTileBytes, gbase + kQBytes + 4 * kTileBytes};   // hi, lo (+ buffer)
-  unsigned char* gP[2] = {gbase + kQBytes + 6 * kTileBytes, gbase + kQBytes + 6 * kTileBytes + 2 * kPBytes};
-  __shared__ float s_lv[16];
+  unsigned char* gK = gbase + kQBytes;
+  unsigned char* gV = gK + 4 * kTileBytes;
+  __shared__ uint64_t s_lut[256];                  // code byte -> (L[low nibble], L[high nibble])
   __shared__ uint32_t s_tmem;
-  __shared__ __align__(8) uint64_t s_mbar[2];      // S ready, O ready
+  // 0-1 K full, 2-3 K empty, 4-5 V full, 6-7 V empty, 8-11 S full (2s + j), 12-15 P full, 16-17 O done
+  __shared__ __align__(8) uint64_t s_bar[18];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int set = warp >> 2, quad = warp & 3;       // accumulator set, TMEM lane quadrant
-  const int qt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
-  if (tid < 16) s_lv[tid] = p.lv.v[tid];
+  const int qt = static_cast<int>(gridDim.x) - 1 - static_cast<int>(blockIdx.x);   // longest causal rows first
+  const int h = blockIdx.y, b = blockIdx.z;
+  for (int i = tid; i < 256; i += kTcThreads) s_lut[i] = pack2(p.lv.v[i & 15], p.lv.v[i >> 4]);
   pdl_enter();
   const int len = min(max(p.seq_lens[b], 0), p.T);
   const int q0 = qt * kTcQ;
@@ -118,16 +157,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) prefill_tc_kernel(const __grid_
     }
     return;
   }
-  const uint32_t mb_s = static_cast<uint32_t>(__cvta_generic_to_shared(&s_mbar[0]));
-  const uint32_t mb_o = static_cast<uint32_t>(__cvta_generic_to_shared(&s_mbar[1]));
+  const uint32_t bar0 = static_cast<uint32_t>(__cvta_generic_to_shared(&s_bar[0]));
+  auto bar = [&](int i) { return bar0 + 8u * static_cast<uint32_t>(i); };
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::
                      "r"(static_cast<uint32_t>(__cvta_generic_to_shared(&s_tmem))), "n"(kCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 32) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(mb_s));
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(mb_o));
+    for (int i = 0; i < 18; ++i) {
+      const bool many = i < 2 || (i >= 4 && i < 6) || (i >= 12 && i < 16);   // thread arrivals
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(bar(i)), "r"(many ? 128 : 1));
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   // ---- Q (fp16, exact) into the K-major A layout: core (row group, dim group)
@@ -144,203 +185,238 @@ __global__ void __launch_bounds__(kTcThreads, 1) prefill_tc_kernel(const __grid_
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = s_tmem;
-  const uint32_t tS = tmem + set * kTcK;                     // this thread's set: S columns
-  const uint32_t tO = tmem + 2 * kTcK + set * HD;            //                    O columns
-  const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
-  const int rloc = quad * 32 + lane;                          // row within the set
-  const int row = q0 + set * 128 + rloc;                      // query row in the sequence
-  const long long row_base = (static_cast<long long>(b) * p.H + h) * p.Tc;
-  const long long srow_base = GRP ? ((static_cast<long long>(b) * p.H + h) >> p.hpb_shift) * p.Tc : row_base;
-  const int nblk = GRP ? 1 : HD >> p.blk_shift;
   const int last_key = min(q0 + kTcQ, len);
-  float m_ref = -INFINITY, lsum = 0.0f;
-  constexpr uint32_t idS = umma_idesc_f16(128, kTcK, false);
-  constexpr uint32_t idO = umma_idesc_f16(128, HD, true);
-  // dequantise the K tile and V tile `buf` for keys [k0, k0 + 64).  Item =
-  // one key row of one 8-dim group (16 B hi + 16 B lo); the row index within
-  // the core matrix varies fastest across lanes, so a warp stores 4 whole core
-  // matrices (512 contiguous bytes: no bank conflicts); each thread's items
-  // load first, then convert.
-  constexpr int kItems = 2 * kTcK * DG;               // (tensor, key, dim group)
-  constexpr int kPer = kItems / kTcThreads;            // 8 (hd 128) / 4 (hd 64)
-  auto dequant = [&](int k0, int buf) {
-    uint32_t w[kPer];
-    float sc[kPer];
-#pragma unroll
-    for (int u = 0; u < kPer; ++u) {
-      const int it = tid + u * kTcThreads;
-      const int j = it & 7, dg = (it >> 3) % DG, kg = (it >> 3) / DG % (kTcK / 8), isv = it >= kItems / 2;
-      const int tok = k0 + kg * 8 + j;
-      w[u] = 0u;
-      sc[u] = 0.0f;
-      if (tok < len) {
-        const uint8_t* codes = isv ? p.vc : p.kc;
-        const void* scales = isv ? p.vs : p.ks;
-        w[u] = *reinterpret_cast<const uint32_t*>(codes + (row_base + tok) * (HD / 2) + dg * 4);
-        const long long si = GRP ? srow_base + tok : (row_base + tok) * nblk + ((dg * 8) >> p.blk_shift);
-        sc[u] = F16S ? __half2float(reinterpret_cast<const __half*>(scales)[si])
-                     : reinterpret_cast<const float*>(scales)[si];
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < kPer; ++u) {
-      const int it = tid + u * kTcThreads;
-      const int j = it & 7, dg = (it >> 3) % DG, kg = (it >> 3) / DG % (kTcK / 8), isv = it >= kItems / 2;
-      uint32_t hh[4], ll[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float x0 = __fmul_rn(sc[u], s_lv[(w[u] >> (8 * e)) & 15u]);        // RN32(s * L[code])
-        const float x1 = __fmul_rn(sc[u], s_lv[(w[u] >> (8 * e + 4)) & 15u]);
-        split2(x0, x1, hh[e], ll[e]);
-      }
-      const uint32_t off = (kg * DG + dg) * 128 + j * 16;
-      *reinterpret_cast<uint4*>((isv ? gV[0] + buf * kTileBytes : gK[0]) + off) = make_uint4(hh[0], hh[1], hh[2], hh[3]);
-      *reinterpret_cast<uint4*>((isv ? gV[1] + buf * kTileBytes : gK[1]) + off) = make_uint4(ll[0], ll[1], ll[2], ll[3]);
-    }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    tc_fence_before();
-    __syncthreads();
-  };
-  auto issue_s = [&]() {       // S_s = Q_s K_hi^T + Q_s K_lo^T
-    if (tid == 0) {
+  const int ntiles = (last_key + kTcK - 1) / kTcK;
+  if (warp < kTcSoftW) {
+    // ================= softmax: one query row per thread
+    const int set = warp >> 2, quad = warp & 3;       // row set, TMEM lane quadrant
+    const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+    const int row = q0 + set * 128 + quad * 32 + lane;
+    const uint32_t tO = tmem + set * HD + lane_off;
+    const bool pos_scale = p.scale_log2 >= 0.0f;
+    float m_ref = -INFINITY;
+    uint64_t lsum = pack2(0.0f, 0.0f);                 // two partial sums
+    for (int t = 0; t < ntiles; ++t) {
+      const int k0 = t * kTcK, j = t & 1;
+      const uint32_t tS = tmem + kSP + (2 * set + j) * kTcK + lane_off;
+      mbar_wait_tc(bar(8 + 2 * set + j), (t >> 1) & 1);
       tc_fence_after();
+      float sv[kTcK];
+      {
+        uint32_t v[32];
+        tmem_ld32(tS, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int c = 0; c < 32; ++c) sv[c] = __uint_as_float(v[c]);
+        tmem_ld32(tS + 32, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int c = 0; c < 32; ++c) sv[32 + c] = __uint_as_float(v[c]);
+      }
+      // masked max of the raw scores (scale_log2 >= 0; a negative scale takes the min)
+      const bool interior = k0 + kTcK <= q0 + 1 && k0 + kTcK <= len;   // every key valid for every row
+      if (!interior) {
+#pragma unroll
+        for (int c = 0; c < kTcK; ++c) {
+          const int key = k0 + c;
+          if (!(key <= row && key < len)) sv[c] = pos_scale ? -INFINITY : INFINITY;
+        }
+      }
+      float mx = pos_scale ? -INFINITY : INFINITY;
+      if (pos_scale) {
+#pragma unroll
+        for (int c = 0; c < kTcK; ++c) mx = fmaxf(mx, sv[c]);
+      } else {
+#pragma unroll
+        for (int c = 0; c < kTcK; ++c) mx = fminf(mx, sv[c]);
+      }
+      mx = fabsf(mx) == INFINITY ? -INFINITY : mx * p.scale_log2;
+      // lazy reference max: rescale only when the max grows by more than 2^8
+      const bool grow = mx > m_ref + 8.0f;
+      float corr = 1.0f;
+      if (grow) {
+        corr = m_ref == -INFINITY ? 0.0f : fast_exp2(m_ref - mx);
+        m_ref = mx;
+        lsum = fmul2(lsum, pack2(corr, corr));
+      }
+      if (t > 0 && __any_sync(0xffffffffu, grow && corr != 1.0f)) {
+        mbar_wait_tc(bar(16 + set), (t - 1) & 1);       // P.V(t - 1) done: O stable
+        tc_fence_after();
+#pragma unroll 1
+        for (int c = 0; c < HD; c += 32) {
+          uint32_t v[32];
+          tmem_ld32(tO + c, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * corr);
+          tmem_st32(tO + c, v);
+        }
+      }
+      const float moff = m_ref == -INFINITY ? 0.0f : m_ref;
+      const uint64_t sc2 = pack2(p.scale_log2, p.scale_log2), mo2 = pack2(-moff, -moff);
+      // P over the row's S columns: hi at [0, 32), lo at [32, 64) (key 2c, 2c+1 in column c)
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf) {
+        uint32_t hh[16], ll[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const float2 x = unpack2(ffma2(pack2(sv[hf * 32 + 2 * e], sv[hf * 32 + 2 * e + 1]), sc2, mo2));
+          const uint64_t pp = pack2(fast_exp2(x.x), fast_exp2(x.y));
+          lsum = fadd2_tc(lsum, pp);
+          split2_tc(pp, hh[e], ll[e]);
+        }
+        tmem_st16(tS + hf * 16, hh);
+        tmem_st16(tS + 32 + hf * 16, ll);
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive_tc(bar(12 + 2 * set + j));
+    }
+    // P.V(n - 1) done.  A parity wait only tells apart adjacent phases, and
+    // P.V(n - 2) may still be running (S(n - 1), which this thread has seen
+    // complete, was issued before it), so wait for phase n - 2 first.  (The
+    // rescale wait above needs no such step: S(t) was issued after P.V(t - 2).)
+    if (ntiles >= 2) mbar_wait_tc(bar(16 + set), (ntiles - 2) & 1);
+    mbar_wait_tc(bar(16 + set), (ntiles - 1) & 1);
+    tc_fence_after();
+    // ---- epilogue: O / l for rows < len (0 beyond)
+    const float2 l2 = unpack2(lsum);
+    const float lsum1 = l2.x + l2.y;
+    const float inv = lsum1 > 0.0f ? 1.0f / lsum1 : 0.0f;
+#pragma unroll 1
+    for (int c = 0; c < HD; c += 32) {
+      uint32_t v[32];
+      tmem_ld32(tO + c, v);
+      tmem_wait_ld();
+      if (row < p.T) {
+        float* o = outb + row * rstride + c;
+#pragma unroll
+        for (int i = 0; i < 32; i += 4)
+          *reinterpret_cast<float4*>(o + i) =
+              row < len ? make_float4(__uint_as_float(v[i]) * inv, __uint_as_float(v[i + 1]) * inv,
+                                      __uint_as_float(v[i + 2]) * inv, __uint_as_float(v[i + 3]) * inv)
+                        : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+      }
+    }
+  } else if (warp < kTcSoftW + kTcDqW) {
+    // ================= dequantisation: K(t), V(t) into ring stage t & 1
+    const int dt = tid - kTcSoftW * 32;
+    const long long row_base = (static_cast<long long>(b) * p.H + h) * p.Tc;
+    const long long srow_base = GRP ? ((static_cast<long long>(b) * p.H + h) >> p.hpb_shift) * p.Tc : row_base;
+    const int nblk = GRP ? 1 : HD >> p.blk_shift;
+    // Item = 32 dims (16 code bytes, one scale: blk >= 32) of one key; the
+    // key's row within the core matrix varies fastest across lanes, so a warp
+    // loads 512 contiguous bytes of codes and each 16-byte store instruction
+    // writes 4 whole core matrices.  K(t) and V(t) codes load together.
+    constexpr int kQuads = HD / 32;
+    constexpr int kPer = kTcK * kQuads / (kTcDqW * 32);   // 2 (hd 128) / 1 (hd 64)
+    int key[kPer], soff[kPer];
+    uint32_t coff[kPer], doff[kPer];
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int it = dt + u * kTcDqW * 32;
+      const int j = it & 7, q = (it >> 3) % kQuads, kg = (it >> 3) / kQuads;
+      key[u] = kg * 8 + j;
+      coff[u] = static_cast<uint32_t>(key[u] * (HD / 2) + q * 16);
+      doff[u] = static_cast<uint32_t>((kg * DG + 4 * q) * 128 + j * 16);
+      soff[u] = GRP ? key[u] : key[u] * nblk + ((q * 32) >> p.blk_shift);
+    }
+    struct Raw {
+      uint4 w[kPer];
+      float s[kPer];
+    };
+    auto load = [&](const uint8_t* codes, const void* scales, int k0, Raw& r) {
+      const uint8_t* cb = codes + (row_base + k0) * (HD / 2);
+      const long long sb = GRP ? srow_base + k0 : (row_base + k0) * nblk;
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        r.w[u] = make_uint4(0u, 0u, 0u, 0u);
+        r.s[u] = 0.0f;
+        if (k0 + key[u] < len) {
+          r.w[u] = *reinterpret_cast<const uint4*>(cb + coff[u]);
+          r.s[u] = F16S ? __half2float(reinterpret_cast<const __half*>(scales)[sb + soff[u]])
+                        : reinterpret_cast<const float*>(scales)[sb + soff[u]];
+        }
+      }
+    };
+    auto convert = [&](const Raw& r, unsigned char* dhi) {
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        const uint64_t s2 = pack2(r.s[u], r.s[u]);
+        const uint32_t ww[4] = {r.w[u].x, r.w[u].y, r.w[u].z, r.w[u].w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {                  // dim group 4q + i
+          uint32_t hh[4], ll[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e)                  // RN32(s * L[code]) for dims 8i + 2e, + 1
+            split2_tc(fmul2(s2, s_lut[(ww[i] >> (8 * e)) & 0xffu]), hh[e], ll[e]);
+          *reinterpret_cast<uint4*>(dhi + doff[u] + i * 128) = make_uint4(hh[0], hh[1], hh[2], hh[3]);
+          *reinterpret_cast<uint4*>(dhi + kTileBytes + doff[u] + i * 128) = make_uint4(ll[0], ll[1], ll[2], ll[3]);
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    };
+    for (int t = 0; t < ntiles; ++t) {
+      const int st = t & 1;
+      const uint32_t ph = ((t >> 1) & 1) ^ 1;          // a fresh barrier passes parity 1
+      Raw rk, rv;
+      load(p.kc, p.ks, t * kTcK, rk);
+      load(p.vc, p.vs, t * kTcK, rv);
+      mbar_wait_tc(bar(2 + st), ph);
+      convert(rk, gK + st * 2 * kTileBytes);
+      mbar_arrive_tc(bar(0 + st));
+      mbar_wait_tc(bar(6 + st), ph);
+      convert(rv, gV + st * 2 * kTileBytes);
+      mbar_arrive_tc(bar(4 + st));
+    }
+  } else if (lane == 0) {
+    // ================= MMA issue (one thread)
+    constexpr uint32_t idS = umma_idesc_f16(128, kTcK, false);
+    constexpr uint32_t idO = umma_idesc_f16(128, HD, true);
+    auto issue_s = [&](int t) {         // S_s(t) = Q_s K_hi^T + Q_s K_lo^T, s = 0, 1
+      const int st = t & 1;
+      mbar_wait_tc(bar(0 + st), (t >> 1) & 1);
+      tc_fence_after();
+      const uint32_t kh = sK + st * 2 * kTileBytes, kl = kh + kTileBytes;
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
+        const uint32_t d = tmem + kSP + (2 * s + st) * kTcK;
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
           const uint64_t a = umma_sdesc(sQ + s * (kQBytes / 2) + kk * 256, 128, DG * 128);
-          umma_f16(tmem + s * kTcK, a, umma_sdesc(sKh + kk * 256, 128, DG * 128), idS, kk > 0);
-          umma_f16(tmem + s * kTcK, a, umma_sdesc(sKl + kk * 256, 128, DG * 128), idS, 1u);
+          umma_f16(d, a, umma_sdesc(kh + kk * 256, 128, DG * 128), idS, kk > 0);
+          umma_f16(d, a, umma_sdesc(kl + kk * 256, 128, DG * 128), idS, 1u);
         }
+        umma_commit(bar(8 + 2 * s + st));
       }
-      umma_commit(mb_s);
-    }
-  };
-  // Pipeline per tile t: softmax(t) -> issue P.V(t) -> dequantise tile t + 1
-  // (K single-buffered: S(t) is complete; V double-buffered: P.V(t) reads
-  // V(t) meanwhile) -> issue S(t + 1).  P and the O rescale wait for P.V(t-1).
-  const int ntiles = (last_key + kTcK - 1) / kTcK;
-  dequant(0, 0);
-  issue_s();
-  for (int tile = 0; tile < ntiles; ++tile) {
-    const int k0 = tile * kTcK;
-    mbar_wait_tc(mb_s, tile & 1);
-    tc_fence_after();
-    float sv[kTcK];
-    {
-      uint32_t v[32];
-      tmem_ld32(tS + lane_off, v);
-      tmem_wait_ld();
-#pragma unroll
-      for (int c = 0; c < 32; ++c) sv[c] = __uint_as_float(v[c]);
-      tmem_ld32(tS + lane_off + 32, v);
-      tmem_wait_ld();
-#pragma unroll
-      for (int c = 0; c < 32; ++c) sv[32 + c] = __uint_as_float(v[c]);
-    }
-    float mx = -INFINITY;
-    if (k0 + kTcK <= q0 + 1 && k0 + kTcK <= len) {       // interior tile: every key valid for every row
-#pragma unroll
-      for (int c = 0; c < kTcK; ++c) {
-        sv[c] *= p.scale_log2;
-        mx = fmaxf(mx, sv[c]);
-      }
-    } else {
-#pragma unroll
-      for (int c = 0; c < kTcK; ++c) {
-        const int key = k0 + c;
-        sv[c] = (key <= row && key < len) ? sv[c] * p.scale_log2 : -INFINITY;
-        mx = fmaxf(mx, sv[c]);
-      }
-    }
-    // lazy reference max: rescale only when the max grows by more than 2^8
-    const bool grow = mx > m_ref + 8.0f;
-    float corr = 1.0f;
-    if (grow) {
-      corr = m_ref == -INFINITY ? 0.0f : fast_exp2(m_ref - mx);
-      m_ref = mx;
-      lsum *= corr;
-    }
-    if (tile > 0) {
-      mbar_wait_tc(mb_o, (tile - 1) & 1);       // P.V(t - 1) done: O stable, P free
-      tc_fence_after();
-    }
-    if (tile > 0 && __any_sync(0xffffffffu, grow && corr != 1.0f)) {
-#pragma unroll
-      for (int c = 0; c < HD; c += 32) {
-        uint32_t v[32];
-        tmem_ld32(tO + lane_off + c, v);
-        tmem_wait_ld();
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) * corr);
-        tmem_st32(tO + lane_off + c, v);
-      }
-      tmem_wait_st();
-    }
-    const float moff = m_ref == -INFINITY ? 0.0f : m_ref;
-    unsigned char* ph = gP[0] + set * kPBytes;
-    unsigned char* pl = gP[1] + set * kPBytes;
-#pragma unroll
-    for (int kg = 0; kg < kTcK / 8; ++kg) {
-      uint32_t hh[4], ll[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float p0 = fast_exp2(sv[kg * 8 + 2 * e] - moff);
-        const float p1 = fast_exp2(sv[kg * 8 + 2 * e + 1] - moff);
-        lsum += p0 + p1;
-        split2(p0, p1, hh[e], ll[e]);
-      }
-      const uint32_t off = ((rloc >> 3) * (kTcK / 8) + kg) * 128 + (rloc & 7) * 16;
-      *reinterpret_cast<uint4*>(ph + off) = make_uint4(hh[0], hh[1], hh[2], hh[3]);
-      *reinterpret_cast<uint4*>(pl + off) = make_uint4(ll[0], ll[1], ll[2], ll[3]);
-    }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    tc_fence_before();
-    __syncthreads();
-    // O_s += P_hi V_hi + P_lo V_hi + P_hi V_lo  (V buffer tile & 1)
-    if (tid == 0) {
-      tc_fence_after();
-      const uint32_t vb = (tile & 1) * kTileBytes;
+      umma_commit(bar(2 + st));         // K stage free once both S are done
+    };
+    issue_s(0);
+    for (int t = 0; t < ntiles; ++t) {
+      if (t + 1 < ntiles) issue_s(t + 1);
+      const int st = t & 1;
+      mbar_wait_tc(bar(4 + st), (t >> 1) & 1);
+      const uint32_t vh = sV + st * 2 * kTileBytes, vl = vh + kTileBytes;
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
+        mbar_wait_tc(bar(12 + 2 * s + st), (t >> 1) & 1);
+        tc_fence_after();
+        const uint32_t ph = tmem + kSP + (2 * s + st) * kTcK, pl = ph + 32;
+        const uint32_t d = tmem + s * HD;
 #pragma unroll
         for (int kk = 0; kk < kTcK / 16; ++kk) {
-          const uint64_t ah = umma_sdesc(sPh + s * kPBytes + kk * 256, 128, (kTcK / 8) * 128);
-          const uint64_t al = umma_sdesc(sPl + s * kPBytes + kk * 256, 128, (kTcK / 8) * 128);
-          const uint64_t bh = umma_sdesc(sVh + vb + kk * 2 * DG * 128, DG * 128, 128);
-          const uint64_t bl = umma_sdesc(sVl + vb + kk * 2 * DG * 128, DG * 128, 128);
-          const uint32_t d = tmem + 2 * kTcK + s * HD;
-          umma_f16(d, ah, bh, idO, (tile > 0 || kk > 0) ? 1u : 0u);
-          umma_f16(d, al, bh, idO, 1u);
-          umma_f16(d, ah, bl, idO, 1u);
+          const uint64_t bh = umma_sdesc(vh + kk * 2 * DG * 128, DG * 128, 128);
+          const uint64_t bl = umma_sdesc(vl + kk * 2 * DG * 128, DG * 128, 128);
+          umma_f16_ts(d, ph + kk * 8, bh, idO, (t > 0 || kk > 0) ? 1u : 0u);
+          umma_f16_ts(d, pl + kk * 8, bh, idO, 1u);
+          umma_f16_ts(d, ph + kk * 8, bl, idO, 1u);
         }
+        umma_commit(bar(16 + s));
       }
-      umma_commit(mb_o);
-    }
-    if (tile + 1 < ntiles) {
-      dequant(k0 + kTcK, (tile + 1) & 1);        // overlaps P.V(t)
-      issue_s();
+      umma_commit(bar(6 + st));         // V stage free
     }
   }
-  mbar_wait_tc(mb_o, (ntiles - 1) & 1);
-  tc_fence_after();
-  // ---- epilogue: O / l for rows < len (0 beyond)
-  const float inv = lsum > 0.0f ? 1.0f / lsum : 0.0f;
-#pragma unroll
-  for (int c = 0; c < HD; c += 32) {
-    uint32_t v[32];
-    tmem_ld32(tO + lane_off + c, v);
-    tmem_wait_ld();
-    if (row < p.T) {
-      float* o = outb + row * rstride + c;
-#pragma unroll
-      for (int j = 0; j < 32; j += 4)
-        *reinterpret_cast<float4*>(o + j) =
-            row < len ? make_float4(__uint_as_float(v[j]) * inv, __uint_as_float(v[j + 1]) * inv,
-                                    __uint_as_float(v[j + 2]) * inv, __uint_as_float(v[j + 3]) * inv)
-                      : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-    }
-  }
+  __syncwarp();
   tc_fence_before();
   __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "n"(kCols));

@@ -110,6 +110,78 @@ __global__ void __launch_bounds__(128) probe(const __half* A, const __half* B, f
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "n"(128));
 }
 
+
+// A in TMEM: row r of A at TMEM lane r, K elements packed two fp16 per 32-bit
+// column (element 2c in the low half).  B K-major in shared memory.
+template <int N, int K>
+__global__ void __launch_bounds__(128) probe_ta(const __half* A, const __half* B, float* D, int swap_halves) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  unsigned char* sB = sm;
+  __shared__ uint32_t s_tmem;
+  __shared__ __align__(8) uint64_t s_mbar;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int i = tid; i < N * K; i += 128) {
+    const int n = i / K, k = i % K;
+    *reinterpret_cast<__half*>(sB + kmaj_off(n, k, K)) = B[i];
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::
+                     "r"(static_cast<uint32_t>(__cvta_generic_to_shared(&s_tmem))), "n"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(static_cast<uint32_t>(__cvta_generic_to_shared(&s_mbar))));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = s_tmem;
+  const uint32_t ta = tmem + 128;            // A columns [128, 128 + K/2)
+  // row tid -> lane tid
+  for (int c = 0; c < K / 2; ++c) {
+    __half lo = A[tid * K + 2 * c], hi = A[tid * K + 2 * c + 1];
+    if (swap_halves) { __half t = lo; lo = hi; hi = t; }
+    const uint32_t w = static_cast<uint32_t>(__half_as_ushort(lo)) | (static_cast<uint32_t>(__half_as_ushort(hi)) << 16);
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" :: "r"(ta + (static_cast<uint32_t>(warp * 32) << 16) + c), "r"(w) : "memory");
+  }
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t mbar = static_cast<uint32_t>(__cvta_generic_to_shared(&s_mbar));
+  if (tid == 0) {
+    const uint32_t b0 = static_cast<uint32_t>(__cvta_generic_to_shared(sB));
+    constexpr uint32_t id = idesc_f16(M, N, false);
+#pragma unroll
+    for (int s = 0; s < K / 16; ++s) {
+      const uint64_t bd = sdesc(b0 + s * 256, 128, (K / 8) * 128);
+      const uint32_t acc = s > 0;
+      asm volatile(
+          "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+          "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n"
+          :: "r"(tmem), "r"(ta + s * 8), "l"(bd), "r"(id), "r"(acc));
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" :: "r"(mbar) : "memory");
+  }
+  asm volatile(
+      "{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n@!p bra W_%=;\n}\n"
+      :: "r"(mbar) : "memory");
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  for (int c = 0; c < N; c += 8) {
+    uint32_t v[8];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "r"(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    for (int j = 0; j < 8; ++j) D[tid * N + c + j] = __uint_as_float(v[j]);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "n"(256));
+}
+
 template <int N, int K, bool BMN>
 bool run(const char* name, uint32_t lbo_b = 0, uint32_t sbo_b = 0) {
   std::vector<__half> A(M * K), B(N * K);
@@ -146,8 +218,51 @@ bool run(const char* name, uint32_t lbo_b = 0, uint32_t sbo_b = 0) {
   return bad == 0;
 }
 
+
+template <int N, int K>
+bool run_ta(const char* name, int swap) {
+  std::vector<__half> A(M * K), B(N * K);
+  std::vector<float> Af(M * K), Bf(N * K);
+  for (int i = 0; i < M * K; ++i) { Af[i] = static_cast<float>((i * 7 + 3) % 11 - 5); A[i] = __float2half(Af[i]); }
+  for (int i = 0; i < N * K; ++i) { Bf[i] = static_cast<float>((i * 5 + 1) % 9 - 4); B[i] = __float2half(Bf[i]); }
+  __half *dA, *dB;
+  float* dD;
+  CK(cudaMalloc(&dA, M * K * 2));
+  CK(cudaMalloc(&dB, N * K * 2));
+  CK(cudaMalloc(&dD, M * N * 4));
+  CK(cudaMemcpy(dA, A.data(), M * K * 2, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dB, B.data(), N * K * 2, cudaMemcpyHostToDevice));
+  CK(cudaMemset(dD, 0, M * N * 4));
+  const int smem = N * K * 2;
+  CK(cudaFuncSetAttribute(probe_ta<N, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  probe_ta<N, K><<<1, 128, smem>>>(dA, dB, dD, swap);
+  CK(cudaGetLastError());
+  CK(cudaDeviceSynchronize());
+  std::vector<float> D(M * N);
+  CK(cudaMemcpy(D.data(), dD, M * N * 4, cudaMemcpyDeviceToHost));
+  int bad = 0;
+  for (int r = 0; r < M; ++r)
+    for (int n = 0; n < N; ++n) {
+      float ref = 0;
+      for (int k = 0; k < K; ++k) ref += Af[r * K + k] * Bf[n * K + k];
+      if (D[r * N + n] != ref) {
+        if (bad < 3) printf("  mismatch r=%d n=%d got %f want %f\n", r, n, D[r * N + n], ref);
+        ++bad;
+      }
+    }
+  printf("%-40s %s (%d bad)\n", name, bad ? "FAIL" : "ok", bad);
+  cudaFree(dA); cudaFree(dB); cudaFree(dD);
+  return bad == 0;
+}
+
 int main(int argc, char** argv) {
   setvbuf(stdout, nullptr, _IONBF, 0);
+  if (argc > 1 && argv[1][0] == 't') {   // A in TMEM
+    run_ta<64, 64>("A in TMEM, N=64, K=64, even elem low", 0);
+    run_ta<64, 64>("A in TMEM, N=64, K=64, even elem high", 1);
+    run_ta<128, 64>("A in TMEM, N=128, K=64, even elem low", 0);
+    return 0;
+  }
   if (argc > 1) {       // MN-major only, the layout the prefill kernel uses
     return run<128, 64, true>("MN-major B, N=128, K=64, lbo=K-grp sbo=N-grp", (128 / 8) * 128, 128) &&
            run<64, 64, true>("MN-major B, N=64, K=64, lbo=K-grp sbo=N-grp", (64 / 8) * 128, 128) ? 0 : 1;
