@@ -298,6 +298,21 @@ int nqkv_abi_version(void) { return NQKV_ABI_VERSION; }
 __attribute__((used)) static const char kBuildIdTag[] = "NQKV_BUILD_ID=" NQKV_BUILD_ID;
 const char* nqkv_build_id(void) { return kBuildIdTag + 14; }
 
+#ifdef NQKV_PF_TRACE
+// development builds only: mapped host buffer the prefill kernel writes its progress to
+unsigned* nqkv_pf_trace_host(void) {
+  static unsigned* h = nullptr;
+  if (!h) {
+    if (cudaHostAlloc(&h, 4096, cudaHostAllocMapped) != cudaSuccess) return nullptr;
+    memset(h, 0, 4096);
+    unsigned* d = nullptr;
+    cudaHostGetDevicePointer(&d, h, 0);
+    cudaMemcpyToSymbol(g_pf_trace, &d, sizeof(d));
+  }
+  return h;
+}
+#endif
+
 const char* nqkv_status_string(int status) {
   switch (status) {
     case NQKV_OK: return "ok";

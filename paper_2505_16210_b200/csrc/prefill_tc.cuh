@@ -24,11 +24,20 @@
 #include "prefill.cuh"
 
 namespace nqkv {
+#ifdef NQKV_PF_TRACE
+__device__ unsigned* g_pf_trace;     // development builds: see PF_TR below
+#endif
 
 constexpr int kTcQ = 256;        // queries per CTA (2 x M = 128)
 constexpr int kTcK = 64;         // keys per tile
-constexpr int kTcSoftW = 8;      // softmax warps (4 per row set)
-constexpr int kTcDqW = 4;        // dequantisation warps
+#ifndef NQKV_PF_SOFTW
+#define NQKV_PF_SOFTW 8
+#endif
+constexpr int kTcSoftW = NQKV_PF_SOFTW;   // softmax warps: 8 (4 per row set) or 4 (both sets)
+#ifndef NQKV_PF_DQW
+#define NQKV_PF_DQW 4
+#endif
+constexpr int kTcDqW = NQKV_PF_DQW;   // dequantisation warps
 constexpr int kTcThreads = (kTcSoftW + kTcDqW + 1) * 32;   // + the MMA warp
 
 template <int HD>
@@ -100,6 +109,28 @@ __device__ __forceinline__ void mbar_wait_tc(uint32_t mbar, uint32_t phase) {
       "{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra W_%=;\n}\n"
       :: "r"(mbar), "r"(phase) : "memory");
 }
+// the same with a suspend-time hint: a waiting warp sleeps instead of
+// spinning (its retries would take issue slots from the other roles)
+__device__ __forceinline__ void mbar_wait_tc_sleep(uint32_t mbar, uint32_t phase) {
+#ifdef NQKV_PF_TRACE
+  for (;;) {
+    uint32_t ok;
+    asm volatile("{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 100000;\nselp.u32 %0, 1, 0, p;\n}\n"
+                 : "=r"(ok) : "r"(mbar), "r"(phase) : "memory");
+    if (ok) return;
+    if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (threadIdx.x & 31) == 0 && g_pf_trace) {
+      uint64_t st;
+      asm volatile("ld.shared.b64 %0, [%1];" : "=l"(st) : "r"(mbar));
+      *reinterpret_cast<volatile unsigned*>(g_pf_trace + (threadIdx.x >> 5) * 4 + 3) = static_cast<unsigned>(st >> 32);
+      *reinterpret_cast<volatile unsigned*>(g_pf_trace + 64 + (threadIdx.x >> 5) * 2) = static_cast<unsigned>(st);
+      *reinterpret_cast<volatile unsigned*>(g_pf_trace + 65 + (threadIdx.x >> 5) * 2) = mbar;
+    }
+  }
+#endif
+  asm volatile(
+      "{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n@!p bra W_%=;\n}\n"
+      :: "r"(mbar), "r"(phase) : "memory");
+}
 // (hi, lo) fp16 split of an fp32 pair: hi = RN16(x), lo = RN16(x - hi), with
 // x - hi (exact in fp32) from the mixed-precision FMA hi * -1 + x
 __device__ __forceinline__ void split2_tc(uint64_t xy, uint32_t& hi, uint32_t& lo) {
@@ -122,6 +153,19 @@ __device__ __forceinline__ void mbar_arrive_tc(uint32_t mbar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(mbar) : "memory");
 }
 
+#ifdef NQKV_PF_TRACE
+// development: progress of CTA (0, 0, 0)'s warps in mapped host memory, readable while it runs
+#define PF_TR(slot, val)                                                                 \
+  do {                                                                                   \
+    if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (threadIdx.x & 31) == 0 && g_pf_trace) { \
+      *reinterpret_cast<volatile unsigned*>(g_pf_trace + (threadIdx.x >> 5) * 4 + (slot)) = (val); \
+      __threadfence_system();                                                            \
+    }                                                                                    \
+  } while (0)
+#else
+#define PF_TR(slot, val) do { } while (0)
+#endif
+
 template <int HD, bool F16S, bool GRP>
 __global__ void __launch_bounds__(kTcThreads, 1) prefill_tc_kernel(const __grid_constant__ PrefillParams p) {
   constexpr int DG = HD / 8;                       // 8-dim groups
@@ -139,8 +183,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) prefill_tc_kernel(const __grid_
   unsigned char* gV = gK + 4 * kTileBytes;
   __shared__ uint64_t s_lut[256];                  // code byte -> (L[low nibble], L[high nibble])
   __shared__ uint32_t s_tmem;
-  // 0-1 K full, 2-3 K empty, 4-5 V full, 6-7 V empty, 8-11 S full (2s + j), 12-15 P full, 16-17 O done
-  __shared__ __align__(8) uint64_t s_bar[18];
+  // 0-1 K full, 2-3 K empty, 4-5 V full, 6-7 V empty, 8-11 S full (2s + j), 12-15 P full, 16-17 O done,
+  // 18 all MMAs done
+  __shared__ __align__(8) uint64_t s_bar[19];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int qt = static_cast<int>(gridDim.x) - 1 - static_cast<int>(blockIdx.x);   // longest causal rows first
   const int h = blockIdx.y, b = blockIdx.z;
@@ -165,9 +210,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) prefill_tc_kernel(const __grid_
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 32) {
-    for (int i = 0; i < 18; ++i) {
-      const bool many = i < 2 || (i >= 4 && i < 6) || (i >= 12 && i < 16);   // thread arrivals
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(bar(i)), "r"(many ? 128 : 1));
+    for (int i = 0; i < 19; ++i) {
+      const bool dq = i < 2 || (i >= 4 && i < 6);      // arrivals of every dequantisation thread
+      const bool sm = i >= 12 && i < 16;                 // of the 128 threads of a row set
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(bar(i)), "r"(dq ? kTcDqW * 32 : sm ? 128 : 1));
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -188,18 +234,25 @@ __global__ void __launch_bounds__(kTcThreads, 1) prefill_tc_kernel(const __grid_
   const int last_key = min(q0 + kTcQ, len);
   const int ntiles = (last_key + kTcK - 1) / kTcK;
   if (warp < kTcSoftW) {
-    // ================= softmax: one query row per thread
-    const int set = warp >> 2, quad = warp & 3;       // row set, TMEM lane quadrant
+    // ================= softmax: one query row per thread and row set (8
+    // warps: one set each; 4 warps: both sets, set 0 then set 1 per tile)
+    const int quad = warp & 3;                        // TMEM lane quadrant
     const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
-    const int row = q0 + set * 128 + quad * 32 + lane;
-    const uint32_t tO = tmem + set * HD + lane_off;
     const bool pos_scale = p.scale_log2 >= 0.0f;
-    float m_ref = -INFINITY;
-    uint64_t lsum = pack2(0.0f, 0.0f);                 // two partial sums
-    for (int t = 0; t < ntiles; ++t) {
+    struct RowState {
+      float m_ref;
+      uint64_t lsum;                                  // two partial sums
+    };
+    auto tile_step = [&](int set, RowState& rs, int t) {
+      const int row = q0 + set * 128 + quad * 32 + lane;
+      const uint32_t tO = tmem + set * HD + lane_off;
+      float& m_ref = rs.m_ref;
+      uint64_t& lsum = rs.lsum;
       const int k0 = t * kTcK, j = t & 1;
       const uint32_t tS = tmem + kSP + (2 * set + j) * kTcK + lane_off;
-      mbar_wait_tc(bar(8 + 2 * set + j), (t >> 1) & 1);
+      PF_TR(0, (0x1u << 12) | (set << 8) | t);
+      mbar_wait_tc_sleep(bar(8 + 2 * set + j), (t >> 1) & 1);
+      PF_TR(1, (0x1u << 12) | (set << 8) | t);
       tc_fence_after();
       float sv[kTcK];
       {
@@ -240,7 +293,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) prefill_tc_kernel(const __grid_
         lsum = fmul2(lsum, pack2(corr, corr));
       }
       if (t > 0 && __any_sync(0xffffffffu, grow && corr != 1.0f)) {
-        mbar_wait_tc(bar(16 + set), (t - 1) & 1);       // P.V(t - 1) done: O stable
+        PF_TR(0, (0x2u << 12) | (set << 8) | t);
+        mbar_wait_tc_sleep(bar(16 + set), (t - 1) & 1);       // P.V(t - 1) done: O stable
+        PF_TR(1, (0x2u << 12) | (set << 8) | t);
         tc_fence_after();
 #pragma unroll 1
         for (int c = 0; c < HD; c += 32) {
@@ -271,13 +326,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) prefill_tc_kernel(const __grid_
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive_tc(bar(12 + 2 * set + j));
-    }
-    // P.V(n - 1) done.  A parity wait only tells apart adjacent phases, and
-    // P.V(n - 2) may still be running (S(n - 1), which this thread has seen
-    // complete, was issued before it), so wait for phase n - 2 first.  (The
-    // rescale wait above needs no such step: S(t) was issued after P.V(t - 2).)
-    if (ntiles >= 2) mbar_wait_tc(bar(16 + set), (ntiles - 2) & 1);
-    mbar_wait_tc(bar(16 + set), (ntiles - 1) & 1);
+      PF_TR(2, (0x3u << 12) | (set << 8) | t);
+    };
+    auto finish = [&](int set, const RowState& rs) {
+    const int row = q0 + set * 128 + quad * 32 + lane;
+    const uint32_t tO = tmem + set * HD + lane_off;
+    const uint64_t lsum = rs.lsum;
+    // every MMA done: a barrier of its own that completes once.  (A parity
+    // wait only tells apart adjacent phases; here P.V(n - 2) may be running
+    // or P.V(n - 1) long complete.  The rescale wait above is unambiguous:
+    // S(t), complete there, was issued after P.V(t - 2).)
+    PF_TR(0, (0x4u << 12) | (set << 8));
+    mbar_wait_tc_sleep(bar(18), 0);
+    PF_TR(1, (0x4u << 12) | (set << 8));
     tc_fence_after();
     // ---- epilogue: O / l for rows < len (0 beyond)
     const float2 l2 = unpack2(lsum);
@@ -298,6 +359,21 @@ __global__ void __launch_bounds__(kTcThreads, 1) prefill_tc_kernel(const __grid_
                         : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
       }
     }
+    };
+    if constexpr (kTcSoftW == 8) {
+      const int set = warp >> 2;
+      RowState rs{-INFINITY, pack2(0.0f, 0.0f)};
+      for (int t = 0; t < ntiles; ++t) tile_step(set, rs, t);
+      finish(set, rs);
+    } else {
+      RowState r0{-INFINITY, pack2(0.0f, 0.0f)}, r1{-INFINITY, pack2(0.0f, 0.0f)};
+      for (int t = 0; t < ntiles; ++t) {
+        tile_step(0, r0, t);
+        tile_step(1, r1, t);
+      }
+      finish(0, r0);
+      finish(1, r1);
+    }
   } else if (warp < kTcSoftW + kTcDqW) {
     // ================= dequantisation: K(t), V(t) into ring stage t & 1
     const int dt = tid - kTcSoftW * 32;
@@ -309,14 +385,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) prefill_tc_kernel(const __grid_
     // loads 512 contiguous bytes of codes and each 16-byte store instruction
     // writes 4 whole core matrices.  K(t) and V(t) codes load together.
     constexpr int kQuads = HD / 32;
-    constexpr int kPer = kTcK * kQuads / (kTcDqW * 32);   // 2 (hd 128) / 1 (hd 64)
+    constexpr int kItems = kTcK * kQuads;
+    constexpr int kPer = (kItems + kTcDqW * 32 - 1) / (kTcDqW * 32);   // 2 (hd 128) / 1 (hd 64) at 4 warps
     int key[kPer], soff[kPer];
     uint32_t coff[kPer], doff[kPer];
 #pragma unroll
     for (int u = 0; u < kPer; ++u) {
       const int it = dt + u * kTcDqW * 32;
       const int j = it & 7, q = (it >> 3) % kQuads, kg = (it >> 3) / kQuads;
-      key[u] = kg * 8 + j;
+      key[u] = it < kItems ? kg * 8 + j : (1 << 29);     // no such item: never loaded or stored
       coff[u] = static_cast<uint32_t>(key[u] * (HD / 2) + q * 16);
       doff[u] = static_cast<uint32_t>((kg * DG + 4 * q) * 128 + j * 16);
       soff[u] = GRP ? key[u] : key[u] * nblk + ((q * 32) >> p.blk_shift);
@@ -325,14 +402,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) prefill_tc_kernel(const __grid_
       uint4 w[kPer];
       float s[kPer];
     };
-    auto load = [&](const uint8_t* codes, const void* scales, int k0, Raw& r) {
+    auto load = [&](const uint8_t* codes, const void* scales, int k0, Raw& r, int dep) {
       const uint8_t* cb = codes + (row_base + k0) * (HD / 2);
       const long long sb = GRP ? srow_base + k0 : (row_base + k0) * nblk;
 #pragma unroll
       for (int u = 0; u < kPer; ++u) {
         r.w[u] = make_uint4(0u, 0u, 0u, 0u);
         r.s[u] = 0.0f;
-        if (k0 + key[u] < len) {
+        if (k0 + key[u] + dep < len) {
           r.w[u] = *reinterpret_cast<const uint4*>(cb + coff[u]);
           r.s[u] = F16S ? __half2float(reinterpret_cast<const __half*>(scales)[sb + soff[u]])
                         : reinterpret_cast<const float*>(scales)[sb + soff[u]];
@@ -342,6 +419,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) prefill_tc_kernel(const __grid_
     auto convert = [&](const Raw& r, unsigned char* dhi) {
 #pragma unroll
       for (int u = 0; u < kPer; ++u) {
+        if (kItems % (kTcDqW * 32) != 0 && key[u] >= kTcK) continue;
         const uint64_t s2 = pack2(r.s[u], r.s[u]);
         const uint32_t ww[4] = {r.w[u].x, r.w[u].y, r.w[u].z, r.w[u].w};
 #pragma unroll
@@ -356,18 +434,34 @@ __global__ void __launch_bounds__(kTcThreads, 1) prefill_tc_kernel(const __grid_
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     };
+    // Tile t + 1's loads are issued once tile t's data has arrived (their
+    // predicate carries `dep`, 0 computed from tile t's first code word):
+    // ptxas keeps all these loads on one scoreboard, so loads issued earlier
+    // would make the wait for tile t's data also wait for them.
+    uint32_t zero;
+    asm volatile("mov.u32 %0, 0;" : "=r"(zero));
+    Raw rk, rv;
+    load(p.kc, p.ks, 0, rk, 0);
+    load(p.vc, p.vs, 0, rv, 0);
     for (int t = 0; t < ntiles; ++t) {
       const int st = t & 1;
       const uint32_t ph = ((t >> 1) & 1) ^ 1;          // a fresh barrier passes parity 1
-      Raw rk, rv;
-      load(p.kc, p.ks, t * kTcK, rk);
-      load(p.vc, p.vs, t * kTcK, rv);
-      mbar_wait_tc(bar(2 + st), ph);
+      const int dep = static_cast<int>(rk.w[0].x & zero);
+      Raw nk, nv;
+      const int kn = t + 1 < ntiles ? (t + 1) * kTcK : len;   // past the end: no loads
+      load(p.kc, p.ks, kn, nk, dep);
+      load(p.vc, p.vs, kn, nv, dep);
+      PF_TR(0, (0x5u << 12) | t);
+      mbar_wait_tc_sleep(bar(2 + st), ph);
       convert(rk, gK + st * 2 * kTileBytes);
       mbar_arrive_tc(bar(0 + st));
-      mbar_wait_tc(bar(6 + st), ph);
+      PF_TR(0, (0x6u << 12) | t);
+      mbar_wait_tc_sleep(bar(6 + st), ph);
       convert(rv, gV + st * 2 * kTileBytes);
       mbar_arrive_tc(bar(4 + st));
+      PF_TR(1, (0x7u << 12) | t);
+      rk = nk;
+      rv = nv;
     }
   } else if (lane == 0) {
     // ================= MMA issue (one thread)
@@ -375,7 +469,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) prefill_tc_kernel(const __grid_
     constexpr uint32_t idO = umma_idesc_f16(128, HD, true);
     auto issue_s = [&](int t) {         // S_s(t) = Q_s K_hi^T + Q_s K_lo^T, s = 0, 1
       const int st = t & 1;
+      PF_TR(0, (0x8u << 12) | t);
       mbar_wait_tc(bar(0 + st), (t >> 1) & 1);
+      PF_TR(1, (0x8u << 12) | t);
       tc_fence_after();
       const uint32_t kh = sK + st * 2 * kTileBytes, kl = kh + kTileBytes;
 #pragma unroll
@@ -395,11 +491,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) prefill_tc_kernel(const __grid_
     for (int t = 0; t < ntiles; ++t) {
       if (t + 1 < ntiles) issue_s(t + 1);
       const int st = t & 1;
+      PF_TR(0, (0x9u << 12) | t);
       mbar_wait_tc(bar(4 + st), (t >> 1) & 1);
       const uint32_t vh = sV + st * 2 * kTileBytes, vl = vh + kTileBytes;
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
+        PF_TR(0, (0xAu << 12) | (s << 8) | t);
         mbar_wait_tc(bar(12 + 2 * s + st), (t >> 1) & 1);
+        PF_TR(1, (0xAu << 12) | (s << 8) | t);
         tc_fence_after();
         const uint32_t ph = tmem + kSP + (2 * s + st) * kTcK, pl = ph + 32;
         const uint32_t d = tmem + s * HD;
@@ -415,6 +514,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) prefill_tc_kernel(const __grid_
       }
       umma_commit(bar(6 + st));         // V stage free
     }
+    umma_commit(bar(18));
   }
   __syncwarp();
   tc_fence_before();
