@@ -6,19 +6,27 @@
 //
 // CTA = 256 queries of one (b, h) in two sets of 128 rows (one tcgen05
 // M = 128 accumulator each), warp-specialised (FlashAttention-4 style):
-//   - 4 dequantisation warps fill a 2-stage ring of K and V tiles (64 keys)
-//     in shared memory: fp16 hi and lo, no-swizzle canonical core-matrix
-//     layout (8 keys x 8 dims per 128-byte core matrix).  K serves as the
-//     K-major B operand of S = Q K^T, V as the MN-major B operand of P V;
-//   - one thread issues the MMAs: S_s(t+1) = Q_s K_hi^T + Q_s K_lo^T into a
-//     double-buffered TMEM S region per set while the softmax of tile t runs,
-//     then O_s += P_hi V_hi + P_lo V_hi + P_hi V_lo with P read from TMEM;
-//   - 8 softmax warps, one query row per thread (= TMEM lane, tcgen05.ld
-//     32x32b): causal mask, online softmax with a lazy reference max (O is
-//     rescaled in TMEM only when the row max grows by more than 2^8),
-//     P = exp2(s - m) split into hi / lo fp16 and written over the row's S
-//     columns (tcgen05.st), the A operand of P V.
-// Hand-offs are mbarriers (K/V full/empty, S full, P full, O done).  The
+//   - the softmax threads (one query row each) first write their q row into
+//     TMEM: Q is the TMEM A operand of S = Q K^T, so the MMAs read only K
+//     from shared memory (the shared-memory port is the scarce resource:
+//     an SS-mode M = 128, N = 64 MMA needs 192 B/clk of operand reads);
+//   - dequantisation warps fill a 3-stage ring of K and V tiles (64 keys) in
+//     shared memory: fp16 hi and lo, no-swizzle canonical core-matrix
+//     layout (8 keys x 8 dims per 128-byte core matrix).  K is the K-major
+//     B operand of S = Q K^T, V the MN-major B operand of P V;
+//   - one thread issues the MMAs, the two row sets ping-ponging:
+//     P.V_0(t), S_0(t+1), P.V_1(t), S_1(t+1), ... with
+//     S_s = Q_s K_hi^T + Q_s K_lo^T and O_s += P_hi V_hi + P_lo V_hi + P_hi V_lo,
+//     so the tensor cores work on one set while the other set's softmax runs;
+//   - 8 softmax warps (4 per set), one query row per thread (= TMEM lane,
+//     tcgen05.ld 32x32b): causal mask, online softmax with a lazy reference
+//     max (O is rescaled in TMEM only when the row max grows by more than
+//     2^8), P = exp2(s - m) split into hi / lo fp16 and written over the
+//     row's S columns (tcgen05.st) as the TMEM A operand of P V.
+// TMEM (512 columns): O_s at s * HD, S/P_s at 2 HD + 64 s, Q_s after them.
+// S_s(t) is issued after P.V_s(t - 1) and MMAs complete in issue order, so
+// "S_s(t) complete" also means O_s is stable and P_s(t - 1) consumed.
+// Hand-offs are mbarriers (K/V full/empty, S full, P full, all done).  The
 // output rows are read from TMEM, normalised and stored (fp32).
 #pragma once
 #include "prefill.cuh"
@@ -30,10 +38,8 @@ __device__ unsigned* g_pf_trace;     // development builds: see PF_TR below
 
 constexpr int kTcQ = 256;        // queries per CTA (2 x M = 128)
 constexpr int kTcK = 64;         // keys per tile
-#ifndef NQKV_PF_SOFTW
-#define NQKV_PF_SOFTW 8
-#endif
-constexpr int kTcSoftW = NQKV_PF_SOFTW;   // softmax warps: 8 (4 per row set) or 4 (both sets)
+constexpr int kTcSoftW = 8;      // softmax warps (4 per row set)
+constexpr int kTcStages = 3;     // K/V ring depth
 #ifndef NQKV_PF_DQW
 #define NQKV_PF_DQW 4
 #endif
@@ -42,8 +48,8 @@ constexpr int kTcThreads = (kTcSoftW + kTcDqW + 1) * 32;   // + the MMA warp
 
 template <int HD>
 constexpr size_t prefill_tc_smem_bytes() {
-  // Q (256 x HD) + 2 stages x (K hi/lo + V hi/lo) (64 x HD each) + alignment slack
-  return static_cast<size_t>(kTcQ) * HD * 2 + 8 * static_cast<size_t>(kTcK) * HD * 2 + 1024;
+  // 3 stages x (K hi/lo + V hi/lo) (64 x HD fp16 each) + alignment slack
+  return static_cast<size_t>(kTcStages) * 4 * kTcK * HD * 2 + 1024;
 }
 
 __device__ __forceinline__ uint64_t umma_sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -169,23 +175,19 @@ __device__ __forceinline__ void mbar_arrive_tc(uint32_t mbar) {
 template <int HD, bool F16S, bool GRP>
 __global__ void __launch_bounds__(kTcThreads, 1) prefill_tc_kernel(const __grid_constant__ PrefillParams p) {
   constexpr int DG = HD / 8;                       // 8-dim groups
-  constexpr uint32_t kQBytes = kTcQ * HD * 2, kTileBytes = kTcK * HD * 2;
+  constexpr uint32_t kTileBytes = kTcK * HD * 2, kStageBytes = 4 * kTileBytes;   // K hi, K lo, V hi, V lo
   constexpr uint32_t kCols = 512;
-  constexpr uint32_t kSP = 2 * HD;                 // TMEM: O_s at s * HD; S/P (set s, buffer j) at kSP + (2s + j) * 64
-  static_assert(kSP + 4 * kTcK <= kCols, "TMEM columns");
+  constexpr uint32_t kSP = 2 * HD;                 // TMEM: O_s at s * HD, S/P_s at kSP + 64 s, Q_s at kQc + HD/2 s
+  constexpr uint32_t kQc = kSP + 2 * kTcK;
+  static_assert(kQc + HD <= kCols, "TMEM columns");
   extern __shared__ __align__(1024) unsigned char tc_smem[];
   const uint32_t sbase = (static_cast<uint32_t>(__cvta_generic_to_shared(tc_smem)) + 1023u) & ~1023u;
   unsigned char* gbase = tc_smem + (sbase - static_cast<uint32_t>(__cvta_generic_to_shared(tc_smem)));
-  // layout: Q | K stage 0 (hi, lo) | K stage 1 | V stage 0 (hi, lo) | V stage 1
-  const uint32_t sQ = sbase, sK = sQ + kQBytes, sV = sK + 4 * kTileBytes;
-  unsigned char* gQ = gbase;
-  unsigned char* gK = gbase + kQBytes;
-  unsigned char* gV = gK + 4 * kTileBytes;
   __shared__ uint64_t s_lut[256];                  // code byte -> (L[low nibble], L[high nibble])
   __shared__ uint32_t s_tmem;
-  // 0-1 K full, 2-3 K empty, 4-5 V full, 6-7 V empty, 8-11 S full (2s + j), 12-15 P full, 16-17 O done,
-  // 18 all MMAs done
-  __shared__ __align__(8) uint64_t s_bar[19];
+  // [0,3) K full, [3,6) K empty, [6,9) V full, [9,12) V empty, 12-13 S full, 14-15 P full, 16 all MMAs done
+  constexpr int kBars = 17;
+  __shared__ __align__(8) uint64_t s_bar[kBars];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int qt = static_cast<int>(gridDim.x) - 1 - static_cast<int>(blockIdx.x);   // longest causal rows first
   const int h = blockIdx.y, b = blockIdx.z;
@@ -210,23 +212,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) prefill_tc_kernel(const __grid_
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 32) {
-    for (int i = 0; i < 19; ++i) {
-      const bool dq = i < 2 || (i >= 4 && i < 6);      // arrivals of every dequantisation thread
-      const bool sm = i >= 12 && i < 16;                 // of the 128 threads of a row set
+    for (int i = 0; i < kBars; ++i) {
+      const bool dq = i < 3 || (i >= 6 && i < 9);      // arrivals of every dequantisation thread
+      const bool sm = i == 14 || i == 15;                // of the 128 threads of a row set
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(bar(i)), "r"(dq ? kTcDqW * 32 : sm ? 128 : 1));
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  // ---- Q (fp16, exact) into the K-major A layout: core (row group, dim group)
-  const __half* qb = p.q + (static_cast<long long>(b) * p.T) * rstride + static_cast<long long>(h) * HD;
-  for (int it = tid; it < kTcQ * DG; it += kTcThreads) {     // (row group, dim group, row): row fastest
-    const int j = it & 7, dg = (it >> 3) % DG, rg = (it >> 3) / DG;
-    const int row = q0 + rg * 8 + j;
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (row < len) v = *reinterpret_cast<const uint4*>(qb + row * rstride + dg * 8);
-    *reinterpret_cast<uint4*>(gQ + (rg * DG + dg) * 128 + j * 16) = v;
-  }
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -234,24 +226,39 @@ __global__ void __launch_bounds__(kTcThreads, 1) prefill_tc_kernel(const __grid_
   const int last_key = min(q0 + kTcQ, len);
   const int ntiles = (last_key + kTcK - 1) / kTcK;
   if (warp < kTcSoftW) {
-    // ================= softmax: one query row per thread and row set (8
-    // warps: one set each; 4 warps: both sets, set 0 then set 1 per tile)
-    const int quad = warp & 3;                        // TMEM lane quadrant
+    // ================= softmax: one query row per thread
+    const int set = warp >> 2, quad = warp & 3;       // row set, TMEM lane quadrant
     const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+    const int row = q0 + set * 128 + quad * 32 + lane;
+    const uint32_t tO = tmem + set * HD + lane_off;
+    const uint32_t tS = tmem + kSP + set * kTcK + lane_off;
+    // ---- the q row (fp16, exact) into TMEM: the A operand of S (two fp16 per column)
+    {
+      const __half* qr = p.q + (static_cast<long long>(b) * p.T + min(row, p.T - 1)) * rstride +
+                         static_cast<long long>(h) * HD;
+      const uint32_t tQ = tmem + kQc + set * (HD / 2) + lane_off;
+#pragma unroll
+      for (int c = 0; c < HD / 2; c += 16) {
+        uint32_t v[16];
+#pragma unroll
+        for (int i = 0; i < 16; i += 4) {
+          uint4 w = make_uint4(0u, 0u, 0u, 0u);
+          if (row < len) w = *reinterpret_cast<const uint4*>(qr + 2 * (c + i));
+          v[i] = w.x; v[i + 1] = w.y; v[i + 2] = w.z; v[i + 3] = w.w;
+        }
+        tmem_st16(tQ + c, v);
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive_tc(bar(14 + set));                 // P-full phase 0 doubles as "Q written"
+    }
     const bool pos_scale = p.scale_log2 >= 0.0f;
-    struct RowState {
-      float m_ref;
-      uint64_t lsum;                                  // two partial sums
-    };
-    auto tile_step = [&](int set, RowState& rs, int t) {
-      const int row = q0 + set * 128 + quad * 32 + lane;
-      const uint32_t tO = tmem + set * HD + lane_off;
-      float& m_ref = rs.m_ref;
-      uint64_t& lsum = rs.lsum;
-      const int k0 = t * kTcK, j = t & 1;
-      const uint32_t tS = tmem + kSP + (2 * set + j) * kTcK + lane_off;
+    float m_ref = -INFINITY;
+    uint64_t lsum = pack2(0.0f, 0.0f);               // two partial sums
+    for (int t = 0; t < ntiles; ++t) {
+      const int k0 = t * kTcK;
       PF_TR(0, (0x1u << 12) | (set << 8) | t);
-      mbar_wait_tc_sleep(bar(8 + 2 * set + j), (t >> 1) & 1);
+      mbar_wait_tc_sleep(bar(12 + set), t & 1);      // S_s(t) done: also P.V_s(t - 1) (issue order)
       PF_TR(1, (0x1u << 12) | (set << 8) | t);
       tc_fence_after();
       float sv[kTcK];
@@ -292,11 +299,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) prefill_tc_kernel(const __grid_
         m_ref = mx;
         lsum = fmul2(lsum, pack2(corr, corr));
       }
-      if (t > 0 && __any_sync(0xffffffffu, grow && corr != 1.0f)) {
-        PF_TR(0, (0x2u << 12) | (set << 8) | t);
-        mbar_wait_tc_sleep(bar(16 + set), (t - 1) & 1);       // P.V(t - 1) done: O stable
-        PF_TR(1, (0x2u << 12) | (set << 8) | t);
-        tc_fence_after();
+      if (t > 0 && __any_sync(0xffffffffu, grow && corr != 1.0f)) {   // O_s is stable: see above
 #pragma unroll 1
         for (int c = 0; c < HD; c += 32) {
           uint32_t v[32];
@@ -325,19 +328,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) prefill_tc_kernel(const __grid_
       }
       tmem_wait_st();
       tc_fence_before();
-      mbar_arrive_tc(bar(12 + 2 * set + j));
+      mbar_arrive_tc(bar(14 + set));                 // P-full phase t + 1
       PF_TR(2, (0x3u << 12) | (set << 8) | t);
-    };
-    auto finish = [&](int set, const RowState& rs) {
-    const int row = q0 + set * 128 + quad * 32 + lane;
-    const uint32_t tO = tmem + set * HD + lane_off;
-    const uint64_t lsum = rs.lsum;
-    // every MMA done: a barrier of its own that completes once.  (A parity
-    // wait only tells apart adjacent phases; here P.V(n - 2) may be running
-    // or P.V(n - 1) long complete.  The rescale wait above is unambiguous:
-    // S(t), complete there, was issued after P.V(t - 2).)
+    }
     PF_TR(0, (0x4u << 12) | (set << 8));
-    mbar_wait_tc_sleep(bar(18), 0);
+    mbar_wait_tc_sleep(bar(16), 0);                  // every MMA done (completes once)
     PF_TR(1, (0x4u << 12) | (set << 8));
     tc_fence_after();
     // ---- epilogue: O / l for rows < len (0 beyond)
@@ -359,23 +354,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) prefill_tc_kernel(const __grid_
                         : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
       }
     }
-    };
-    if constexpr (kTcSoftW == 8) {
-      const int set = warp >> 2;
-      RowState rs{-INFINITY, pack2(0.0f, 0.0f)};
-      for (int t = 0; t < ntiles; ++t) tile_step(set, rs, t);
-      finish(set, rs);
-    } else {
-      RowState r0{-INFINITY, pack2(0.0f, 0.0f)}, r1{-INFINITY, pack2(0.0f, 0.0f)};
-      for (int t = 0; t < ntiles; ++t) {
-        tile_step(0, r0, t);
-        tile_step(1, r1, t);
-      }
-      finish(0, r0);
-      finish(1, r1);
-    }
   } else if (warp < kTcSoftW + kTcDqW) {
-    // ================= dequantisation: K(t), V(t) into ring stage t & 1
+    // ================= dequantisation: K(t), V(t) into ring stage t % 3
     const int dt = tid - kTcSoftW * 32;
     const long long row_base = (static_cast<long long>(b) * p.H + h) * p.Tc;
     const long long srow_base = GRP ? ((static_cast<long long>(b) * p.H + h) >> p.hpb_shift) * p.Tc : row_base;
@@ -444,21 +424,22 @@ __global__ void __launch_bounds__(kTcThreads, 1) prefill_tc_kernel(const __grid_
     load(p.kc, p.ks, 0, rk, 0);
     load(p.vc, p.vs, 0, rv, 0);
     for (int t = 0; t < ntiles; ++t) {
-      const int st = t & 1;
-      const uint32_t ph = ((t >> 1) & 1) ^ 1;          // a fresh barrier passes parity 1
+      const int st = t % kTcStages;
+      const uint32_t ph = ((t / kTcStages) & 1) ^ 1;   // a fresh barrier passes parity 1
       const int dep = static_cast<int>(rk.w[0].x & zero);
       Raw nk, nv;
       const int kn = t + 1 < ntiles ? (t + 1) * kTcK : len;   // past the end: no loads
       load(p.kc, p.ks, kn, nk, dep);
       load(p.vc, p.vs, kn, nv, dep);
+      unsigned char* stg = gbase + st * kStageBytes;
       PF_TR(0, (0x5u << 12) | t);
-      mbar_wait_tc_sleep(bar(2 + st), ph);
-      convert(rk, gK + st * 2 * kTileBytes);
+      mbar_wait_tc_sleep(bar(3 + st), ph);
+      convert(rk, stg);
       mbar_arrive_tc(bar(0 + st));
       PF_TR(0, (0x6u << 12) | t);
-      mbar_wait_tc_sleep(bar(6 + st), ph);
-      convert(rv, gV + st * 2 * kTileBytes);
-      mbar_arrive_tc(bar(4 + st));
+      mbar_wait_tc_sleep(bar(9 + st), ph);
+      convert(rv, stg + 2 * kTileBytes);
+      mbar_arrive_tc(bar(6 + st));
       PF_TR(1, (0x7u << 12) | t);
       rk = nk;
       rv = nv;
@@ -467,54 +448,60 @@ __global__ void __launch_bounds__(kTcThreads, 1) prefill_tc_kernel(const __grid_
     // ================= MMA issue (one thread)
     constexpr uint32_t idS = umma_idesc_f16(128, kTcK, false);
     constexpr uint32_t idO = umma_idesc_f16(128, HD, true);
-    auto issue_s = [&](int t) {         // S_s(t) = Q_s K_hi^T + Q_s K_lo^T, s = 0, 1
-      const int st = t & 1;
-      PF_TR(0, (0x8u << 12) | t);
-      mbar_wait_tc(bar(0 + st), (t >> 1) & 1);
-      PF_TR(1, (0x8u << 12) | t);
-      tc_fence_after();
-      const uint32_t kh = sK + st * 2 * kTileBytes, kl = kh + kTileBytes;
+    auto issue_s = [&](int s, int t) {  // S_s(t) = Q_s K_hi^T + Q_s K_lo^T
+      const uint32_t kh = sbase + (t % kTcStages) * kStageBytes, kl = kh + kTileBytes;
+      const uint32_t d = tmem + kSP + s * kTcK, a = tmem + kQc + s * (HD / 2);
 #pragma unroll
-      for (int s = 0; s < 2; ++s) {
-        const uint32_t d = tmem + kSP + (2 * s + st) * kTcK;
-#pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk) {
-          const uint64_t a = umma_sdesc(sQ + s * (kQBytes / 2) + kk * 256, 128, DG * 128);
-          umma_f16(d, a, umma_sdesc(kh + kk * 256, 128, DG * 128), idS, kk > 0);
-          umma_f16(d, a, umma_sdesc(kl + kk * 256, 128, DG * 128), idS, 1u);
-        }
-        umma_commit(bar(8 + 2 * s + st));
+      for (int kk = 0; kk < HD / 16; ++kk) {
+        umma_f16_ts(d, a + kk * 8, umma_sdesc(kh + kk * 256, 128, DG * 128), idS, kk > 0);
+        umma_f16_ts(d, a + kk * 8, umma_sdesc(kl + kk * 256, 128, DG * 128), idS, 1u);
       }
-      umma_commit(bar(2 + st));         // K stage free once both S are done
+      umma_commit(bar(12 + s));
     };
-    issue_s(0);
+    auto issue_pv = [&](int s, int t) { // O_s += P_hi V_hi + P_lo V_hi + P_hi V_lo
+      const uint32_t vh = sbase + (t % kTcStages) * kStageBytes + 2 * kTileBytes, vl = vh + kTileBytes;
+      const uint32_t ph = tmem + kSP + s * kTcK, pl = ph + 32, d = tmem + s * HD;
+#pragma unroll
+      for (int kk = 0; kk < kTcK / 16; ++kk) {
+        const uint64_t bh = umma_sdesc(vh + kk * 2 * DG * 128, DG * 128, 128);
+        const uint64_t bl = umma_sdesc(vl + kk * 2 * DG * 128, DG * 128, 128);
+        umma_f16_ts(d, ph + kk * 8, bh, idO, (t > 0 || kk > 0) ? 1u : 0u);
+        umma_f16_ts(d, pl + kk * 8, bh, idO, 1u);
+        umma_f16_ts(d, ph + kk * 8, bl, idO, 1u);
+      }
+    };
+    auto wait_k = [&](int t) {
+      PF_TR(0, (0x8u << 12) | t);
+      mbar_wait_tc(bar(0 + t % kTcStages), (t / kTcStages) & 1);
+      tc_fence_after();
+    };
+    // Q rows written (P-full phase 0 of both sets)
+    mbar_wait_tc(bar(14), 0);
+    mbar_wait_tc(bar(15), 0);
+    wait_k(0);
+    issue_s(0, 0);
+    issue_s(1, 0);
+    umma_commit(bar(3 + 0));             // K stage 0 free once both S are done
     for (int t = 0; t < ntiles; ++t) {
-      if (t + 1 < ntiles) issue_s(t + 1);
-      const int st = t & 1;
       PF_TR(0, (0x9u << 12) | t);
-      mbar_wait_tc(bar(4 + st), (t >> 1) & 1);
-      const uint32_t vh = sV + st * 2 * kTileBytes, vl = vh + kTileBytes;
+      mbar_wait_tc(bar(6 + t % kTcStages), (t / kTcStages) & 1);      // V(t)
+      const bool more = t + 1 < ntiles;
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
         PF_TR(0, (0xAu << 12) | (s << 8) | t);
-        mbar_wait_tc(bar(12 + 2 * s + st), (t >> 1) & 1);
+        mbar_wait_tc(bar(14 + s), (t + 1) & 1);    // P_s(t): phase t + 1 (phase 0 = Q)
         PF_TR(1, (0xAu << 12) | (s << 8) | t);
         tc_fence_after();
-        const uint32_t ph = tmem + kSP + (2 * s + st) * kTcK, pl = ph + 32;
-        const uint32_t d = tmem + s * HD;
-#pragma unroll
-        for (int kk = 0; kk < kTcK / 16; ++kk) {
-          const uint64_t bh = umma_sdesc(vh + kk * 2 * DG * 128, DG * 128, 128);
-          const uint64_t bl = umma_sdesc(vl + kk * 2 * DG * 128, DG * 128, 128);
-          umma_f16_ts(d, ph + kk * 8, bh, idO, (t > 0 || kk > 0) ? 1u : 0u);
-          umma_f16_ts(d, pl + kk * 8, bh, idO, 1u);
-          umma_f16_ts(d, ph + kk * 8, bl, idO, 1u);
+        issue_pv(s, t);
+        if (more) {
+          if (s == 0) wait_k(t + 1);
+          issue_s(s, t + 1);
         }
-        umma_commit(bar(16 + s));
       }
-      umma_commit(bar(6 + st));         // V stage free
+      umma_commit(bar(9 + t % kTcStages));        // V stage free
+      if (more) umma_commit(bar(3 + (t + 1) % kTcStages));   // K stage free
     }
-    umma_commit(bar(18));
+    umma_commit(bar(16));
   }
   __syncwarp();
   tc_fence_before();
