@@ -41,7 +41,7 @@ constexpr int kTcK = 64;         // keys per tile
 constexpr int kTcSoftW = 8;      // softmax warps (4 per row set)
 constexpr int kTcStages = 3;     // K/V ring depth
 #ifndef NQKV_PF_DQW
-#define NQKV_PF_DQW 4
+#define NQKV_PF_DQW 7
 #endif
 constexpr int kTcDqW = NQKV_PF_DQW;   // dequantisation warps
 constexpr int kTcThreads = (kTcSoftW + kTcDqW + 1) * 32;   // + the MMA warp
@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) prefill_tc_kernel(const __grid_
   extern __shared__ __align__(1024) unsigned char tc_smem[];
   const uint32_t sbase = (static_cast<uint32_t>(__cvta_generic_to_shared(tc_smem)) + 1023u) & ~1023u;
   unsigned char* gbase = tc_smem + (sbase - static_cast<uint32_t>(__cvta_generic_to_shared(tc_smem)));
-  __shared__ uint64_t s_lut[256];                  // code byte -> (L[low nibble], L[high nibble])
+  __shared__ float s_lv[16];                       // the levels: 16 words in 16 banks (no conflicts)
   __shared__ uint32_t s_tmem;
   // [0,3) K full, [3,6) K empty, [6,9) V full, [9,12) V empty, 12-13 S full, 14-15 P full, 16 all MMAs done
   constexpr int kBars = 17;
@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) prefill_tc_kernel(const __grid_
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int qt = static_cast<int>(gridDim.x) - 1 - static_cast<int>(blockIdx.x);   // longest causal rows first
   const int h = blockIdx.y, b = blockIdx.z;
-  for (int i = tid; i < 256; i += kTcThreads) s_lut[i] = pack2(p.lv.v[i & 15], p.lv.v[i >> 4]);
+  if (tid < 16) s_lv[tid] = p.lv.v[tid];
   pdl_enter();
   const int len = min(max(p.seq_lens[b], 0), p.T);
   const int q0 = qt * kTcQ;
@@ -407,7 +407,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) prefill_tc_kernel(const __grid_
           uint32_t hh[4], ll[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e)                  // RN32(s * L[code]) for dims 8i + 2e, + 1
-            split2_tc(fmul2(s2, s_lut[(ww[i] >> (8 * e)) & 0xffu]), hh[e], ll[e]);
+            split2_tc(fmul2(s2, pack2(s_lv[(ww[i] >> (8 * e)) & 15u], s_lv[(ww[i] >> (8 * e + 4)) & 15u])),
+                      hh[e], ll[e]);
           *reinterpret_cast<uint4*>(dhi + doff[u] + i * 128) = make_uint4(hh[0], hh[1], hh[2], hh[3]);
           *reinterpret_cast<uint4*>(dhi + kTileBytes + doff[u] + i * 128) = make_uint4(ll[0], ll[1], ll[2], ll[3]);
         }
