@@ -14,3 +14,6 @@ $CMD > $O/${R}_bench_small_plain2.log 2>&1 && \
 $CMD > $O/${R}_bench_small_plain3.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:quantize_kernel -s 2 -c 1 -o $O/${R}_quantize $CMD > $O/${R}_ncu_quant.log 2>&1
 ls -la $O | tail -20
+# prefill (c4 prompt, tools/prefill_one.py): plain run, then one full capture
+python tools/prefill_one.py > $O/${R}_prefill_plain.log 2>&1 && \
+  ncu --set full --clock-control none --import-source on -k regex:prefill_tc -s 1 -c 1 -o $O/${R}_prefill python tools/prefill_one.py > $O/${R}_ncu_prefill.log 2>&1

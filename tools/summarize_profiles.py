@@ -46,12 +46,24 @@ KEYS = ("Duration", "DRAM Throughput", "Memory Throughput", "L1/TEX Cache Throug
         "Dynamic Shared Memory Per Block", "Mem Busy", "Max Bandwidth")
 RAW = ("dram__bytes_read.sum", "dram__bytes_write.sum", "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed",
        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "sm__inst_executed.sum",
-       "l1tex__lsu_writeback_active.avg.pct_of_peak_sustained_elapsed")
+       "l1tex__lsu_writeback_active.avg.pct_of_peak_sustained_elapsed",
+       "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+       "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+       "l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+       "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active")
+
+
+def page(tag, name, args):
+    """An ncu page as csv text: from the report if it is here, else from the
+    csv that tools/profile_shrink.sh wrote on the GPU box."""
+    rep = os.path.join(G, f"{R}_{tag}.ncu-rep")
+    if os.path.exists(rep):
+        return subprocess.run(["ncu", "-i", rep] + args, capture_output=True, text=True).stdout
+    return open(os.path.join(G, f"{R}_{tag}_{name}.csv"), encoding="latin-1").read()
 
 
 def ncu_report(tag):
-    rep = os.path.join(G, f"{R}_{tag}.ncu-rep")
-    det = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True, text=True).stdout
+    det = page(tag, "details", ["--page", "details", "--csv"])
     rows = list(csv.reader(det.splitlines()))
     hdr = rows[0]
     lines = [f"# ncu --set full ({R}, {tag}): " + rows[1][hdr.index("Kernel Name")][:90]]
@@ -59,7 +71,7 @@ def ncu_report(tag):
         d = dict(zip(hdr, r))
         if d.get("Metric Name") in KEYS:
             lines.append(f"{d['Section Name'][:34]:34s} {d['Metric Name']:34s} {d['Metric Value']:>14s} {d['Metric Unit']}")
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    raw = page(tag, "raw", ["--page", "raw", "--csv"])
     rr = list(csv.reader(raw.splitlines()))
     h, u, v = rr[0], rr[1], rr[2]
     vals = {}
@@ -67,10 +79,9 @@ def ncu_report(tag):
         if name in RAW:
             lines.append(f"{'raw':34s} {name:70s} {val:>14s} {unit}")
             vals[name] = (val, unit)
-    src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
-                         capture_output=True, text=True).stdout
+    src = page(tag, "sass", ["--page", "source", "--csv", "--print-source", "sass"])
     tmp = os.path.join(G, f"{R}_{tag}_sass.csv")
-    open(tmp, "w").write(src)
+    open(tmp, "w", encoding="latin-1").write(src)
     hot = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_sass_hot.py"), tmp, "12"],
                          capture_output=True, text=True).stdout
     txt = "\n".join(lines) + "\n\n# warp-stall sampling (top SASS)\n" + hot
@@ -81,7 +92,9 @@ def ncu_report(tag):
 
 launches()
 dv = ncu_report("decode")
-ncu_report("quantize")
+qv = ncu_report("quantize")
+if os.path.exists(os.path.join(G, f"{R}_prefill_details.csv")) or os.path.exists(os.path.join(G, f"{R}_prefill.ncu-rep")):
+    ncu_report("prefill")
 
 
 def to_bytes(val, unit):
@@ -96,5 +109,8 @@ if os.path.exists(tp):
 rd = to_bytes(*dv["dram__bytes_read.sum"])
 wr = to_bytes(*dv["dram__bytes_write.sum"])
 tr[WL] = {"decode_dram_bytes_per_launch": rd + wr, "read": rd, "write": wr, "source": f"profiles/{R}_decode_ncu.txt"}
+if "dram__bytes_read.sum" in qv:
+    tr[WL]["quantize_dram_bytes_per_launch"] = to_bytes(*qv["dram__bytes_read.sum"]) + to_bytes(*qv["dram__bytes_write.sum"])
+    tr[WL]["quantize_source"] = f"profiles/{R}_quantize_ncu.txt"
 json.dump(tr, open(tp, "w"), indent=1)
 print(tr)
