@@ -69,6 +69,9 @@ constexpr int kMinTokensPerCta = 512;  // below this a CTA's table build would d
 #ifndef NQKV_SPLIT
 #define NQKV_SPLIT -1            // split K/V ring: 1 on, 0 off, -1 hd 64 only (measured)
 #endif
+#ifndef NQKV_V16
+#define NQKV_V16 0               // V levels as 16-bit fixed point in a 4-byte pair LUT (see lds_v16)
+#endif
 #ifndef NQKV_PF
 #define NQKV_PF 0                // bulk L2 prefetch distance in a warp's own stages (0: off; measured: no gain)
 #endif
@@ -261,6 +264,20 @@ __device__ __forceinline__ uint64_t lds_v(uint32_t off) {
   asm volatile("ld.shared.b64 %0, [%1+0x400];" : "=l"(v) : "r"(off));
   return v;
 }
+// V pair LUT entry, 16-bit fixed point (NQKV_V16): (u[lo] | u[hi] << 16),
+// u = RN(L * 32767) + 32768.  Returned as the fp32 pair (u[lo], u[hi]) * 2^-149:
+// the payload IS the bit pattern of a subnormal float, so the value is exact
+// and linear in u (no offset to cancel); weights carry a 2^100 factor so the
+// products are normal.
+__device__ __forceinline__ uint64_t lds_v16(uint32_t off) {
+  uint64_t v;
+  asm volatile("{.reg .b32 e, a, b;\n ld.shared.b32 e, [%1+0x400];\n and.b32 a, e, 65535;\n"
+               " shr.u32 b, e, 16;\n mov.b64 %0, {a, b};}" : "=l"(v) : "r"(off));
+  return v;
+}
+constexpr float kV16WScale = 0x1p100f;                      // weight factor
+constexpr float kV16Out = 0x1p49f / 32767.0f;               // o * 2^49 / 32767 ...
+constexpr float kV16Bias = 32768.0f / 32767.0f;             // ... - W * 32768 / 32767
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t s) {
   uint32_t d;
   asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(s));
@@ -1074,11 +1091,20 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
   // V LUT (independent of the previous kernel); levels via shared memory
   // (a divergent constant-bank index would serialise)
   __syncthreads();
+#if NQKV_V16
+  for (int i = tid; i < 256 * 8; i += NT) {      // 16 B = four lane copies per store
+    const int e = i >> 3;
+    const uint32_t u = static_cast<uint32_t>(__float2int_rn(s_lv[e & 15] * 32767.0f) + 32768) |
+                       (static_cast<uint32_t>(__float2int_rn(s_lv[e >> 4] * 32767.0f) + 32768) << 16);
+    *reinterpret_cast<uint4*>(smem + Sm::kV + e * 256 + (i & 7) * 16) = make_uint4(u, u, u, u);
+  }
+#else
   for (int i = tid; i < 256 * 16; i += NT) {     // 16 B = two lane copies per store
     const int e = i >> 4;
     const float lo = s_lv[e & 15], hi = s_lv[e >> 4];
     *reinterpret_cast<float4*>(smem + Sm::kV + e * 256 + (i & 15) * 16) = make_float4(lo, hi, lo, hi);
   }
+#endif
   const uint32_t* s_one = reinterpret_cast<const uint32_t*>(smem + Sm::kOne);
   WalkState* s_ws = reinterpret_cast<WalkState*>(smem + Sm::kWalk);
   static_assert(sizeof(WalkState) == 80, "walk state layout");
@@ -1556,7 +1582,7 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
     rotA |= static_cast<uint32_t>((i + rho) & 7) << (4 * i);
     rotB |= static_cast<uint32_t>((i + 4 + rho) & 7) << (4 * i);
   }
-  const uint32_t vsel = static_cast<uint32_t>(lane) * 8u;
+  const uint32_t vsel = static_cast<uint32_t>(lane) * (NQKV_V16 ? 4u : 8u);
 
   uint32_t jsel[8];
   auto set_jsel = [&](int slot) {
@@ -1567,12 +1593,18 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
 
   uint64_t o2[8];
   float m = -INFINITY, l = 0.0f;
+#if NQKV_V16
+  float wsum = 0.0f;           // sum of this lane's V weights (the fixed-point offset)
+#endif
   bool any = false;            // this warp consumed a stage of the current piece
   auto reset_state = [&]() {
 #pragma unroll
     for (int j = 0; j < 8; ++j) o2[j] = 0;
     m = -INFINITY;
     l = 0.0f;
+#if NQKV_V16
+    wsum = 0.0f;
+#endif
     any = false;
   };
 
@@ -1632,6 +1664,9 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
         const float corr = up ? fast_exp2(m - mt) : 1.0f;   // m = -inf -> 0
         m = up ? mt : m;
         l *= corr;
+#if NQKV_V16
+        wsum *= corr;
+#endif
         const uint64_t c2 = pack2(corr, corr);
 #pragma unroll
         for (int j = 0; j < 8; ++j) o2[j] = fmul2(o2[j], c2);
@@ -1641,8 +1676,14 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
       const float pr = fast_exp2(sj - (m == -INFINITY ? 0.0f : m));
       l += pr;                        // this lane's slot only (reduced in end_piece)
       const float w = pr * Rg.vs[0];
+#if NQKV_V16
+      wsum += w;                      // this lane's slot only (reduced in end_piece, like l)
+      const float ws = w * kV16WScale;
+#else
+      const float ws = w;
+#endif
 #pragma unroll
-      for (int i = 0; i < kTPS; ++i) wv[i] = __shfl_sync(0xffffffffu, w, (lane & ~3) | i);
+      for (int i = 0; i < kTPS; ++i) wv[i] = __shfl_sync(0xffffffffu, ws, (lane & ~3) | i);
     } else {
 #pragma unroll
       for (int o = 1; o < LPT; o <<= 1) {
@@ -1662,6 +1703,9 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
         const float corr = fast_exp2(m - mt);   // m = -inf -> 0
         m = mt;
         l *= corr;
+#if NQKV_V16
+        wsum *= corr;
+#endif
         const uint64_t c2 = pack2(corr, corr);
 #pragma unroll
         for (int j = 0; j < 8; ++j) o2[j] = fmul2(o2[j], c2);
@@ -1671,6 +1715,10 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
         const float pr = fast_exp2(s[i] - m);   // masked: exp2(-inf) = 0
         l += pr;
         wv[i] = pr * Rg.vs[i];
+#if NQKV_V16
+        wsum += wv[i];
+        wv[i] *= kV16WScale;
+#endif
       }
     }
   };
@@ -1684,8 +1732,13 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
       const uint64_t w2 = pack2(wv[i], wv[i]);
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
+#if NQKV_V16
+        o2[k] = ffma2(lds_v16(prmt(Rg.v[i].x, vsel, 0x7604 | (k << 4))), w2, o2[k]);
+        o2[4 + k] = ffma2(lds_v16(prmt(Rg.v[i].y, vsel, 0x7604 | (k << 4))), w2, o2[4 + k]);
+#else
         o2[k] = ffma2(lds_v(prmt(Rg.v[i].x, vsel, 0x7604 | (k << 4))), w2, o2[k]);
         o2[4 + k] = ffma2(lds_v(prmt(Rg.v[i].y, vsel, 0x7604 | (k << 4))), w2, o2[4 + k]);
+#endif
       }
     }
   };
@@ -1698,7 +1751,12 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
       if constexpr (RS) {             // l: one slot per lane (hd 128: lanes sub, sub ^ 4 alike)
 #pragma unroll
         for (int o = 1; o < LPT; o <<= 1)
-          if (o != 4) l += __shfl_xor_sync(0xffffffffu, l, o);
+          if (o != 4) {
+            l += __shfl_xor_sync(0xffffffffu, l, o);
+#if NQKV_V16
+            wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
+#endif
+          }
         // bring the row groups to the warp max (a group that saw no token has
         // m = -inf, l = 0, o = 0: its factor is 0)
         float M = m;
@@ -1706,6 +1764,9 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
         for (int o = LPT; o < 32; o <<= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
         const float f = m == -INFINITY ? 0.0f : fast_exp2(m - M);
         l *= f;
+#if NQKV_V16
+        wsum *= f;
+#endif
         const uint64_t f2 = pack2(f, f);
 #pragma unroll
         for (int j = 0; j < 8; ++j) o2[j] = fmul2(o2[j], f2);
@@ -1714,9 +1775,18 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
 #pragma unroll
       for (int o = LPT; o < 32; o <<= 1) {
         l += __shfl_xor_sync(0xffffffffu, l, o);
+#if NQKV_V16
+        wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
+#endif
 #pragma unroll
         for (int j = 0; j < 8; ++j) o2[j] = fadd2(o2[j], shfl_xor64(o2[j], o));
       }
+#if NQKV_V16
+      // sum_t w_t L = (sum_t w_t u_t - 32768 W) / 32767, o = 2^-49 sum_t w_t u_t
+      const uint64_t sc2 = pack2(kV16Out, kV16Out), b2 = pack2(-wsum * kV16Bias, -wsum * kV16Bias);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o2[j] = ffma2(o2[j], sc2, b2);
+#endif
     }
     if (g == 0) {
       float* dst = s_o + (slot * NC + warp) * HD + sub * kLaneDims;
@@ -1758,7 +1828,11 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
   // use of its first word waits for it), the next stage's loads are issued
   // into the other buffer and stay in flight while this stage is computed.
   uint32_t zero;
+#if !defined(NQKV_DEPZERO) || NQKV_DEPZERO
+  zero = static_cast<uint32_t>(p.early) >> 1;   // always 0, but not a constant ptxas can fold
+#else
   asm volatile("mov.u32 %0, 0;" : "=r"(zero));
+#endif
   auto close_to = [&](int pi) {
     while (cpi < pi) {
       end_piece(cpi);

@@ -205,7 +205,11 @@ __global__ void __launch_bounds__(256, 4) quantize_kernel(const __grid_constant_
   // data has arrived (`dep`, always 0, is computed from its first word):
   // otherwise the wait for a unit would also wait for the loads just issued.
   uint32_t zero;
+#if !defined(NQKV_QDEPZERO) || NQKV_QDEPZERO
+  zero = static_cast<uint32_t>(p.v256) >> 2;   // always 0, but not a constant ptxas can fold
+#else
   asm volatile("mov.u32 %0, 0;" : "=r"(zero));
+#endif
   uint32_t u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   Buf A{}, Bb{};
   load(u, A, 0u);

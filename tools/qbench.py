@@ -12,7 +12,7 @@ if not os.environ.get("NQKV_LIB"):
 from paper_2505_16210_b200 import nqkv as N  # noqa: E402
 
 flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
-for (B, T, H, hd) in [(8, 2048, 32, 64), (32, 1988, 32, 128), (4, 8192, 40, 128)]:
+for (B, T, H, hd) in [(8, 2048, 32, 64), (32, 1988, 32, 128), (4, 8192, 40, 128), (64, 4096, 12, 128)]:
     x = torch.randn(B, T, H, hd, device="cuda").half()
     Tc = -(-(T + 1) // 64) * 64
     codes = torch.zeros(B, H, Tc, hd // 2, dtype=torch.uint8, device="cuda")

@@ -258,8 +258,22 @@ __global__ void __launch_bounds__(NW * 32, 1) stream_kernel(const __grid_constan
   uint32_t c65536, magic;
   asm volatile("mov.u32 %0, 65536;" : "=r"(c65536));
   asm volatile("mov.u32 %0, 0x43800000;" : "=r"(magic));
-  float m = -INFINITY, l = 0.0f;
+  float m = -INFINITY, l = 0.0f, wsum = 0.0f;
   uint32_t sink = 0;
+  // PRMT register LUT planes (7-bit bytes): entry c of plane P = byte (c & 3) of TP(c >> 2)
+  uint32_t TL0 = 0, TL1 = 0, TL2 = 0, TL3 = 0, TH0 = 0, TH1 = 0, TH2 = 0, TH3 = 0;
+#pragma unroll
+  for (int c = 0; c < 16; ++c) {
+    const int u = __float2int_rn(a.lv[c] * 16000.0f) + 16384;
+    const uint32_t lb = static_cast<uint32_t>(u & 127) << (8 * (c & 3));
+    const uint32_t hb = static_cast<uint32_t>((u >> 8) & 127) << (8 * (c & 3));
+    switch (c >> 2) {
+      case 0: TL0 |= lb; TH0 |= hb; break;
+      case 1: TL1 |= lb; TH1 |= hb; break;
+      case 2: TL2 |= lb; TH2 |= hb; break;
+      default: TL3 |= lb; TH3 |= hb; break;
+    }
+  }
 
   // per-lane cursors (advanced by NC stages per consumed stage); slot i at
   // immediate offset i*4 rows
@@ -354,7 +368,7 @@ __global__ void __launch_bounds__(NW * 32, 1) stream_kernel(const __grid_constan
     float wv[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) wv[i] = __shfl_sync(0xffffffffu, w, (lane & ~3) | i);
-    if (V16) {
+    if (V16 && !(OPT & 0x100)) {
       const float W = wv[0] + wv[1] + wv[2] + wv[3];
       const uint64_t mW = pack2(-256.0f * W, -256.0f * W);
 #pragma unroll
@@ -365,21 +379,64 @@ __global__ void __launch_bounds__(NW * 32, 1) stream_kernel(const __grid_constan
       for (int i = 0; i < 4; ++i) o2[i] = fadd2(o2[i], pack2(wv[i], __uint_as_float(R.v[i].x ^ R.v[i].y)));
       return;
     }
+    constexpr int VA = (OPT >> 4) & 15;     // words per lane-stage decoded in registers (PRMT LUT)
+    if (VA > 0) {
+      float Wa = 0.0f;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (2 * i < VA) Wa += wv[i];
+      wsum += Wa;
+    }
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const uint64_t w2 = pack2(wv[i], wv[i]);
+      if (VA > 0 && 2 * i < VA) {
+        const float ws = wv[i] * 0x1p100f;
+        const uint64_t w2s = pack2(ws, ws);
+        auto word = [&](uint32_t w, int ob) {
+          const uint32_t xw = w ^ 0x88888888u;
+          const uint32_t sa[2] = {w, w >> 16}, sb[2] = {xw, xw >> 16};
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t lo = prmt(TL0, TL1, sa[h]) | prmt(TL2, TL3, sb[h]);
+            const uint32_t hi = prmt(TH0, TH1, sa[h]) | prmt(TH2, TH3, sb[h]);
+            const uint64_t f01 = pack2(__uint_as_float(prmt(lo, hi, 0xC40C)), __uint_as_float(prmt(lo, hi, 0xD51D)));
+            const uint64_t f23 = pack2(__uint_as_float(prmt(lo, hi, 0xE62E)), __uint_as_float(prmt(lo, hi, 0xF73F)));
+            o2[ob + 2 * h] = ffma2(f01, w2s, o2[ob + 2 * h]);
+            o2[ob + 2 * h + 1] = ffma2(f23, w2s, o2[ob + 2 * h + 1]);
+          }
+        };
+        word(R.v[i].x, 0);
+        if (2 * i + 1 < VA) {
+          word(R.v[i].y, 4);
+        } else {
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            o2[4 + k] = ffma2(lds_v(prmt(R.v[i].y, vsel, 0x7604 | (k << 4))), w2, o2[4 + k]);
+        }
+        continue;
+      }
       if (V16) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const uint32_t ex = lds_v16(prmt(R.v[i].x, vsel, 0x7604 | (k << 4)));
           const uint32_t ey = lds_v16(prmt(R.v[i].y, vsel, 0x7604 | (k << 4)));
           uint64_t fx, fy;
+          if (OPT & 0x100) {     // denormal payload: value = u * 2^-149, weights pre-scaled by 2^100
+            asm("{.reg .b32 a, b;\n and.b32 a, %1, 65535;\n shr.u32 b, %1, 16;\n mov.b64 %0, {a, b};}" : "=l"(fx) : "r"(ex));
+            asm("{.reg .b32 a, b;\n and.b32 a, %1, 65535;\n shr.u32 b, %1, 16;\n mov.b64 %0, {a, b};}" : "=l"(fy) : "r"(ey));
+            const float ws = wv[i] * 0x1p100f;
+            const uint64_t w2s = pack2(ws, ws);
+            o2[k] = ffma2(fx, w2s, o2[k]);
+            o2[4 + k] = ffma2(fy, w2s, o2[4 + k]);
+          } else {
           asm("{.reg .b32 a, b;\n mad.hi.u32 a, %1, %2, %3;\n prmt.b32 b, %1, %3, 0x7610;\n mov.b64 %0, {a, b};}"
               : "=l"(fx) : "r"(ex), "r"(c65536), "r"(magic));
           asm("{.reg .b32 a, b;\n mad.hi.u32 a, %1, %2, %3;\n prmt.b32 b, %1, %3, 0x7610;\n mov.b64 %0, {a, b};}"
               : "=l"(fy) : "r"(ey), "r"(c65536), "r"(magic));
           o2[k] = ffma2(fx, w2, o2[k]);
           o2[4 + k] = ffma2(fy, w2, o2[4 + k]);
+          }
         }
       } else {
 #pragma unroll
@@ -479,7 +536,7 @@ __global__ void __launch_bounds__(NW * 32, 1) stream_kernel(const __grid_constan
       consume(R);
     }
   }
-  float acc = l + m + __uint_as_float(sink & 0x3fffffff);
+  float acc = l + m + wsum + __uint_as_float(sink & 0x3fffffff);
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     const float2 f = unpack2(o2[j]);
@@ -561,16 +618,19 @@ int main(int argc, char** argv) {
   for (int i = 0; i < 16; ++i) a.lv[i] = L[i];
   const double bytes = static_cast<double>(rows) * (2 * ROWB + 16);
   printf("grid %d, %lld rows/CTA, %.1f MB\n", grid, rpc, bytes / 1e6);
+  if (getenv("SX_OLD")) {
   run<0, 16, 2, 1, 0, 1, false>("LDG D2 compute fp32 V", a, grid, bytes);
   run<0, 16, 2, 1, 0, 0, false>("LDG D2 loads only", a, grid, bytes);
-  g_pad = 0x16000;   // + 88 KB: 216 KB of shared memory (the decode kernel's footprint)
-  run<0, 16, 2, 1, 0, 1, false>("LDG D2 compute fp32 V, 216 KB smem", a, grid, bytes);
-  run<0, 16, 2, 1, 0, 0, false>("LDG D2 loads only, 216 KB smem", a, grid, bytes);
-  run<2, 16, 1, 2, 0, 1, false>("cp.async DW2 compute fp32 V, +smem", a, grid, bytes);
-  g_pad = 0x8000;
-  run<0, 16, 2, 1, 0, 1, false>("LDG D2 compute fp32 V, 160 KB smem", a, grid, bytes);
-  g_pad = 0x10000;
-  run<0, 16, 2, 1, 0, 1, false>("LDG D2 compute fp32 V, 192 KB smem", a, grid, bytes);
+  }
+  g_pad = 0x16000;   // 216 KB of shared memory (the decode kernel's footprint)
+  for (int rep = 0; rep < 2; ++rep) {
+  run<0, 16, 2, 1, 0, 1, false>("LDG D2 fp32 V (current)", a, grid, bytes);
+  run<0, 16, 2, 1, 0, 1, true>("LDG D2 V16 magic", a, grid, bytes);
+  run<0, 16, 2, 1, 0, 1, true, 0x100>("LDG D2 V16 denormal", a, grid, bytes);
+  run<0, 16, 2, 1, 0, 1, true, 0x102>("LDG D2 V16 denormal no loads", a, grid, bytes);
+  run<0, 16, 2, 1, 0, 1, false, 0x02>("LDG D2 fp32 V no loads", a, grid, bytes);
+  run<0, 16, 2, 1, 0, 0, false>("LDG D2 loads only", a, grid, bytes);
+  }
   g_pad = 0;
   return 0;
 }
