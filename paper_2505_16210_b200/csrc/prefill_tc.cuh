@@ -420,7 +420,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) prefill_tc_kernel(const __grid_
     // ptxas keeps all these loads on one scoreboard, so loads issued earlier
     // would make the wait for tile t's data also wait for them.
     uint32_t zero;
+#if !defined(NQKV_PDEPZERO) || NQKV_PDEPZERO
+    zero = static_cast<uint32_t>(p.hpb_shift) >> 8;   // always 0, but not a constant ptxas can fold
+#else
     asm volatile("mov.u32 %0, 0;" : "=r"(zero));
+#endif
     Raw rk, rv;
     load(p.kc, p.ks, 0, rk, 0);
     load(p.vc, p.vs, 0, rv, 0);
