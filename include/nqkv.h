@@ -57,8 +57,9 @@
 extern "C" {
 #endif
 
-#define NQKV_ABI_VERSION 3   /* 2: blk 256 / head-group scales; NQKV_SCALE_F16 moved to 0x10000;
-                                3: nqkv_prefill_attention, nqkv_build_id */
+#define NQKV_ABI_VERSION 4   /* 2: blk 256 / head-group scales; NQKV_SCALE_F16 moved to 0x10000;
+                                3: nqkv_prefill_attention, nqkv_build_id;
+                                4: struct nqkv_kv_layout for grouped-query / paged caches, the *_kv calls */
 
 typedef enum {
   NQKV_OK = 0,
@@ -282,7 +283,62 @@ int nqkv_prefill_attention(const void* q, const uint8_t* k_codes, const void* k_
                            int B, int H, int hd, int blk, int Tc, int T, float softmax_scale,
                            float* out, void* stream);
 
-/* Test hook: the kernels' code function on fp32 inputs already normalised/* Test hook: the kernels' code function on fp32 inputs already normalised
+/* KV layouts.  The paper calls both orthogonal to
+ * NQKV (multi-query / grouped attention reduce the number of
+ * KV heads; PagedAttention's paged KV memory); neither
+ * changes an encoded byte or the attention arithmetic, only which cache row
+ * a (sequence, head, token) reads (readings R15, R16).
+ *   kv_heads       cache heads H_kv (0: = H).  Grouped-query attention: H is
+ *                  a multiple of H_kv and H / H_kv a power of two; query head
+ *                  h reads cache head h / (H / H_kv).  With blk > hd a block
+ *                  spans adjacent CACHE heads.
+ *   block_table    NULL: contiguous cache [B][H_kv][Tc][...] (as the plain
+ *                  calls).  Else paged: device int32 [B][pages_per_seq] (4-byte
+ *                  aligned, caller-owned); codes [n_pages][H_kv][page_size][hd/2],
+ *                  scales [n_pages][H_kv][page_size][hd/blk] fp32
+ *                  ([n_pages][H_kv*hd/blk][page_size][1] when blk > hd);
+ *                  token t of sequence b is row t % page_size of page
+ *                  block_table[b][t / page_size].  Page ids out of [0, n_pages)
+ *                  are undefined behaviour (not checked on the device).
+ *   pages_per_seq  row stride of block_table; pages_per_seq * page_size >= Tc
+ *                  (Tc = the per-sequence token capacity, seq_lens <= Tc)
+ *   page_size      tokens per page: a power of two >= 64
+ *   n_pages        pages in the cache tensors; n_pages * H_kv * page_size * hd/2
+ *                  < 2^32
+ * Errors: NQKV_ERR_SHAPE (H % H_kv, capacity, sizes), NQKV_ERR_UNSUPPORTED
+ * (group or page size not a power of two, page_size < 64, fp16 scales with a
+ * paged decode), NQKV_ERR_ALIGN (block_table). */
+typedef struct nqkv_kv_layout {
+  int kv_heads;
+  const int32_t* block_table;
+  int pages_per_seq;
+  int page_size;
+  int n_pages;
+} nqkv_kv_layout;
+
+/* nqkv_decode_attention over a KV layout (attention only: append with
+ * nqkv_quantize_kv).  Same semantics, workspace (sized with the QUERY head
+ * count H) and errors as nqkv_decode_attention; q/out are [B][H][hd]. */
+int nqkv_decode_attention_kv(const void* q, const uint8_t* k_codes, const void* k_scales,
+                             const uint8_t* v_codes, const void* v_scales,
+                             const int32_t* d_seq_lens, int B, int H, int hd, int blk, int Tc,
+                             const nqkv_kv_layout* kv, float softmax_scale, float* out,
+                             void* workspace, size_t ws_bytes, void* stream);
+/* nqkv_prefill_attention over a KV layout; q/out [B][T][H][hd]. */
+int nqkv_prefill_attention_kv(const void* q, const uint8_t* k_codes, const void* k_scales,
+                              const uint8_t* v_codes, const void* v_scales,
+                              const int32_t* d_seq_lens, int B, int H, int hd, int blk, int Tc,
+                              int T, const nqkv_kv_layout* kv, float softmax_scale, float* out,
+                              void* stream);
+/* nqkv_quantize into a paged cache (kv->block_table non-NULL) or the
+ * contiguous one.  x holds the CACHE heads: kv_heads must be 0 or H.  Rows
+ * d_pos[b] .. d_pos[b]+n_new-1 (< Tc) are written; the pages holding them
+ * must be in block_table. */
+int nqkv_quantize_kv(const void* x, int64_t stride_b, int64_t stride_t, int64_t stride_h, int B,
+                     int H, int hd, int n_new, int blk, const int32_t* d_pos, int Tc,
+                     const nqkv_kv_layout* kv, uint8_t* codes, void* scales, void* stream);
+
+/* Test hook: the kernels' code function on fp32 inputs already normalised
  * to [-1, 1] (values outside are clamped).  d_n device float[count],
  * d_codes device uint8[count]. */
 int nqkv_encode_normalized(const float* d_n, int64_t count, uint8_t* d_codes, void* stream);

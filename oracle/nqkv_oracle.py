@@ -235,6 +235,47 @@ def dequantize(codes: np.ndarray, scales: np.ndarray, blk: int, n_tokens: int | 
 
 
 # --------------------------------------------------------------------------
+# KV layouts orthogonal to the method
+# --------------------------------------------------------------------------
+def kv_group(h_q: int, h_kv: int) -> int:
+    """Query heads per cache head (grouped-query attention, reading R15)."""
+    if h_kv <= 0 or h_q % h_kv:
+        raise ValueError("the number of query heads must be a multiple of the KV heads")
+    return h_q // h_kv
+
+
+def paged_to_contiguous(pages: np.ndarray, block_table, page_size: int, n_tokens: int) -> np.ndarray:
+    """A paged cache, the layout of PagedAttention that PAPER.md:62, 103
+    calls orthogonal to NQKV (reading R16), as the contiguous one: token t
+    of sequence b lives in row t % P of page block_table[b][t // P];
+    pages: [n_pages][H][P][w] -> [B][H][n_tokens][w] (rows the table does not
+    cover are zero).  A plain gather: it does no arithmetic of the method."""
+    bt = np.asarray(block_table)
+    B = bt.shape[0]
+    n_pages, H, P, w = pages.shape
+    if P != page_size:
+        raise ValueError("page size mismatch")
+    out = np.zeros((B, H, n_tokens, w), pages.dtype)
+    for b in range(B):
+        for t in range(n_tokens):
+            if t // P < bt.shape[1]:
+                out[b, :, t, :] = pages[int(bt[b, t // P]), :, t % P, :]
+    return out
+
+
+def contiguous_to_paged(cache: np.ndarray, block_table, page_size: int, n_pages: int) -> np.ndarray:
+    """Inverse of paged_to_contiguous for the rows the table covers:
+    [B][H][Tc][w] -> [n_pages][H][P][w] (pages no sequence uses are zero)."""
+    bt = np.asarray(block_table)
+    B, H, Tc, w = cache.shape
+    out = np.zeros((n_pages, H, page_size, w), cache.dtype)
+    for b in range(B):
+        for t in range(min(Tc, bt.shape[1] * page_size)):
+            out[int(bt[b, t // page_size]), :, t % page_size, :] = cache[b, :, t, :]
+    return out
+
+
+# --------------------------------------------------------------------------
 # a5-a7. decode attention over the dequantised cache (float64)
 # --------------------------------------------------------------------------
 def decode_attention(q: np.ndarray, k_codes, k_scales, v_codes, v_scales, seq_lens, blk: int,
@@ -246,8 +287,14 @@ def decode_attention(q: np.ndarray, k_codes, k_scales, v_codes, v_scales, seq_le
     token appended this step (append-before-attend).  Positions
     >= seq_lens[b] are not part of the sequence.  seq_lens[b] == 0 -> zeros
     (reading R12).  Computed in float64 over the fp32 dequantised values.
+
+    Grouped-query layout (reading R15): the cache may hold fewer
+    heads than q (H_kv | H); query head h reads cache head h // (H / H_kv),
+    consecutive query heads sharing one KV head (the multi-query / grouped
+    attention the paper names as orthogonal to NQKV).
     """
     B, H, hd = q.shape
+    g = kv_group(H, k_codes.shape[1])
     if softmax_scale is None:
         softmax_scale = 1.0 / math.sqrt(hd)
     out = np.zeros((B, H, hd), np.float64)
@@ -259,11 +306,11 @@ def decode_attention(q: np.ndarray, k_codes, k_scales, v_codes, v_scales, seq_le
         V = dequantize(v_codes[b:b + 1], v_scales[b:b + 1], blk, L, np.float32, levels32)[0]
         for h in range(H):
             qh = q[b, h].astype(np.float64)
-            s = (K[h].astype(np.float64) @ qh) * float(softmax_scale)
+            s = (K[h // g].astype(np.float64) @ qh) * float(softmax_scale)
             s = s - s.max()
             p = np.exp(s)
             p = p / p.sum()
-            out[b, h] = p @ V[h].astype(np.float64)
+            out[b, h] = p @ V[h // g].astype(np.float64)
     return out
 
 
@@ -280,6 +327,7 @@ def prefill_attention(q: np.ndarray, k_codes, k_scales, v_codes, v_scales, seq_l
     Returns float64 [B][T][H][hd]; rows i >= seq_lens[b] are 0.
     """
     B, T, H, hd = q.shape
+    g = kv_group(H, k_codes.shape[1])
     if softmax_scale is None:
         softmax_scale = 1.0 / math.sqrt(hd)
     out = np.zeros((B, T, H, hd), np.float64)
@@ -291,12 +339,12 @@ def prefill_attention(q: np.ndarray, k_codes, k_scales, v_codes, v_scales, seq_l
         V = dequantize(v_codes[b:b + 1], v_scales[b:b + 1], blk, L, np.float32, levels32)[0]
         for h in range(H):
             Q = q[b, :L, h].astype(np.float64)                        # [L, hd]
-            S = (Q @ K[h].astype(np.float64).T) * float(softmax_scale)  # [L, L]
+            S = (Q @ K[h // g].astype(np.float64).T) * float(softmax_scale)  # [L, L]
             S[np.triu_indices(L, 1)] = -np.inf                         # causal: j <= i
             S = S - S.max(axis=1, keepdims=True)
             P = np.exp(S)
             P = P / P.sum(axis=1, keepdims=True)
-            out[b, :L, h] = P @ V[h].astype(np.float64)
+            out[b, :L, h] = P @ V[h // g].astype(np.float64)
     return out
 
 

@@ -101,6 +101,10 @@ struct DecodeParams {
   const int* plan;             // optional per-step schedule (nqkv_decode_plan); nullptr: computed here
   int early;                   // NQKV_EARLY_START: plan and cache readable before the PDL wait
   int hpb_shift;               // blk > hd: scale rows [B][H >> hpb_shift][Tc] (blk_shift = log2 hd)
+  // KV layouts (readings R15, R16):
+  int kv_shift;                // grouped-query: query head h reads cache head h >> kv_shift
+  const int32_t* bt;           // paged cache (kernel template PAGED): block table [B][bt_stride];
+  int bt_stride, page_shift;   // token t of sequence b: page bt[b][t >> page_shift], row t & (P - 1)
   unsigned long long* trace;   // NQKV_TRACE builds: per-warp globaltimer stamps [grid][NW][16]
   // fused all-gather epilogue (kernel template GATHER):
   // every output row goes straight to all gather_g ranks' buffers
@@ -1038,7 +1042,7 @@ void merge_fn(const DecodeParams& p, unsigned char* smem, int k, Sched sc,
 }
 
 // GRP: blk > hd (a block spans 2^hpb_shift heads; instantiated with BLK = HD)
-template <int HD, int BLK, int NW, bool F16S, bool GRP, bool GATHER>
+template <int HD, int BLK, int NW, bool F16S, bool GRP, bool GATHER, bool PAGED = false>
 __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constant__ DecodeParams p) {
   constexpr int SB = F16S ? 2 : 4;   // bytes per stored block scale
   using Ge = Geo<HD>;
@@ -1280,10 +1284,12 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
     return walk_next_ws(*s_ws, s_len, p.H, g1, pc, k);
   };
   auto nstages = [&](const Piece& pc) { return (pc.t1 - pc.t0 + ST - 1) / ST; };
-  auto rowbase = [&](const Piece& pc) { return (pc.b * p.H + pc.h) * p.Tc; };
+  // cache rows of a piece: its KV head (query head h >> kv_shift, R15)
+  auto kvhead = [&](const Piece& pc) { return pc.b * (p.H >> p.kv_shift) + (pc.h >> p.kv_shift); };
+  auto rowbase = [&](const Piece& pc) { return kvhead(pc) * p.Tc; };
   // scale row base: the head group's row when a block spans heads (blk > hd)
   auto srowbase = [&](const Piece& pc) {
-    if constexpr (GRP) return ((pc.b * p.H + pc.h) >> p.hpb_shift) * p.Tc;
+    if constexpr (GRP) return (kvhead(pc) >> p.hpb_shift) * p.Tc;
     else return rowbase(pc);
   };
   auto load_quad = [&](const Piece& pc, int qd) -> uint4 {
@@ -1330,14 +1336,24 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
   const long long vdelta = p.vc - p.kc;
   uint32_t soff = 0;
   int nvl = 0, left = 0, lpi = 0;
+  int ptok = 0;                  // PAGED: first token of the cursor's stage
   bool lvalid = warp < NC;
   constexpr int KSTEP = NC * ST * (HD / 2), SSTEP = NC * ST * NBLK * SB;
   auto set_cursor = [&](const Piece& lp, int ls, int lro, int lns) {
     const int ltok = lp.t0 + ls * ST;
-    const uint32_t r = static_cast<uint32_t>(rowbase(lp) + ltok + g);
-    const uint32_t rs = GRP ? static_cast<uint32_t>(srowbase(lp) + ltok + g) : r;
-    kcp = p.kc + (r * (HD / 2) + sub * 8);
-    soff = (rs * NBLK + sidx) * SB + soff_rs;
+    if constexpr (PAGED) {
+      // paged cache (R16): the cursor keeps the token, the sequence's
+      // block-table row (in kcp) and the KV head (in soff); rows are found
+      // per stage in load_stage
+      ptok = ltok;
+      kcp = reinterpret_cast<const uint8_t*>(p.bt + static_cast<long long>(lp.b) * p.bt_stride);
+      soff = static_cast<uint32_t>(lp.h >> p.kv_shift);
+    } else {
+      const uint32_t r = static_cast<uint32_t>(rowbase(lp) + ltok + g);
+      const uint32_t rs = GRP ? static_cast<uint32_t>(srowbase(lp) + ltok + g) : r;
+      kcp = p.kc + (r * (HD / 2) + sub * 8);
+      soff = (rs * NBLK + sidx) * SB + soff_rs;
+    }
     nvl = lp.t1 - ltok - g;                 // slot i of this lane holds a row iff i*G < nvl
     left = (lns - 1 - ls) / NC;             // this warp's further stages in the piece
     if (lane == 0) {
@@ -1367,8 +1383,12 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
     if (!lvalid) return false;
     if (left > 0) {
       --left;
-      kcp += KSTEP;
-      soff += SSTEP;
+      if constexpr (PAGED) {
+        ptok += NC * ST;
+      } else {
+        kcp += KSTEP;
+        soff += SSTEP;
+      }
       nvl -= NC * ST;
       return true;
     }
@@ -1394,6 +1414,51 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
     // ptxas puts every global load of this loop on one scoreboard, so the
     // next stage's loads must not issue before the wait for the current
     // stage's data -- otherwise that wait would also wait for them.
+    if constexpr (PAGED) {
+      // The stage's ST tokens span at most two pages (P >= 64 > ST): their
+      // ids are read (L1) after the wait, then each slot's row is
+      // (page * H_kv + kv head) * P + t % P in [n_pages][H_kv][P] storage.
+      const int32_t* btp = reinterpret_cast<const int32_t*>(kcp);
+      const int ps = p.page_shift, pm = (1 << ps) - 1;
+      const int hkv = p.H >> p.kv_shift;
+      const int tend = ptok + min(ST, nvl + g) - 1;      // last row of the stage in the piece
+      const int pa = __ldg(btp + (ptok >> ps) + dep);
+      const int pb = __ldg(btp + (max(tend, ptok) >> ps) + dep);
+      auto row_of = [&](int t) -> uint32_t {
+        const int pg = ((t >> ps) == (ptok >> ps)) ? pa : pb;
+        return static_cast<uint32_t>((pg * hkv + static_cast<int>(soff)) << ps) + static_cast<uint32_t>(t & pm);
+      };
+      auto srow_of = [&](int t) -> uint32_t {
+        if constexpr (GRP) {
+          const int pg = ((t >> ps) == (ptok >> ps)) ? pa : pb;
+          return static_cast<uint32_t>((pg * (hkv >> p.hpb_shift) + (static_cast<int>(soff) >> p.hpb_shift)) << ps) +
+                 static_cast<uint32_t>(t & pm);
+        } else {
+          return row_of(t);
+        }
+      };
+#pragma unroll
+      for (int i = 0; i < kTPS; ++i) {
+        if (i * G < nvl) {
+          const uint32_t r = row_of(ptok + g + i * G);
+          Rg.k[i] = ldg_stream_64(p.kc + (r * (HD / 2) + sub * 8));
+          Rg.v[i] = ldg_stream_64(p.vc + (r * (HD / 2) + sub * 8));
+          if constexpr (!RS) {
+            const uint32_t so = (srow_of(ptok + g + i * G) * NBLK + sidx) * SB;
+            Rg.ks[i] = ld_scale<F16S>(p.ks, so);
+            Rg.vs[i] = ld_scale<F16S>(p.vs, so);
+          }
+        }
+      }
+      if constexpr (RS) {
+        if ((sub & 3) * G < nvl) {
+          const uint32_t so = (srow_of(ptok + g + (sub & 3) * G) * NBLK + sidx) * SB;
+          Rg.ks[0] = ld_scale<F16S>(p.ks, so);
+          Rg.vs[0] = ld_scale<F16S>(p.vs, so);
+        }
+      }
+      return;
+    }
     const uint8_t* vcp = kcp + vdelta;
     const uint8_t* ksp = static_cast<const uint8_t*>(p.ks) + soff;
     const uint8_t* vsp = static_cast<const uint8_t*>(p.vs) + soff;

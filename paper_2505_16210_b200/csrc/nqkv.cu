@@ -148,9 +148,9 @@ cudaError_t launch_pdl(void (*kern)(P), dim3 grid, dim3 block, size_t smem, cuda
   return cudaLaunchKernelEx(&cfg, kern, prm);
 }
 
-template <int HD, int BLK, bool F16S, bool GRP, bool GATHER>
+template <int HD, int BLK, bool F16S, bool GRP, bool GATHER, bool PAGED = false>
 int launch_decode_blk(const DecodeParams& p, cudaStream_t st) {
-  auto kern = decode_kernel<HD, BLK, kDecodeWarps, F16S, GRP, GATHER>;
+  auto kern = decode_kernel<HD, BLK, kDecodeWarps, F16S, GRP, GATHER, PAGED>;
   const size_t smem = Smem<HD, kDecodeWarps>::kBytes;
   static bool attr_set = false;
   static std::mutex mu;
@@ -182,9 +182,70 @@ int launch_decode_g(const DecodeParams& p, cudaStream_t st) {
   }
 }
 
+// paged cache (reading R16): fp32 scales, no fused gather
+template <int HD>
+int launch_decode_paged(const DecodeParams& p, cudaStream_t st) {
+  if (p.hpb_shift) return launch_decode_blk<HD, HD, false, true, false, true>(p, st);
+  switch (p.blk_shift) {
+    case 5: return launch_decode_blk<HD, 32, false, false, false, true>(p, st);
+    case 6: return launch_decode_blk<HD, 64, false, false, false, true>(p, st);
+    default:
+      if constexpr (HD == 128) return launch_decode_blk<HD, 128, false, false, false, true>(p, st);
+      else return NQKV_ERR_UNSUPPORTED;
+  }
+}
+
 template <int HD, bool F16S>
 int launch_decode(const DecodeParams& p, cudaStream_t st) {
+  if (p.bt) {
+    if constexpr (F16S) return NQKV_ERR_UNSUPPORTED;
+    else return launch_decode_paged<HD>(p, st);
+  }
   return p.peer_out ? launch_decode_g<HD, F16S, true>(p, st) : launch_decode_g<HD, F16S, false>(p, st);
+}
+
+// KV layout of a call (nqkv_kv_layout, validated): grouped-query head
+// mapping (R15) and the paged cache (R16)
+struct KvLayout {
+  int kv_shift = 0;
+  const int32_t* bt = nullptr;
+  int bt_stride = 0, page_shift = 0;
+  long long n_pages = 0;
+};
+
+int log2_exact(long long v) {
+  if (v <= 0 || (v & (v - 1))) return -1;
+  int s = 0;
+  while ((1ll << s) < v) ++s;
+  return s;
+}
+
+// H query heads over a cache described by `kv` (may be null: MHA, contiguous)
+int kv_layout_of(const nqkv_kv_layout* kv, int H, int hd, int blk, int Tc, KvLayout& out, int& H_kv) {
+  out = KvLayout();
+  H_kv = H;
+  if (!kv) return NQKV_OK;
+  H_kv = kv->kv_heads ? kv->kv_heads : H;
+  if (H_kv < 0 || (H_kv > 0 && H % H_kv)) return NQKV_ERR_SHAPE;
+  if (H_kv > 0) {
+    out.kv_shift = log2_exact(H / H_kv);
+    if (out.kv_shift < 0) return NQKV_ERR_UNSUPPORTED;        // group size: a power of two
+  }
+  if (kv->block_table) {
+    const int ps = log2_exact(kv->page_size);
+    if (ps < 6) return NQKV_ERR_UNSUPPORTED;                    // P: power of two >= 64
+    if (kv->n_pages <= 0 || kv->pages_per_seq <= 0) return NQKV_ERR_SHAPE;
+    if (static_cast<long long>(kv->pages_per_seq) * kv->page_size < Tc) return NQKV_ERR_SHAPE;
+    if (static_cast<long long>(kv->n_pages) * H_kv * kv->page_size * (hd / 2) >= (1ll << 32))
+      return NQKV_ERR_SHAPE;                                    // 32-bit row offsets
+    if (reinterpret_cast<uintptr_t>(kv->block_table) & 3u) return NQKV_ERR_ALIGN;
+    out.bt = kv->block_table;
+    out.bt_stride = kv->pages_per_seq;
+    out.page_shift = ps;
+    out.n_pages = kv->n_pages;
+  }
+  (void)blk;
+  return NQKV_OK;
 }
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
@@ -218,14 +279,20 @@ int decode_common(const void* q, const uint8_t* k_codes, const void* k_scales,
                   const void* k_new, const void* v_new, int64_t new_sb, int64_t new_sh, int B,
                   int H, int hd, int blk, int Tc, float softmax_scale, float* out, void* workspace,
                   size_t ws_bytes, const void* plan, int flags, cudaStream_t st,
-                  const GatherArgs* ga = nullptr) {
+                  const GatherArgs* ga = nullptr, const nqkv_kv_layout* kv = nullptr) {
   if (!q || !k_codes || !k_scales || !v_codes || !v_scales || !d_seq_lens || (!out && !ga))
     return NQKV_ERR_NULL;
   if (int s = check_geometry(hd, blk)) return s;
   if (B < 0 || H < 0 || Tc <= 0 || Tc % 64 || B > kMaxBatch) return NQKV_ERR_SHAPE;
-  if (!heads_fit(H, hd, blk)) return NQKV_ERR_SHAPE;
+  KvLayout lay;
+  int H_kv = H;
+  if (int s = kv_layout_of(kv, H, hd, blk_of(blk), Tc, lay, H_kv)) return s;
+  if (kv && (k_new || plan || ga)) return NQKV_ERR_UNSUPPORTED;   // layouts: attention-only calls
+  if (lay.bt && f16s_of(blk)) return NQKV_ERR_UNSUPPORTED;
+  if (!heads_fit(H_kv, hd, blk_of(blk))) return NQKV_ERR_SHAPE;
   if (static_cast<long long>(B) * H * Tc >= (1ll << 31)) return NQKV_ERR_SHAPE;
-  if (static_cast<long long>(B) * H * Tc * (hd / 2) >= (1ll << 32)) return NQKV_ERR_SHAPE;  // 32-bit offsets
+  if (!lay.bt && static_cast<long long>(B) * H_kv * Tc * (hd / 2) >= (1ll << 32))
+    return NQKV_ERR_SHAPE;  // 32-bit offsets
   const bool f16s = f16s_of(blk);
   blk = blk_of(blk);
   if (!aligned16(q) || !aligned16(k_codes) || !aligned16(v_codes) || (out && !aligned16(out)) ||
@@ -259,6 +326,10 @@ int decode_common(const void* q, const uint8_t* k_codes, const void* k_scales,
   // read from the head group's scale row
   p.blk_shift = blk_shift_of(blk > hd ? hd : blk);
   p.hpb_shift = hpb_shift_of(hd, blk);
+  p.kv_shift = lay.kv_shift;
+  p.bt = lay.bt;
+  p.bt_stride = lay.bt_stride;
+  p.page_shift = lay.page_shift;
   p.min_tokens = kMinTokensPerCta;
   p.scale_log2 = softmax_scale * 1.4426950408889634f;
   p.lv = make_levels();
@@ -343,15 +414,19 @@ int nqkv_thresholds(float thresholds[15]) {
   return NQKV_OK;
 }
 
-int nqkv_quantize(const void* x, int64_t stride_b, int64_t stride_t, int64_t stride_h, int B,
-                  int H, int hd, int n_new, int blk, const int32_t* d_pos, int Tc,
-                  uint8_t* codes, void* scales, void* stream) {
+static int quantize_common(const void* x, int64_t stride_b, int64_t stride_t, int64_t stride_h,
+                           int B, int H, int hd, int n_new, int blk, const int32_t* d_pos, int Tc,
+                           uint8_t* codes, void* scales, void* stream, const nqkv_kv_layout* kv) {
   if (!x || !d_pos || !codes || !scales) return NQKV_ERR_NULL;
   if (int s = check_geometry(hd, blk)) return s;
   const bool f16s = f16s_of(blk);
   blk = blk_of(blk);
   if (B < 0 || H < 0 || n_new < 0 || Tc <= 0 || Tc % 64) return NQKV_ERR_SHAPE;
   if (!heads_fit(H, hd, blk)) return NQKV_ERR_SHAPE;
+  KvLayout lay;
+  int H_kv = H;
+  if (int s = kv_layout_of(kv, H, hd, blk, Tc, lay, H_kv)) return s;
+  if (H_kv != H) return NQKV_ERR_SHAPE;      // x holds the cache's (KV) heads
   if (!aligned16(x) || !aligned16(codes) || !scale_aligned(scales, f16s) ||
       (stride_b % 8) || (stride_t % 8) || (stride_h % 8))
     return NQKV_ERR_ALIGN;
@@ -376,6 +451,9 @@ int nqkv_quantize(const void* x, int64_t stride_b, int64_t stride_t, int64_t str
   p.cpr = make_fastdiv(static_cast<uint32_t>(H * (hd / 16)));
   p.nnew = make_fastdiv(static_cast<uint32_t>(n_new));
   p.tab = make_bucket_tab();
+  p.bt = lay.bt;
+  p.bt_stride = lay.bt_stride;
+  p.page_shift = lay.page_shift;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   // one warp per 64-chunk unit, grid-strided over one wave of resident CTAs
 #ifndef NQKV_Q_CTAS_PER_SM
@@ -398,6 +476,21 @@ int nqkv_quantize(const void* x, int64_t stride_b, int64_t stride_t, int64_t str
   };
   e = f16s ? launch(std::true_type{}) : launch(std::false_type{});
   return e == cudaSuccess ? NQKV_OK : cuda_fail(e);
+}
+
+int nqkv_quantize(const void* x, int64_t stride_b, int64_t stride_t, int64_t stride_h, int B,
+                  int H, int hd, int n_new, int blk, const int32_t* d_pos, int Tc,
+                  uint8_t* codes, void* scales, void* stream) {
+  return quantize_common(x, stride_b, stride_t, stride_h, B, H, hd, n_new, blk, d_pos, Tc, codes,
+                         scales, stream, nullptr);
+}
+
+int nqkv_quantize_kv(const void* x, int64_t stride_b, int64_t stride_t, int64_t stride_h, int B,
+                     int H, int hd, int n_new, int blk, const int32_t* d_pos, int Tc,
+                     const nqkv_kv_layout* kv, uint8_t* codes, void* scales, void* stream) {
+  if (!kv) return NQKV_ERR_NULL;
+  return quantize_common(x, stride_b, stride_t, stride_h, B, H, hd, n_new, blk, d_pos, Tc, codes,
+                         scales, stream, kv);
 }
 
 int nqkv_dequantize(const uint8_t* codes, const void* scales, int B, int H, int Tc, int hd,
@@ -451,6 +544,17 @@ int nqkv_decode_attention(const void* q, const uint8_t* k_codes, const void* k_s
   return decode_common(q, k_codes, k_scales, v_codes, v_scales, d_seq_lens, nullptr, nullptr, 0,
                        0, B, H, hd, blk, Tc, softmax_scale, out, workspace, ws_bytes, nullptr, 0,
                        static_cast<cudaStream_t>(stream));
+}
+
+int nqkv_decode_attention_kv(const void* q, const uint8_t* k_codes, const void* k_scales,
+                             const uint8_t* v_codes, const void* v_scales,
+                             const int32_t* d_seq_lens, int B, int H, int hd, int blk, int Tc,
+                             const nqkv_kv_layout* kv, float softmax_scale, float* out,
+                             void* workspace, size_t ws_bytes, void* stream) {
+  if (!kv) return NQKV_ERR_NULL;
+  return decode_common(q, k_codes, k_scales, v_codes, v_scales, d_seq_lens, nullptr, nullptr, 0,
+                       0, B, H, hd, blk, Tc, softmax_scale, out, workspace, ws_bytes, nullptr, 0,
+                       static_cast<cudaStream_t>(stream), nullptr, kv);
 }
 
 size_t nqkv_decode_plan_bytes(void) { return static_cast<size_t>(kPlanInts) * sizeof(int); }
@@ -536,16 +640,22 @@ int nqkv_gather_wait(const unsigned* d_flags, int n, const unsigned* d_epoch, vo
   return e == cudaSuccess ? NQKV_OK : cuda_fail(e);
 }
 
-int nqkv_prefill_attention(const void* q, const uint8_t* k_codes, const void* k_scales,
-                           const uint8_t* v_codes, const void* v_scales, const int32_t* d_seq_lens,
-                           int B, int H, int hd, int blk, int Tc, int T, float softmax_scale,
-                           float* out, void* stream) {
+static int prefill_common(const void* q, const uint8_t* k_codes, const void* k_scales,
+                          const uint8_t* v_codes, const void* v_scales, const int32_t* d_seq_lens,
+                          int B, int H, int hd, int blk, int Tc, int T, float softmax_scale,
+                          float* out, void* stream, const nqkv_kv_layout* kv) {
   if (!q || !k_codes || !k_scales || !v_codes || !v_scales || !d_seq_lens || !out) return NQKV_ERR_NULL;
   if (int s = check_geometry(hd, blk)) return s;
   const bool f16s = f16s_of(blk);
   blk = blk_of(blk);
   if (B < 0 || H < 0 || T < 0 || Tc <= 0 || Tc % 64 || T > Tc) return NQKV_ERR_SHAPE;
-  if (!heads_fit(H, hd, blk)) return NQKV_ERR_SHAPE;
+  KvLayout lay;
+  int H_kv = H;
+  if (int s = kv_layout_of(kv, H, hd, blk, Tc, lay, H_kv)) return s;
+#if NQKV_PREFILL_MMA_SYNC
+  if (kv) return NQKV_ERR_UNSUPPORTED;       // the comparison build has no KV layouts
+#endif
+  if (!heads_fit(H_kv, hd, blk)) return NQKV_ERR_SHAPE;
   if (static_cast<long long>(B) * H * Tc >= (1ll << 31) || B > 65535 || H > 65535) return NQKV_ERR_SHAPE;
   if (!aligned16(q) || !aligned16(k_codes) || !aligned16(v_codes) || !aligned16(out) ||
       !scale_aligned(k_scales, f16s) || !scale_aligned(v_scales, f16s))
@@ -561,6 +671,10 @@ int nqkv_prefill_attention(const void* q, const uint8_t* k_codes, const void* k_
   p.hpb_shift = hpb_shift_of(hd, blk);
   p.scale_log2 = softmax_scale * 1.4426950408889634f;
   p.lv = make_levels();
+  p.kv_shift = lay.kv_shift;
+  p.bt = lay.bt;
+  p.bt_stride = lay.bt_stride;
+  p.page_shift = lay.page_shift;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool grp = blk > hd;
   cudaError_t e;
@@ -600,6 +714,24 @@ int nqkv_prefill_attention(const void* q, const uint8_t* k_codes, const void* k_
   }
 #endif
   return e == cudaSuccess ? NQKV_OK : cuda_fail(e);
+}
+
+int nqkv_prefill_attention(const void* q, const uint8_t* k_codes, const void* k_scales,
+                           const uint8_t* v_codes, const void* v_scales, const int32_t* d_seq_lens,
+                           int B, int H, int hd, int blk, int Tc, int T, float softmax_scale,
+                           float* out, void* stream) {
+  return prefill_common(q, k_codes, k_scales, v_codes, v_scales, d_seq_lens, B, H, hd, blk, Tc, T,
+                        softmax_scale, out, stream, nullptr);
+}
+
+int nqkv_prefill_attention_kv(const void* q, const uint8_t* k_codes, const void* k_scales,
+                              const uint8_t* v_codes, const void* v_scales,
+                              const int32_t* d_seq_lens, int B, int H, int hd, int blk, int Tc,
+                              int T, const nqkv_kv_layout* kv, float softmax_scale, float* out,
+                              void* stream) {
+  if (!kv) return NQKV_ERR_NULL;
+  return prefill_common(q, k_codes, k_scales, v_codes, v_scales, d_seq_lens, B, H, hd, blk, Tc, T,
+                        softmax_scale, out, stream, kv);
 }
 
 int nqkv_encode_normalized(const float* d_n, int64_t count, uint8_t* d_codes, void* stream) {

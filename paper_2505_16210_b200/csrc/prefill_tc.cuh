@@ -357,8 +357,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) prefill_tc_kernel(const __grid_
   } else if (warp < kTcSoftW + kTcDqW) {
     // ================= dequantisation: K(t), V(t) into ring stage t % 3
     const int dt = tid - kTcSoftW * 32;
-    const long long row_base = (static_cast<long long>(b) * p.H + h) * p.Tc;
-    const long long srow_base = GRP ? ((static_cast<long long>(b) * p.H + h) >> p.hpb_shift) * p.Tc : row_base;
+    const int hkv = p.H >> p.kv_shift, kvh = h >> p.kv_shift;
+    const long long row_base = (static_cast<long long>(b) * hkv + kvh) * p.Tc;
+    const long long srow_base = GRP ? ((static_cast<long long>(b) * hkv + kvh) >> p.hpb_shift) * p.Tc : row_base;
     const int nblk = GRP ? 1 : HD >> p.blk_shift;
     // Item = 32 dims (16 code bytes, one scale: blk >= 32) of one key; the
     // key's row within the core matrix varies fastest across lanes, so a warp
@@ -383,8 +384,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) prefill_tc_kernel(const __grid_
       float s[kPer];
     };
     auto load = [&](const uint8_t* codes, const void* scales, int k0, Raw& r, int dep) {
-      const uint8_t* cb = codes + (row_base + k0) * (HD / 2);
-      const long long sb = GRP ? srow_base + k0 : (row_base + k0) * nblk;
+      long long rb = row_base + k0, srb = srow_base + k0;
+      if (p.bt && k0 < len) {     // paged (R16): a 64-key tile lies in one page (P >= 64)
+        const long long pg = __ldg(p.bt + static_cast<long long>(b) * p.bt_stride + (k0 >> p.page_shift));
+        const int within = k0 & ((1 << p.page_shift) - 1);
+        rb = ((pg * hkv + kvh) << p.page_shift) + within;
+        srb = GRP ? ((pg * (hkv >> p.hpb_shift) + (kvh >> p.hpb_shift)) << p.page_shift) + within : rb;
+      }
+      const uint8_t* cb = codes + rb * (HD / 2);
+      const long long sb = GRP ? srb : rb * nblk;
 #pragma unroll
       for (int u = 0; u < kPer; ++u) {
         r.w[u] = make_uint4(0u, 0u, 0u, 0u);

@@ -20,6 +20,10 @@ struct QuantParams {
   FastDiv cpr;                   // chunks per token row (b, t): H * hd / 16
   FastDiv nnew;                  // n_new
   BucketTab tab;
+  // paged cache (reading R16): row pos of sequence b is row
+  // pos & (P - 1) of page bt[b][pos >> page_shift] in [n_pages][H][P] storage
+  const int32_t* bt;             // nullptr: contiguous [B][H][Tc]
+  int bt_stride, page_shift;
 };
 
 // Bucket table replicated per lane: entry e for lane l at shared address
@@ -157,11 +161,18 @@ __global__ void __launch_bounds__(256, 4) quantize_kernel(const __grid_constant_
     const int pos = __ldg(p.pos + bb) + static_cast<int>(t);
     if (pos < 0 || pos >= p.Tc) return;
     const uint32_t h = within >> LOG_CPT, cr = within & (CPT - 1);
-    const long long rr = (static_cast<long long>(bb) * p.H + h) * p.Tc + pos;
+    // row of (b, h, pos): contiguous, or in its page (R16)
+    long long base = static_cast<long long>(bb), rowin = pos, rows = p.Tc;
+    if (p.bt) {
+      base = __ldg(p.bt + static_cast<long long>(bb) * p.bt_stride + (pos >> p.page_shift));
+      rowin = pos & ((1 << p.page_shift) - 1);
+      rows = 1ll << p.page_shift;
+    }
+    const long long rr = (base * p.H + h) * rows + rowin;
     *reinterpret_cast<uint4*>(p.codes + rr * (HD / 2) + cr * 8) = words;
     if (scale_writer) {
       // blk > hd: one scale per (token, head group): [B][H >> hpb_shift][Tc]
-      const long long si = BLK > HD ? ((static_cast<long long>(bb) * p.H + h) >> p.hpb_shift) * p.Tc + pos
+      const long long si = BLK > HD ? ((base * p.H + h) >> p.hpb_shift) * rows + rowin
                                     : rr * nblk + ((cr * 16) >> p.blk_shift);
       if constexpr (F16S)
         reinterpret_cast<__half*>(p.scales)[si] = __float2half_rn(s);   // exact: s is an fp16 value

@@ -25,6 +25,17 @@ _lib = ctypes.CDLL(_LIB_PATH)
 _vp, _i32, _i64, _sz = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_size_t
 _fp = ctypes.POINTER(ctypes.c_float)
 
+
+class KvLayout(ctypes.Structure):
+    """nqkv_kv_layout (include/nqkv.h): grouped-query head mapping and the
+    paged cache (readings R15, R16)."""
+    _fields_ = [("kv_heads", ctypes.c_int), ("block_table", ctypes.c_void_p),
+                ("pages_per_seq", ctypes.c_int), ("page_size", ctypes.c_int),
+                ("n_pages", ctypes.c_int)]
+
+
+_lp = ctypes.POINTER(KvLayout)
+
 _SIGS = {
     "nqkv_abi_version": (_i32, []),
     "nqkv_status_string": (ctypes.c_char_p, [_i32]),
@@ -56,6 +67,12 @@ _SIGS = {
     "nqkv_prefill_attention": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32,
                                       _i32, ctypes.c_float, _vp, _vp]),
     "nqkv_build_id": (ctypes.c_char_p, []),
+    "nqkv_decode_attention_kv": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32,
+                                        _lp, ctypes.c_float, _vp, _vp, _sz, _vp]),
+    "nqkv_prefill_attention_kv": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32,
+                                         _i32, _lp, ctypes.c_float, _vp, _vp]),
+    "nqkv_quantize_kv": (_i32, [_vp, _i64, _i64, _i64, _i32, _i32, _i32, _i32, _i32, _vp, _i32, _lp,
+                                _vp, _vp, _vp]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -63,7 +80,7 @@ for _name, (_res, _args) in _SIGS.items():
     _f.argtypes = _args
 
 EXPORTED = tuple(_SIGS)
-ABI_VERSION = 3
+ABI_VERSION = 4
 if _lib.nqkv_abi_version() != ABI_VERSION:
     raise ImportError("libnqkv.so ABI version mismatch; rebuild")
 
@@ -230,6 +247,70 @@ def nqkv_prefill_attention(q: torch.Tensor, k_codes: torch.Tensor, k_scales: tor
                                        _blkarg(blk, k_scales, v_scales), Tc, T,
                                        float(softmax_scale), _ptr(out), _stream(stream)),
            "nqkv_prefill_attention")
+    return out
+
+
+def kv_layout(kv_heads: int = 0, block_table: torch.Tensor | None = None, page_size: int = 0,
+              n_pages: int = 0) -> KvLayout:
+    """nqkv_kv_layout: kv_heads (0 = as many as query heads); block_table
+    int32 [B, pages_per_seq] on the device for a paged cache."""
+    if block_table is not None:
+        assert block_table.dtype == torch.int32 and block_table.is_contiguous()
+        return KvLayout(kv_heads, block_table.data_ptr(), block_table.shape[1], page_size, n_pages)
+    return KvLayout(kv_heads, None, 0, 0, 0)
+
+
+def nqkv_quantize_kv(x: torch.Tensor, pos: torch.Tensor, codes: torch.Tensor, scales: torch.Tensor,
+                     blk: int, layout: KvLayout, Tc: int, stream=None) -> None:
+    """nqkv_quantize into the cache `layout` describes (paged: codes
+    [n_pages, H, P, hd/2], scales [n_pages, H, P, hd/blk]; Tc = the
+    per-sequence capacity)."""
+    B, n_new, H, hd = x.shape
+    assert x.dtype == torch.float16 and x.stride(3) == 1 and pos.dtype == torch.int32
+    assert codes.dtype == torch.uint8 and codes.is_contiguous() and scales.is_contiguous()
+    _check(_lib.nqkv_quantize_kv(_ptr(x), x.stride(0), x.stride(1), x.stride(2), B, H, hd, n_new,
+                                 _blkarg(blk, scales), _ptr(pos), Tc, ctypes.byref(layout),
+                                 _ptr(codes), _ptr(scales), _stream(stream)), "nqkv_quantize_kv")
+
+
+def nqkv_decode_attention_kv(q: torch.Tensor, k_codes, k_scales, v_codes, v_scales, seq_lens,
+                             blk: int, layout: KvLayout, Tc: int, workspace: torch.Tensor,
+                             softmax_scale: float | None = None, out: torch.Tensor | None = None,
+                             stream=None) -> torch.Tensor:
+    """nqkv_decode_attention over a KV layout: q [B, H, hd] (query heads),
+    cache as `layout` says; Tc = the per-sequence capacity."""
+    B, H, hd = q.shape
+    if softmax_scale is None:
+        softmax_scale = 1.0 / math.sqrt(hd)
+    if out is None:
+        out = torch.empty((B, H, hd), dtype=torch.float32, device=q.device)
+    assert q.dtype == torch.float16 and q.is_contiguous() and out.is_contiguous()
+    assert seq_lens.dtype == torch.int32
+    _check(_lib.nqkv_decode_attention_kv(_ptr(q), _ptr(k_codes), _ptr(k_scales), _ptr(v_codes),
+                                         _ptr(v_scales), _ptr(seq_lens), B, H, hd,
+                                         _blkarg(blk, k_scales, v_scales), Tc, ctypes.byref(layout),
+                                         float(softmax_scale), _ptr(out), _ptr(workspace),
+                                         workspace.numel() * workspace.element_size(),
+                                         _stream(stream)), "nqkv_decode_attention_kv")
+    return out
+
+
+def nqkv_prefill_attention_kv(q: torch.Tensor, k_codes, k_scales, v_codes, v_scales, seq_lens,
+                              blk: int, layout: KvLayout, Tc: int, softmax_scale: float | None = None,
+                              out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """nqkv_prefill_attention over a KV layout: q [B, T, H, hd]."""
+    B, T, H, hd = q.shape
+    if softmax_scale is None:
+        softmax_scale = 1.0 / math.sqrt(hd)
+    if out is None:
+        out = torch.empty((B, T, H, hd), dtype=torch.float32, device=q.device)
+    assert q.dtype == torch.float16 and q.is_contiguous() and out.is_contiguous()
+    assert seq_lens.dtype == torch.int32
+    _check(_lib.nqkv_prefill_attention_kv(_ptr(q), _ptr(k_codes), _ptr(k_scales), _ptr(v_codes),
+                                          _ptr(v_scales), _ptr(seq_lens), B, H, hd,
+                                          _blkarg(blk, k_scales, v_scales), Tc, T,
+                                          ctypes.byref(layout), float(softmax_scale), _ptr(out),
+                                          _stream(stream)), "nqkv_prefill_attention_kv")
     return out
 
 

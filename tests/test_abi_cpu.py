@@ -27,7 +27,7 @@ def test_exports_every_declared_symbol():
     lib = ctypes.CDLL(N._LIB_PATH)
     for name in declared:
         assert hasattr(lib, name)
-    assert lib.nqkv_abi_version() == 3
+    assert lib.nqkv_abi_version() == 4
 
 
 def test_host_levels_and_thresholds_match_oracle_bits():
@@ -181,3 +181,42 @@ def test_build_id_matches_sources():
     assert bld.built_id() == bld.source_id()
     assert N._lib.nqkv_build_id().decode() == bld.source_id()
     assert not bld.needs_build()
+
+
+def _dkv(lay, **kw):
+    a = dict(q=FAKE, B=2, H=8, hd=128, blk=64, Tc=512, ws=FAKE, wsb=1 << 30)
+    a.update(kw)
+    return N._lib.nqkv_decode_attention_kv(a["q"], FAKE, FAKE, FAKE, FAKE, FAKE, a["B"], a["H"], a["hd"],
+                                           a["blk"], a["Tc"], None if lay is None else ctypes.byref(lay),
+                                           0.1, FAKE, a["ws"], a["wsb"], None)
+
+
+def test_kv_layout_argument_errors():
+    # grouped-query (R15) and paged (R16) layouts: host-checkable errors, no launch
+    L = N.KvLayout
+    assert _dkv(None) == -1
+    assert _dkv(L(3, None, 0, 0, 0)) == -2            # 8 query heads over 3 KV heads
+    assert _dkv(L(8, None, 0, 0, 0), B=0) == 0         # nothing to do
+    assert _dkv(L(2, None, 0, 0, 0), B=0) == 0         # group 4: valid
+    assert _dkv(L(0, None, 0, 0, 0), H=12, B=0) == 0
+    assert _dkv(L(4, None, 0, 0, 0), H=12) == -3      # group 3: not a power of two
+    assert _dkv(L(2, FAKE, 8, 32, 64)) == -3          # page_size < 64
+    assert _dkv(L(2, FAKE, 8, 96, 64)) == -3          # not a power of two
+    assert _dkv(L(2, FAKE, 4, 64, 64)) == -2          # 4 pages x 64 < Tc = 512
+    assert _dkv(L(2, FAKE, 8, 64, 0)) == -2           # no pages
+    assert _dkv(L(2, FAKE + 2, 8, 64, 64)) == -4      # block table alignment
+    assert _dkv(L(2, FAKE, 8, 64, 1 << 20)) == -2     # 32-bit row offsets
+    assert _dkv(L(2, FAKE, 8, 64, 64), blk=64 | N.SCALE_F16) == -3   # paged: fp32 scales
+    assert _dkv(L(2, FAKE, 8, 64, 64), B=0) == 0
+    # quantize: x holds the cache heads
+    q = N._lib.nqkv_quantize_kv
+    lay = L(6, None, 0, 0, 0)
+    assert q(FAKE, 64 * 12 * 512, 64 * 12, 64, 1, 12, 64, 512, 64, FAKE, 512, ctypes.byref(lay), FAKE, FAKE, None) == -2
+    lay = L(0, FAKE, 8, 64, 64)
+    assert q(FAKE, 64 * 12 * 512, 64 * 12, 64, 0, 12, 64, 512, 64, FAKE, 512, ctypes.byref(lay), FAKE, FAKE, None) == 0
+    assert q(FAKE, 64 * 12 * 512, 64 * 12, 64, 1, 12, 64, 512, 64, FAKE, 512, None, FAKE, FAKE, None) == -1
+    p = N._lib.nqkv_prefill_attention_kv
+    assert p(FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, 1, 8, 64, 64, 512, 16, ctypes.byref(L(3, None, 0, 0, 0)),
+             0.1, FAKE, None) == -2
+    assert p(FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, 0, 8, 64, 64, 512, 16, ctypes.byref(L(2, None, 0, 0, 0)),
+             0.1, FAKE, None) == 0

@@ -669,3 +669,72 @@ def test_prefill_rows_equal_decode_steps():
         for b, L in enumerate([10, 6]):
             if i < L:
                 assert np.max(np.abs(out[b, i] - dec[b])) < 1e-12
+
+
+# ------------------------------------------- KV layouts --
+def test_gqa_is_mha_over_repeated_kv_heads():
+    # reading R15: query head h reads KV head h // g.  Pinned to
+    # the (separately pinned) MHA oracle on a cache whose heads are repeated
+    # g times -- a mapping h % H_kv or a wrong group size fails this.
+    rng = np.random.default_rng(31)
+    B, Hkv, g, hd, T = 2, 2, 4, 64, 9
+    k = rng.standard_normal((B, T, Hkv, hd)).astype(np.float16)
+    v = rng.standard_normal((B, T, Hkv, hd)).astype(np.float16)
+    kc, ks = _cache_from(k, 64)
+    vc, vs = _cache_from(v, 64)
+    rep = lambda a: np.repeat(a, g, axis=1)      # noqa: E731  kv head j -> query heads j*g .. j*g+g-1
+    q = rng.standard_normal((B, Hkv * g, hd)).astype(np.float16)
+    a = O.decode_attention(q, kc, ks, vc, vs, [T, 5], 64)
+    b = O.decode_attention(q, rep(kc), rep(ks), rep(vc), rep(vs), [T, 5], 64)
+    assert np.array_equal(a, b)
+    qp = rng.standard_normal((B, T, Hkv * g, hd)).astype(np.float16)
+    a = O.prefill_attention(qp, kc, ks, vc, vs, [T, 5], 64)
+    b = O.prefill_attention(qp, rep(kc), rep(ks), rep(vc), rep(vs), [T, 5], 64)
+    assert np.array_equal(a, b)
+    with pytest.raises(ValueError):
+        O.decode_attention(q[:, :7], kc, ks, vc, vs, [T, 5], 64)
+
+
+def test_gqa_single_token_closed_form():
+    # SPEC.md:251 per group: one cached token -> every query head of the group
+    # returns that KV head's dequantised value
+    rng = np.random.default_rng(32)
+    k = rng.standard_normal((1, 1, 2, 64)).astype(np.float16)
+    v = rng.standard_normal((1, 1, 2, 64)).astype(np.float16)
+    kc, ks = _cache_from(k, 64)
+    vc, vs = _cache_from(v, 64)
+    q = rng.standard_normal((1, 6, 64)).astype(np.float16)
+    out = O.decode_attention(q, kc, ks, vc, vs, [1], 64)
+    vhat = O.dequantize(vc, vs, 64, 1)[0, :, 0]        # [2][hd]
+    for h in range(6):
+        assert np.array_equal(out[0, h], vhat[h // 3].astype(np.float64))
+
+
+def test_paged_layout_identity_table_is_a_reshape():
+    # reading R16: with block_table[b][j] = b * maxp + j the paged cache is the
+    # contiguous one cut into pages: a numpy reshape/transpose, independent of
+    # the oracle's per-token gather
+    rng = np.random.default_rng(33)
+    B, H, P, maxp, w = 3, 2, 64, 4, 32
+    cont = rng.integers(0, 256, (B, H, P * maxp, w), dtype=np.uint8)
+    bt = np.arange(B * maxp, dtype=np.int32).reshape(B, maxp)
+    pages = cont.reshape(B, H, maxp, P, w).transpose(0, 2, 1, 3, 4).reshape(B * maxp, H, P, w)
+    assert np.array_equal(O.paged_to_contiguous(pages, bt, P, P * maxp), cont)
+    assert np.array_equal(O.contiguous_to_paged(cont, bt, P, B * maxp), pages)
+
+
+def test_paged_layout_permuted_pages_round_trip():
+    # any injective page assignment: contiguous -> paged -> contiguous is the
+    # identity on covered rows, and every used page holds exactly its rows
+    rng = np.random.default_rng(34)
+    B, H, P, maxp, w = 2, 3, 64, 3, 8
+    n_pages = 9
+    cont = rng.integers(0, 256, (B, H, P * maxp, w), dtype=np.uint8)
+    bt = rng.permutation(n_pages)[:B * maxp].reshape(B, maxp).astype(np.int32)
+    pages = O.contiguous_to_paged(cont, bt, P, n_pages)
+    assert np.array_equal(O.paged_to_contiguous(pages, bt, P, P * maxp), cont)
+    for b in range(B):
+        for j in range(maxp):
+            assert np.array_equal(pages[bt[b, j]], cont[b, :, j * P:(j + 1) * P])
+    unused = sorted(set(range(n_pages)) - set(bt.ravel().tolist()))
+    assert all(not pages[u].any() for u in unused)

@@ -172,7 +172,11 @@ __global__ void __launch_bounds__(NW * 32, 1) stream_kernel(const __grid_constan
       const uint32_t uh = static_cast<uint32_t>(__float2int_rn((hi + 1.0f) * 32768.0f));
       reinterpret_cast<uint32_t*>(smem)[e * 32 + l] = (ul > 65535u ? 65535u : ul) | ((uh > 65535u ? 65535u : uh) << 16);
     } else {
-      reinterpret_cast<float2*>(smem)[e * 32 + l] = make_float2(lo, hi);
+      if (OPT & 0x200) {    // 16 copies at a 128-byte stride (32 KB)
+        if (l < 16) reinterpret_cast<float2*>(smem)[e * 16 + l] = make_float2(lo, hi);
+      } else {
+        reinterpret_cast<float2*>(smem)[e * 32 + l] = make_float2(lo, hi);
+      }
     }
   }
   // q-table (one per CTA: the CTA streams one sequence)
@@ -251,7 +255,8 @@ __global__ void __launch_bounds__(NW * 32, 1) stream_kernel(const __grid_constan
   uint32_t jsel[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) jsel[k] = static_cast<uint32_t>(sub * 8 + ((k + rho) & 7)) * 4u;
-  const uint32_t vsel = static_cast<uint32_t>(lane) * (V16 ? 4u : 8u);
+  const uint32_t vsel = (OPT & 0x200) ? static_cast<uint32_t>(lane & 15) * 16u
+                                      : static_cast<uint32_t>(lane) * (V16 ? 4u : 8u);
   uint64_t o2[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) o2[j] = 0;
@@ -441,8 +446,13 @@ __global__ void __launch_bounds__(NW * 32, 1) stream_kernel(const __grid_constan
       } else {
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          o2[k] = ffma2(lds_v(prmt(R.v[i].x, vsel, 0x7604 | (k << 4))), w2, o2[k]);
-          o2[4 + k] = ffma2(lds_v(prmt(R.v[i].y, vsel, 0x7604 | (k << 4))), w2, o2[4 + k]);
+          if (OPT & 0x200) {
+            o2[k] = ffma2(lds_v(prmt(R.v[i].x, vsel, 0x7604 | (k << 4)) >> 1), w2, o2[k]);
+            o2[4 + k] = ffma2(lds_v(prmt(R.v[i].y, vsel, 0x7604 | (k << 4)) >> 1), w2, o2[4 + k]);
+          } else {
+            o2[k] = ffma2(lds_v(prmt(R.v[i].x, vsel, 0x7604 | (k << 4))), w2, o2[k]);
+            o2[4 + k] = ffma2(lds_v(prmt(R.v[i].y, vsel, 0x7604 | (k << 4))), w2, o2[4 + k]);
+          }
         }
       }
     }
@@ -621,6 +631,28 @@ int main(int argc, char** argv) {
   if (getenv("SX_OLD")) {
   run<0, 16, 2, 1, 0, 1, false>("LDG D2 compute fp32 V", a, grid, bytes);
   run<0, 16, 2, 1, 0, 0, false>("LDG D2 loads only", a, grid, bytes);
+  }
+  g_pad = 0x16000;   // 216 KB of shared memory (the decode kernel's footprint)
+  for (int rep = 0; rep < 2; ++rep) {
+  const int pads[] = {0x8000, 0x16000};
+  for (int pd : pads) {
+    g_pad = pd;
+    char nm[64];
+    snprintf(nm, sizeof(nm), "LDG D2 fp32 V, %d KB smem", (0x20000 + pd) / 1024);
+    run<0, 16, 2, 1, 0, 1, false>(nm, a, grid, bytes);
+    snprintf(nm, sizeof(nm), "LDG D2 V 16 copies, %d KB smem", (0x20000 + pd) / 1024);
+    run<0, 16, 2, 1, 0, 1, false, 0x200>(nm, a, grid, bytes);
+  }
+  g_pad = 0;
+  }
+  g_pad = 0x16000;   // 216 KB of shared memory (the decode kernel's footprint)
+  for (int rep = 0; rep < 2; ++rep) {
+  g_pad = 0x16000;
+  run<0, 16, 2, 1, 0, 1, false>("LDG D2 fp32 V (current), 216 KB", a, grid, bytes);
+  g_pad = 0;
+  run<0, 16, 2, 1, 0, 1, false>("LDG D2 fp32 V (current), 128 KB", a, grid, bytes);
+  run<2, 16, 1, 2, 0, 1, false>("cp.async ring 2", a, grid, bytes);
+  run<3, 16, 1, 2, 0, 1, false>("TMA per-warp ring 2", a, grid, bytes);
   }
   g_pad = 0x16000;   // 216 KB of shared memory (the decode kernel's footprint)
   for (int rep = 0; rep < 2; ++rep) {
