@@ -510,6 +510,72 @@ def prefill_config(dev, peak_tflops, name="c4", heads=40):
                          "note": "algorithmic causal FLOPs; the fp16 hi/lo operand splits do ~2.5x that on the tensor cores"}}
 
 
+def layouts_config(dev, peak):
+    """§8(f) row 4 KV layouts at the c5 shard's shape (64 x 12 heads x 4097
+    tokens, hd 128, blk 64): decode attention launches (unplanned, back to
+    back; one layer's cache is 3.4x L2) over the contiguous cache, the same
+    rows in a paged cache of 256-token pages in shuffled order, and
+    grouped-query (48 query heads over the 12 KV heads).  Algorithmic bytes
+    count the cache once (+ q/out of every query head)."""
+    import numpy as np
+    import torch
+    from paper_2505_16210_b200 import nqkv as N
+    B, Hkv, hd, blk, T, P = 64, 12, 128, 64, 4097, 256
+    maxp = -(-T // P)
+    n_pages = B * maxp
+    Tc = maxp * P
+    g = torch.Generator(device=dev).manual_seed(0)
+    perm = np.random.default_rng(0).permutation(n_pages).reshape(B, maxp)
+    bt = torch.tensor(perm, dtype=torch.int32, device=dev)
+    ck = torch.zeros(B, Hkv, Tc, hd // 2, dtype=torch.uint8, device=dev)
+    cs = torch.zeros(B, Hkv, Tc, hd // blk, dtype=torch.float32, device=dev)
+    cv, cvs = torch.zeros_like(ck), torch.zeros_like(cs)
+    pk = torch.zeros(n_pages, Hkv, P, hd // 2, dtype=torch.uint8, device=dev)
+    ps = torch.zeros(n_pages, Hkv, P, hd // blk, dtype=torch.float32, device=dev)
+    pv, pvs = torch.zeros_like(pk), torch.zeros_like(ps)
+    lay = N.kv_layout(0, bt, P, n_pages)
+    z = torch.zeros(B, dtype=torch.int32, device=dev)
+    for codes, scales, pc, pcs in ((ck, cs, pk, ps), (cv, cvs, pv, pvs)):
+        x = torch.randn(B, T, Hkv, hd, generator=g, device=dev).half()
+        N.nqkv_quantize(x, z, codes, scales, blk)
+        N.nqkv_quantize_kv(x, z, pc, pcs, blk, lay, Tc)
+        del x
+    L = torch.full((B,), T, dtype=torch.int32, device=dev)
+    res = {}
+    cases = [("contiguous", Hkv, lambda q, ws, o: N.nqkv_decode_attention(q, ck, cs, cv, cvs, L, blk, ws, out=o)),
+             ("paged-256", Hkv, lambda q, ws, o: N.nqkv_decode_attention_kv(q, pk, ps, pv, pvs, L, blk, lay, Tc, ws, out=o)),
+             ("gqa-4", 4 * Hkv, lambda q, ws, o: N.nqkv_decode_attention_kv(q, ck, cs, cv, cvs, L, blk,
+                                                                            N.kv_layout(Hkv), Tc, ws, out=o))]
+    for name, H, call in cases:
+        q = torch.randn(B, H, hd, generator=g, device=dev).half()
+        ws = N.make_workspace(B, H, hd, Tc, dev)
+        o = torch.empty(B, H, hd, device=dev)
+        for _ in range(3):
+            call(q, ws, o)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n = 20
+        a.record()
+        for _ in range(n):
+            call(q, ws, o)
+        b.record()
+        torch.cuda.synchronize()
+        us = a.elapsed_time(b) / n * 1e3
+        nbytes = B * T * Hkv * hd * 2 * (0.5 + 4 / blk) + B * H * hd * (2 + 4)
+        res[name] = {"query_heads": H, "kv_heads": Hkv, "us_per_launch": us,
+                     "bytes_per_launch": nbytes,
+                     "decode_roofline": {"achieved": nbytes / (us * 1e-6) / 1e9, "peak": peak,
+                                         "unit": "GB/s", "frac": nbytes / (us * 1e-6) / 1e9 / peak}}
+        del q, ws, o
+    del ck, cs, cv, cvs, pk, ps, pv, pvs
+    torch.cuda.empty_cache()
+    res["workload"] = (f"c5 shard shape: B={B}, {Hkv} KV heads, hd {hd}, {T} tokens, blk {blk}; "
+                       f"paged: {P}-token pages, shuffled block table; gqa-4: 4 query heads per KV head "
+                       f"(each query head streams its KV head: KV bytes counted once)")
+    res["timing"] = "back-to-back unplanned nqkv_decode_attention(_kv) launches, CUDA events, mean of 20"
+    return res
+
+
 def run_ours(args, w, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -556,6 +622,10 @@ def run_ours(args, w, rank, world, local_rank):
             configs["prefill-c4"] = prefill_config(dev, tfp)
         except Exception as e:  # noqa: BLE001
             configs["prefill-c4"] = {"error": str(e)[:200]}
+        try:
+            configs["kv-layouts"] = layouts_config(dev, peak)
+        except Exception as e:  # noqa: BLE001
+            configs["kv-layouts"] = {"error": str(e)[:200]}
     line = {
         "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True,

@@ -1337,6 +1337,7 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
   uint32_t soff = 0;
   int nvl = 0, left = 0, lpi = 0;
   int ptok = 0;                  // PAGED: first token of the cursor's stage
+  int npa = -1;                  // PAGED: page id of the cursor's stage, read one stage early (-1: not read)
   bool lvalid = warp < NC;
   constexpr int KSTEP = NC * ST * (HD / 2), SSTEP = NC * ST * NBLK * SB;
   auto set_cursor = [&](const Piece& lp, int ls, int lro, int lns) {
@@ -1346,8 +1347,15 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
       // block-table row (in kcp) and the KV head (in soff); rows are found
       // per stage in load_stage
       ptok = ltok;
+      npa = -1;
       kcp = reinterpret_cast<const uint8_t*>(p.bt + static_cast<long long>(lp.b) * p.bt_stride);
       soff = static_cast<uint32_t>(lp.h >> p.kv_shift);
+      // the piece's page ids into L1 now: the per-stage lookups then hit L1
+      // instead of adding an L2 round trip before each stage's loads
+      if (lane < 2) {
+        const int32_t* pp = reinterpret_cast<const int32_t*>(kcp) + (ltok >> p.page_shift) + 32 * lane;
+        asm volatile("prefetch.global.L1 [%0];" :: "l"(pp));
+      }
     } else {
       const uint32_t r = static_cast<uint32_t>(rowbase(lp) + ltok + g);
       const uint32_t rs = GRP ? static_cast<uint32_t>(srowbase(lp) + ltok + g) : r;
@@ -1422,7 +1430,46 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
       const int ps = p.page_shift, pm = (1 << ps) - 1;
       const int hkv = p.H >> p.kv_shift;
       const int tend = ptok + min(ST, nvl + g) - 1;      // last row of the stage in the piece
-      const int pa = __ldg(btp + (ptok >> ps) + dep);
+      // page id of this stage: read by the previous stage's load_stage (its
+      // load completed with that stage's data), else now (after the wait)
+      const int pa = npa >= 0 ? npa : __ldg(btp + (ptok >> ps) + dep);
+      // ... and the next stage's (same piece: `left` stages to go), issued
+      // after this stage's code loads below
+      auto look_ahead = [&]() {
+        npa = left > 0 ? __ldg(btp + ((ptok + NC * ST) >> ps)) : -1;
+      };
+      if ((ptok & pm) + ST <= pm + 1) {
+        // common case: the whole stage lies in one page -- slot rows are
+        // consecutive there, as in the contiguous layout
+        const uint32_t r0 = static_cast<uint32_t>((pa * hkv + static_cast<int>(soff)) << ps) +
+                            static_cast<uint32_t>((ptok & pm) + g);
+        uint32_t s0 = r0;
+        if constexpr (GRP)
+          s0 = static_cast<uint32_t>((pa * (hkv >> p.hpb_shift) + (static_cast<int>(soff) >> p.hpb_shift)) << ps) +
+               static_cast<uint32_t>((ptok & pm) + g);
+        const uint8_t* kp = p.kc + (r0 * (HD / 2) + sub * 8);
+        const uint8_t* vp = p.vc + (r0 * (HD / 2) + sub * 8);
+        const uint32_t so = (s0 * NBLK + sidx) * SB;
+#pragma unroll
+        for (int i = 0; i < kTPS; ++i) {
+          if (i * G < nvl) {
+            Rg.k[i] = ldg_stream_64(kp + i * G * (HD / 2));
+            Rg.v[i] = ldg_stream_64(vp + i * G * (HD / 2));
+            if constexpr (!RS) {
+              Rg.ks[i] = ld_scale<F16S>(p.ks, so + i * G * NBLK * SB);
+              Rg.vs[i] = ld_scale<F16S>(p.vs, so + i * G * NBLK * SB);
+            }
+          }
+        }
+        if constexpr (RS) {
+          if ((sub & 3) * G < nvl) {
+            Rg.ks[0] = ld_scale<F16S>(p.ks, so + soff_rs);
+            Rg.vs[0] = ld_scale<F16S>(p.vs, so + soff_rs);
+          }
+        }
+        look_ahead();
+        return;
+      }
       const int pb = __ldg(btp + (max(tend, ptok) >> ps) + dep);
       auto row_of = [&](int t) -> uint32_t {
         const int pg = ((t >> ps) == (ptok >> ps)) ? pa : pb;
@@ -1457,6 +1504,7 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
           Rg.vs[0] = ld_scale<F16S>(p.vs, so);
         }
       }
+      look_ahead();
       return;
     }
     const uint8_t* vcp = kcp + vdelta;
