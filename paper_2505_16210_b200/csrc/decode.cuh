@@ -72,6 +72,9 @@ constexpr int kMinTokensPerCta = 512;  // below this a CTA's table build would d
 #ifndef NQKV_V16
 #define NQKV_V16 0               // V levels as 16-bit fixed point in a 4-byte pair LUT (see lds_v16)
 #endif
+#ifndef NQKV_R64
+#define NQKV_R64 4               // q-table ring depth at hd 64 (two tables per 64 KB block)
+#endif
 #ifndef NQKV_PF
 #define NQKV_PF 0                // bulk L2 prefetch distance in a warp's own stages (0: off; measured: no gain)
 #endif
@@ -189,7 +192,7 @@ struct Geo {
   static constexpr int LPT = HD / kLaneDims;  // lanes per token row (4 / 8)
   static constexpr int G = 32 / LPT;          // token groups per warp (8 / 4)
   static constexpr int ST = G * kTPS;         // tokens per warp stage
-  static constexpr int R = HD == 64 ? 4 : 2;  // q-table ring depth
+  static constexpr int R = HD == 64 ? NQKV_R64 : 2;  // q-table ring depth
   static constexpr int PPL = HD / 64;         // table pairs per producer lane (1 / 2)
 };
 
@@ -204,7 +207,7 @@ struct Smem {
   static constexpr int R = Geo<HD>::R;
   static constexpr uint32_t kV = 0;
   static constexpr uint32_t kK = 0x10000;
-  static constexpr uint32_t kLv = kK + 0x20000;           // float[16]
+  static constexpr uint32_t kLv = kK + (HD == 64 ? (R + 1) / 2 : R) * 0x10000u;   // float[16]
   static constexpr uint32_t kTab = kLv + 64;              // float2[kNumBuckets]
   static constexpr uint32_t kMbar = kTab + 272;           // u64 full[R], done[R]
   static constexpr uint32_t kMl = kMbar + 16 * R;         // float2 [R][NC]
