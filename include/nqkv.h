@@ -287,7 +287,7 @@ int nqkv_prefill_attention(const void* q, const uint8_t* k_codes, const void* k_
  * NQKV (multi-query / grouped attention reduce the number of
  * KV heads; PagedAttention's paged KV memory); neither
  * changes an encoded byte or the attention arithmetic, only which cache row
- * a (sequence, head, token) reads (readings R15, R16).
+ * a (sequence, head, token) reads (readings R16, R17).
  *   kv_heads       cache heads H_kv (0: = H).  Grouped-query attention: H is
  *                  a multiple of H_kv and H / H_kv a power of two; query head
  *                  h reads cache head h / (H / H_kv).  With blk > hd a block

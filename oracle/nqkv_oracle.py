@@ -238,7 +238,7 @@ def dequantize(codes: np.ndarray, scales: np.ndarray, blk: int, n_tokens: int | 
 # KV layouts orthogonal to the method
 # --------------------------------------------------------------------------
 def kv_group(h_q: int, h_kv: int) -> int:
-    """Query heads per cache head (grouped-query attention, reading R15)."""
+    """Query heads per cache head (grouped-query attention, reading R16)."""
     if h_kv <= 0 or h_q % h_kv:
         raise ValueError("the number of query heads must be a multiple of the KV heads")
     return h_q // h_kv
@@ -246,7 +246,7 @@ def kv_group(h_q: int, h_kv: int) -> int:
 
 def paged_to_contiguous(pages: np.ndarray, block_table, page_size: int, n_tokens: int) -> np.ndarray:
     """A paged cache, the layout of PagedAttention that PAPER.md:62, 103
-    calls orthogonal to NQKV (reading R16), as the contiguous one: token t
+    calls orthogonal to NQKV (reading R17), as the contiguous one: token t
     of sequence b lives in row t % P of page block_table[b][t // P];
     pages: [n_pages][H][P][w] -> [B][H][n_tokens][w] (rows the table does not
     cover are zero).  A plain gather: it does no arithmetic of the method."""
@@ -288,7 +288,7 @@ def decode_attention(q: np.ndarray, k_codes, k_scales, v_codes, v_scales, seq_le
     >= seq_lens[b] are not part of the sequence.  seq_lens[b] == 0 -> zeros
     (reading R12).  Computed in float64 over the fp32 dequantised values.
 
-    Grouped-query layout (reading R15): the cache may hold fewer
+    Grouped-query layout (reading R16): the cache may hold fewer
     heads than q (H_kv | H); query head h reads cache head h // (H / H_kv),
     consecutive query heads sharing one KV head (the multi-query / grouped
     attention the paper names as orthogonal to NQKV).

@@ -104,7 +104,7 @@ struct DecodeParams {
   const int* plan;             // optional per-step schedule (nqkv_decode_plan); nullptr: computed here
   int early;                   // NQKV_EARLY_START: plan and cache readable before the PDL wait
   int hpb_shift;               // blk > hd: scale rows [B][H >> hpb_shift][Tc] (blk_shift = log2 hd)
-  // KV layouts (readings R15, R16):
+  // KV layouts (readings R16, R17):
   int kv_shift;                // grouped-query: query head h reads cache head h >> kv_shift
   const int32_t* bt;           // paged cache (kernel template PAGED): block table [B][bt_stride];
   int bt_stride, page_shift;   // token t of sequence b: page bt[b][t >> page_shift], row t & (P - 1)
@@ -1287,7 +1287,7 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
     return walk_next_ws(*s_ws, s_len, p.H, g1, pc, k);
   };
   auto nstages = [&](const Piece& pc) { return (pc.t1 - pc.t0 + ST - 1) / ST; };
-  // cache rows of a piece: its KV head (query head h >> kv_shift, R15)
+  // cache rows of a piece: its KV head (query head h >> kv_shift, R16)
   auto kvhead = [&](const Piece& pc) { return pc.b * (p.H >> p.kv_shift) + (pc.h >> p.kv_shift); };
   auto rowbase = [&](const Piece& pc) { return kvhead(pc) * p.Tc; };
   // scale row base: the head group's row when a block spans heads (blk > hd)
@@ -1346,7 +1346,7 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
   auto set_cursor = [&](const Piece& lp, int ls, int lro, int lns) {
     const int ltok = lp.t0 + ls * ST;
     if constexpr (PAGED) {
-      // paged cache (R16): the cursor keeps the token, the sequence's
+      // paged cache (R17): the cursor keeps the token, the sequence's
       // block-table row (in kcp) and the KV head (in soff); rows are found
       // per stage in load_stage
       ptok = ltok;

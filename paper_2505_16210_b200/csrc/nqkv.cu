@@ -182,7 +182,7 @@ int launch_decode_g(const DecodeParams& p, cudaStream_t st) {
   }
 }
 
-// paged cache (reading R16): fp32 scales, no fused gather
+// paged cache (reading R17): fp32 scales, no fused gather
 template <int HD>
 int launch_decode_paged(const DecodeParams& p, cudaStream_t st) {
   if (p.hpb_shift) return launch_decode_blk<HD, HD, false, true, false, true>(p, st);
@@ -205,7 +205,7 @@ int launch_decode(const DecodeParams& p, cudaStream_t st) {
 }
 
 // KV layout of a call (nqkv_kv_layout, validated): grouped-query head
-// mapping (R15) and the paged cache (R16)
+// mapping (R16) and the paged cache (R17)
 struct KvLayout {
   int kv_shift = 0;
   const int32_t* bt = nullptr;

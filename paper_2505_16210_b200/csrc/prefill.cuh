@@ -34,7 +34,7 @@ struct PrefillParams {
   int B, H, T, Tc, blk_shift, hpb_shift;
   float scale_log2;          // softmax_scale * log2(e)
   Levels lv;
-  // KV layouts (tcgen05 kernel; readings R15, R16): query head h
+  // KV layouts (tcgen05 kernel; readings R16, R17): query head h
   // reads cache head h >> kv_shift; paged cache: key t of sequence b is row
   // t & (P - 1) of page bt[b][t >> page_shift] in [n_pages][H_kv][P] storage
   int kv_shift;

@@ -385,7 +385,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) prefill_tc_kernel(const __grid_
     };
     auto load = [&](const uint8_t* codes, const void* scales, int k0, Raw& r, int dep) {
       long long rb = row_base + k0, srb = srow_base + k0;
-      if (p.bt && k0 < len) {     // paged (R16): a 64-key tile lies in one page (P >= 64)
+      if (p.bt && k0 < len) {     // paged (R17): a 64-key tile lies in one page (P >= 64)
         const long long pg = __ldg(p.bt + static_cast<long long>(b) * p.bt_stride + (k0 >> p.page_shift));
         const int within = k0 & ((1 << p.page_shift) - 1);
         rb = ((pg * hkv + kvh) << p.page_shift) + within;

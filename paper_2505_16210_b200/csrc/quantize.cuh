@@ -20,7 +20,7 @@ struct QuantParams {
   FastDiv cpr;                   // chunks per token row (b, t): H * hd / 16
   FastDiv nnew;                  // n_new
   BucketTab tab;
-  // paged cache (reading R16): row pos of sequence b is row
+  // paged cache (reading R17): row pos of sequence b is row
   // pos & (P - 1) of page bt[b][pos >> page_shift] in [n_pages][H][P] storage
   const int32_t* bt;             // nullptr: contiguous [B][H][Tc]
   int bt_stride, page_shift;
@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(256, 4) quantize_kernel(const __grid_constant_
     const int pos = __ldg(p.pos + bb) + static_cast<int>(t);
     if (pos < 0 || pos >= p.Tc) return;
     const uint32_t h = within >> LOG_CPT, cr = within & (CPT - 1);
-    // row of (b, h, pos): contiguous, or in its page (R16)
+    // row of (b, h, pos): contiguous, or in its page (R17)
     long long base = static_cast<long long>(bb), rowin = pos, rows = p.Tc;
     if (p.bt) {
       base = __ldg(p.bt + static_cast<long long>(bb) * p.bt_stride + (pos >> p.page_shift));

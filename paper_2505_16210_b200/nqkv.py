@@ -28,7 +28,7 @@ _fp = ctypes.POINTER(ctypes.c_float)
 
 class KvLayout(ctypes.Structure):
     """nqkv_kv_layout (include/nqkv.h): grouped-query head mapping and the
-    paged cache (readings R15, R16)."""
+    paged cache (readings R16, R17)."""
     _fields_ = [("kv_heads", ctypes.c_int), ("block_table", ctypes.c_void_p),
                 ("pages_per_seq", ctypes.c_int), ("page_size", ctypes.c_int),
                 ("n_pages", ctypes.c_int)]

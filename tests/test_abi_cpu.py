@@ -192,7 +192,7 @@ def _dkv(lay, **kw):
 
 
 def test_kv_layout_argument_errors():
-    # grouped-query (R15) and paged (R16) layouts: host-checkable errors, no launch
+    # grouped-query (R16) and paged (R17) layouts: host-checkable errors, no launch
     L = N.KvLayout
     assert _dkv(None) == -1
     assert _dkv(L(3, None, 0, 0, 0)) == -2            # 8 query heads over 3 KV heads

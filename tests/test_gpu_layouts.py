@@ -1,4 +1,4 @@
-"""KV layouts on the GPU (readings R15, R16):
+"""KV layouts on the GPU (readings R16, R17):
 grouped-query head mapping and the paged cache, through the C ABI's *_kv
 calls.  Bars as everywhere: codes and scales bit-exact against the oracle,
 attention within 2e-3 of the float64 oracle; and, because a layout only

@@ -673,7 +673,7 @@ def test_prefill_rows_equal_decode_steps():
 
 # ------------------------------------------- KV layouts --
 def test_gqa_is_mha_over_repeated_kv_heads():
-    # reading R15: query head h reads KV head h // g.  Pinned to
+    # reading R16: query head h reads KV head h // g.  Pinned to
     # the (separately pinned) MHA oracle on a cache whose heads are repeated
     # g times -- a mapping h % H_kv or a wrong group size fails this.
     rng = np.random.default_rng(31)
@@ -711,7 +711,7 @@ def test_gqa_single_token_closed_form():
 
 
 def test_paged_layout_identity_table_is_a_reshape():
-    # reading R16: with block_table[b][j] = b * maxp + j the paged cache is the
+    # reading R17: with block_table[b][j] = b * maxp + j the paged cache is the
     # contiguous one cut into pages: a numpy reshape/transpose, independent of
     # the oracle's per-token gather
     rng = np.random.default_rng(33)
