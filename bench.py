@@ -276,7 +276,7 @@ def measure(args, w, heads, dev, world, group, layers=None, steps=None, warmup=N
     q_ms = runner.prefill(flush=flush)
     T = int(runner.lens0.max())
     elems = w.batch * T * runner.Hl * w.head_dim
-    q_bytes = elems * (2 + 0.5 + 4.0 / w.blk)
+    q_bytes = 2 * elems * (2 + 0.5 + 4.0 / w.blk)      # K and V: one nqkv_quantize_pair launch
     q_gbs = [q_bytes / (t * 1e-3) / 1e9 for t in q_ms]
     del flush
     torch.cuda.synchronize()
@@ -658,7 +658,7 @@ def run_ours(args, w, rank, world, local_rank):
                                         "timed graphs carry none)"},
         "quantize_roofline": {"bound": "hbm", "achieved": r["quantize_gbs"], "peak": peak,
                               "unit": "GB/s", "frac": r["quantize_gbs"] / peak, "traffic": q_traffic,
-                              "kernel": "quantize_kernel (nqkv_quantize, bulk prefill, L2 flushed)",
+                              "kernel": "quantize_kernel (nqkv_quantize_pair: a layer's K and V per launch, bulk prefill, L2 flushed)",
                               "bytes_per_launch": r["quantize_bytes_per_launch"],
                               "launches": r["quantize_launches"]},
         "cpu_baseline": cpu,

@@ -283,6 +283,16 @@ int nqkv_prefill_attention(const void* q, const uint8_t* k_codes, const void* k_
                            int B, int H, int hd, int blk, int Tc, int T, float softmax_scale,
                            float* out, void* stream);
 
+/* K and V of a layer in ONE launch (the fused K+V variant SURVEY.md 8(b)
+ * allows): exactly nqkv_quantize(x_k -> k_codes/k_scales) followed by
+ * nqkv_quantize(x_v -> v_codes/v_scales), same strides, geometry and d_pos
+ * for both, with half the launches (one ramp-up and tail per layer).  Errors
+ * as nqkv_quantize; x_k and x_v must agree modulo 32 bytes. */
+int nqkv_quantize_pair(const void* x_k, const void* x_v, int64_t stride_b, int64_t stride_t,
+                       int64_t stride_h, int B, int H, int hd, int n_new, int blk,
+                       const int32_t* d_pos, int Tc, uint8_t* k_codes, void* k_scales,
+                       uint8_t* v_codes, void* v_scales, void* stream);
+
 /* KV layouts.  The paper calls both orthogonal to
  * NQKV (multi-query / grouped attention reduce the number of
  * KV heads; PagedAttention's paged KV memory); neither

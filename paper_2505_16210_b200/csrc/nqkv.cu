@@ -416,8 +416,12 @@ int nqkv_thresholds(float thresholds[15]) {
 
 static int quantize_common(const void* x, int64_t stride_b, int64_t stride_t, int64_t stride_h,
                            int B, int H, int hd, int n_new, int blk, const int32_t* d_pos, int Tc,
-                           uint8_t* codes, void* scales, void* stream, const nqkv_kv_layout* kv) {
+                           uint8_t* codes, void* scales, void* stream, const nqkv_kv_layout* kv,
+                           const void* x2 = nullptr, uint8_t* codes2 = nullptr,
+                           void* scales2 = nullptr) {
   if (!x || !d_pos || !codes || !scales) return NQKV_ERR_NULL;
+  const bool pair = x2 != nullptr;
+  if (pair && (!codes2 || !scales2)) return NQKV_ERR_NULL;
   if (int s = check_geometry(hd, blk)) return s;
   const bool f16s = f16s_of(blk);
   blk = blk_of(blk);
@@ -430,10 +434,14 @@ static int quantize_common(const void* x, int64_t stride_b, int64_t stride_t, in
   if (!aligned16(x) || !aligned16(codes) || !scale_aligned(scales, f16s) ||
       (stride_b % 8) || (stride_t % 8) || (stride_h % 8))
     return NQKV_ERR_ALIGN;
+  if (pair && (!aligned16(x2) || !aligned16(codes2) || !scale_aligned(scales2, f16s) ||
+               ((reinterpret_cast<uintptr_t>(x) ^ reinterpret_cast<uintptr_t>(x2)) & 31u)))
+    return NQKV_ERR_ALIGN;                   // both tensors take the same load width
   if (tables_status() != 0) return NQKV_ERR_INTERNAL;
   const long long rows = static_cast<long long>(B) * n_new;   // token rows (b, t)
   if (rows == 0 || H == 0) return NQKV_OK;
-  const long long chunks = rows * H * (hd / 16);               // 16-element chunks
+  const long long chunks1 = rows * H * (hd / 16);              // 16-element chunks per tensor
+  const long long chunks = pair ? 2 * chunks1 : chunks1;
   if (chunks >= (1ll << 31)) return NQKV_ERR_SHAPE;
   QuantParams p;
   p.x = static_cast<const __half*>(x);
@@ -443,6 +451,10 @@ static int quantize_common(const void* x, int64_t stride_b, int64_t stride_t, in
   p.blk_shift = blk_shift_of(blk);
   p.hpb_shift = hpb_shift_of(hd, blk);
   p.total = static_cast<uint32_t>(chunks);
+  p.total1 = static_cast<uint32_t>(chunks1);
+  p.x2 = static_cast<const __half*>(x2);
+  p.codes2 = codes2;
+  p.scales2 = scales2;
   p.v256 = ((reinterpret_cast<uintptr_t>(x) & 31u) == 0 && stride_b % 16 == 0 && stride_t % 16 == 0 &&
             stride_h % 16 == 0) ? 1 : 0;
   if (stride_h == hd && stride_t == static_cast<int64_t>(H) * hd &&
@@ -462,17 +474,23 @@ static int quantize_common(const void* x, int64_t stride_b, int64_t stride_t, in
   const dim3 grid(static_cast<unsigned>(grid_for((chunks + 1) / 2, 256, NQKV_Q_CTAS_PER_SM)));
   cudaError_t e;
   const size_t sm = kQuantSmem;
-  auto launch = [&](auto f16s_tag) {
+  auto launch_l = [&](auto f16s_tag, auto lay_tag) {
     constexpr bool F = decltype(f16s_tag)::value;
+    constexpr int Y = decltype(lay_tag)::value;
     if (hd == 64)
-      return blk == 32    ? launch_pdl(quantize_kernel<64, 32, F>, grid, dim3(256), sm, st, p)
-             : blk == 64  ? launch_pdl(quantize_kernel<64, 64, F>, grid, dim3(256), sm, st, p)
-             : blk == 128 ? launch_pdl(quantize_kernel<64, 128, F>, grid, dim3(256), sm, st, p)
-                          : launch_pdl(quantize_kernel<64, 256, F>, grid, dim3(256), sm, st, p);
-    return blk == 32    ? launch_pdl(quantize_kernel<128, 32, F>, grid, dim3(256), sm, st, p)
-           : blk == 64  ? launch_pdl(quantize_kernel<128, 64, F>, grid, dim3(256), sm, st, p)
-           : blk == 128 ? launch_pdl(quantize_kernel<128, 128, F>, grid, dim3(256), sm, st, p)
-                        : launch_pdl(quantize_kernel<128, 256, F>, grid, dim3(256), sm, st, p);
+      return blk == 32    ? launch_pdl(quantize_kernel<64, 32, F, Y>, grid, dim3(256), sm, st, p)
+             : blk == 64  ? launch_pdl(quantize_kernel<64, 64, F, Y>, grid, dim3(256), sm, st, p)
+             : blk == 128 ? launch_pdl(quantize_kernel<64, 128, F, Y>, grid, dim3(256), sm, st, p)
+                          : launch_pdl(quantize_kernel<64, 256, F, Y>, grid, dim3(256), sm, st, p);
+    return blk == 32    ? launch_pdl(quantize_kernel<128, 32, F, Y>, grid, dim3(256), sm, st, p)
+           : blk == 64  ? launch_pdl(quantize_kernel<128, 64, F, Y>, grid, dim3(256), sm, st, p)
+           : blk == 128 ? launch_pdl(quantize_kernel<128, 128, F, Y>, grid, dim3(256), sm, st, p)
+                        : launch_pdl(quantize_kernel<128, 256, F, Y>, grid, dim3(256), sm, st, p);
+  };
+  auto launch = [&](auto f16s_tag) {
+    if (pair) return launch_l(f16s_tag, std::integral_constant<int, 1>{});
+    if (lay.bt) return launch_l(f16s_tag, std::integral_constant<int, 2>{});
+    return launch_l(f16s_tag, std::integral_constant<int, 0>{});
   };
   e = f16s ? launch(std::true_type{}) : launch(std::false_type{});
   return e == cudaSuccess ? NQKV_OK : cuda_fail(e);
@@ -483,6 +501,15 @@ int nqkv_quantize(const void* x, int64_t stride_b, int64_t stride_t, int64_t str
                   uint8_t* codes, void* scales, void* stream) {
   return quantize_common(x, stride_b, stride_t, stride_h, B, H, hd, n_new, blk, d_pos, Tc, codes,
                          scales, stream, nullptr);
+}
+
+int nqkv_quantize_pair(const void* x_k, const void* x_v, int64_t stride_b, int64_t stride_t,
+                       int64_t stride_h, int B, int H, int hd, int n_new, int blk,
+                       const int32_t* d_pos, int Tc, uint8_t* k_codes, void* k_scales,
+                       uint8_t* v_codes, void* v_scales, void* stream) {
+  if (!x_v) return NQKV_ERR_NULL;
+  return quantize_common(x_k, stride_b, stride_t, stride_h, B, H, hd, n_new, blk, d_pos, Tc, k_codes,
+                         k_scales, stream, nullptr, x_v, v_codes, v_scales);
 }
 
 int nqkv_quantize_kv(const void* x, int64_t stride_b, int64_t stride_t, int64_t stride_h, int B,

@@ -14,7 +14,13 @@ struct QuantParams {
   void* scales;                  // fp32, or fp16 (template F16S; exact for fp16 inputs)
   int B, n_new, H, Tc, blk_shift;
   int hpb_shift;                 // blk > hd: a block spans 2^hpb_shift heads
-  uint32_t total;                // 16-element chunks: B * n_new * H * hd / 16
+  uint32_t total;                // 16-element chunks: B * n_new * H * hd / 16 (x2 two tensors)
+  // fused K + V call (nqkv_quantize_pair): chunks [total1, total) are the
+  // second tensor's (x2 -> codes2 / scales2, same strides and geometry)
+  uint32_t total1;
+  const __half* x2;
+  uint8_t* codes2;
+  void* scales2;
   int v256;                      // bit 0: x and strides 32-byte aligned (256-bit loads);
                                  // bit 1: x contiguous [B][n_new][H][hd]
   FastDiv cpr;                   // chunks per token row (b, t): H * hd / 16
@@ -113,7 +119,10 @@ __device__ __forceinline__ float absmax16(const uint4 a, const uint4 b) {
 // blk = 32).  Units are strided over the warps of the grid; the next unit's
 // loads are issued before the current one is encoded (ping-pong registers).
 // When x is contiguous ([B][n_new][H][hd] packed), chunk c starts at x + 16c.
-template <int HD, int BLK, bool F16S>
+// LAYOUT: 0 one tensor, contiguous cache; 1 K and V pair (nqkv_quantize_pair);
+// 2 one tensor into a paged cache (nqkv_quantize_kv; R17).  Separate
+// instantiations: the plain kernel carries no layout code.
+template <int HD, int BLK, bool F16S, int LAYOUT = 0>
 __global__ void __launch_bounds__(256, 4) quantize_kernel(const __grid_constant__ QuantParams p) {
   constexpr int CPT = HD / 16;                 // chunks per (token, head)
   constexpr int LOG_CPT = CPT == 4 ? 2 : 3;
@@ -129,18 +138,23 @@ __global__ void __launch_bounds__(256, 4) quantize_kernel(const __grid_constant_
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
   const int nblk = HD >> p.blk_shift;
   const bool contig = p.v256 > 1;
-  auto src_of = [&](uint32_t c) -> const __half* {
-    if (contig) return p.x + static_cast<unsigned long long>(c) * 16u;
+  // chunk c of the call -> (tensor, chunk within it); a lane's two chunks
+  // and a block never straddle the tensors (total1 is a multiple of a row)
+  auto src_of = [&](const __half* x, uint32_t c) -> const __half* {
+    if (contig) return x + static_cast<unsigned long long>(c) * 16u;
     const uint32_t row = fdiv(c, p.cpr), within = c - row * p.cpr.d;
     const uint32_t b = fdiv(row, p.nnew), t = row - b * p.nnew.d;
-    return p.x + b * p.sb + t * p.st + (within >> LOG_CPT) * p.sh + (within & (CPT - 1)) * 16;
+    return x + b * p.sb + t * p.st + (within >> LOG_CPT) * p.sh + (within & (CPT - 1)) * 16;
   };
   struct Buf { uint4 v[4]; };
   auto load = [&](uint32_t unit, Buf& B, uint32_t dep) {
-    const uint32_t c = unit * 64u + 2u * lane + dep;
+    uint32_t c = unit * 64u + 2u * lane + dep;
     if (c < p.total) {
-      const __half* s0 = src_of(c);
-      const __half* s1 = contig ? s0 + 16 : src_of(c + 1);
+      const bool sec = LAYOUT == 1 && c >= p.total1;
+      const __half* x = sec ? p.x2 : p.x;
+      if (sec) c -= p.total1;
+      const __half* s0 = src_of(x, c);
+      const __half* s1 = contig ? s0 + 16 : src_of(x, c + 1);
       if (p.v256 & 1) {
         ldg_stream_256(s0, B.v[0], B.v[1]);
         ldg_stream_256(s1, B.v[2], B.v[3]);
@@ -156,6 +170,10 @@ __global__ void __launch_bounds__(256, 4) quantize_kernel(const __grid_constant_
   // row: one 16-byte store of both code words, and the block scale (both
   // chunks share a block: blk >= 32) by the block's first lane
   auto store_pair = [&](uint32_t c, uint4 words, float s, bool scale_writer) {
+    const bool sec = LAYOUT == 1 && c >= p.total1;
+    uint8_t* const codes = sec ? p.codes2 : p.codes;
+    void* const scales = sec ? p.scales2 : p.scales;
+    if (sec) c -= p.total1;
     const uint32_t row = fdiv(c, p.cpr), within = c - row * p.cpr.d;
     const uint32_t bb = fdiv(row, p.nnew), t = row - bb * p.nnew.d;
     const int pos = __ldg(p.pos + bb) + static_cast<int>(t);
@@ -163,21 +181,21 @@ __global__ void __launch_bounds__(256, 4) quantize_kernel(const __grid_constant_
     const uint32_t h = within >> LOG_CPT, cr = within & (CPT - 1);
     // row of (b, h, pos): contiguous, or in its page (R17)
     long long base = static_cast<long long>(bb), rowin = pos, rows = p.Tc;
-    if (p.bt) {
+    if (LAYOUT == 2) {
       base = __ldg(p.bt + static_cast<long long>(bb) * p.bt_stride + (pos >> p.page_shift));
       rowin = pos & ((1 << p.page_shift) - 1);
       rows = 1ll << p.page_shift;
     }
     const long long rr = (base * p.H + h) * rows + rowin;
-    *reinterpret_cast<uint4*>(p.codes + rr * (HD / 2) + cr * 8) = words;
+    *reinterpret_cast<uint4*>(codes + rr * (HD / 2) + cr * 8) = words;
     if (scale_writer) {
       // blk > hd: one scale per (token, head group): [B][H >> hpb_shift][Tc]
       const long long si = BLK > HD ? ((base * p.H + h) >> p.hpb_shift) * rows + rowin
                                     : rr * nblk + ((cr * 16) >> p.blk_shift);
       if constexpr (F16S)
-        reinterpret_cast<__half*>(p.scales)[si] = __float2half_rn(s);   // exact: s is an fp16 value
+        reinterpret_cast<__half*>(scales)[si] = __float2half_rn(s);   // exact: s is an fp16 value
       else
-        reinterpret_cast<float*>(p.scales)[si] = s;
+        reinterpret_cast<float*>(scales)[si] = s;
     }
   };
   auto encode = [&](uint32_t unit, const Buf& B) {

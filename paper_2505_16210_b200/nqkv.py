@@ -71,6 +71,8 @@ _SIGS = {
                                         _lp, ctypes.c_float, _vp, _vp, _sz, _vp]),
     "nqkv_prefill_attention_kv": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32,
                                          _i32, _lp, ctypes.c_float, _vp, _vp]),
+    "nqkv_quantize_pair": (_i32, [_vp, _vp, _i64, _i64, _i64, _i32, _i32, _i32, _i32, _i32, _vp, _i32,
+                                  _vp, _vp, _vp, _vp, _vp]),
     "nqkv_quantize_kv": (_i32, [_vp, _i64, _i64, _i64, _i32, _i32, _i32, _i32, _i32, _vp, _i32, _lp,
                                 _vp, _vp, _vp]),
 }
@@ -160,6 +162,22 @@ def nqkv_quantize(x: torch.Tensor, pos: torch.Tensor, codes: torch.Tensor, scale
                               _blkarg(blk, scales),
                               _ptr(pos), Tc, _ptr(codes), _ptr(scales), _stream(stream)),
            "nqkv_quantize")
+
+
+def nqkv_quantize_pair(k: torch.Tensor, v: torch.Tensor, pos: torch.Tensor, k_codes: torch.Tensor,
+                       k_scales: torch.Tensor, v_codes: torch.Tensor, v_scales: torch.Tensor,
+                       blk: int, stream=None) -> None:
+    """K and V of a layer appended in one launch (= two nqkv_quantize calls)."""
+    B, n_new, H, hd = k.shape
+    Tc = k_codes.shape[2]
+    assert v.shape == k.shape and v.stride() == k.stride() and k.dtype == v.dtype == torch.float16
+    assert k.stride(3) == 1 and pos.dtype == torch.int32
+    for c, s in ((k_codes, k_scales), (v_codes, v_scales)):
+        assert c.dtype == torch.uint8 and c.is_contiguous() and s.is_contiguous() and tuple(c.shape[:2]) == (B, H)
+    _check(_lib.nqkv_quantize_pair(_ptr(k), _ptr(v), k.stride(0), k.stride(1), k.stride(2), B, H, hd,
+                                   n_new, _blkarg(blk, k_scales, v_scales), _ptr(pos), Tc,
+                                   _ptr(k_codes), _ptr(k_scales), _ptr(v_codes), _ptr(v_scales),
+                                   _stream(stream)), "nqkv_quantize_pair")
 
 
 def nqkv_dequantize(codes: torch.Tensor, scales: torch.Tensor, blk: int, n_tokens: int | None = None,
@@ -446,8 +464,12 @@ class KVCache:
         self.v_scales = torch.zeros_like(self.k_scales)
 
     def append(self, k: torch.Tensor, v: torch.Tensor, pos: torch.Tensor, stream=None) -> None:
-        nqkv_quantize(k, pos, self.k_codes, self.k_scales, self.blk, stream)
-        nqkv_quantize(v, pos, self.v_codes, self.v_scales, self.blk, stream)
+        if k.stride() == v.stride() and (k.data_ptr() - v.data_ptr()) % 32 == 0:
+            nqkv_quantize_pair(k, v, pos, self.k_codes, self.k_scales, self.v_codes, self.v_scales,
+                               self.blk, stream)       # one launch for K and V
+        else:
+            nqkv_quantize(k, pos, self.k_codes, self.k_scales, self.blk, stream)
+            nqkv_quantize(v, pos, self.v_codes, self.v_scales, self.blk, stream)
 
     def attend(self, q: torch.Tensor, seq_lens: torch.Tensor, workspace: torch.Tensor,
                out: torch.Tensor | None = None, stream=None) -> torch.Tensor:

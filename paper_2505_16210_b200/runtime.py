@@ -142,15 +142,14 @@ class DecodeRunner:
         for l, c in enumerate(self.caches):
             K, V = W.layer_kv(self.w, l, heads=self.heads, tokens=T, device=self.gen_dev)
             K, V = K.to(self.dev), V.to(self.dev)
-            for x, codes, scales in ((K, c.k_codes, c.k_scales), (V, c.v_codes, c.v_scales)):
-                if flush is not None:
-                    flush.sum()         # read-only L2 sweep: evicts without dirty write-backs
-                e0 = torch.cuda.Event(enable_timing=True)
-                e1 = torch.cuda.Event(enable_timing=True)
-                e0.record()
-                N.nqkv_quantize(x, zero, codes, scales, self.blk)
-                e1.record()
-                times.append((e0, e1))
+            if flush is not None:
+                flush.sum()             # read-only L2 sweep: evicts without dirty write-backs
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            c.append(K, V, zero)        # K and V of the layer: one nqkv_quantize_pair launch
+            e1.record()
+            times.append((e0, e1))
             del K, V
         torch.cuda.synchronize()
         return [a.elapsed_time(b) for a, b in times]

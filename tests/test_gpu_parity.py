@@ -1024,3 +1024,37 @@ def test_prefill_attention_config_prompt_sampled(N, cfg):
             ref = O.decode_attention(qn[b:b + 1, i], kc[b:b + 1], ks[b:b + 1], vc[b:b + 1], vs[b:b + 1], [i + 1], w.blk)
             assert np.max(np.abs(on[b, i] - ref[0])) <= ATOL, (b, i)
         assert np.all(on[b, n:] == 0)
+
+
+@pytest.mark.parametrize("hd,blk", [(64, 32), (64, 256), (128, 64), (128, 128)])
+def test_quantize_pair_equals_two_calls_and_oracle(N, hd, blk):
+    """nqkv_quantize_pair (K and V in one launch) writes exactly what two
+    nqkv_quantize calls write, bit for bit, and what the oracle writes;
+    strided inputs, a row count that is not a multiple of the 64-chunk unit."""
+    hpb = _hpb(hd, blk)
+    B, T, H = 3, 37, 2 * hpb
+    Tc = 64
+    kv = _rand_kv(B, T, 2 * H, hd, seed=hd * blk)         # K and V interleaved by head: strided views
+    k, v = kv[:, :, :H], kv[:, :, H:]
+    pos = torch.tensor([0, 5, 27], dtype=torch.int32, device=DEV)
+    shape = N.scales_shape(B, H, Tc, hd, blk)
+    outs = []
+    for pair in (True, False):
+        kc = torch.zeros(B, H, Tc, hd // 2, dtype=torch.uint8, device=DEV)
+        vc = torch.zeros_like(kc)
+        ks = torch.zeros(shape, dtype=torch.float32, device=DEV)
+        vs = torch.zeros_like(ks)
+        kd, vd = kv.to(DEV)[:, :, :H], kv.to(DEV)[:, :, H:]
+        if pair:
+            N.nqkv_quantize_pair(kd, vd, pos, kc, ks, vc, vs, blk)
+        else:
+            N.nqkv_quantize(kd, pos, kc, ks, blk)
+            N.nqkv_quantize(vd, pos, vc, vs, blk)
+        torch.cuda.synchronize()
+        outs.append([t.cpu().numpy() for t in (kc, ks, vc, vs)])
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
+    okc, oks = _oracle_cache(k.contiguous(), pos.tolist(), blk, Tc)
+    ovc, ovs = _oracle_cache(v.contiguous(), pos.tolist(), blk, Tc)
+    for a, b in zip(outs[0], (okc, oks, ovc, ovs)):
+        assert np.array_equal(a, b)
