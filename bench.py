@@ -515,8 +515,9 @@ def layouts_config(dev, peak):
     tokens, hd 128, blk 64): decode attention launches (unplanned, back to
     back; one layer's cache is 3.4x L2) over the contiguous cache, the same
     rows in a paged cache of 256-token pages in shuffled order, and
-    grouped-query (48 query heads over the 12 KV heads).  Algorithmic bytes
-    count the cache once (+ q/out of every query head)."""
+    grouped-query (48 query heads over the 12 KV heads; the group-native
+    kernel, decode_gqa.cuh).  Algorithmic bytes count the cache once (+ q/out
+    of every query head)."""
     import numpy as np
     import torch
     from paper_2505_16210_b200 import nqkv as N
@@ -571,7 +572,8 @@ def layouts_config(dev, peak):
     torch.cuda.empty_cache()
     res["workload"] = (f"c5 shard shape: B={B}, {Hkv} KV heads, hd {hd}, {T} tokens, blk {blk}; "
                        f"paged: {P}-token pages, shuffled block table; gqa-4: 4 query heads per KV head "
-                       f"(each query head streams its KV head: KV bytes counted once)")
+                       f"(group-native kernel: each KV head streamed once for its 4 query heads; "
+                       f"KV bytes counted once)")
     res["timing"] = "back-to-back unplanned nqkv_decode_attention(_kv) launches, CUDA events, mean of 20"
     return res
 

@@ -26,6 +26,7 @@
 #include "../../include/nqkv.h"
 #include "common.cuh"
 #include "decode.cuh"
+#include "decode_gqa.cuh"
 #include "nqkv_internal.h"
 #include "quantize.cuh"
 #include "prefill.cuh"
@@ -253,16 +254,111 @@ size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 // workspace: [B*H] int arrival counters (zero between launches) | partials
 // [kMaxGrid][2][hd + 2] fp32
 struct WsLayout {
-  size_t cnt, part, gctr, total;
+  size_t cnt, part, gctr, gqa, total;
+  long long gqa_records;
 };
+
+// grouped-query kernel (decode_gqa.cuh): chunk partials of (hd + 2) floats
+long long gqa_records_of(long long B, long long H) {
+  const long long r = B * H * kGqaMaxChunkCap;
+  return r < kGqaMaxRecords ? r : kGqaMaxRecords;
+}
 
 WsLayout ws_layout(long long B, long long H, int hd) {
   WsLayout w;
   w.cnt = 0;
   w.part = align_up(static_cast<size_t>(B * H) * sizeof(int), 256);
   w.gctr = align_up(w.part + static_cast<size_t>(kMaxGrid) * 2 * (hd + 2) * sizeof(unsigned long long), 256);
-  w.total = w.gctr + 256;       // [0]: gather CTA-completion counter (zero between calls)
+  w.gqa = w.gctr + 256;         // gctr[0]: gather CTA-completion counter (zero between calls)
+  w.gqa_records = gqa_records_of(B, H);
+  w.total = align_up(w.gqa + static_cast<size_t>(w.gqa_records) * (hd + 2) * sizeof(float), 256);
   return w;
+}
+
+bool gqa_native_enabled() {     // NQKV_GQA_NATIVE=0: GQA through the per-query-head MHA kernel
+  static const bool on = [] {
+    const char* e = std::getenv("NQKV_GQA_NATIVE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+template <int HD, int GN, bool PAGED>
+int launch_gqa_t(const GqaParams& p, long long items, cudaStream_t st) {
+  auto kern = gqa_decode_kernel<HD, GN, PAGED>;
+  constexpr size_t smem = gqa_smem_bytes<HD, GN>();
+  static bool attr_set = false;
+  static std::mutex mu;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (!attr_set) {
+      const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 static_cast<int>(smem));
+      if (e != cudaSuccess) return cuda_fail(e);
+      attr_set = true;
+    }
+  }
+  const cudaError_t e = launch_pdl(kern, dim3(static_cast<unsigned>(items)), dim3(kGqaWarps * 32),
+                                   smem, st, p);
+  return e == cudaSuccess ? NQKV_OK : cuda_fail(e);
+}
+
+// chunks per (b, kv head, sub-group): the count whose CTA waves fill the last
+// wave best (3 CTAs per SM), chunks of >= 256 tokens of capacity, within the
+// workspace's partial records
+int gqa_chunks(long long groups, long long B, long long H, int Tc) {
+  const long long slots = static_cast<long long>(device_sms()) * kGqaCtasPerSm;
+  long long ncmax = gqa_records_of(B, H) / (B * H);
+  if (ncmax > kGqaMaxChunkCap) ncmax = kGqaMaxChunkCap;
+  int best = 1;
+  double best_eff = -1.0;
+  for (int n = 1; n <= ncmax; ++n) {
+    if (n > 1 && Tc / n < 256) break;
+    const double waves = static_cast<double>(groups * n) / static_cast<double>(slots);
+    const double eff = waves / std::ceil(waves);
+    if (eff > best_eff + 0.02) {
+      best_eff = eff;
+      best = n;
+    }
+  }
+  return best;
+}
+
+template <bool PAGED>
+int launch_gqa_p(const GqaParams& p, int hd, int GN, long long items, cudaStream_t st) {
+  if (hd == 64)
+    return GN == 4 ? launch_gqa_t<64, 4, PAGED>(p, items, st) : launch_gqa_t<64, 2, PAGED>(p, items, st);
+  return GN == 4 ? launch_gqa_t<128, 4, PAGED>(p, items, st) : launch_gqa_t<128, 2, PAGED>(p, items, st);
+}
+
+int launch_gqa(const DecodeParams& dp, int H_kv, int hd, int blk, float* part, long long records,
+               cudaStream_t st) {
+  const int g = 1 << dp.kv_shift;
+  const int GN = g >= 4 ? 4 : g;
+  GqaParams p;
+  p.q = dp.q;
+  p.kc = dp.kc; p.ks = static_cast<const float*>(dp.ks);
+  p.vc = dp.vc; p.vs = static_cast<const float*>(dp.vs);
+  p.seq_lens = dp.seq_lens;
+  p.out = dp.out;
+  p.cnt = dp.cnt;
+  p.part = part;
+  p.B = dp.B; p.H = dp.H; p.Hkv = H_kv; p.Tc = dp.Tc;
+  p.nsg = g / GN;
+  p.kv_shift = dp.kv_shift;
+  p.blk_shift = blk_shift_of(blk);
+  p.bt = dp.bt;
+  p.bt_stride = dp.bt_stride;
+  p.page_shift = dp.page_shift;
+  p.scale_log2 = dp.scale_log2;
+  p.zero = 0;
+  p.lv = dp.lv;
+  const long long groups = static_cast<long long>(dp.B) * H_kv * p.nsg;
+  p.nc = gqa_chunks(groups, dp.B, dp.H, dp.Tc);
+  if (p.nc > 1 && groups * p.nc * GN > records) return NQKV_ERR_WORKSPACE;
+  const long long items = groups * p.nc;
+  if (items >= (1ll << 31)) return NQKV_ERR_SHAPE;
+  return p.bt ? launch_gqa_p<true>(p, hd, GN, items, st) : launch_gqa_p<false>(p, hd, GN, items, st);
 }
 
 // fused all-gather epilogue arguments (nqkv_decode_step_gather)
@@ -345,6 +441,12 @@ int decode_common(const void* q, const uint8_t* k_codes, const void* k_scales,
   p.h_total = ga ? ga->H_total : H;
   p.epoch = ga ? ga->epoch : 0u;
   p.epoch_ptr = ga ? ga->epoch_ptr : nullptr;
+  // grouped-query attention over an fp32-scale cache (contiguous or paged)
+  // with blk <= hd: the group-native kernel (each KV head streamed once per
+  // <= 4 query heads)
+  if (lay.kv_shift > 0 && !f16s && blk <= hd && !plan && !k_new && !ga &&
+      gqa_native_enabled())
+    return launch_gqa(p, H_kv, hd, blk, reinterpret_cast<float*>(ws + w.gqa), w.gqa_records, st);
 #ifdef NQKV_TRACE
   if (const char* t = std::getenv("NQKV_TRACE_PTR"))
     p.trace = reinterpret_cast<unsigned long long*>(std::strtoull(t, nullptr, 0));

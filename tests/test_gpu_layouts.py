@@ -63,7 +63,7 @@ GEOMS = [(64, 32), (64, 64), (64, 256), (128, 32), (128, 64), (128, 128), (128, 
 
 
 @pytest.mark.parametrize("hd,blk", GEOMS)
-@pytest.mark.parametrize("group", [2, 8])
+@pytest.mark.parametrize("group", [2, 4, 8])
 def test_gqa_decode_matches_oracle(N, hd, blk, group):
     hpb = blk // hd if blk > hd else 1
     Hkv = 2 * hpb
