@@ -283,10 +283,19 @@ bool gqa_native_enabled() {     // NQKV_GQA_NATIVE=0: GQA through the per-query-
   return on;
 }
 
+bool gqa_tc_enabled() {         // NQKV_GQA_TC=0: K scores with FFMA2 instead of mma.sync
+  static const bool on = [] {
+    const char* e = std::getenv("NQKV_GQA_TC");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 template <int HD, int GN, bool PAGED>
 int launch_gqa_t(const GqaParams& p, long long items, cudaStream_t st) {
-  auto kern = gqa_decode_kernel<HD, GN, PAGED>;
-  constexpr size_t smem = gqa_smem_bytes<HD, GN>();
+  const bool tc = gqa_tc_enabled();
+  auto kern = tc ? gqa_tc_kernel<HD, GN, PAGED> : gqa_decode_kernel<HD, GN, PAGED>;
+  const size_t smem = tc ? gqa_tc_smem_bytes<HD, GN>() : gqa_smem_bytes<HD, GN>();
   static bool attr_set = false;
   static std::mutex mu;
   {
