@@ -227,3 +227,42 @@ def test_paged_decode_c5_shape_sampled(N):
         ref = O.decode_attention(q[b:b + 1].cpu().numpy(), ckc[b:b + 1].cpu().numpy(), cks[b:b + 1].cpu().numpy(),
                                  cvc[b:b + 1].cpu().numpy(), cvs[b:b + 1].cpu().numpy(), [T], blk)
         assert np.max(np.abs(outp[b:b + 1].cpu().numpy() - ref)) <= ATOL
+
+
+def test_gqa_decode_c5_shape_sampled(N):
+    """The bench's gqa-4 case at full size (64 x 48 query heads over 12 KV
+    heads x 4097 tokens, hd 128, blk 64; 3072 CTAs, several chunks per
+    group merged across CTAs): the group-native kernel against the oracle
+    on sampled sequences (every query head of each), ragged lengths, the
+    workspace left zero, and the paged cache bit-identical."""
+    B, Hkv, grp, hd, blk, P = 64, 12, 4, 128, 64, 256
+    H = Hkv * grp
+    rng = np.random.default_rng(11)
+    lens = [4097] * B
+    lens[5], lens[17], lens[40] = 1, 0, 2500
+    T = max(lens)
+    maxp = -(-T // P)
+    n_pages = B * maxp
+    bt = _table(B, maxp, n_pages, 7)
+    Tc = maxp * P
+    g = torch.Generator(device=DEV).manual_seed(4)
+    k = torch.randn(B, T, Hkv, hd, generator=g, device=DEV).half()
+    v = torch.randn(B, T, Hkv, hd, generator=g, device=DEV).half()
+    ckc, cks = _contig(N, k, blk, Tc)
+    cvc, cvs = _contig(N, v, blk, Tc)
+    pkc, pks = _paged(N, k, blk, P, n_pages, bt, T)
+    pvc, pvs = _paged(N, v, blk, P, n_pages, bt, T)
+    del k, v
+    q = torch.randn(B, H, hd, generator=g, device=DEV).half()
+    L = torch.tensor(lens, dtype=torch.int32, device=DEV)
+    ws = N.make_workspace(B, H, hd, Tc, DEV)
+    outc = N.nqkv_decode_attention_kv(q, ckc, cks, cvc, cvs, L, blk, N.kv_layout(Hkv), Tc, ws)
+    outp = N.nqkv_decode_attention_kv(q, pkc, pks, pvc, pvs, L, blk,
+                                      N.kv_layout(Hkv, bt, P, n_pages), Tc, ws)
+    torch.cuda.synchronize()
+    assert not ws.any()
+    assert torch.equal(outp, outc)
+    for b in (0, 5, 17, 40, int(rng.integers(0, B)), 63):
+        ref = O.decode_attention(q[b:b + 1].cpu().numpy(), ckc[b:b + 1].cpu().numpy(), cks[b:b + 1].cpu().numpy(),
+                                 cvc[b:b + 1].cpu().numpy(), cvs[b:b + 1].cpu().numpy(), [lens[b]], blk)
+        assert np.max(np.abs(outc[b:b + 1].cpu().numpy() - ref)) <= ATOL
