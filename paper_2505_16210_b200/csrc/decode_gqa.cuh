@@ -452,10 +452,21 @@ __device__ __forceinline__ void mma_16816(float (&d)[4], uint32_t a0, uint32_t a
                : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
                : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
+// predicated loads that leave the register UNDEFINED when off (no zeroing
+// move): only for values whose rows are masked afterwards -- K words and K
+// scales (the row's scores become -inf) and V words (their weight is 0; the
+// V scale, which multiplies the weight, is loaded zeroing)
 __device__ __forceinline__ uint32_t gqa_ld32c(const void* p, bool on) {   // L1-allocating
   uint32_t r;
-  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n mov.b32 %0, 0;\n"
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n"
                " @q ld.global.nc.u32 %0, [%1];\n}"
+               : "=r"(r) : "l"(p), "r"(static_cast<int>(on)));
+  return r;
+}
+__device__ __forceinline__ uint32_t gqa_ld32u(const void* p, bool on) {   // streaming
+  uint32_t r;
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n"
+               " @q ld.global.nc.L1::no_allocate.u32 %0, [%1];\n}"
                : "=r"(r) : "l"(p), "r"(static_cast<int>(on)));
   return r;
 }
@@ -602,7 +613,7 @@ gqa_tc_kernel(const __grid_constant__ GqaParams p) {
 #pragma unroll
         for (int i = 0; i < NSEG; ++i) {
           bf.k[hr][i] = gqa_ld32c(kr + hr * 8 * (HD / 2) + 16 * i, ok);
-          bf.ks[hr][i] = __uint_as_float(gqa_ld32p(sr + soff[i], ok));
+          bf.ks[hr][i] = __uint_as_float(gqa_ld32u(sr + soff[i], ok));
         }
         sr += 8 * nblk;
       }
@@ -613,7 +624,7 @@ gqa_tc_kernel(const __grid_constant__ GqaParams p) {
 #pragma unroll
       for (int i = 0; i < SV; ++i) {
         const bool ok = i * TPR < nv;
-        bf.v[i] = gqa_ld32p(vr + i * TPR * (HD / 2), ok);
+        bf.v[i] = gqa_ld32u(vr + i * TPR * (HD / 2), ok);
         bf.vs[i] = __uint_as_float(gqa_ld32p(vsr, ok));
         vsr += vsstride;
       }
