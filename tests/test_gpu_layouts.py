@@ -266,3 +266,49 @@ def test_gqa_decode_c5_shape_sampled(N):
         ref = O.decode_attention(q[b:b + 1].cpu().numpy(), ckc[b:b + 1].cpu().numpy(), cks[b:b + 1].cpu().numpy(),
                                  cvc[b:b + 1].cpu().numpy(), cvs[b:b + 1].cpu().numpy(), [lens[b]], blk)
         assert np.max(np.abs(outc[b:b + 1].cpu().numpy() - ref)) <= ATOL
+
+
+@pytest.mark.parametrize("env", [{"NQKV_GQA_TC": "0"}, {"NQKV_GQA_NATIVE": "0"}])
+def test_gqa_alternative_paths_match_oracle(N, env):
+    """The non-default grouped-query paths (read once per process from the
+    environment, so run in a child process): the group-native kernel with
+    FFMA2 scores (NQKV_GQA_TC=0) and the per-query-head MHA kernel
+    (NQKV_GQA_NATIVE=0), groups 2/4/8 at hd 64 and 128, within 2e-3 of the
+    oracle."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = r'''
+import numpy as np, torch, sys
+sys.path.insert(0, %r)
+from paper_2505_16210_b200 import nqkv as N
+from oracle import nqkv_oracle as O
+for hd, blk, group in ((64, 64, 2), (128, 64, 4), (128, 32, 8), (64, 32, 4)):
+    Hkv, B, lens = 2, 3, [0, 9, 1300]
+    H, T = Hkv * group, max(lens)
+    Tc = -(-T // 64) * 64
+    g = torch.Generator().manual_seed(hd + blk + group)
+    k = torch.randn(B, T, Hkv, hd, generator=g).half()
+    v = torch.randn(B, T, Hkv, hd, generator=g).half()
+    q = torch.randn(B, H, hd, generator=g).half()
+    kc = torch.zeros(B, Hkv, Tc, hd // 2, dtype=torch.uint8, device="cuda")
+    ks = torch.zeros(B, Hkv, Tc, hd // blk, device="cuda")
+    vc, vs = torch.zeros_like(kc), torch.zeros_like(ks)
+    z = torch.zeros(B, dtype=torch.int32, device="cuda")
+    N.nqkv_quantize(k.cuda(), z, kc, ks, blk)
+    N.nqkv_quantize(v.cuda(), z, vc, vs, blk)
+    L = torch.tensor(lens, dtype=torch.int32, device="cuda")
+    ws = N.make_workspace(B, H, hd, Tc, "cuda")
+    out = N.nqkv_decode_attention_kv(q.cuda(), kc, ks, vc, vs, L, blk, N.kv_layout(Hkv), Tc, ws)
+    torch.cuda.synchronize()
+    ref = O.decode_attention(q.numpy(), kc.cpu().numpy(), ks.cpu().numpy(), vc.cpu().numpy(),
+                             vs.cpu().numpy(), lens, blk)
+    err = float(np.max(np.abs(out.cpu().numpy().astype(np.float64) - ref)))
+    assert err <= 2e-3, (hd, blk, group, err)
+    assert not ws.any()
+print("ok")
+''' % root
+    r = subprocess.run([sys.executable, "-c", script], env={**os.environ, **env}, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
