@@ -32,6 +32,12 @@
 #include "prefill.cuh"
 
 namespace nqkv {
+#ifndef NQKV_PF_WARP_ISSUE
+#define NQKV_PF_WARP_ISSUE 0       // 1: whole-warp MMA issue with elect.sync (measured: see DESIGN 6.4)
+#endif
+#ifndef NQKV_PF_MMAW
+#define NQKV_PF_MMAW 1             // MMA-issuing warps: 1 (both row sets) or 2 (one per row set; measured slower)
+#endif
 #ifdef NQKV_PF_TRACE
 __device__ unsigned* g_pf_trace;     // development builds: see PF_TR below
 #endif
@@ -41,10 +47,11 @@ constexpr int kTcK = 64;         // keys per tile
 constexpr int kTcSoftW = 8;      // softmax warps (4 per row set)
 constexpr int kTcStages = 3;     // K/V ring depth
 #ifndef NQKV_PF_DQW
-#define NQKV_PF_DQW 7
+#define NQKV_PF_DQW (8 - NQKV_PF_MMAW)
 #endif
 constexpr int kTcDqW = NQKV_PF_DQW;   // dequantisation warps
-constexpr int kTcThreads = (kTcSoftW + kTcDqW + 1) * 32;   // + the MMA warp
+constexpr int kTcMmaW = NQKV_PF_MMAW;
+constexpr int kTcThreads = (kTcSoftW + kTcDqW + kTcMmaW) * 32;   // + the MMA warp(s)
 
 template <int HD>
 constexpr size_t prefill_tc_smem_bytes() {
@@ -78,6 +85,23 @@ __device__ __forceinline__ void umma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, ui
 }
 __device__ __forceinline__ void umma_commit(uint32_t mbar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" :: "r"(mbar) : "memory");
+}
+// Warp-wide issue (NQKV_PF_WARP_ISSUE): the whole MMA warp runs the issue
+// loop with warp-uniform operands and ONE elected lane issues each
+// instruction.  Issued from a single thread (lane == 0), the compiler wraps
+// every tcgen05.mma in an elect / R2UR / BRA.U.ANY loop (its operands live
+// in uniform registers), ~8 instructions per MMA.
+__device__ __forceinline__ void umma_f16_ts_w(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc,
+                                              uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p, e;\nsetp.ne.b32 p, %4, 0;\nelect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n"
+      :: "r"(tmem_d), "r"(tmem_a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit_w(uint32_t mbar) {
+  asm volatile("{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+               "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n"
+               :: "r"(mbar) : "memory");
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -215,7 +239,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) prefill_tc_kernel(const __grid_
     for (int i = 0; i < kBars; ++i) {
       const bool dq = i < 3 || (i >= 6 && i < 9);      // arrivals of every dequantisation thread
       const bool sm = i == 14 || i == 15;                // of the 128 threads of a row set
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(bar(i)), "r"(dq ? kTcDqW * 32 : sm ? 128 : 1));
+      // K/V-empty (3-5, 9-11) and all-done (16): one commit per MMA warp
+      const bool mw = (i >= 3 && i < 6) || (i >= 9 && i < 12) || i == 16;
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(bar(i)),
+                   "r"(dq ? kTcDqW * 32 : sm ? 128 : mw ? kTcMmaW : 1));
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -457,27 +484,44 @@ __global__ void __launch_bounds__(kTcThreads, 1) prefill_tc_kernel(const __grid_
       rk = nk;
       rv = nv;
     }
+#if NQKV_PF_WARP_ISSUE
+  } else {
+    // ================= MMA issue (the whole warp; one elected lane per instruction)
+#define umma_f16_ts umma_f16_ts_w
+#define umma_commit umma_commit_w
+    // One CTA per SM allocating all 512 columns: the allocation starts at
+    // column 0.  A compile-time base keeps every MMA operand warp-uniform
+    // (uniform registers, no per-instruction elect loop).
+    if (tmem != 0u) __trap();
+    constexpr uint32_t tmem_u = 0u;
+#define tmem tmem_u
+#else
   } else if (lane == 0) {
     // ================= MMA issue (one thread)
+#endif
     constexpr uint32_t idS = umma_idesc_f16(128, kTcK, false);
     constexpr uint32_t idO = umma_idesc_f16(128, HD, true);
     auto issue_s = [&](int s, int t) {  // S_s(t) = Q_s K_hi^T + Q_s K_lo^T
       const uint32_t kh = sbase + (t % kTcStages) * kStageBytes, kl = kh + kTileBytes;
       const uint32_t d = tmem + kSP + s * kTcK, a = tmem + kQc + s * (HD / 2);
+      // descriptors built once per tile; a k-step advances the start address
+      // field (bits 0-13, 16-byte units; smem addresses < 2^18 never carry out)
+      const uint64_t dh = umma_sdesc(kh, 128, DG * 128), dl = umma_sdesc(kl, 128, DG * 128);
 #pragma unroll
       for (int kk = 0; kk < HD / 16; ++kk) {
-        umma_f16_ts(d, a + kk * 8, umma_sdesc(kh + kk * 256, 128, DG * 128), idS, kk > 0);
-        umma_f16_ts(d, a + kk * 8, umma_sdesc(kl + kk * 256, 128, DG * 128), idS, 1u);
+        umma_f16_ts(d, a + kk * 8, dh + static_cast<uint64_t>(kk * 16), idS, kk > 0);
+        umma_f16_ts(d, a + kk * 8, dl + static_cast<uint64_t>(kk * 16), idS, 1u);
       }
       umma_commit(bar(12 + s));
     };
     auto issue_pv = [&](int s, int t) { // O_s += P_hi V_hi + P_lo V_hi + P_hi V_lo
       const uint32_t vh = sbase + (t % kTcStages) * kStageBytes + 2 * kTileBytes, vl = vh + kTileBytes;
       const uint32_t ph = tmem + kSP + s * kTcK, pl = ph + 32, d = tmem + s * HD;
+      const uint64_t bh0 = umma_sdesc(vh, DG * 128, 128), bl0 = umma_sdesc(vl, DG * 128, 128);
 #pragma unroll
       for (int kk = 0; kk < kTcK / 16; ++kk) {
-        const uint64_t bh = umma_sdesc(vh + kk * 2 * DG * 128, DG * 128, 128);
-        const uint64_t bl = umma_sdesc(vl + kk * 2 * DG * 128, DG * 128, 128);
+        const uint64_t bh = bh0 + static_cast<uint64_t>(kk * 2 * DG * 8);   // + kk * 2 * DG * 128 bytes
+        const uint64_t bl = bl0 + static_cast<uint64_t>(kk * 2 * DG * 8);
         umma_f16_ts(d, ph + kk * 8, bh, idO, (t > 0 || kk > 0) ? 1u : 0u);
         umma_f16_ts(d, pl + kk * 8, bh, idO, 1u);
         umma_f16_ts(d, ph + kk * 8, bl, idO, 1u);
@@ -488,6 +532,30 @@ __global__ void __launch_bounds__(kTcThreads, 1) prefill_tc_kernel(const __grid_
       mbar_wait_tc(bar(0 + t % kTcStages), (t / kTcStages) & 1);
       tc_fence_after();
     };
+#if NQKV_PF_MMAW == 2
+    // one MMA warp per row set: the two sets' MMAs are issued concurrently
+    // (per-thread commits track only the issuing thread's MMAs; a K/V stage
+    // is free once BOTH warps committed it: count-2 barriers)
+    const int s = warp - (kTcSoftW + kTcDqW);
+    mbar_wait_tc(bar(14 + s), 0);        // Q_s rows written (P-full phase 0)
+    wait_k(0);
+    issue_s(s, 0);
+    umma_commit(bar(3 + 0));
+    for (int t = 0; t < ntiles; ++t) {
+      mbar_wait_tc(bar(6 + t % kTcStages), (t / kTcStages) & 1);      // V(t)
+      const bool more = t + 1 < ntiles;
+      mbar_wait_tc(bar(14 + s), (t + 1) & 1);    // P_s(t): phase t + 1 (phase 0 = Q)
+      tc_fence_after();
+      issue_pv(s, t);
+      if (more) {
+        wait_k(t + 1);
+        issue_s(s, t + 1);
+      }
+      umma_commit(bar(9 + t % kTcStages));        // V stage free (this warp's share)
+      if (more) umma_commit(bar(3 + (t + 1) % kTcStages));   // K stage free (this warp's share)
+    }
+    umma_commit(bar(16));
+#else
     // Q rows written (P-full phase 0 of both sets)
     mbar_wait_tc(bar(14), 0);
     mbar_wait_tc(bar(15), 0);
@@ -515,7 +583,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) prefill_tc_kernel(const __grid_
       if (more) umma_commit(bar(3 + (t + 1) % kTcStages));   // K stage free
     }
     umma_commit(bar(16));
+#endif
   }
+#if NQKV_PF_WARP_ISSUE
+#undef umma_f16_ts
+#undef umma_commit
+#undef tmem
+#endif
   __syncwarp();
   tc_fence_before();
   __syncthreads();
