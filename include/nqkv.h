@@ -130,8 +130,10 @@ int nqkv_dequantize(const uint8_t* codes, const void* scales, int B, int H, int 
 /* Bytes of workspace nqkv_decode_attention / nqkv_decode_step need for this
  * geometry (0 for an unsupported hd).  Layout: [0, nqkv_decode_counter_bytes)
  * int32 per-(b, h) arrival counters, then per-CTA split-partial records of
- * tagged 64-bit words (value | valid << 32).  The WHOLE workspace must be
- * ZERO before the first call; every completed call leaves it zero again. */
+ * tagged 64-bit words (value | valid << 32), then the grouped-query kernel's
+ * chunk partials (min(B*H*64, 16384) records of hd + 2 floats; H = query
+ * heads).  The WHOLE workspace must be ZERO before the first call; every
+ * completed call leaves it zero again. */
 size_t nqkv_decode_workspace_bytes(int B, int H, int hd, int Tc);
 size_t nqkv_decode_counter_bytes(int B, int H);
 
