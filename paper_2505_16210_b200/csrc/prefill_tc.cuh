@@ -64,6 +64,13 @@ __device__ __forceinline__ uint64_t umma_sdesc(uint32_t saddr, uint32_t lbo, uin
   return static_cast<uint64_t>((saddr >> 4) & 0x3FFF) | (static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16) |
          (static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32) | (static_cast<uint64_t>(1) << 46);
 }
+// start-address field += v (16-byte units); opaque to the compiler so the
+// descriptor stays one register pair advanced by one add per k-step
+__device__ __forceinline__ uint64_t desc_add(uint64_t d, uint32_t v) {
+  uint64_t r;
+  asm volatile("add.u64 %0, %1, %2;" : "=l"(r) : "l"(d), "l"(static_cast<uint64_t>(v)));
+  return r;
+}
 // kind::f16 instruction descriptor: fp16 A/B, fp32 D, A K-major, B K- or MN-major
 __host__ __device__ constexpr uint32_t umma_idesc_f16(int m, int n, bool b_mn) {
   return (1u << 4) | (static_cast<uint32_t>(b_mn) << 16) | (static_cast<uint32_t>(n >> 3) << 17) |
@@ -507,10 +514,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) prefill_tc_kernel(const __grid_
       // descriptors built once per tile; a k-step advances the start address
       // field (bits 0-13, 16-byte units; smem addresses < 2^18 never carry out)
       const uint64_t dh = umma_sdesc(kh, 128, DG * 128), dl = umma_sdesc(kl, 128, DG * 128);
+      uint64_t dhk = dh, dlk = dl;
 #pragma unroll
       for (int kk = 0; kk < HD / 16; ++kk) {
-        umma_f16_ts(d, a + kk * 8, dh + static_cast<uint64_t>(kk * 16), idS, kk > 0);
-        umma_f16_ts(d, a + kk * 8, dl + static_cast<uint64_t>(kk * 16), idS, 1u);
+        umma_f16_ts(d, a + kk * 8, dhk, idS, kk > 0);
+        umma_f16_ts(d, a + kk * 8, dlk, idS, 1u);
+        dhk = desc_add(dhk, 16u);
+        dlk = desc_add(dlk, 16u);
       }
       umma_commit(bar(12 + s));
     };
@@ -520,8 +530,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) prefill_tc_kernel(const __grid_
       const uint64_t bh0 = umma_sdesc(vh, DG * 128, 128), bl0 = umma_sdesc(vl, DG * 128, 128);
 #pragma unroll
       for (int kk = 0; kk < kTcK / 16; ++kk) {
-        const uint64_t bh = bh0 + static_cast<uint64_t>(kk * 2 * DG * 8);   // + kk * 2 * DG * 128 bytes
-        const uint64_t bl = bl0 + static_cast<uint64_t>(kk * 2 * DG * 8);
+        const uint64_t bh = kk ? desc_add(bh0, static_cast<uint32_t>(kk * 2 * DG * 8)) : bh0;   // + kk * 2 * DG * 128 B
+        const uint64_t bl = kk ? desc_add(bl0, static_cast<uint32_t>(kk * 2 * DG * 8)) : bl0;
         umma_f16_ts(d, ph + kk * 8, bh, idO, (t > 0 || kk > 0) ? 1u : 0u);
         umma_f16_ts(d, pl + kk * 8, bh, idO, 1u);
         umma_f16_ts(d, ph + kk * 8, bl, idO, 1u);
