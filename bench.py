@@ -270,7 +270,8 @@ def measure(args, w, heads, dev, world, group, layers=None, steps=None, warmup=N
 
     steps = args.steps if steps is None else steps
     warmup = args.warmup if warmup is None else warmup
-    runner = DecodeRunner(w, heads, dev, group=group, world=world, layers=layers)
+    runner = DecodeRunner(w, heads, dev, group=group, world=world, layers=layers,
+                          gather_mode=getattr(args, "gather", "overlap"))
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     flush = torch.empty(max(2 * l2, 256 << 20) // 4, dtype=torch.float32, device=dev)
     q_ms = runner.prefill(flush=flush)
@@ -642,7 +643,10 @@ def run_ours(args, w, rank, world, local_rank):
             "execution": "per-step CUDA graph; per-step plan kernel + one fused nqkv_decode_step "
                          "launch per layer (append + attend, PDL-chained)",
             "parallelism": f"head-sharded x{world} ({args.scaling})" +
-                           (", NCCL all-gather of outputs on a side stream" if world > 1 else ""),
+                           ({"overlap": ", NCCL all-gather of each layer's outputs on a side stream",
+                             "serialized": ", NCCL all-gather of each layer's outputs, serialized",
+                             "per_step": ", one NCCL all-gather of all layers' outputs per step"}
+                            [args.gather] if world > 1 else ""),
         },
         "roofline": {"bound": "hbm", "achieved": r["decode_gbs"], "peak": peak, "unit": "GB/s",
                      "frac": r["decode_gbs"] / peak, "traffic": traffic,
@@ -684,6 +688,9 @@ def main():
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-configs", action="store_true")
+    ap.add_argument("--gather", default="overlap", choices=["overlap", "serialized", "per_step"],
+                    help="N > 1: per-layer all-gather overlapped on a side stream (default), "
+                         "serialized on the compute stream, or one per step (SURVEY 8(e))")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

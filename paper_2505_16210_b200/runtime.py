@@ -31,7 +31,7 @@ class DecodeRunner:
     def __init__(self, w: W.Workload, heads: range, device, group=None, world: int = 1,
                  step_slots: int | None = None, layers: int | None = None, fused: bool = True,
                  gen_device=None, planned: bool = True, fused_gather: bool | None = None,
-                 nccl_gather: bool | None = None):
+                 nccl_gather: bool | None = None, gather_mode: str = "overlap"):
         self.w = w
         self.fused = fused
         if fused_gather is None:
@@ -82,8 +82,19 @@ class DecodeRunner:
         # NCCL all-gather of each layer's outputs on a side stream: always at
         # world > 1; selectable at world 1 (tests run it under graph capture)
         self.nccl_gather = (world > 1 if nccl_gather is None else nccl_gather) and not self.fused_gather
+        # "overlap" -- per layer on a side stream beside the next
+        # layer's attention (default); "serialized" -- per layer on the compute
+        # stream (the honest, unoverlapped number); "per_step" -- one
+        # all-gather of every layer's outputs at the end of the step
+        if gather_mode not in ("overlap", "serialized", "per_step"):
+            raise ValueError(f"gather_mode {gather_mode!r}")
+        self.gather_mode = gather_mode
         if self.fused_gather:
             self._setup_fused_gather(group, world)
+        elif self.nccl_gather and gather_mode == "per_step":
+            # rank-major [world, L, B, Hl, hd]: gathered_layer(l) assembles a layer
+            self.gathered = torch.empty((world, self.L, self.B, self.Hl, self.hd),
+                                        dtype=torch.float32, device=self.dev)
         elif self.nccl_gather:
             self.gathered = torch.empty((self.L, world * self.B, self.Hl, self.hd),
                                         dtype=torch.float32, device=self.dev)
@@ -161,6 +172,13 @@ class DecodeRunner:
         gathered [L, B, world*H, hd] outputs with the fused gather."""
         return self.out_of(self._last)
 
+    def gathered_layer(self, l: int) -> torch.Tensor:
+        """Layer l's gathered outputs [world*B, Hl, hd] (rank-major, as
+        sharding.assemble takes them) in any NCCL gather mode."""
+        if self.gather_mode == "per_step":
+            return sharding.step_gather_layer(self.gathered, l)
+        return self.gathered[l]
+
     def out_of(self, s: int) -> torch.Tensor:
         """Output buffer written by step (graph) slot s."""
         if self.fused_gather:
@@ -198,12 +216,17 @@ class DecodeRunner:
                 c.attend(x[l, 2], lens, self.ws, out=out[l])
             if events is not None:
                 events[l][1].record()
-            if self.nccl_gather:
+            if self.nccl_gather and self.gather_mode == "overlap":
                 self.comm.wait_stream(cur)
                 with torch.cuda.stream(self.comm):
                     sharding.all_gather_heads(out[l], self.gathered[l], self.group)
-        if self.nccl_gather:
+            elif self.nccl_gather and self.gather_mode == "serialized":
+                sharding.all_gather_heads(out[l], self.gathered[l], self.group)
+        if self.nccl_gather and self.gather_mode == "overlap":
             cur.wait_stream(self.comm)
+        elif self.nccl_gather and self.gather_mode == "per_step":
+            sharding.all_gather_heads(out, self.gathered.view(self.world * self.L, self.B, self.Hl, self.hd),
+                                      self.group)
 
     def _step_fused_gather(self, x, lens, parity, events=None) -> None:
         N.nqkv_gather_epoch_bump(self.epoch)

@@ -54,3 +54,11 @@ def assemble(gathered: torch.Tensor, world: int) -> torch.Tensor:
     GB, Hl, hd = gathered.shape
     B = GB // world
     return gathered.view(world, B, Hl, hd).permute(1, 0, 2, 3).reshape(B, world * Hl, hd)
+
+
+def step_gather_layer(gathered: torch.Tensor, layer: int) -> torch.Tensor:
+    """Per-step gather (one all-gather of every layer's [L, B, H_local, hd]
+    outputs, rank-major [G, L, B, H_local, hd]) -> layer `layer`'s
+    [G*B, H_local, hd] (rank-major, as assemble takes it)."""
+    G, L, B, Hl, hd = gathered.shape
+    return gathered[:, layer].reshape(G * B, Hl, hd)

@@ -53,16 +53,26 @@ def _worker(rank, world, port, mode, out_path):
         else:
             heads = sharding.weak_head_range(rank, w.heads // world, group)
         local = torch.from_numpy(_heads_output(heads, w))
-        gathered = sharding.gather_buffer(local, world)
-        sharding.all_gather_heads(local, gathered)
-        full = sharding.assemble(gathered, world)
+        if mode == "per_step":
+            # one all-gather of two "layers" of outputs ([L, B, H_local, hd]),
+            # split back per layer (the runtime's per-step gather mode)
+            layers = torch.stack([local, 2.0 * local])
+            gathered = torch.empty((world * 2,) + tuple(local.shape), dtype=local.dtype)
+            sharding.all_gather_heads(layers, gathered)
+            g5 = gathered.view((world, 2) + tuple(local.shape))
+            full = torch.stack([sharding.assemble(sharding.step_gather_layer(g5, l), world)
+                                for l in range(2)])
+        else:
+            gathered = sharding.gather_buffer(local, world)
+            sharding.all_gather_heads(local, gathered)
+            full = sharding.assemble(gathered, world)
         if rank == 0:
             torch.save(full, out_path)
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode", ["strong", "weak", "strong256"])
+@pytest.mark.parametrize("mode", ["strong", "weak", "strong256", "per_step"])
 def test_head_sharded_all_gather_matches_unsharded(tmp_path, mode):
     world = 2
     out = str(tmp_path / "full.pt")
@@ -70,6 +80,8 @@ def test_head_sharded_all_gather_matches_unsharded(tmp_path, mode):
     full = torch.load(out).numpy()
     w = WORK256 if mode == "strong256" else WORK
     ref = _heads_output(range(w.heads), w)
+    if mode == "per_step":
+        ref = np.stack([ref, 2.0 * ref])
     assert full.shape == ref.shape
     assert np.array_equal(full, ref)
 

@@ -951,6 +951,21 @@ def test_runtime_nccl_side_stream_gather_world1(N):
         torch.cuda.synchronize()
         assert torch.equal(r.gathered, r.out_of(1))
         assert r.launches_per_step() == 3 + 1
+        # the other gather modes: serialized per layer, one per step
+        for mode in ("serialized", "per_step"):
+            r2 = DecodeRunner(w, range(w.heads), DEV, group=dist.group.WORLD, world=1, step_slots=2,
+                              layers=3, nccl_gather=True, gather_mode=mode)
+            r2.prefill()
+            r2.step(0)
+            torch.cuda.synchronize()
+            for l in range(3):
+                assert torch.equal(r2.gathered_layer(l), r2.out_of(0)[l])
+            r2.capture(timing_slots=())
+            r2.gathered.zero_()
+            r2.replay(1)
+            torch.cuda.synchronize()
+            for l in range(3):
+                assert torch.equal(r2.gathered_layer(l), r2.out_of(1)[l])
     finally:
         dist.destroy_process_group()
 
