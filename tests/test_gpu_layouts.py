@@ -312,3 +312,33 @@ print("ok")
     r = subprocess.run([sys.executable, "-c", script], env={**os.environ, **env}, capture_output=True,
                        text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("hd,blk", [(64, 64), (128, 32), (128, 128)])
+def test_gqa_decode_fp16_scales_equals_fp32(N, hd, blk):
+    """Grouped-query decode over a cache with fp16 block scales (lossless for
+    fp16 inputs; this combination runs the per-query-head MHA kernel) and over
+    the fp32-scale cache (the group-native kernel): both within 2e-3 of the
+    oracle and of each other, the workspace left zero."""
+    Hkv, group = 2, 4
+    H = Hkv * group
+    lens = [0, 1, 333, 1200]
+    B, T = len(lens), max(lens)
+    Tc = -(-T // 64) * 64
+    k, v = _kv(B, T, Hkv, hd, 21), _kv(B, T, Hkv, hd, 22)
+    kc, ks = _contig(N, k, blk, Tc)
+    vc, vs = _contig(N, v, blk, Tc)
+    ks16, vs16 = ks.half(), vs.half()             # exact: every scale is an fp16 absmax
+    assert torch.equal(ks16.float(), ks) and torch.equal(vs16.float(), vs)
+    q = torch.randn(B, H, hd, generator=torch.Generator().manual_seed(23)).half().to(DEV)
+    L = torch.tensor(lens, dtype=torch.int32, device=DEV)
+    ws = N.make_workspace(B, H, hd, Tc, DEV)
+    o16 = N.nqkv_decode_attention_kv(q, kc, ks16, vc, vs16, L, blk, N.kv_layout(Hkv), Tc, ws)
+    o32 = N.nqkv_decode_attention_kv(q, kc, ks, vc, vs, L, blk, N.kv_layout(Hkv), Tc, ws)
+    torch.cuda.synchronize()
+    assert not ws.any()
+    ref = O.decode_attention(q.cpu().numpy(), kc.cpu().numpy(), ks.cpu().numpy(), vc.cpu().numpy(),
+                             vs.cpu().numpy(), lens, blk)
+    for o in (o16, o32):
+        assert np.max(np.abs(o.cpu().numpy().astype(np.float64) - ref)) <= ATOL
+    assert torch.max(torch.abs(o16 - o32)).item() <= ATOL
