@@ -331,14 +331,15 @@ typedef struct nqkv_kv_layout {
 /* nqkv_decode_attention over a KV layout (attention only: append with
  * nqkv_quantize_kv).  Same semantics, workspace (sized with the QUERY head
  * count H) and errors as nqkv_decode_attention; q/out are [B][H][hd].
- * Grouped-query calls (H > H_kv) with fp32 scales and blk <= hd run a
- * group-native kernel: one CTA streams a chunk of ONE cache head once for up
+ * Grouped-query calls (H > H_kv) with blk <= hd (fp32 scales; fp16 scales on
+ * a contiguous cache) run a group-native kernel: one CTA streams a chunk of ONE cache head once for up
  * to 4 query heads of its group (groups of 8: two sub-groups), chunks
  * [len*c/nc, len*(c+1)/nc) merged by the last-arriving CTA in chunk order
  * (nc from B, H, H_kv, Tc and the SM count, so the result is reproducible
  * call to call; it equals the MHA kernel's up to fp32 reassociation).  Other
- * grouped-query calls (fp16 scales, blk > hd, or NQKV_GQA_NATIVE=0 in the
- * environment, read once) stream each cache head once per query head. */
+ * grouped-query calls (blk > hd, fp16 scales with NQKV_GQA_TC=0, or
+ * NQKV_GQA_NATIVE=0 in the environment, read once) stream each cache head
+ * once per query head. */
 int nqkv_decode_attention_kv(const void* q, const uint8_t* k_codes, const void* k_scales,
                              const uint8_t* v_codes, const void* v_scales,
                              const int32_t* d_seq_lens, int B, int H, int hd, int blk, int Tc,

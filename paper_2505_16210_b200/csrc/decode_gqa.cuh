@@ -25,6 +25,8 @@
 // group arrival counter), in chunk order -- results depend on (B, H, seq_lens,
 // nc) only.
 #pragma once
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace nqkv {
@@ -44,9 +46,9 @@ constexpr size_t gqa_smem_bytes() {
 struct GqaParams {
   const __half* q;           // [B][H][hd]
   const uint8_t* kc;         // [B][Hkv][Tc][hd/2]
-  const float* ks;           // [B][Hkv][Tc][hd/blk]
+  const void* ks;            // [B][Hkv][Tc][hd/blk] fp32, or fp16 (gqa_tc_kernel template F16S)
   const uint8_t* vc;
-  const float* vs;
+  const void* vs;
   const int32_t* seq_lens;   // [B]
   float* out;                // [B][H][hd]
   int* cnt;                  // [B*H] arrival counters (zero between launches)
@@ -221,8 +223,8 @@ gqa_decode_kernel(const __grid_constant__ GqaParams p) {
   const uint8_t* kbase = p.kc + sl * 4;
   const uint8_t* vbase = p.vc + sl * 4;
   const int sblk = (sl * 8) >> p.blk_shift;
-  const float* ksbase = p.ks + sblk;
-  const float* vsbase = p.vs + sblk;
+  const float* ksbase = static_cast<const float*>(p.ks) + sblk;
+  const float* vsbase = static_cast<const float*>(p.vs) + sblk;
   const int32_t* btrow = PAGED ? p.bt + static_cast<size_t>(b) * p.bt_stride : nullptr;
   const size_t page_rows = PAGED ? static_cast<size_t>(p.Hkv) << p.page_shift : 0;   // rows per page
   const int pmask = PAGED ? (1 << p.page_shift) - 1 : 0;
@@ -463,6 +465,19 @@ __device__ __forceinline__ uint32_t gqa_ld32c(const void* p, bool on) {   // L1-
                : "=r"(r) : "l"(p), "r"(static_cast<int>(on)));
   return r;
 }
+// 16-bit (fp16 block scale) forms: zeroing and undefined-when-off
+__device__ __forceinline__ float gqa_ldh(const void* p, bool on, bool zeroing) {
+  unsigned short r;
+  if (zeroing)
+    asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n mov.b16 %0, 0;\n"
+                 " @q ld.global.nc.L1::no_allocate.u16 %0, [%1];\n}"
+                 : "=h"(r) : "l"(p), "r"(static_cast<int>(on)));
+  else
+    asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n"
+                 " @q ld.global.nc.L1::no_allocate.u16 %0, [%1];\n}"
+                 : "=h"(r) : "l"(p), "r"(static_cast<int>(on)));
+  return __half2float(__ushort_as_half(r));
+}
 __device__ __forceinline__ uint32_t gqa_ld32u(const void* p, bool on) {   // streaming
   uint32_t r;
   asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n"
@@ -477,7 +492,7 @@ constexpr size_t gqa_tc_smem_bytes() {
          static_cast<size_t>(kGqaWarps) * 16 * GN * 4 + 16;
 }
 
-template <int HD, int GN, bool PAGED>
+template <int HD, int GN, bool PAGED, bool F16S>
 __global__ void __launch_bounds__(kGqaWarps * 32, kGqaCtasPerSm)
 gqa_tc_kernel(const __grid_constant__ GqaParams p) {
   constexpr int NSEG = HD / 32;              // 32-dim segments = 16-byte quarter rows
@@ -576,7 +591,16 @@ gqa_tc_kernel(const __grid_constant__ GqaParams p) {
   int soff[NSEG];
 #pragma unroll
   for (int i = 0; i < NSEG; ++i) soff[i] = (32 * i) >> p.blk_shift;
-  const int vsstride = TPR * nblk;            // V scale floats between a lane's slots
+  const int vsstride = TPR * nblk;            // V scale elements between a lane's slots
+  using SE = typename std::conditional<F16S, __half, float>::type;   // scale element
+  const SE* ksp = static_cast<const SE*>(p.ks);
+  const SE* vsp = static_cast<const SE*>(p.vs);
+  // zeroing: the V scale (it multiplies a masked row's zero weight); K scales
+  // of masked rows may stay undefined (their scores become -inf)
+  auto lds = [&](const SE* ptr, bool ok, bool zeroing) -> float {
+    if constexpr (F16S) return gqa_ldh(ptr, ok, zeroing);
+    else return __uint_as_float(zeroing ? gqa_ld32p(ptr, ok) : gqa_ld32u(ptr, ok));
+  };
   auto load = [&](Buf& bf, int st, int dep) {
     const int tb = t0 + st * 16 + dep;
     if constexpr (PAGED) {
@@ -586,11 +610,11 @@ gqa_tc_kernel(const __grid_constant__ GqaParams p) {
         const bool ok = t < t1;
         const size_t row = row_of(ok ? t : t0);
         const uint8_t* kr = p.kc + row * (HD / 2) + 4 * c;
-        const float* sr = p.ks + row * nblk;
+        const SE* sr = ksp + row * nblk;
 #pragma unroll
         for (int i = 0; i < NSEG; ++i) {
           bf.k[hr][i] = gqa_ld32c(kr + 16 * i, ok);
-          bf.ks[hr][i] = __uint_as_float(gqa_ld32p(sr + soff[i], ok));
+          bf.ks[hr][i] = lds(sr + soff[i], ok, true);
         }
       }
 #pragma unroll
@@ -599,13 +623,13 @@ gqa_tc_kernel(const __grid_constant__ GqaParams p) {
         const bool ok = t < t1;
         const size_t row = row_of(ok ? t : t0);
         bf.v[i] = gqa_ld32p(p.vc + row * (HD / 2) + 4 * sl, ok);
-        bf.vs[i] = __uint_as_float(gqa_ld32p(p.vs + row * nblk + vblk, ok));
+        bf.vs[i] = lds(vsp + row * nblk + vblk, ok, true);
       }
     } else {
       // one base pointer per stream and stage; slots / rows / segments are offsets
       const size_t rk = row0 + static_cast<size_t>(tb + g);
       const uint8_t* kr = p.kc + rk * (HD / 2) + 4 * c;
-      const float* sr = p.ks + rk * nblk;
+      const SE* sr = ksp + rk * nblk;
       const int nk = t1 - tb - g;             // row g valid iff 0 < nk, row g + 8 iff 8 < nk
 #pragma unroll
       for (int hr = 0; hr < 2; ++hr) {
@@ -613,19 +637,19 @@ gqa_tc_kernel(const __grid_constant__ GqaParams p) {
 #pragma unroll
         for (int i = 0; i < NSEG; ++i) {
           bf.k[hr][i] = gqa_ld32c(kr + hr * 8 * (HD / 2) + 16 * i, ok);
-          bf.ks[hr][i] = __uint_as_float(gqa_ld32u(sr + soff[i], ok));
+          bf.ks[hr][i] = lds(sr + soff[i], ok, false);
         }
         sr += 8 * nblk;
       }
       const size_t rv = row0 + static_cast<size_t>(tb + r);
       const uint8_t* vr = p.vc + rv * (HD / 2) + 4 * sl;
-      const float* vsr = p.vs + rv * nblk + vblk;
+      const SE* vsr = vsp + rv * nblk + vblk;
       const int nv = t1 - tb - r;
 #pragma unroll
       for (int i = 0; i < SV; ++i) {
         const bool ok = i * TPR < nv;
         bf.v[i] = gqa_ld32u(vr + i * TPR * (HD / 2), ok);
-        bf.vs[i] = __uint_as_float(gqa_ld32p(vsr, ok));
+        bf.vs[i] = lds(vsr, ok, true);
         vsr += vsstride;
       }
     }

@@ -291,10 +291,11 @@ bool gqa_tc_enabled() {         // NQKV_GQA_TC=0: K scores with FFMA2 instead of
   return on;
 }
 
-template <int HD, int GN, bool PAGED>
+template <int HD, int GN, bool PAGED, bool F16S>
 int launch_gqa_t(const GqaParams& p, long long items, cudaStream_t st) {
-  const bool tc = gqa_tc_enabled();
-  auto kern = tc ? gqa_tc_kernel<HD, GN, PAGED> : gqa_decode_kernel<HD, GN, PAGED>;
+  // fp16 scales: tensor-core kernel only (the dispatch guarantees it)
+  const bool tc = F16S || gqa_tc_enabled();
+  auto kern = tc ? gqa_tc_kernel<HD, GN, PAGED, F16S> : gqa_decode_kernel<HD, GN, PAGED>;
   const size_t smem = tc ? gqa_tc_smem_bytes<HD, GN>() : gqa_smem_bytes<HD, GN>();
   static bool attr_set = false;
   static std::mutex mu;
@@ -333,21 +334,22 @@ int gqa_chunks(long long groups, long long B, long long H, int Tc) {
   return best;
 }
 
-template <bool PAGED>
+template <bool PAGED, bool F16S>
 int launch_gqa_p(const GqaParams& p, int hd, int GN, long long items, cudaStream_t st) {
   if (hd == 64)
-    return GN == 4 ? launch_gqa_t<64, 4, PAGED>(p, items, st) : launch_gqa_t<64, 2, PAGED>(p, items, st);
-  return GN == 4 ? launch_gqa_t<128, 4, PAGED>(p, items, st) : launch_gqa_t<128, 2, PAGED>(p, items, st);
+    return GN == 4 ? launch_gqa_t<64, 4, PAGED, F16S>(p, items, st) : launch_gqa_t<64, 2, PAGED, F16S>(p, items, st);
+  return GN == 4 ? launch_gqa_t<128, 4, PAGED, F16S>(p, items, st)
+                 : launch_gqa_t<128, 2, PAGED, F16S>(p, items, st);
 }
 
-int launch_gqa(const DecodeParams& dp, int H_kv, int hd, int blk, float* part, long long records,
-               cudaStream_t st) {
+int launch_gqa(const DecodeParams& dp, int H_kv, int hd, int blk, bool f16s, float* part,
+               long long records, cudaStream_t st) {
   const int g = 1 << dp.kv_shift;
   const int GN = g >= 4 ? 4 : g;
   GqaParams p;
   p.q = dp.q;
-  p.kc = dp.kc; p.ks = static_cast<const float*>(dp.ks);
-  p.vc = dp.vc; p.vs = static_cast<const float*>(dp.vs);
+  p.kc = dp.kc; p.ks = dp.ks;
+  p.vc = dp.vc; p.vs = dp.vs;
   p.seq_lens = dp.seq_lens;
   p.out = dp.out;
   p.cnt = dp.cnt;
@@ -367,7 +369,8 @@ int launch_gqa(const DecodeParams& dp, int H_kv, int hd, int blk, float* part, l
   if (p.nc > 1 && groups * p.nc * GN > records) return NQKV_ERR_WORKSPACE;
   const long long items = groups * p.nc;
   if (items >= (1ll << 31)) return NQKV_ERR_SHAPE;
-  return p.bt ? launch_gqa_p<true>(p, hd, GN, items, st) : launch_gqa_p<false>(p, hd, GN, items, st);
+  if (f16s) return launch_gqa_p<false, true>(p, hd, GN, items, st);   // contiguous only (dispatch)
+  return p.bt ? launch_gqa_p<true, false>(p, hd, GN, items, st) : launch_gqa_p<false, false>(p, hd, GN, items, st);
 }
 
 // fused all-gather epilogue arguments (nqkv_decode_step_gather)
@@ -453,9 +456,9 @@ int decode_common(const void* q, const uint8_t* k_codes, const void* k_scales,
   // grouped-query attention over an fp32-scale cache (contiguous or paged)
   // with blk <= hd: the group-native kernel (each KV head streamed once per
   // <= 4 query heads)
-  if (lay.kv_shift > 0 && !f16s && blk <= hd && !plan && !k_new && !ga &&
-      gqa_native_enabled())
-    return launch_gqa(p, H_kv, hd, blk, reinterpret_cast<float*>(ws + w.gqa), w.gqa_records, st);
+  if (lay.kv_shift > 0 && blk <= hd && !plan && !k_new && !ga && gqa_native_enabled() &&
+      (!f16s || (gqa_tc_enabled() && !lay.bt)))
+    return launch_gqa(p, H_kv, hd, blk, f16s, reinterpret_cast<float*>(ws + w.gqa), w.gqa_records, st);
 #ifdef NQKV_TRACE
   if (const char* t = std::getenv("NQKV_TRACE_PTR"))
     p.trace = reinterpret_cast<unsigned long long*>(std::strtoull(t, nullptr, 0));
