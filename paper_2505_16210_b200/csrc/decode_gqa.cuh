@@ -31,8 +31,14 @@
 
 namespace nqkv {
 
-constexpr int kGqaWarps = 4;        // per CTA (3 CTAs per SM: 170 registers per thread)
-constexpr int kGqaCtasPerSm = 3;
+#ifndef NQKV_GQA_WARPS
+#define NQKV_GQA_WARPS 4
+#endif
+#ifndef NQKV_GQA_CTAS
+#define NQKV_GQA_CTAS 3
+#endif
+constexpr int kGqaWarps = NQKV_GQA_WARPS;      // per CTA (4 x 3 CTAs per SM: 170 registers per thread)
+constexpr int kGqaCtasPerSm = NQKV_GQA_CTAS;
 constexpr int kGqaSlots = 4;        // token slots per lane per stage
 constexpr int kGqaMaxChunkCap = 64;          // chunks per (b, kv head, sub-group)
 constexpr long long kGqaMaxRecords = 16384;  // partial records (hd + 2 floats) in the workspace
