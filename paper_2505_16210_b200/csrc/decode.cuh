@@ -1530,6 +1530,15 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
         Rg.vs[0] = ld_scale<F16S>(vsp, 0);
       }
     }
+#if NQKV_PF > 0
+    // bulk L2 prefetch of this warp's stage NQKV_PF ahead in the piece (lane
+    // 0's cursor is the stage's first row; K and V rows are contiguous)
+    if (lane == 0 && left >= NQKV_PF) {
+      const uint8_t* a = kcp + NQKV_PF * KSTEP;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(a), "r"(ST * (HD / 2)) : "memory");
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(a + vdelta), "r"(ST * (HD / 2)) : "memory");
+    }
+#endif
   };
   // two-stage register ring, unrolled as buffers A and B
   StageRegs RA, RB;
