@@ -31,13 +31,21 @@ cache.k_scales.uniform_(0.5, 2)
 cache.v_scales.uniform_(0.5, 2)
 q = torch.randn(B, H, hd, device="cuda").half()
 L = torch.full((B,), T, dtype=torch.int32, device="cuda")
+if os.environ.get("RAGGED"):           # lengths uniform in [T // 2, T] (BASELINE c3's recipe at T = 2049)
+    L = torch.randint(T // 2, T + 1, (B,), generator=torch.Generator().manual_seed(0),
+                      dtype=torch.int64).to(torch.int32).cuda()
 ws = N.make_workspace(B, H, hd, Tc, "cuda")
 flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
 warm = os.environ.get("WARM") == "1"    # trace the 2nd of two back-to-back launches (no flush between)
 planned = os.environ.get("PLAN") == "1"
 plan = N.make_plan("cuda")
-N.nqkv_decode_plan(L, H, Tc, False, plan, hd=hd)
-if planned:
+fused = os.environ.get("FUSED") == "1"   # fused append + attend (the runtime's step), planned
+N.nqkv_decode_plan(L, H, Tc, fused, plan, hd=hd)
+if fused:
+    kn = torch.randn(B, H, hd, device="cuda").half()
+    vn = torch.randn(B, H, hd, device="cuda").half()
+    cache.attend = lambda q_, L_, ws_: cache.step_planned(kn, vn, q_, L_, ws_, plan)
+elif planned:
     cache.attend = lambda q_, L_, ws_: cache.attend_planned(q_, L_, ws_, plan)
 for _ in range(5):
     flush.sum()                         # read-only L2 sweep (no dirty lines): HBM-honest timing
@@ -69,7 +77,7 @@ print(f"consumer wait on full barriers: med {w.median():.2f} max {w.max():.2f} u
 
 # per-CTA: slowest consumer loop end vs number of pieces in the CTA's range
 import numpy as np  # noqa: E402
-lens_h = [T] * B
+lens_h = L.cpu().tolist()
 N = B * H * T
 C = min(148, max(1, -(-N // 512)))
 pref = np.cumsum([0] + [H * n for n in lens_h])
