@@ -75,6 +75,9 @@ constexpr int kMinTokensPerCta = 512;  // below this a CTA's table build would d
 #ifndef NQKV_R64
 #define NQKV_R64 4               // q-table ring depth at hd 64 (two tables per 64 KB block)
 #endif
+#ifndef NQKV_LATE_APPEND
+#define NQKV_LATE_APPEND 1       // producer: release a piece's consumers before its appended token
+#endif
 #ifndef NQKV_PF
 #define NQKV_PF 0                // bulk L2 prefetch distance in a warp's own stages (0: off; measured: no gain)
 #endif
@@ -183,8 +186,14 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 #ifdef NQKV_TRACE
 #define TRACE(k) do { if (p.trace && lane == 0) p.trace[(blockIdx.x * NW + warp) * 16 + (k)] = gtimer(); } while (0)
+// producer phase durations (trace builds): accumulated, stored in slots
+// 4 (mb_done waits), 5 (merges), 13 (table builds), 15 (appended tokens)
+#define PT_START(t) const unsigned long long t = gtimer()
+#define PT_ACC(acc, t) acc += gtimer() - t
 #else
 #define TRACE(k) do { } while (0)
+#define PT_START(t) do { } while (0)
+#define PT_ACC(acc, t) do { } while (0)
 #endif
 
 template <int HD>
@@ -1655,15 +1664,27 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
     Piece pc = p0;
     TRACE(3);
     if (lane == 0) s_pc[0] = pc;
+#if NQKV_LATE_APPEND
+    // consumers need only the table; the appended-token state is read by the
+    // piece's merge (this warp, later): release them first
+    __syncwarp();
+    if (lane == 0) mbar_arrive(mb_full);
+    new_state(0, pc);
+    __syncwarp();
+#else
     new_state(0, pc);
     __syncwarp();
     if (lane == 0) mbar_arrive(mb_full);
+#endif
     TRACE(8);
     empties(cta, sc.C);
     Piece nx = pc;
     bool more = walk_next(nx, 0);
     uint4 qn = more ? load_quad(nx, lane % Q) : make_uint4(0, 0, 0, 0);
     int k = 0;
+#ifdef NQKV_TRACE
+    unsigned long long acc_w = 0, acc_m = 0, acc_b = 0, acc_n = 0;
+#endif
     while (more) {
       pc = nx;
       ++k;
@@ -1671,16 +1692,42 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_kernel(const __grid_constan
       more = walk_next(nx, k);
       if (more) qn = load_quad(nx, lane % Q);
       if (k >= R) {
-        mbar_wait_sleep(mb_done + 8 * ((k - R) % R), ((k - R) / R) & 1);
+        {
+          PT_START(t0w);
+          mbar_wait_sleep(mb_done + 8 * ((k - R) % R), ((k - R) / R) & 1);
+          PT_ACC(acc_w, t0w);
+        }
+        PT_START(t0m);
         merge_fn<HD, NW, GATHER>(p, smem, k - R, sc, cta, g0);
+        PT_ACC(acc_m, t0m);
       }
-      if (k >= R0) build_fn<HD, NW>(smem, k % R, qc, p.scale_log2);
-      __syncwarp();
+      {
+        PT_START(t0b);
+        if (k >= R0) build_fn<HD, NW>(smem, k % R, qc, p.scale_log2);
+        __syncwarp();
+        PT_ACC(acc_b, t0b);
+      }
       if (lane == 0) s_pc[k % R] = pc;
-      new_state(k, pc);
+#if NQKV_LATE_APPEND
       __syncwarp();
       if (lane == 0) mbar_arrive(mb_full + 8 * (k % R));
+#endif
+      {
+        PT_START(t0n);
+        new_state(k, pc);
+        __syncwarp();
+        PT_ACC(acc_n, t0n);
+      }
+#if !NQKV_LATE_APPEND
+      if (lane == 0) mbar_arrive(mb_full + 8 * (k % R));
+#endif
     }
+#ifdef NQKV_TRACE
+    if (p.trace && lane == 0) {
+      unsigned long long* tw = p.trace + (blockIdx.x * NW + warp) * 16;
+      tw[4] = acc_w; tw[5] = acc_m; tw[13] = acc_b; tw[15] = acc_n;
+    }
+#endif
     TRACE(9);
     for (int j = max(0, k + 1 - R); j <= k; ++j) {
       // the last piece: try to take the last-arriver role early (after the

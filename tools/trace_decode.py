@@ -60,11 +60,16 @@ for _ in range(5):
 t = tr.view(148, NW, 16).cpu()
 t0 = t[:, :, 0][t[:, :, 0] > 0].min()
 names = ["entry", "pdl_wait", "prefix", "prod: start", "loads issued", "V LUT", "table0", "sync", "full0", "loop end", "exit", "prod: last done", "last odd step", "g0/g1", ""]
+# producer phase sums (ns) in slots 4, 5, 13, 15 of the producer warp
+pw = t[:, NW - 1, :].double()
+for k, n in ((4, "waits on consumers"), (5, "merges"), (13, "table builds"), (15, "appended tokens")):
+    col = pw[:, k] / 1000.0
+    print(f"producer sum {n:20s} med {col.median():7.2f} max {col.max():7.2f} us")
 for role, sl in (("consumer", slice(0, NW - 1)), ("producer", slice(NW - 1, NW))):
     x = t[:, sl, :].reshape(-1, 16)
     x = x[x[:, 0] > 0]
     for k, n in enumerate(names):
-        if not n:
+        if not n or (role == "producer" and k in (4, 5, 13, 15)):
             continue
         col = x[:, k]
         col = col[col > 0]
